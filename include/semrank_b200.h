@@ -1,0 +1,239 @@
+/*
+ * semrank_b200.h — C-ABI of the B200-native prefill relevance ranker.
+ *
+ * Drop-in boundary for the reference scorer path (reference = semrank C++,
+ * /root/reference/proj). Every entry point cites the reference interface it
+ * replaces. Plain pointers and sizes only; no C++ or torch types cross it.
+ * A C++ facade with the reference's own type names (semrank::ModelConfig,
+ * ScoreRequest, ScoreResult, ScoringEngine) lives in semrank_b200.hpp.
+ *
+ * Conventions
+ *   - Every function returns an sr_status (0 = OK). On failure a thread-local
+ *     message is available from sr_last_error().
+ *   - Host buffers are borrowed for the duration of the call and never kept.
+ *   - One engine = one device + one CUDA stream; calls on one engine are
+ *     serialised (ScoringEngine::score holds a mutex, engine.cpp:389-392).
+ *   - There is no CPU fallback: scoring needs an sm_100 device and fails with
+ *     SR_CUDA otherwise.
+ */
+#ifndef SEMRANK_B200_H_
+#define SEMRANK_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SR_ABI_VERSION 1
+
+/* Status codes. 1..15 mirror semrank::ErrorCode in declaration order
+ * (include/semrank/error.hpp:13-29) so a facade can rethrow
+ * semrank::Error{ErrorCode(status - 1)}. */
+typedef enum sr_status {
+  SR_OK = 0,
+  SR_LENGTH_OVERFLOW = 1,
+  SR_MASK_INVALID = 2,
+  SR_SPEC_VIOLATION = 3,
+  SR_PAYLOAD_INVALID = 4,
+  SR_SCHEMA_UNKNOWN = 5,
+  SR_ALIGNMENT = 6,
+  SR_DIVERGENCE = 7,
+  SR_PARAMETER = 8,
+  SR_DEGENERATE_INPUT = 9,
+  SR_UNDEFINED_METRIC = 10,
+  SR_STATE_INVALID = 11,
+  SR_OVERSIZE_ITEM = 12,
+  SR_CONSISTENCY = 13,
+  SR_RECONCILIATION = 14,
+  SR_IO = 15,
+  SR_CUDA = 100,
+  SR_NCCL = 101
+} sr_status;
+
+/* ScoreMode (engine.hpp:15). */
+typedef enum sr_score_mode {
+  SR_MODE_NAIVE = 0,
+  SR_MODE_IBPC = 1,
+  SR_MODE_MULTI_ITEM = 2,
+  SR_MODE_MIXED = 3
+} sr_score_mode;
+
+/* Weight-init schemes for sr_weights_init. */
+typedef enum sr_init_scheme {
+  SR_INIT_REFERENCE = 0, /* init_model (model.cpp:94-134): N(0, 0.08^2) clamped to +-1 */
+  SR_INIT_FAN_IN = 1     /* same stream/order, std 1/sqrt(fan_in), residual outputs /sqrt(2L) */
+} sr_init_scheme;
+
+/* ModelConfig (model.hpp:24-40). head_names/head_arity have n_task_heads
+ * entries (HeadSpec, model.hpp:16-19). */
+typedef struct sr_model_config {
+  int32_t n_layers;
+  int32_t d_model;
+  int32_t n_heads;
+  int32_t d_ff;
+  int32_t vocab_size;
+  int32_t max_seq;
+  int32_t yes_token_id;
+  int32_t no_token_id;
+  int32_t n_task_heads;
+  const char* const* head_names;
+  const int32_t* head_arity;
+} sr_model_config;
+
+/* FlopReport (engine.hpp:38-44). */
+typedef struct sr_flop_report {
+  double attention_units;
+  double linear_units;
+  double t_q;
+  double t_i_mean;
+  double n_items;
+} sr_flop_report;
+
+/* ScoreRequest / ScoreItem (engine.hpp:20-33), flattened.
+ *   token modes: item i = item_tokens[item_offsets[i] .. item_offsets[i+1])
+ *   mixed mode : item i = item_rows[item_offsets[i]*d .. item_offsets[i+1]*d)
+ *                ([n_emb_tokens x d_model] fp32 soft-token rows)
+ * item_ids may be NULL (ids = 0..n_items-1); they are the doc ids used by the
+ * top-k tie rule (score desc, doc_id asc). */
+typedef struct sr_request {
+  const int32_t* prefix_tokens;
+  int32_t t_q;
+  int32_t n_items;
+  const int32_t* item_offsets; /* [n_items + 1], item_offsets[0] == 0 */
+  const int32_t* item_tokens;
+  const float* item_rows;
+  const int64_t* item_ids;
+  int32_t mode; /* sr_score_mode */
+} sr_request;
+
+/* ScoreResult (engine.hpp:53-59) plus the caller-side top-k. Any output
+ * pointer may be NULL. scores is [n_items x n_tasks] with column 0 =
+ * relevance and columns 1.. = task heads in config order (sr_task_count). */
+typedef struct sr_result {
+  double* scores;
+  int32_t k;            /* top-k length requested (0 = none) */
+  int64_t* topk_ids;    /* [k] */
+  double* topk_scores;  /* [k] relevance */
+  int32_t* topk_index;  /* [k] position in the request's item list */
+  sr_flop_report flops; /* filled on success */
+  double kv_incremental_per_item;
+  int32_t k_returned;   /* min(k, n_items) */
+} sr_result;
+
+typedef struct sr_weights sr_weights;
+typedef struct sr_engine sr_engine;
+typedef struct sr_comm sr_comm;
+typedef struct sr_plan sr_plan;
+
+/* ------------------------------------------------------------ diagnostics */
+const char* sr_last_error(void);
+/* error_code_name (error.cpp:8-27) for 1..15, "cuda"/"nccl"/"ok" otherwise. */
+const char* sr_status_name(int32_t status);
+int32_t sr_abi_version(void);
+
+/* ------------------------------------------------- host-side (no GPU needed) */
+/* ModelConfig::validate (model.cpp:29-50). */
+int32_t sr_config_validate(const sr_model_config* cfg);
+/* ModelConfig::default_toy (model.cpp:52-57). Pointers inside are static. */
+void sr_config_default_toy(sr_model_config* out);
+/* 1 (relevance) + number of task heads. */
+int32_t sr_task_count(const sr_model_config* cfg);
+
+/* ModelWeights (model.hpp:56-67) on the host. Tensors are in the SRNKWTS1
+ * canonical order (weights_io.cpp:47-71). */
+int32_t sr_weights_init(const sr_model_config* cfg, uint64_t seed, int32_t scheme,
+                        sr_weights** out); /* init_model, model.cpp:94-134 */
+int32_t sr_weights_load(const char* path, sr_weights** out);         /* weights_io.cpp:137-196 */
+int32_t sr_weights_save(const sr_weights* w, const char* path);      /* weights_io.cpp:104-135 */
+int32_t sr_weights_from_tensors(const sr_model_config* cfg, const char* version,
+                                const float* const* tensors, sr_weights** out);
+void sr_weights_free(sr_weights* w);
+/* Config view; pointers stay valid while w lives. */
+int32_t sr_weights_config(const sr_weights* w, sr_model_config* out);
+const char* sr_weights_version(const sr_weights* w);
+size_t sr_weights_tensor_count(const sr_weights* w);
+int32_t sr_weights_tensor(const sr_weights* w, size_t i, const char** name, float** data,
+                          size_t* numel);
+
+/* flops (engine.cpp:30-47). */
+int32_t sr_flops(int32_t mode, int64_t t_q, int64_t t_i, int64_t n_items, sr_flop_report* out);
+/* MultiItemMask::allowed_pair_count (engine.cpp:147-155). */
+int32_t sr_multi_item_pair_count(int32_t prefix_len, const int32_t* item_lengths, int32_t n,
+                                 int64_t* out);
+/* build_multi_item_mask + to_attention_mask (engine.cpp:157-184): per packed
+ * item row, {prefix_end, span_start} pairs (2 ints per row). */
+int32_t sr_multi_item_mask(int32_t prefix_len, const int32_t* item_lengths, int32_t n,
+                           int32_t* entries_out, int32_t cap_rows, int32_t* n_rows_out);
+/* plan_batches (engine.cpp:278-326). requests given as prefix lengths and
+ * flattened per-request item lengths (req_item_off[r]..req_item_off[r+1]).
+ * Output entries: (batch, request_index, item_begin, item_end) quadruples. */
+int32_t sr_plan_batches(int32_t n_requests, const int32_t* prefix_len,
+                        const int32_t* req_item_off, const int32_t* item_len,
+                        int64_t max_batch_tokens, int32_t* entries_out, int32_t cap_entries,
+                        int32_t* n_entries_out, int64_t* batch_tokens_out, int32_t cap_batches,
+                        int32_t* n_batches_out);
+/* Host top-k with the caller comparator (score desc, id asc, index asc). */
+int32_t sr_topk_host(const double* scores, const int64_t* ids, int32_t n, int32_t k,
+                     int64_t* ids_out, double* scores_out, int32_t* index_out);
+
+/* ------------------------------------------------------------------ engine */
+/* ScoringEngine(const ModelWeights&) (engine.hpp:109-119), bound to a device:
+ * converts the GEMM weights to bf16 K-major on the device once. */
+int32_t sr_engine_create(const sr_weights* w, int32_t device, sr_engine** out);
+void sr_engine_destroy(sr_engine* e);
+/* ScoringEngine::score / score_by_mode (engine.cpp:379-392) + top-k. */
+int32_t sr_engine_score(sr_engine* e, const sr_request* req, sr_result* res);
+/* Batched multi-query scoring (plan_batches generalisation): n_req requests
+ * packed into one device pass; res[i] receives request i's result. */
+int32_t sr_engine_score_batch(sr_engine* e, const sr_request* reqs, int32_t n_req,
+                              sr_result* res);
+/* Debug/parity: final-LN hidden row at each item's last position
+ * ([n_items x d_model] fp32), i.e. the row task_scores() consumes. */
+int32_t sr_engine_item_hidden(sr_engine* e, const sr_request* req, float* hidden_out);
+/* Device / stream the engine runs on. */
+int32_t sr_engine_device(const sr_engine* e);
+void* sr_engine_stream(const sr_engine* e);
+
+/* Resident-input path (benchmarking / serving loops): a plan owns packed
+ * device inputs and a captured CUDA graph for one request shape. */
+int32_t sr_plan_create(sr_engine* e, const sr_request* req, int32_t k, sr_plan** out);
+int32_t sr_plan_run(sr_plan* p);         /* enqueue on the engine stream; async */
+int32_t sr_plan_sync(sr_plan* p);
+int32_t sr_plan_fetch(sr_plan* p, sr_result* res); /* D2H of scores + top-k */
+int32_t sr_plan_kernel_count(const sr_plan* p, int32_t* launches);
+void sr_plan_destroy(sr_plan* p);
+
+/* ------------------------------------------------------- multi-GPU (NCCL) */
+/* Candidate sharding: every rank holds the full weights, scores its shard
+ * of the items (with global item ids) and the per-rank top-k lists are merged
+ * with one ncclAllGather; every rank returns the global top-k. */
+int32_t sr_nccl_unique_id(uint8_t out[128]);
+int32_t sr_comm_create(int32_t nranks, int32_t rank, const uint8_t id[128], int32_t device,
+                       sr_comm** out);
+void sr_comm_destroy(sr_comm* c);
+int32_t sr_engine_score_sharded(sr_engine* e, sr_comm* c, const sr_request* local_shard,
+                                sr_result* res);
+int32_t sr_plan_run_sharded(sr_plan* p, sr_comm* c); /* resident variant */
+
+/* --------------------------------------- kernel-level entry points (tests) */
+/* All pointers are device pointers; stream may be NULL (legacy stream). */
+/* C[M x N] = A[M x K] . B[N x K]^T ; epi 0 bf16, 1 gelu->bf16, 2 fp32 C += acc, 3 fp32. */
+int32_t sr_kernel_gemm(const void* a_bf16, const void* b_bf16, int32_t M, int32_t N, int32_t K,
+                       void* c, int32_t ldc, int32_t epi, void* stream);
+/* Segment-masked attention. qkv [M x 3d] bf16, spans [M x 4] int32
+ * {prefix_begin, prefix_end, span_start, 0}; out [M x d] bf16. Tiles are
+ * planned internally. */
+int32_t sr_kernel_attention(const void* qkv, const int32_t* spans_host, int32_t M,
+                            int32_t n_heads, int32_t head_dim, void* out, void* stream);
+int32_t sr_kernel_layernorm(const float* x, const float* gain, void* out_bf16, int32_t M,
+                            int32_t d, void* stream);
+int32_t sr_kernel_topk(const double* scores, const int64_t* ids, int32_t n, int32_t k,
+                       int64_t* ids_out_host, double* scores_out_host, int32_t* index_out_host);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SEMRANK_B200_H_ */

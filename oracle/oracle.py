@@ -1,0 +1,229 @@
+"""ctypes bindings of the CPU oracles. TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+--impl reference legs may import this module; the product never does.
+
+  Port  : build/liboracle.so   — C restatement (semrank_oracle.c), always buildable
+  Ref   : _ref/libsemrank_ref.so — the reference's own sources compiled in place
+          (present only where /root/reference existed at build time)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_PATH = os.path.join(HERE, "build", "liboracle.so")
+REF_PATH = os.path.join(HERE, "_ref", "libsemrank_ref.so")
+
+i32p = C.POINTER(C.c_int32)
+f32p = C.POINTER(C.c_float)
+f64p = C.POINTER(C.c_double)
+i64p = C.POINTER(C.c_int64)
+
+
+class OrConfig(C.Structure):
+    _fields_ = [("n_layers", C.c_int), ("d_model", C.c_int), ("n_heads", C.c_int),
+                ("d_ff", C.c_int), ("vocab_size", C.c_int), ("max_seq", C.c_int),
+                ("yes_token_id", C.c_int), ("no_token_id", C.c_int), ("n_task_heads", C.c_int),
+                ("head_arity", C.c_int * 16), ("head_names", (C.c_char * 32) * 16)]
+
+
+_port = None
+_ref = None
+
+
+def build_port() -> None:
+    subprocess.run(["make", "-s", "-C", HERE, "build/liboracle.so"], check=True)
+
+
+def port():
+    global _port
+    if _port is None:
+        if not os.path.exists(PORT_PATH):
+            build_port()
+        lib = C.CDLL(PORT_PATH)
+        lib.or_init.restype = C.c_void_p
+        lib.or_init.argtypes = [C.POINTER(OrConfig), C.c_uint64, C.c_int]
+        lib.or_load.restype = C.c_void_p
+        lib.or_load.argtypes = [C.c_char_p]
+        lib.or_save.argtypes = [C.c_void_p, C.c_char_p]
+        lib.or_free.argtypes = [C.c_void_p]
+        lib.or_round_bf16.argtypes = [C.c_void_p]
+        lib.or_tensor_count.argtypes = [C.c_void_p]
+        lib.or_tensor.restype = f32p
+        lib.or_tensor.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_size_t),
+                                  C.POINTER(C.c_char_p)]
+        lib.or_version.restype = C.c_char_p
+        lib.or_version.argtypes = [C.c_void_p]
+        lib.or_score.argtypes = [C.c_void_p, i32p, C.c_int, i32p, i32p, f32p, C.c_int, f64p, f32p,
+                                 C.c_int]
+        lib.or_prefill.argtypes = [C.c_void_p, i32p, C.c_int, f32p]
+        lib.or_attention.argtypes = [f32p, f32p, f32p, f32p, C.c_int, C.c_int, C.c_int, i32p]
+        lib.or_bench_tokens.argtypes = [C.c_uint64, C.c_char_p, C.c_int, C.c_int, C.c_int, i32p]
+        lib.or_uniform_ints.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int, i64p]
+        _port = lib
+    return _port
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_PATH)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        lib = C.CDLL(REF_PATH)
+        lib.ref_last_error.restype = C.c_char_p
+        lib.ref_set_parallel.argtypes = [C.c_int]
+        for fn in (lib.ref_init_save, lib.ref_init_fanin_save):
+            fn.argtypes = [i32p, C.c_int32, C.POINTER(C.c_char_p), i32p, C.c_uint64, C.c_char_p]
+        lib.ref_score.argtypes = [C.c_char_p, C.c_int32, i32p, C.c_int32, i32p, i32p, f32p,
+                                  C.c_int32, f64p, f64p, f64p]
+        lib.ref_prefill.argtypes = [C.c_char_p, i32p, C.c_int32, f32p]
+        lib.ref_attention.argtypes = [f32p, f32p, f32p, f32p, C.c_int32, C.c_int32, C.c_int32,
+                                      i32p]
+        lib.ref_flops.argtypes = [C.c_int32, C.c_int64, C.c_int64, C.c_int64, f64p]
+        lib.ref_plan_batches.argtypes = [C.c_int32, i32p, i32p, i32p, C.c_int64, i32p, C.c_int32,
+                                         i32p, i64p]
+        lib.ref_uniform_ints.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int32, i64p]
+        _ref = lib
+    return _ref
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t) if a is not None else None
+
+
+def config_struct(cfg) -> OrConfig:
+    """From a paper_2602_07309_b200.ModelConfig-like object (duck-typed)."""
+    c = OrConfig()
+    c.n_layers, c.d_model, c.n_heads, c.d_ff = cfg.n_layers, cfg.d_model, cfg.n_heads, cfg.d_ff
+    c.vocab_size, c.max_seq = cfg.vocab_size, cfg.max_seq
+    c.yes_token_id, c.no_token_id = cfg.yes_token_id, cfg.no_token_id
+    c.n_task_heads = len(cfg.head_specs)
+    for i, h in enumerate(cfg.head_specs):
+        c.head_arity[i] = h.arity
+        c.head_names[i].value = h.name.encode()
+    return c
+
+
+class OracleWeights:
+    """Weights held by the C restatement."""
+
+    def __init__(self, handle):
+        self.h = C.c_void_p(handle)
+        if not self.h.value:
+            raise RuntimeError("oracle: weight load/init failed")
+        self.cfg = OrConfig()
+        # config read back through the tensor table is enough for tests
+
+    @staticmethod
+    def init(cfg, seed: int, scheme: int = 0) -> "OracleWeights":
+        c = config_struct(cfg)
+        w = OracleWeights(port().or_init(C.byref(c), seed, scheme))
+        w.cfg = c
+        return w
+
+    @staticmethod
+    def load(path: str, cfg=None) -> "OracleWeights":
+        w = OracleWeights(port().or_load(path.encode()))
+        if cfg is not None:
+            w.cfg = config_struct(cfg)
+        return w
+
+    def __del__(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            port().or_free(self.h)
+            self.h = C.c_void_p()
+
+    def save(self, path: str) -> None:
+        if port().or_save(self.h, path.encode()) != 0:
+            raise RuntimeError("oracle: save failed")
+
+    def round_bf16(self) -> None:
+        port().or_round_bf16(self.h)
+
+    def tensors(self):
+        lib = port()
+        out = {}
+        for i in range(lib.or_tensor_count(self.h)):
+            n = C.c_size_t()
+            name = C.c_char_p()
+            ptr = lib.or_tensor(self.h, i, C.byref(n), C.byref(name))
+            out[name.value.decode()] = np.ctypeslib.as_array(ptr, shape=(n.value,)).copy()
+        return out
+
+    @property
+    def version(self) -> str:
+        return port().or_version(self.h).decode()
+
+    def score(self, prefix, items=None, rows=None, n_tasks=6, threads=0, hidden=False):
+        """items: list of token lists, or rows: list of [n x d] arrays (mixed)."""
+        prefix = np.ascontiguousarray(prefix, np.int32)
+        seq = items if items is not None else rows
+        lens = [len(x) if items is not None else np.asarray(x).shape[0] for x in seq]
+        off = np.zeros(len(lens) + 1, np.int32)
+        off[1:] = np.cumsum(lens)
+        tok = np.ascontiguousarray(np.concatenate([np.asarray(x, np.int32) for x in items]), np.int32) \
+            if items is not None else None
+        rw = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float32).reshape(-1) for x in rows]),
+                                  np.float32) if rows is not None else None
+        scores = np.zeros((len(lens), n_tasks))
+        d = int(self.cfg.d_model) if self.cfg.d_model else 0
+        hid = np.zeros((len(lens), d), np.float32) if hidden else None
+        st = port().or_score(self.h, _p(prefix, i32p), len(prefix), _p(off, i32p), _p(tok, i32p),
+                             _p(rw, f32p), len(lens), _p(scores, f64p), _p(hid, f32p), threads)
+        if st != 0:
+            raise ValueError("oracle: request violates a reference precondition")
+        return (scores, hid) if hidden else scores
+
+
+def bench_tokens(seed: int, t_q: int, t_i: int, n_items: int, stream: str = "bench"):
+    """cmd_bench token stream (semrank_main.cpp:602-616)."""
+    out = np.zeros(t_q + t_i * n_items, np.int32)
+    port().or_bench_tokens(seed, stream.encode(), t_q, t_i, n_items, _p(out, i32p))
+    return out[:t_q], [out[t_q + i * t_i: t_q + (i + 1) * t_i] for i in range(n_items)]
+
+
+def uniform_ints(seed: int, lo: int, hi: int, n: int):
+    out = np.zeros(n, np.int64)
+    port().or_uniform_ints(seed, lo, hi, n, _p(out, i64p))
+    return out
+
+
+def ref_score(weights_path: str, mode: int, prefix, items=None, rows=None, n_tasks=6):
+    lib = ref()
+    prefix = np.ascontiguousarray(prefix, np.int32)
+    seq = items if items is not None else rows
+    lens = [len(x) if items is not None else np.asarray(x).shape[0] for x in seq]
+    off = np.zeros(len(lens) + 1, np.int32)
+    off[1:] = np.cumsum(lens)
+    tok = np.ascontiguousarray(np.concatenate([np.asarray(x, np.int32) for x in items]), np.int32) \
+        if items is not None else None
+    rw = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float32).reshape(-1) for x in rows]),
+                              np.float32) if rows is not None else None
+    scores = np.zeros((len(lens), n_tasks))
+    fl = np.zeros(5)
+    kv = np.zeros(1)
+    st = lib.ref_score(weights_path.encode(), mode, _p(prefix, i32p), len(prefix), _p(off, i32p),
+                       _p(tok, i32p), _p(rw, f32p), len(lens), _p(scores, f64p), _p(fl, f64p),
+                       _p(kv, f64p))
+    if st != 0:
+        raise RuntimeError(f"reference error {st}: {lib.ref_last_error().decode()}")
+    return scores, fl, float(kv[0])
+
+
+def ref_init_save(cfg, seed: int, path: str, fan_in: bool = False) -> None:
+    lib = ref()
+    dims = np.array([cfg.n_layers, cfg.d_model, cfg.n_heads, cfg.d_ff, cfg.vocab_size,
+                     cfg.max_seq, cfg.yes_token_id, cfg.no_token_id], np.int32)
+    names = (C.c_char_p * max(1, len(cfg.head_specs)))(*[h.name.encode() for h in cfg.head_specs])
+    ar = np.array([h.arity for h in cfg.head_specs] or [1], np.int32)
+    fn = lib.ref_init_fanin_save if fan_in else lib.ref_init_save
+    st = fn(_p(dims, i32p), len(cfg.head_specs), names, _p(ar, i32p), seed, path.encode())
+    if st != 0:
+        raise RuntimeError(lib.ref_last_error().decode())

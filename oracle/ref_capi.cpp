@@ -1,0 +1,256 @@
+// ref_capi.cpp — C harness around the UNMODIFIED reference sources.
+//
+// TEST INFRASTRUCTURE ONLY (see oracle/semrank_oracle.c header). Built by
+// oracle/Makefile together with /root/reference/proj/src/{model,kernels,
+// engine,tokenizer,error,weights_io,prompt}.cpp compiled in place into
+// oracle/_ref/libsemrank_ref.so. Used to (a) generate the golden vectors in
+// tests/golden/, (b) pin the C restatement, (c) time the reference CPU path
+// for bench.py's cpu_baseline / --impl reference arm. Nothing here is
+// shipped or called by the product.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "semrank/engine.hpp"
+#include "semrank/error.hpp"
+#include "semrank/kernels.hpp"
+#include "semrank/model.hpp"
+#include "semrank/rng.hpp"
+#include "semrank/weights_io.hpp"
+
+using namespace semrank;
+
+namespace {
+thread_local std::string g_err;
+std::mutex g_mu;
+std::map<std::string, std::shared_ptr<ModelWeights>> g_weights;
+
+std::shared_ptr<ModelWeights> weights_for(const char* path) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  auto it = g_weights.find(path);
+  if (it != g_weights.end()) return it->second;
+  auto w = std::make_shared<ModelWeights>(load_weights(path));
+  g_weights[path] = w;
+  return w;
+}
+
+ModelConfig make_config(const int32_t* dims, int32_t n_heads_task, const char* const* names,
+                        const int32_t* arity) {
+  ModelConfig c;
+  c.n_layers = dims[0];
+  c.d_model = dims[1];
+  c.n_heads = dims[2];
+  c.d_ff = dims[3];
+  c.vocab_size = dims[4];
+  c.max_seq = dims[5];
+  c.yes_token_id = dims[6];
+  c.no_token_id = dims[7];
+  for (int i = 0; i < n_heads_task; ++i) c.head_specs.push_back({names[i], arity[i]});
+  return c;
+}
+
+template <typename F>
+int run(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return 1 + static_cast<int>(e.code());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 99;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+void ref_set_parallel(int parallel) {
+  kernels::set_default_exec(parallel ? kernels::Exec::Parallel : kernels::Exec::Serial);
+}
+
+void ref_forget_weights() {
+  std::lock_guard<std::mutex> lock(g_mu);
+  g_weights.clear();
+}
+
+// dims = {n_layers, d_model, n_heads, d_ff, vocab_size, max_seq, yes, no}
+int ref_init_save(const int32_t* dims, int32_t n_heads_task, const char* const* names,
+                  const int32_t* arity, uint64_t seed, const char* path) {
+  return run([&] {
+    const auto w = init_model(make_config(dims, n_heads_task, names, arity), seed);
+    save_weights(w, path);
+  });
+}
+
+// Fan-in scaled variant, built with the reference's own Rng and
+// container: same substream ("init"), same draw order as init_model
+// (model.cpp:94-134), only the per-tensor std differs.
+int ref_init_fanin_save(const int32_t* dims, int32_t n_heads_task, const char* const* names,
+                        const int32_t* arity, uint64_t seed, const char* path) {
+  return run([&] {
+    const ModelConfig cfg = make_config(dims, n_heads_task, names, arity);
+    cfg.validate();
+    Rng rng = Rng::substream(seed, "init");
+    ModelWeights w;
+    w.config = cfg;
+    char buf[40];
+    std::snprintf(buf, sizeof(buf), "fanin-%016llx", static_cast<unsigned long long>(seed));
+    w.version = buf;
+    auto fill = [&](std::vector<float>& t, size_t n, double sd) {
+      t.resize(n);
+      for (auto& v : t) v = static_cast<float>(std::clamp(rng.normal(0.0, sd), -1.0, 1.0));
+    };
+    const size_t d = cfg.d_model, F = cfg.d_ff;
+    const double e = static_cast<double>(0.08f);
+    const double resid = std::sqrt(2.0 * cfg.n_layers);
+    const double sd = 1.0 / std::sqrt(static_cast<double>(d));
+    fill(w.tok_emb, static_cast<size_t>(cfg.vocab_size) * d, e);
+    fill(w.pos_emb, static_cast<size_t>(cfg.max_seq) * d, e);
+    w.layers.resize(cfg.n_layers);
+    for (auto& l : w.layers) {
+      fill(l.wq, d * d, sd);
+      fill(l.wk, d * d, sd);
+      fill(l.wv, d * d, sd);
+      fill(l.wo, d * d, sd / resid);
+      l.ln1_gain.assign(d, 1.0f);
+      l.ln2_gain.assign(d, 1.0f);
+      fill(l.w_mlp_in, d * F, sd);
+      fill(l.w_mlp_out, F * d, 1.0 / std::sqrt(static_cast<double>(F)) / resid);
+    }
+    w.ln_f_gain.assign(d, 1.0f);
+    fill(w.w_vocab, d * static_cast<size_t>(cfg.vocab_size), sd);
+    for (const auto& s : cfg.head_specs) {
+      TaskHead h;
+      h.name = s.name;
+      h.arity = s.arity;
+      fill(h.w, d * static_cast<size_t>(s.arity), sd);
+      h.b.assign(s.arity, 0.0f);
+      w.heads.push_back(std::move(h));
+    }
+    save_weights(w, path);
+  });
+}
+
+// score_by_mode (engine.cpp:379-387) on a flattened request.
+// scores_out: [n_items x (1 + n_heads)] = relevance, then heads in config order.
+// flops_out: 5 doubles (FlopReport); kv_out: kv_incremental_per_item.
+int ref_score(const char* weights_path, int32_t mode, const int32_t* prefix, int32_t t_q,
+              const int32_t* offsets, const int32_t* tokens, const float* rows, int32_t n_items,
+              double* scores_out, double* flops_out, double* kv_out) {
+  return run([&] {
+    const auto w = weights_for(weights_path);
+    const int d = w->config.d_model;
+    ScoreRequest req;
+    req.request_id = "ref";
+    req.prefix_tokens.assign(prefix, prefix + t_q);
+    req.mode = static_cast<ScoreMode>(mode);
+    for (int i = 0; i < n_items; ++i) {
+      ScoreItem it;
+      it.id = std::to_string(i);
+      if (req.mode == ScoreMode::Mixed) {
+        it.n_emb_tokens = offsets[i + 1] - offsets[i];
+        it.embedding.assign(rows + static_cast<size_t>(offsets[i]) * d,
+                            rows + static_cast<size_t>(offsets[i + 1]) * d);
+      } else {
+        it.tokens.assign(tokens + offsets[i], tokens + offsets[i + 1]);
+      }
+      req.items.push_back(std::move(it));
+    }
+    const ScoreResult r = score_by_mode(*w, req);
+    const int T = 1 + static_cast<int>(w->config.head_specs.size());
+    for (int i = 0; i < n_items; ++i) {
+      const auto& tasks = r.items[i].tasks;
+      scores_out[static_cast<size_t>(i) * T] = tasks.at(kRelevanceTask);
+      for (size_t h = 0; h < w->config.head_specs.size(); ++h)
+        scores_out[static_cast<size_t>(i) * T + 1 + h] = tasks.at(w->config.head_specs[h].name);
+    }
+    if (flops_out) {
+      flops_out[0] = r.flops.attention_units;
+      flops_out[1] = r.flops.linear_units;
+      flops_out[2] = r.flops.t_q;
+      flops_out[3] = r.flops.t_i_mean;
+      flops_out[4] = r.flops.n_items;
+    }
+    if (kv_out) *kv_out = r.kv_incremental_per_item;
+  });
+}
+
+// prefill (model.cpp:251-273) from an empty cache; out_rows [n x d].
+int ref_prefill(const char* weights_path, const int32_t* tokens, int32_t n, float* out_rows) {
+  return run([&] {
+    const auto w = weights_for(weights_path);
+    KVCache cache = KVCache::empty(w->config);
+    std::vector<int> t(tokens, tokens + n);
+    const auto h = prefill(*w, t, cache);
+    std::memcpy(out_rows, h.data(), h.size() * sizeof(float));
+  });
+}
+
+// kernels::attention_serial (kernels.cpp:175-192); spans3 = {prefix_end, span_start, pos}.
+void ref_attention(const float* q, const float* k, const float* v, float* out, int32_t n_new,
+                   int32_t n_heads, int32_t head_dim, const int32_t* spans3) {
+  std::vector<kernels::MaskSpan> spans(n_new);
+  for (int i = 0; i < n_new; ++i) spans[i] = {spans3[3 * i], spans3[3 * i + 1], spans3[3 * i + 2]};
+  kernels::attention_serial(q, k, v, out, n_new, n_heads, head_dim, spans.data());
+}
+
+int ref_flops(int32_t mode, int64_t t_q, int64_t t_i, int64_t n, double* out5) {
+  return run([&] {
+    const auto r = flops(static_cast<ScoreMode>(mode), t_q, t_i, n);
+    out5[0] = r.attention_units;
+    out5[1] = r.linear_units;
+    out5[2] = r.t_q;
+    out5[3] = r.t_i_mean;
+    out5[4] = r.n_items;
+  });
+}
+
+// plan_batches (engine.cpp:278-326) -> (batch, request, begin, end) quadruples.
+int ref_plan_batches(int32_t n_req, const int32_t* prefix_len, const int32_t* req_item_off,
+                     const int32_t* item_len, int64_t budget, int32_t* out, int32_t cap,
+                     int32_t* n_out, int64_t* tokens_out) {
+  return run([&] {
+    std::vector<ScoreRequest> reqs(n_req);
+    for (int r = 0; r < n_req; ++r) {
+      reqs[r].prefix_tokens.assign(prefix_len[r], 1);
+      for (int i = req_item_off[r]; i < req_item_off[r + 1]; ++i) {
+        ScoreItem it;
+        it.tokens.assign(item_len[i], 2);
+        reqs[r].items.push_back(it);
+      }
+    }
+    const auto plan = plan_batches(reqs, budget);
+    int n = 0;
+    for (size_t b = 0; b < plan.size(); ++b) {
+      tokens_out[b] = plan[b].token_count;
+      for (const auto& e : plan[b].entries) {
+        if (n < cap) {
+          out[4 * n] = static_cast<int32_t>(b);
+          out[4 * n + 1] = static_cast<int32_t>(e.request_index);
+          out[4 * n + 2] = static_cast<int32_t>(e.item_begin);
+          out[4 * n + 3] = static_cast<int32_t>(e.item_end);
+        }
+        ++n;
+      }
+    }
+    *n_out = n;
+  });
+}
+
+// Rng(seed).uniform_int stream (rng.hpp:44-47), for seeded test requests.
+void ref_uniform_ints(uint64_t seed, int64_t lo, int64_t hi, int32_t n, int64_t* out) {
+  Rng r(seed);
+  for (int i = 0; i < n; ++i) out[i] = r.uniform_int(lo, hi);
+}
+
+}  // extern "C"

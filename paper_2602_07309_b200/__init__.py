@@ -1,0 +1,12 @@
+"""B200-native prefill relevance ranker (drop-in for the semrank scorer path).
+
+The product is the C-ABI shared library lib/libsemrank_b200.so (hand-written
+sm_100a kernels + C++ host runtime); this package is its Python binding with
+the reference's API names. See DESIGN.md.
+"""
+from .semrank import (  # noqa: F401
+    Batch, BatchEntry, ErrorCode, FlopReport, HeadSpec, ItemScores, ModelConfig, ModelWeights,
+    MultiItemMask, ScoreItem, ScoreMode, ScoreRequest, ScoreResult, ScoringEngine, SemrankError,
+    build_multi_item_mask, flops, init_model, kRelevanceTask, load_weights, plan_batches,
+    save_weights, score_by_mode, score_mode_from_name, score_mode_name, topk_host)
+from ._capi import LIB_PATH  # noqa: F401

@@ -1,0 +1,115 @@
+"""ctypes binding of the C-ABI in include/semrank_b200.h.
+
+The shared library is built in-tree (paper_2602_07309_b200/lib/) by
+``__graft_entry__.build()``. Importing this module fails loudly if it is
+missing: there is no Python or CPU fallback for the scoring path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsemrank_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+        " (the ranker has no CPU fallback)")
+
+lib = C.CDLL(LIB_PATH)
+
+i32, i64, u64, f32, f64, sz = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double, C.c_size_t
+P = C.POINTER
+
+
+class ModelConfigC(C.Structure):
+    _fields_ = [("n_layers", i32), ("d_model", i32), ("n_heads", i32), ("d_ff", i32),
+                ("vocab_size", i32), ("max_seq", i32), ("yes_token_id", i32),
+                ("no_token_id", i32), ("n_task_heads", i32),
+                ("head_names", P(C.c_char_p)), ("head_arity", P(i32))]
+
+
+class FlopReportC(C.Structure):
+    _fields_ = [("attention_units", f64), ("linear_units", f64), ("t_q", f64),
+                ("t_i_mean", f64), ("n_items", f64)]
+
+
+class RequestC(C.Structure):
+    _fields_ = [("prefix_tokens", P(i32)), ("t_q", i32), ("n_items", i32),
+                ("item_offsets", P(i32)), ("item_tokens", P(i32)), ("item_rows", P(f32)),
+                ("item_ids", P(i64)), ("mode", i32)]
+
+
+class ResultC(C.Structure):
+    _fields_ = [("scores", P(f64)), ("k", i32), ("topk_ids", P(i64)), ("topk_scores", P(f64)),
+                ("topk_index", P(i32)), ("flops", FlopReportC),
+                ("kv_incremental_per_item", f64), ("k_returned", i32)]
+
+
+def _sig(name, res, *args):
+    fn = getattr(lib, name)
+    fn.restype = res
+    fn.argtypes = list(args)
+    return fn
+
+
+vp = C.c_void_p
+_sig("sr_last_error", C.c_char_p)
+_sig("sr_status_name", C.c_char_p, i32)
+_sig("sr_abi_version", i32)
+_sig("sr_config_validate", i32, P(ModelConfigC))
+_sig("sr_config_default_toy", None, P(ModelConfigC))
+_sig("sr_task_count", i32, P(ModelConfigC))
+_sig("sr_weights_init", i32, P(ModelConfigC), u64, i32, P(vp))
+_sig("sr_weights_load", i32, C.c_char_p, P(vp))
+_sig("sr_weights_save", i32, vp, C.c_char_p)
+_sig("sr_weights_from_tensors", i32, P(ModelConfigC), C.c_char_p, P(P(f32)), P(vp))
+_sig("sr_weights_free", None, vp)
+_sig("sr_weights_config", i32, vp, P(ModelConfigC))
+_sig("sr_weights_version", C.c_char_p, vp)
+_sig("sr_weights_tensor_count", sz, vp)
+_sig("sr_weights_tensor", i32, vp, sz, P(C.c_char_p), P(P(f32)), P(sz))
+_sig("sr_flops", i32, i32, i64, i64, i64, P(FlopReportC))
+_sig("sr_multi_item_pair_count", i32, i32, P(i32), i32, P(i64))
+_sig("sr_multi_item_mask", i32, i32, P(i32), i32, P(i32), i32, P(i32))
+_sig("sr_plan_batches", i32, i32, P(i32), P(i32), P(i32), i64, P(i32), i32, P(i32), P(i64),
+     i32, P(i32))
+_sig("sr_topk_host", i32, P(f64), P(i64), i32, i32, P(i64), P(f64), P(i32))
+_sig("sr_engine_create", i32, vp, i32, P(vp))
+_sig("sr_engine_destroy", None, vp)
+_sig("sr_engine_score", i32, vp, P(RequestC), P(ResultC))
+_sig("sr_engine_score_batch", i32, vp, P(RequestC), i32, P(ResultC))
+_sig("sr_engine_item_hidden", i32, vp, P(RequestC), P(f32))
+_sig("sr_engine_device", i32, vp)
+_sig("sr_engine_stream", vp, vp)
+_sig("sr_plan_create", i32, vp, P(RequestC), i32, P(vp))
+_sig("sr_plan_run", i32, vp)
+_sig("sr_plan_sync", i32, vp)
+_sig("sr_plan_fetch", i32, vp, P(ResultC))
+_sig("sr_plan_kernel_count", i32, vp, P(i32))
+_sig("sr_plan_destroy", None, vp)
+_sig("sr_nccl_unique_id", i32, P(C.c_uint8))
+_sig("sr_comm_create", i32, i32, i32, P(C.c_uint8), i32, P(vp))
+_sig("sr_comm_destroy", None, vp)
+_sig("sr_engine_score_sharded", i32, vp, vp, P(RequestC), P(ResultC))
+_sig("sr_plan_run_sharded", i32, vp, vp)
+_sig("sr_kernel_gemm", i32, vp, vp, i32, i32, i32, vp, i32, i32, vp)
+_sig("sr_kernel_attention", i32, vp, P(i32), i32, i32, i32, vp, vp)
+_sig("sr_kernel_layernorm", i32, vp, vp, vp, i32, i32, vp)
+_sig("sr_kernel_topk", i32, vp, vp, i32, i32, P(i64), P(f64), P(i32))
+
+# Every symbol the header declares (tests check the library exports them).
+HEADER_SYMBOLS = [
+    "sr_last_error", "sr_status_name", "sr_abi_version", "sr_config_validate",
+    "sr_config_default_toy", "sr_task_count", "sr_weights_init", "sr_weights_load",
+    "sr_weights_save", "sr_weights_from_tensors", "sr_weights_free", "sr_weights_config",
+    "sr_weights_version", "sr_weights_tensor_count", "sr_weights_tensor", "sr_flops",
+    "sr_multi_item_pair_count", "sr_multi_item_mask", "sr_plan_batches", "sr_topk_host",
+    "sr_engine_create", "sr_engine_destroy", "sr_engine_score", "sr_engine_score_batch",
+    "sr_engine_item_hidden", "sr_engine_device", "sr_engine_stream", "sr_plan_create",
+    "sr_plan_run", "sr_plan_sync", "sr_plan_fetch", "sr_plan_kernel_count", "sr_plan_destroy",
+    "sr_nccl_unique_id", "sr_comm_create", "sr_comm_destroy", "sr_engine_score_sharded",
+    "sr_plan_run_sharded", "sr_kernel_gemm", "sr_kernel_attention", "sr_kernel_layernorm",
+    "sr_kernel_topk",
+]

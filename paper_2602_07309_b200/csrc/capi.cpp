@@ -1,0 +1,523 @@
+// extern "C" boundary (include/semrank_b200.h): thin wrappers that map
+// srh::Error to sr_status and keep a thread-local error message.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "host/engine.hpp"
+#include "host/model.hpp"
+#include "host/planner.hpp"
+#include "kernels/launch.h"
+#include "semrank_b200.h"
+
+namespace srh {
+namespace {
+thread_local std::string g_last_error;
+}
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace srh
+
+using srh::guard;
+
+struct sr_weights {
+  srh::ModelWeights w;
+  std::vector<std::string> head_name_store;
+  std::vector<const char*> head_names;
+  std::vector<int32_t> head_arity;
+  std::vector<std::pair<std::string, std::vector<float>*>> table;
+  void refresh() {
+    head_name_store.clear();
+    head_names.clear();
+    head_arity.clear();
+    for (const auto& h : w.config.head_specs) {
+      head_name_store.push_back(h.name);
+      head_arity.push_back(h.arity);
+    }
+    for (const auto& s : head_name_store) head_names.push_back(s.c_str());
+    table = w.tensor_table();
+  }
+};
+
+struct sr_engine {
+  std::unique_ptr<srh::Engine> e;
+};
+
+struct sr_comm {
+  srh::Comm* c = nullptr;
+};
+
+struct sr_plan {
+  sr_engine* owner = nullptr;
+  std::unique_ptr<srh::Plan> p;
+  bool sharded_valid = false;
+};
+
+namespace {
+
+void copy_topk_merged(srh::Plan& p, sr_result* res, cudaStream_t s) {
+  std::vector<srk::TopkEntry> top(p.k);
+  SR_CUDA_CHECK(cudaMemcpyAsync(top.data(), p.merged.ptr, top.size() * sizeof(srk::TopkEntry),
+                                cudaMemcpyDeviceToHost, s));
+  SR_CUDA_CHECK(cudaStreamSynchronize(s));
+  int32_t kr = 0;
+  for (int32_t j = 0; j < std::min(res->k, p.k); ++j) {
+    const auto& e = top[j];
+    if (e.index == INT32_MAX) break;  // sentinel: fewer candidates than k
+    if (res->topk_ids) res->topk_ids[j] = e.id;
+    if (res->topk_scores) res->topk_scores[j] = e.score;
+    if (res->topk_index) res->topk_index[j] = -1;  // global: index is rank-local
+    ++kr;
+  }
+  res->k_returned = kr;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sr_last_error(void) { return srh::g_last_error.c_str(); }
+
+const char* sr_status_name(int32_t status) {
+  static const char* names[] = {"ok",
+                                "length_overflow",
+                                "mask_invalid",
+                                "spec_violation",
+                                "payload_invalid",
+                                "schema_unknown",
+                                "alignment",
+                                "divergence",
+                                "parameter",
+                                "degenerate_input",
+                                "undefined_metric",
+                                "state_invalid",
+                                "oversize_item",
+                                "consistency",
+                                "reconciliation",
+                                "io"};
+  if (status >= 0 && status <= 15) return names[status];
+  if (status == SR_CUDA) return "cuda";
+  if (status == SR_NCCL) return "nccl";
+  return "unknown";
+}
+
+int32_t sr_abi_version(void) { return SR_ABI_VERSION; }
+
+int32_t sr_config_validate(const sr_model_config* cfg) {
+  return guard([&] {
+    if (!cfg) srh::fail(SR_SPEC_VIOLATION, "null config");
+    srh::ModelConfig::from_c(*cfg).validate();
+  });
+}
+
+void sr_config_default_toy(sr_model_config* out) {
+  static const char* names[] = {"click", "apply", "badfit", "shortlist", "dismiss"};
+  static const int32_t arity[] = {1, 1, 1, 1, 1};
+  out->n_layers = 2;
+  out->d_model = 64;
+  out->n_heads = 4;
+  out->d_ff = 256;
+  out->vocab_size = 300;
+  out->max_seq = srh::kDefaultMaxSeq;
+  out->yes_token_id = srh::kTokenYes;
+  out->no_token_id = srh::kTokenNo;
+  out->n_task_heads = 5;
+  out->head_names = names;
+  out->head_arity = arity;
+}
+
+int32_t sr_task_count(const sr_model_config* cfg) { return cfg ? 1 + cfg->n_task_heads : 0; }
+
+int32_t sr_weights_init(const sr_model_config* cfg, uint64_t seed, int32_t scheme,
+                        sr_weights** out) {
+  return guard([&] {
+    if (!cfg || !out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    auto w = std::make_unique<sr_weights>();
+    w->w = srh::init_model(srh::ModelConfig::from_c(*cfg), seed, scheme);
+    w->refresh();
+    *out = w.release();
+  });
+}
+
+int32_t sr_weights_load(const char* path, sr_weights** out) {
+  return guard([&] {
+    if (!path || !out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    auto w = std::make_unique<sr_weights>();
+    w->w = srh::load_weights(path);
+    w->refresh();
+    *out = w.release();
+  });
+}
+
+int32_t sr_weights_save(const sr_weights* w, const char* path) {
+  return guard([&] {
+    if (!w || !path) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    srh::save_weights(w->w, path);
+  });
+}
+
+int32_t sr_weights_from_tensors(const sr_model_config* cfg, const char* version,
+                                const float* const* tensors, sr_weights** out) {
+  return guard([&] {
+    if (!cfg || !tensors || !out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    auto w = std::make_unique<sr_weights>();
+    w->w.config = srh::ModelConfig::from_c(*cfg);
+    w->w.config.validate();
+    w->w.version = version ? version : "";
+    w->w.allocate();
+    size_t i = 0;
+    for (auto& [name, t] : w->w.tensor_table()) {
+      if (!tensors[i]) srh::fail(SR_SPEC_VIOLATION, "null tensor " + name);
+      std::memcpy(t->data(), tensors[i], t->size() * sizeof(float));
+      ++i;
+    }
+    w->refresh();
+    *out = w.release();
+  });
+}
+
+void sr_weights_free(sr_weights* w) { delete w; }
+
+int32_t sr_weights_config(const sr_weights* w, sr_model_config* out) {
+  return guard([&] {
+    if (!w || !out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    const auto& c = w->w.config;
+    out->n_layers = c.n_layers;
+    out->d_model = c.d_model;
+    out->n_heads = c.n_heads;
+    out->d_ff = c.d_ff;
+    out->vocab_size = c.vocab_size;
+    out->max_seq = c.max_seq;
+    out->yes_token_id = c.yes_token_id;
+    out->no_token_id = c.no_token_id;
+    out->n_task_heads = static_cast<int32_t>(c.head_specs.size());
+    out->head_names = w->head_names.data();
+    out->head_arity = w->head_arity.data();
+  });
+}
+
+const char* sr_weights_version(const sr_weights* w) { return w ? w->w.version.c_str() : ""; }
+
+size_t sr_weights_tensor_count(const sr_weights* w) { return w ? w->table.size() : 0; }
+
+int32_t sr_weights_tensor(const sr_weights* w, size_t i, const char** name, float** data,
+                          size_t* numel) {
+  return guard([&] {
+    if (!w || i >= w->table.size()) srh::fail(SR_PARAMETER, "tensor index out of range");
+    if (name) *name = w->table[i].first.c_str();
+    if (data) *data = w->table[i].second->data();
+    if (numel) *numel = w->table[i].second->size();
+  });
+}
+
+int32_t sr_flops(int32_t mode, int64_t t_q, int64_t t_i, int64_t n_items, sr_flop_report* out) {
+  return guard([&] {
+    const auto r = srh::flops(mode, t_q, t_i, n_items);
+    if (out) *out = r;
+  });
+}
+
+int32_t sr_multi_item_pair_count(int32_t prefix_len, const int32_t* item_lengths, int32_t n,
+                                 int64_t* out) {
+  return guard([&] {
+    if (prefix_len < 0) srh::fail(SR_SPEC_VIOLATION, "negative prefix length");
+    for (int i = 0; i < n; ++i)
+      if (item_lengths[i] < 1) srh::fail(SR_SPEC_VIOLATION, "zero-length item in multi-item mask");
+    *out = srh::multi_item_pair_count(prefix_len, item_lengths, n);
+  });
+}
+
+int32_t sr_multi_item_mask(int32_t prefix_len, const int32_t* item_lengths, int32_t n,
+                           int32_t* entries_out, int32_t cap_rows, int32_t* n_rows_out) {
+  return guard([&] {  // engine.cpp:157-184
+    if (prefix_len < 0) srh::fail(SR_SPEC_VIOLATION, "negative prefix length");
+    int32_t rows = 0, cursor = prefix_len;
+    for (int i = 0; i < n; ++i) {
+      const int32_t len = item_lengths[i];
+      if (len < 1) srh::fail(SR_SPEC_VIOLATION, "zero-length item in multi-item mask");
+      for (int32_t p = cursor; p < cursor + len; ++p, ++rows) {
+        if (entries_out && rows < cap_rows) {
+          entries_out[2 * rows] = prefix_len;
+          entries_out[2 * rows + 1] = cursor;
+        }
+      }
+      cursor += len;
+    }
+    if (n_rows_out) *n_rows_out = rows;
+    if (entries_out && rows > cap_rows) srh::fail(SR_PARAMETER, "mask output buffer too small");
+  });
+}
+
+int32_t sr_plan_batches(int32_t n_requests, const int32_t* prefix_len,
+                        const int32_t* req_item_off, const int32_t* item_len,
+                        int64_t max_batch_tokens, int32_t* entries_out, int32_t cap_entries,
+                        int32_t* n_entries_out, int64_t* batch_tokens_out, int32_t cap_batches,
+                        int32_t* n_batches_out) {
+  return guard([&] {
+    std::vector<int32_t> pl(prefix_len, prefix_len + n_requests);
+    std::vector<std::vector<int32_t>> il(n_requests);
+    for (int r = 0; r < n_requests; ++r)
+      il[r].assign(item_len + req_item_off[r], item_len + req_item_off[r + 1]);
+    const auto batches = srh::plan_batches(pl, il, max_batch_tokens);
+    int32_t ne = 0;
+    for (size_t b = 0; b < batches.size(); ++b) {
+      if (batch_tokens_out && static_cast<int32_t>(b) < cap_batches)
+        batch_tokens_out[b] = batches[b].token_count;
+      for (const auto& e : batches[b].entries) {
+        if (entries_out && ne < cap_entries) {
+          entries_out[4 * ne + 0] = static_cast<int32_t>(b);
+          entries_out[4 * ne + 1] = e.request_index;
+          entries_out[4 * ne + 2] = e.item_begin;
+          entries_out[4 * ne + 3] = e.item_end;
+        }
+        ++ne;
+      }
+    }
+    if (n_entries_out) *n_entries_out = ne;
+    if (n_batches_out) *n_batches_out = static_cast<int32_t>(batches.size());
+    if ((entries_out && ne > cap_entries) ||
+        (batch_tokens_out && static_cast<int32_t>(batches.size()) > cap_batches))
+      srh::fail(SR_PARAMETER, "plan output buffers too small");
+  });
+}
+
+int32_t sr_topk_host(const double* scores, const int64_t* ids, int32_t n, int32_t k,
+                     int64_t* ids_out, double* scores_out, int32_t* index_out) {
+  return guard([&] {
+    if (n < 0 || k < 0) srh::fail(SR_PARAMETER, "negative size");
+    const auto top = srh::topk_host(scores, ids, n, k);
+    for (size_t j = 0; j < top.size(); ++j) {
+      if (ids_out) ids_out[j] = top[j].id;
+      if (scores_out) scores_out[j] = top[j].score;
+      if (index_out) index_out[j] = top[j].index;
+    }
+  });
+}
+
+int32_t sr_engine_create(const sr_weights* w, int32_t device, sr_engine** out) {
+  return guard([&] {
+    if (!w || !out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    auto e = std::make_unique<sr_engine>();
+    e->e = std::make_unique<srh::Engine>(w->w, device);
+    *out = e.release();
+  });
+}
+
+void sr_engine_destroy(sr_engine* e) { delete e; }
+
+int32_t sr_engine_score(sr_engine* e, const sr_request* req, sr_result* res) {
+  return guard([&] {
+    if (!e || !req || !res) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    e->e->score(req, 1, res);
+  });
+}
+
+int32_t sr_engine_score_batch(sr_engine* e, const sr_request* reqs, int32_t n_req,
+                              sr_result* res) {
+  return guard([&] {
+    if (!e || !reqs || !res) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    e->e->score(reqs, n_req, res);
+  });
+}
+
+int32_t sr_engine_item_hidden(sr_engine* e, const sr_request* req, float* hidden_out) {
+  return guard([&] {
+    if (!e || !req || !hidden_out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    e->e->item_hidden(*req, hidden_out);
+  });
+}
+
+int32_t sr_engine_device(const sr_engine* e) { return e ? e->e->device() : -1; }
+void* sr_engine_stream(const sr_engine* e) { return e ? e->e->stream() : nullptr; }
+
+int32_t sr_plan_create(sr_engine* e, const sr_request* req, int32_t k, sr_plan** out) {
+  return guard([&] {
+    if (!e || !req || !out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    auto p = std::make_unique<sr_plan>();
+    p->owner = e;
+    p->p = e->e->make_plan(req, 1, k);
+    *out = p.release();
+  });
+}
+
+int32_t sr_plan_run(sr_plan* p) {
+  return guard([&] {
+    if (!p) srh::fail(SR_SPEC_VIOLATION, "null plan");
+    p->owner->e->run_plan(*p->p);
+    p->sharded_valid = false;
+  });
+}
+
+int32_t sr_plan_sync(sr_plan* p) {
+  return guard([&] {
+    if (!p) srh::fail(SR_SPEC_VIOLATION, "null plan");
+    SR_CUDA_CHECK(cudaStreamSynchronize(p->owner->e->stream()));
+  });
+}
+
+int32_t sr_plan_fetch(sr_plan* p, sr_result* res) {
+  return guard([&] {
+    if (!p || !res) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    p->owner->e->fetch(*p->p, res, 1);
+    if (p->sharded_valid) copy_topk_merged(*p->p, res, p->owner->e->stream());
+  });
+}
+
+int32_t sr_plan_kernel_count(const sr_plan* p, int32_t* launches) {
+  return guard([&] {
+    if (!p || !launches) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    *launches = p->p->launches;
+  });
+}
+
+void sr_plan_destroy(sr_plan* p) { delete p; }
+
+int32_t sr_nccl_unique_id(uint8_t out[128]) {
+  return guard([&] { srh::nccl_unique_id(out); });
+}
+
+int32_t sr_comm_create(int32_t nranks, int32_t rank, const uint8_t id[128], int32_t device,
+                       sr_comm** out) {
+  return guard([&] {
+    auto c = std::make_unique<sr_comm>();
+    c->c = srh::comm_create(nranks, rank, id, device);
+    *out = c.release();
+  });
+}
+
+void sr_comm_destroy(sr_comm* c) {
+  if (c) srh::comm_destroy(c->c);
+  delete c;
+}
+
+int32_t sr_engine_score_sharded(sr_engine* e, sr_comm* c, const sr_request* local_shard,
+                                sr_result* res) {
+  return guard([&] {
+    if (!e || !c || !local_shard || !res) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    auto p = e->e->make_plan(local_shard, 1, res->k);
+    e->e->run_plan_sharded(*p, c->c);
+    e->e->fetch(*p, res, 1);
+    if (c->c->nranks > 1) copy_topk_merged(*p, res, e->e->stream());
+  });
+}
+
+int32_t sr_plan_run_sharded(sr_plan* p, sr_comm* c) {
+  return guard([&] {
+    if (!p || !c) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    p->owner->e->run_plan_sharded(*p->p, c->c);
+    p->sharded_valid = c->c->nranks > 1;
+  });
+}
+
+// ------------------------------------------------------------ kernel tests
+int32_t sr_kernel_gemm(const void* a_bf16, const void* b_bf16, int32_t M, int32_t N, int32_t K,
+                       void* c, int32_t ldc, int32_t epi, void* stream) {
+  return guard([&] {
+    const int bn = srk::gemm_pick_bn(N);
+    if (bn == 0) srh::fail(SR_SPEC_VIOLATION, "N must be a multiple of 64");
+    if (K % 8 != 0) srh::fail(SR_SPEC_VIOLATION, "K must be a multiple of 8");
+    CUtensorMap ta, tb;
+    SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&ta, a_bf16, M, K, 128, 64));
+    SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tb, b_bf16, N, K, bn, 64));
+    SR_CUDA_CHECK(srk::gemm_bf16(ta, tb, M, N, K, c, ldc, epi, bn,
+                                 static_cast<cudaStream_t>(stream)));
+    SR_CUDA_CHECK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  });
+}
+
+int32_t sr_kernel_attention(const void* qkv, const int32_t* spans_host, int32_t M,
+                            int32_t n_heads, int32_t head_dim, void* out, void* stream) {
+  return guard([&] {
+    // Tiles: 64-row query tiles; keys = [min prefix_begin, max prefix_end) and
+    // [min span_start, q_end) (ranges merged when they touch).
+    std::vector<srk::RowSpan> spans(M);
+    std::memcpy(spans.data(), spans_host, sizeof(srk::RowSpan) * M);
+    std::vector<srk::AttnTile> tiles;
+    for (int r0 = 0; r0 < M; r0 += 64) {
+      const int r1 = std::min(M, r0 + 64);
+      int pb = INT32_MAX, pe = 0, ss = INT32_MAX;
+      for (int r = r0; r < r1; ++r) {
+        const auto& s = spans[r];
+        if (s.prefix_begin < 0 || s.prefix_end < s.prefix_begin || s.span_start < s.prefix_end ||
+            s.span_start > r)
+          srh::fail(SR_MASK_INVALID, "mask entry " + std::to_string(r) +
+                                         " violates prefix_end <= span_start <= position");
+        if (s.prefix_end > s.prefix_begin) {
+          pb = std::min(pb, s.prefix_begin);
+          pe = std::max(pe, s.prefix_end);
+        }
+        ss = std::min(ss, s.span_start);
+      }
+      srk::AttnTile t{r0, r1, 0, 0, ss, r1, 0, 0};
+      if (pe > 0) {
+        if (pe >= ss) {  // overlapping ranges: one contiguous range
+          t.r2_begin = std::min(pb, ss);
+        } else {
+          t.r1_begin = pb;
+          t.r1_end = pe;
+        }
+      }
+      tiles.push_back(t);
+    }
+    srk::RowSpan* dsp = nullptr;
+    srk::AttnTile* dt = nullptr;
+    SR_CUDA_CHECK(cudaMalloc(&dsp, sizeof(srk::RowSpan) * M));
+    SR_CUDA_CHECK(cudaMalloc(&dt, sizeof(srk::AttnTile) * tiles.size()));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaMemcpy(dsp, spans.data(), sizeof(srk::RowSpan) * M, cudaMemcpyHostToDevice);
+    cudaMemcpy(dt, tiles.data(), sizeof(srk::AttnTile) * tiles.size(), cudaMemcpyHostToDevice);
+    cudaError_t err = srk::attention(static_cast<const __nv_bfloat16*>(qkv), dsp, dt,
+                                     static_cast<int>(tiles.size()),
+                                     static_cast<__nv_bfloat16*>(out), M, n_heads, head_dim, s);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(s);
+    cudaFree(dsp);
+    cudaFree(dt);
+    SR_CUDA_CHECK(err);
+  });
+}
+
+int32_t sr_kernel_layernorm(const float* x, const float* gain, void* out_bf16, int32_t M,
+                            int32_t d, void* stream) {
+  return guard([&] {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    SR_CUDA_CHECK(srk::layer_norm_bf16(x, gain, static_cast<__nv_bfloat16*>(out_bf16), M, d, s));
+    SR_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int32_t sr_kernel_topk(const double* scores, const int64_t* ids, int32_t n, int32_t k,
+                       int64_t* ids_out_host, double* scores_out_host, int32_t* index_out_host) {
+  return guard([&] {
+    if (n <= 0 || k <= 0) srh::fail(SR_PARAMETER, "n and k must be >= 1");
+    int32_t* seg = nullptr;
+    srk::TopkEntry *scratch = nullptr, *out = nullptr;
+    const int chunks = (n + 4095) / 4096;
+    const int32_t off[2] = {0, n};
+    SR_CUDA_CHECK(cudaMalloc(&seg, sizeof(off)));
+    SR_CUDA_CHECK(cudaMalloc(&scratch, sizeof(srk::TopkEntry) * chunks * k));
+    SR_CUDA_CHECK(cudaMalloc(&out, sizeof(srk::TopkEntry) * k));
+    cudaMemcpy(seg, off, sizeof(off), cudaMemcpyHostToDevice);
+    cudaError_t err =
+        srk::topk(scores, 1, ids, seg, 1, n, k, scratch, chunks * k, out, nullptr);
+    std::vector<srk::TopkEntry> h(k);
+    if (err == cudaSuccess)
+      err = cudaMemcpy(h.data(), out, sizeof(srk::TopkEntry) * k, cudaMemcpyDeviceToHost);
+    cudaFree(seg);
+    cudaFree(scratch);
+    cudaFree(out);
+    SR_CUDA_CHECK(err);
+    for (int j = 0; j < std::min(k, n); ++j) {
+      if (ids_out_host) ids_out_host[j] = h[j].id;
+      if (scores_out_host) scores_out_host[j] = h[j].score;
+      if (index_out_host) index_out_host[j] = h[j].index;
+    }
+  });
+}
+
+}  // extern "C"

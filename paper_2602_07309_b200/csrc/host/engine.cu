@@ -1,0 +1,466 @@
+// Device engine implementation: weight conversion, workspace, the packed
+// forward (one launch sequence per request batch), CUDA-graph plans, NCCL.
+//
+// Forward for a packed batch (model.cpp:149-220 restated for B200):
+//   embed+LN1      x = emb + pos (fp32 residual), xn = bf16 LN1(x)
+//   per layer l:   qkv = xn Wqkv^T                 tcgen05 GEMM, bf16 out
+//                  xn  = attention(qkv, spans)     segment-masked, bf16 out
+//                  x  += xn Wo^T                   tcgen05 GEMM, fp32 residual epilogue
+//                  xn  = LN2(x)
+//                  h   = gelu(xn Win^T)            tcgen05 GEMM, GELU epilogue
+//                  x  += h Wout^T                  tcgen05 GEMM, fp32 residual epilogue
+//                  xn  = LN1_{l+1}(x)              (skipped after the last layer)
+//   score head on the items' last rows (final LN fused), then top-k.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "engine.hpp"
+
+namespace srh {
+
+namespace {
+
+template <typename T>
+T* upload(const std::vector<T>& v, std::vector<void*>& allocs) {
+  T* p = nullptr;
+  SR_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(v.size(), 1) * sizeof(T)));
+  allocs.push_back(p);
+  if (!v.empty()) {
+    SR_CUDA_CHECK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    SR_CUDA_CHECK(cudaDeviceSynchronize());  // pageable copies may still be in flight
+  }
+  return p;
+}
+
+void make_weight_map(CUtensorMap* m, const void* w, int rows, int cols) {
+  const int bn = srk::gemm_pick_bn(rows);
+  SR_CUDA_CHECK(srk::make_tmap_bf16_2d(m, w, rows, cols, bn, 64));
+}
+
+}  // namespace
+
+Engine::Engine(const ModelWeights& w, int device) : cfg_(w.config), device_(device) {
+  w.check_shapes();
+  cfg_.validate();
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    fail(SR_CUDA, "no CUDA device: the B200 ranker has no CPU fallback");
+  if (device < 0 || device >= ndev) fail(SR_PARAMETER, "device index out of range");
+  SR_CUDA_CHECK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  SR_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    fail(SR_CUDA, std::string("requires an sm_100 (Blackwell) device, found ") + prop.name);
+  const int d = cfg_.d_model, F = cfg_.d_ff;
+  if (d % 64 != 0 || F % 64 != 0)
+    fail(SR_SPEC_VIOLATION, "d_model and d_ff must be multiples of 64 on the tcgen05 path");
+  const int hd = cfg_.head_dim();
+  if (hd != 16 && hd != 32 && hd != 64 && hd != 128)
+    fail(SR_SPEC_VIOLATION, "head_dim must be one of 16/32/64/128");
+  SR_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+
+  tok_emb_ = upload(w.tok_emb, allocs_);
+  pos_emb_ = upload(w.pos_emb, allocs_);
+  ln_f_ = upload(w.ln_f_gain, allocs_);
+
+  // fp32 [K x N] staging -> bf16 [N x K] (K-major B operand) on the device.
+  float* stage = nullptr;
+  const size_t stage_elems = static_cast<size_t>(std::max(d, F)) * std::max(d, F);
+  SR_CUDA_CHECK(cudaMalloc(&stage, stage_elems * sizeof(float)));
+  auto conv = [&](const std::vector<float>& src, __nv_bfloat16* dst, int K, int N) {
+    // Same-stream copy: a pageable cudaMemcpy may return before its DMA lands,
+    // and stream_ is non-blocking w.r.t. the legacy stream.
+    SR_CUDA_CHECK(cudaMemcpyAsync(stage, src.data(), src.size() * sizeof(float),
+                                  cudaMemcpyHostToDevice, stream_));
+    SR_CUDA_CHECK(srk::transpose_to_bf16(stage, dst, K, N, stream_));
+    SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  };
+  layers_.resize(cfg_.n_layers);
+  for (int l = 0; l < cfg_.n_layers; ++l) {
+    const auto& lw = w.layers[l];
+    auto& L = layers_[l];
+    auto alloc_bf16 = [&](size_t n) {
+      __nv_bfloat16* p = nullptr;
+      SR_CUDA_CHECK(cudaMalloc(&p, n * sizeof(__nv_bfloat16)));
+      allocs_.push_back(p);
+      return p;
+    };
+    L.wqkv = alloc_bf16(static_cast<size_t>(3) * d * d);
+    L.wo = alloc_bf16(static_cast<size_t>(d) * d);
+    L.win = alloc_bf16(static_cast<size_t>(F) * d);
+    L.wout = alloc_bf16(static_cast<size_t>(d) * F);
+    conv(lw.wq, L.wqkv, d, d);
+    conv(lw.wk, L.wqkv + static_cast<size_t>(d) * d, d, d);
+    conv(lw.wv, L.wqkv + static_cast<size_t>(2) * d * d, d, d);
+    conv(lw.wo, L.wo, d, d);
+    conv(lw.w_mlp_in, L.win, d, F);
+    conv(lw.w_mlp_out, L.wout, F, d);
+    L.ln1 = upload(lw.ln1_gain, allocs_);
+    L.ln2 = upload(lw.ln2_gain, allocs_);
+    make_weight_map(&L.tm_qkv, L.wqkv, 3 * d, d);
+    make_weight_map(&L.tm_o, L.wo, d, d);
+    make_weight_map(&L.tm_in, L.win, F, d);
+    make_weight_map(&L.tm_out, L.wout, d, F);
+  }
+  cudaFree(stage);
+
+  // Score-head columns: [w_vocab[:,yes], w_vocab[:,no], head columns...].
+  const int V = cfg_.vocab_size;
+  std::vector<float> cols, bias;
+  std::vector<int32_t> tcol, tar;
+  auto add_col = [&](auto get, float b) {
+    for (int j = 0; j < d; ++j) cols.push_back(get(j));
+    bias.push_back(b);
+  };
+  add_col([&](int j) { return w.w_vocab[static_cast<size_t>(j) * V + cfg_.yes_token_id]; }, 0.f);
+  add_col([&](int j) { return w.w_vocab[static_cast<size_t>(j) * V + cfg_.no_token_id]; }, 0.f);
+  yes_col_ = 0;
+  no_col_ = 1;
+  for (const auto& h : w.heads) {
+    tcol.push_back(static_cast<int32_t>(bias.size()));
+    tar.push_back(h.arity);
+    for (int a = 0; a < h.arity; ++a)
+      add_col([&](int j) { return h.w[static_cast<size_t>(j) * h.arity + a]; }, h.b[a]);
+  }
+  n_cols_ = static_cast<int>(bias.size());
+  head_w_ = upload(cols, allocs_);
+  head_b_ = upload(bias, allocs_);
+  task_col_ = upload(tcol, allocs_);
+  task_arity_ = upload(tar, allocs_);
+  SR_CUDA_CHECK(cudaDeviceSynchronize());
+}
+
+Engine::~Engine() {
+  cache_.clear();
+  cudaSetDevice(device_);
+  for (void* p : allocs_) cudaFree(p);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+Plan::~Plan() {
+  if (graph) cudaGraphExecDestroy(graph);
+}
+
+void Engine::ensure_workspace(int32_t M) {
+  if (M <= ws_rows_) return;
+  const int32_t rows = M + M / 4 + 128;
+  const size_t d = cfg_.d_model, F = cfg_.d_ff;
+  x_.release();
+  xn_.release();
+  qkv_.release();
+  h_.release();
+  SR_CUDA_CHECK(cudaMalloc(&x_.ptr, rows * d * sizeof(float)));
+  x_.cap = rows * d;
+  SR_CUDA_CHECK(cudaMalloc(&xn_.ptr, rows * d * sizeof(__nv_bfloat16)));
+  xn_.cap = rows * d;
+  SR_CUDA_CHECK(cudaMalloc(&qkv_.ptr, rows * 3 * d * sizeof(__nv_bfloat16)));
+  qkv_.cap = rows * 3 * d;
+  SR_CUDA_CHECK(cudaMalloc(&h_.ptr, rows * F * sizeof(__nv_bfloat16)));
+  h_.cap = rows * F;
+  // Rows past M hold stale data; GEMM tiles read them but never store them.
+  SR_CUDA_CHECK(cudaMemset(xn_.ptr, 0, rows * d * sizeof(__nv_bfloat16)));
+  SR_CUDA_CHECK(cudaMemset(h_.ptr, 0, rows * F * sizeof(__nv_bfloat16)));
+  SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tm_xn_, xn_.ptr, rows, d, 128, 64));
+  SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tm_h_, h_.ptr, rows, F, 128, 64));
+  ws_rows_ = rows;
+  ++ws_epoch_;
+}
+
+int32_t Engine::enqueue_forward(Plan& p, float* hidden_out) {
+  const int M = p.pack.M, d = cfg_.d_model, F = cfg_.d_ff, H = cfg_.n_heads;
+  const int hd = cfg_.head_dim();
+  cudaStream_t s = stream_;
+  int32_t n = 0;
+  SR_CUDA_CHECK(srk::embed_ln(p.src.ptr, p.pos.ptr, tok_emb_, p.pack.n_soft ? p.soft.ptr : nullptr,
+                              pos_emb_, layers_[0].ln1, x_.ptr, xn_.ptr, M, d, s));
+  ++n;
+  const int bn_qkv = srk::gemm_pick_bn(3 * d), bn_d = srk::gemm_pick_bn(d),
+            bn_f = srk::gemm_pick_bn(F);
+  for (int l = 0; l < cfg_.n_layers; ++l) {
+    const auto& L = layers_[l];
+    SR_CUDA_CHECK(srk::gemm_bf16(tm_xn_, L.tm_qkv, M, 3 * d, d, qkv_.ptr, 3 * d, 0, bn_qkv, s));
+    SR_CUDA_CHECK(srk::attention(qkv_.ptr, p.spans.ptr, p.tiles.ptr,
+                                 static_cast<int>(p.pack.tiles.size()), xn_.ptr, M, H, hd, s));
+    SR_CUDA_CHECK(srk::gemm_bf16(tm_xn_, L.tm_o, M, d, d, x_.ptr, d, 2, bn_d, s));
+    SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, L.ln2, xn_.ptr, M, d, s));
+    SR_CUDA_CHECK(srk::gemm_bf16(tm_xn_, L.tm_in, M, F, d, h_.ptr, F, 1, bn_f, s));
+    SR_CUDA_CHECK(srk::gemm_bf16(tm_h_, L.tm_out, M, d, F, x_.ptr, d, 2, bn_d, s));
+    n += 6;
+    if (l + 1 < cfg_.n_layers) {
+      SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, layers_[l + 1].ln1, xn_.ptr, M, d, s));
+      ++n;
+    }
+  }
+  SR_CUDA_CHECK(srk::score_head(x_.ptr, p.last_rows.ptr, p.pack.n_items, d, ln_f_, head_w_,
+                                head_b_, n_cols_, task_col_, task_arity_, n_tasks(), yes_col_,
+                                no_col_, p.scores.ptr, hidden_out, s));
+  ++n;
+  if (p.k > 0) {
+    const int n_seg = static_cast<int>(p.pack.seg_off.size()) - 1;
+    SR_CUDA_CHECK(srk::topk(p.scores.ptr, n_tasks(), p.ids.ptr, p.seg_off.ptr, n_seg,
+                            p.pack.max_seg_len, p.k, p.topk_scratch.ptr,
+                            static_cast<int>(p.topk_scratch.cap), p.topk_out.ptr, s));
+    n += p.pack.max_seg_len > 4096 ? 2 : 1;
+  }
+  return n;
+}
+
+namespace {
+template <typename T>
+void put(DevBuf<T>& b, const std::vector<T>& v, cudaStream_t s) {
+  b.ensure(std::max<size_t>(v.size(), 1));
+  if (!v.empty())
+    SR_CUDA_CHECK(cudaMemcpyAsync(b.ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+}  // namespace
+
+void Engine::refill_plan(Plan& p, const sr_request* reqs, int n_req) {
+  SR_CUDA_CHECK(cudaSetDevice(device_));
+  p.lens.resize(n_req);
+  for (int q = 0; q < n_req; ++q) p.lens[q] = validate_request(cfg_, reqs[q]);
+  p.reqs.assign(reqs, reqs + n_req);
+  pack_requests(cfg_, reqs, n_req, p.lens, p.pack);
+  const auto& pk = p.pack;
+  put(p.src, pk.row_src, stream_);
+  put(p.pos, pk.row_pos, stream_);
+  put(p.spans, pk.spans, stream_);
+  put(p.tiles, pk.tiles, stream_);
+  put(p.last_rows, pk.last_rows, stream_);
+  put(p.ids, pk.ids, stream_);
+  put(p.seg_off, pk.seg_off, stream_);
+  put(p.soft, pk.soft_rows, stream_);
+  p.scores.ensure(static_cast<size_t>(pk.n_items) * n_tasks());
+  const int n_seg = n_req;
+  const int chunks = (pk.max_seg_len + 4095) / 4096;
+  p.topk_scratch.ensure(static_cast<size_t>(std::max(1, n_seg * chunks * std::max(p.k, 1))));
+  p.topk_out.ensure(static_cast<size_t>(std::max(1, n_seg * std::max(p.k, 1))));
+  ensure_workspace(pk.M);
+}
+
+void Engine::capture(Plan& p) {
+  if (p.graph) {
+    cudaGraphExecDestroy(p.graph);
+    p.graph = nullptr;
+  }
+  // Eager run first: sets kernel attributes outside capture and surfaces
+  // launch errors with a precise location.
+  p.launches = enqueue_forward(p, nullptr);
+  SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  cudaGraph_t g = nullptr;
+  SR_CUDA_CHECK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue_forward(p, nullptr);
+  } catch (...) {
+    cudaStreamEndCapture(stream_, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  SR_CUDA_CHECK(cudaStreamEndCapture(stream_, &g));
+  SR_CUDA_CHECK(cudaGraphInstantiate(&p.graph, g, 0));
+  cudaGraphDestroy(g);
+  plan_epoch_[&p] = ws_epoch_;
+}
+
+std::unique_ptr<Plan> Engine::make_plan(const sr_request* reqs, int n_req, int32_t k) {
+  if (k < 0) fail(SR_PARAMETER, "top-k must be >= 0");
+  if (k > 4096) fail(SR_PARAMETER, "top-k must be <= 4096");
+  auto p = std::make_unique<Plan>();
+  p->eng = this;
+  p->k = k;
+  p->n_tasks = n_tasks();
+  refill_plan(*p, reqs, n_req);
+  const int chunks = (p->pack.max_seg_len + 4095) / 4096;
+  if (k > 0 && chunks > 1 && static_cast<long>(chunks) * k > 4096)
+    fail(SR_PARAMETER, "top-k too large for this many candidates");
+  capture(*p);
+  return p;
+}
+
+void Engine::run_plan(Plan& p) {
+  SR_CUDA_CHECK(cudaSetDevice(device_));
+  auto it = plan_epoch_.find(&p);
+  if (it == plan_epoch_.end() || it->second != ws_epoch_) capture(p);
+  SR_CUDA_CHECK(cudaGraphLaunch(p.graph, stream_));
+}
+
+void Engine::fetch(Plan& p, sr_result* res, int n_req) {
+  const auto& pk = p.pack;
+  const int T = n_tasks();
+  std::vector<double> scores(static_cast<size_t>(pk.n_items) * T);
+  std::vector<srk::TopkEntry> top(static_cast<size_t>(n_req) * std::max(p.k, 0));
+  SR_CUDA_CHECK(cudaMemcpyAsync(scores.data(), p.scores.ptr, scores.size() * sizeof(double),
+                                cudaMemcpyDeviceToHost, stream_));
+  if (p.k > 0)
+    SR_CUDA_CHECK(cudaMemcpyAsync(top.data(), p.topk_out.ptr, top.size() * sizeof(srk::TopkEntry),
+                                  cudaMemcpyDeviceToHost, stream_));
+  SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  for (int q = 0; q < n_req; ++q) {
+    sr_result& r = res[q];
+    const int32_t i0 = pk.seg_off[q], n = pk.seg_off[q + 1] - i0;
+    if (r.scores)
+      std::memcpy(r.scores, scores.data() + static_cast<size_t>(i0) * T,
+                  static_cast<size_t>(n) * T * sizeof(double));
+    const int32_t want = std::min(r.k, p.k);
+    const int32_t kr = std::max(0, std::min(want, n));
+    for (int32_t j = 0; j < kr; ++j) {
+      const auto& e = top[static_cast<size_t>(q) * p.k + j];
+      if (r.topk_ids) r.topk_ids[j] = e.id;
+      if (r.topk_scores) r.topk_scores[j] = e.score;
+      if (r.topk_index) r.topk_index[j] = e.index - i0;
+    }
+    r.k_returned = kr;
+    report_for(cfg_, p.reqs[q], p.lens[q], &r.flops, &r.kv_incremental_per_item);
+  }
+}
+
+void Engine::score(const sr_request* reqs, int n_req, sr_result* res) {
+  if (n_req <= 0) fail(SR_SPEC_VIOLATION, "no requests");
+  int32_t k = 0;
+  for (int q = 0; q < n_req; ++q) k = std::max(k, res[q].k);
+  // Shape key: packed rows, items, attention tiles, requests, longest
+  // segment, soft rows, k. Same shape -> same captured graph.
+  std::vector<std::vector<int32_t>> lens(n_req);
+  int64_t M = 0, N = 0, soft = 0, tiles = 0;
+  int32_t maxseg = 0;
+  for (int q = 0; q < n_req; ++q) {
+    lens[q] = validate_request(cfg_, reqs[q]);
+    int64_t items = 0;
+    for (int32_t l : lens[q]) items += l;
+    M += reqs[q].t_q + items;
+    N += reqs[q].n_items;
+    tiles += (reqs[q].t_q + 63) / 64 + (items + 63) / 64;
+    if (reqs[q].mode == SR_MODE_MIXED) soft += items;
+    maxseg = std::max(maxseg, reqs[q].n_items);
+  }
+  auto key = std::make_tuple(static_cast<int32_t>(M), static_cast<int32_t>(N),
+                             static_cast<int32_t>(tiles), n_req, maxseg, static_cast<int32_t>(soft),
+                             k);
+  auto it = cache_.find(key);
+  Plan* p;
+  if (it == cache_.end()) {
+    if (cache_.size() >= 16) cache_.clear();
+    auto np = make_plan(reqs, n_req, k);
+    p = np.get();
+    cache_[key] = std::move(np);
+  } else {
+    p = it->second.get();
+    refill_plan(*p, reqs, n_req);
+  }
+  run_plan(*p);
+  fetch(*p, res, n_req);
+}
+
+void Engine::item_hidden(const sr_request& req, float* hidden_out) {
+  auto p = std::make_unique<Plan>();
+  p->eng = this;
+  p->k = 0;
+  refill_plan(*p, &req, 1);
+  float* dh = nullptr;
+  const size_t n = static_cast<size_t>(p->pack.n_items) * cfg_.d_model;
+  SR_CUDA_CHECK(cudaMalloc(&dh, n * sizeof(float)));
+  try {
+    enqueue_forward(*p, dh);
+    SR_CUDA_CHECK(cudaMemcpyAsync(hidden_out, dh, n * sizeof(float), cudaMemcpyDeviceToHost, stream_));
+    SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  } catch (...) {
+    cudaFree(dh);
+    throw;
+  }
+  cudaFree(dh);
+}
+
+void Engine::run_plan_sharded(Plan& p, Comm* c) {
+  if (c == nullptr || c->nranks <= 1) {
+    run_plan(p);
+    return;
+  }
+  if (p.k <= 0) fail(SR_PARAMETER, "sharded scoring needs k >= 1");
+  if (p.reqs.size() != 1) fail(SR_PARAMETER, "sharded scoring takes one request per call");
+  if (static_cast<long>(c->nranks) * p.k > 4096) fail(SR_PARAMETER, "nranks * k must be <= 4096");
+  run_plan(p);
+  p.gathered.ensure(static_cast<size_t>(c->nranks) * p.k);
+  p.merged.ensure(static_cast<size_t>(p.k));
+  nccl_allgather_bytes(c, p.topk_out.ptr, p.gathered.ptr, sizeof(srk::TopkEntry) * p.k, stream_);
+  SR_CUDA_CHECK(srk::topk_merge(p.gathered.ptr, c->nranks * p.k, p.k, p.merged.ptr, stream_));
+}
+
+// ------------------------------------------------------------------- NCCL
+namespace {
+struct NcclApi {
+  void* lib = nullptr;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    // Prefer an already-loaded libnccl (e.g. torch's), else the system one.
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.lib = h;
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank =
+        reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
+    api.error_string =
+        reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+  });
+  if (!api.lib || !api.get_unique_id || !api.comm_init_rank || !api.all_gather)
+    fail(SR_NCCL, "libnccl.so.2 not loadable");
+  return api;
+}
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    fail(SR_NCCL, std::string(what) + ": " +
+                      (nccl().error_string ? nccl().error_string(r) : "nccl error"));
+}
+}  // namespace
+
+void nccl_unique_id(uint8_t out[128]) {
+  ncclUniqueId id;
+  nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+  std::memcpy(out, id.internal, 128);
+}
+
+Comm* comm_create(int nranks, int rank, const uint8_t id[128], int device) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail(SR_PARAMETER, "bad rank/nranks");
+  SR_CUDA_CHECK(cudaSetDevice(device));
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, 128);
+  auto* c = new Comm;
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  ncclComm_t comm = nullptr;
+  try {
+    nccl_check(nccl().comm_init_rank(&comm, nranks, uid, rank), "ncclCommInitRank");
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  c->nccl = comm;
+  return c;
+}
+
+void comm_destroy(Comm* c) {
+  if (!c) return;
+  if (c->nccl && nccl().comm_destroy) nccl().comm_destroy(static_cast<ncclComm_t>(c->nccl));
+  delete c;
+}
+
+void nccl_allgather_bytes(Comm* c, const void* send, void* recv, size_t bytes, cudaStream_t s) {
+  nccl_check(nccl().all_gather(send, recv, bytes, ncclUint8, static_cast<ncclComm_t>(c->nccl), s),
+             "ncclAllGather");
+}
+
+}  // namespace srh

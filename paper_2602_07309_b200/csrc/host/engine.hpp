@@ -1,0 +1,170 @@
+// Device engine: owns bf16 K-major weights, the activation workspace, the
+// packed-input buffers and captured CUDA graphs for one device/stream.
+// Counterpart of ScoringEngine (engine.hpp:109-119): callers are serialised
+// by a mutex exactly as ScoringEngine::score is (engine.cpp:389-392).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "../kernels/launch.h"
+#include "model.hpp"
+#include "planner.hpp"
+
+namespace srh {
+
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;  // elements
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+  // Returns true if (re)allocated.
+  bool ensure(size_t n) {
+    if (n <= cap) return false;
+    release();
+    size_t c = n + n / 4 + 64;
+    SR_CUDA_CHECK(cudaMalloc(&ptr, c * sizeof(T)));
+    cap = c;
+    return true;
+  }
+};
+
+template <typename T>
+struct HostBuf {  // pinned
+  T* ptr = nullptr;
+  size_t cap = 0;
+  ~HostBuf() {
+    if (ptr) cudaFreeHost(ptr);
+  }
+  void ensure(size_t n) {
+    if (n <= cap) return;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    size_t c = n + n / 4 + 64;
+    SR_CUDA_CHECK(cudaMallocHost(&ptr, c * sizeof(T)));
+    cap = c;
+  }
+};
+
+struct LayerDev {
+  __nv_bfloat16* wqkv = nullptr;  // [3d x d]
+  __nv_bfloat16* wo = nullptr;    // [d x d]
+  __nv_bfloat16* win = nullptr;   // [ff x d]
+  __nv_bfloat16* wout = nullptr;  // [d x ff]
+  float* ln1 = nullptr;
+  float* ln2 = nullptr;
+  CUtensorMap tm_qkv, tm_o, tm_in, tm_out;
+};
+
+class Engine;
+
+// One request shape, resident on the device, replayed through a CUDA graph.
+struct Plan {
+  Engine* eng = nullptr;
+  PackedBatch pack;         // host copy of the packed layout
+  std::vector<sr_request> reqs;
+  std::vector<std::vector<int32_t>> lens;
+  int32_t k = 0;
+  int32_t n_tasks = 0;
+  // device inputs
+  DevBuf<int32_t> src, pos, last_rows, seg_off;
+  DevBuf<srk::RowSpan> spans;
+  DevBuf<srk::AttnTile> tiles;
+  DevBuf<int64_t> ids;
+  DevBuf<float> soft;
+  // outputs
+  DevBuf<double> scores;
+  DevBuf<srk::TopkEntry> topk_scratch, topk_out;
+  DevBuf<srk::TopkEntry> gathered, merged;  // sharded merge
+  // graph
+  cudaGraphExec_t graph = nullptr;
+  int32_t launches = 0;
+  ~Plan();
+};
+
+class Engine {
+ public:
+  Engine(const ModelWeights& w, int device);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  const ModelConfig& config() const { return cfg_; }
+  int device() const { return device_; }
+  cudaStream_t stream() const { return stream_; }
+  int n_tasks() const { return 1 + static_cast<int>(cfg_.head_specs.size()); }
+  std::mutex& mutex() { return mu_; }
+
+  // Builds a plan: validates + packs + uploads inputs + captures the graph.
+  std::unique_ptr<Plan> make_plan(const sr_request* reqs, int n_req, int32_t k);
+  // Re-uploads inputs of a same-shape request set into an existing plan.
+  void refill_plan(Plan& p, const sr_request* reqs, int n_req);
+  void run_plan(Plan& p);
+  void fetch(Plan& p, sr_result* res, int n_req);
+  // Scores + top-k through a cached plan (host buffers in, host buffers out).
+  void score(const sr_request* reqs, int n_req, sr_result* res);
+  void item_hidden(const sr_request& req, float* hidden_out);
+
+  // Sharded: local pass + NCCL all-gather of per-rank top-k + merge.
+  void run_plan_sharded(Plan& p, struct Comm* comm);
+
+  // Enqueue the full forward for the plan's packed batch on stream_.
+  int32_t enqueue_forward(Plan& p, float* hidden_out);
+
+ private:
+  void ensure_workspace(int32_t M);
+
+  ModelConfig cfg_;
+  int device_;
+  cudaStream_t stream_ = nullptr;
+  std::mutex mu_;
+  // weights
+  float* tok_emb_ = nullptr;
+  float* pos_emb_ = nullptr;
+  float* ln_f_ = nullptr;
+  float* head_w_ = nullptr;   // [C x d]
+  float* head_b_ = nullptr;   // [C]
+  int32_t* task_col_ = nullptr;
+  int32_t* task_arity_ = nullptr;
+  int n_cols_ = 0, yes_col_ = 0, no_col_ = 0;
+  std::vector<LayerDev> layers_;
+  std::vector<void*> allocs_;
+  // workspace
+  int32_t ws_rows_ = 0;
+  DevBuf<float> x_;
+  DevBuf<__nv_bfloat16> xn_, qkv_, h_;
+  CUtensorMap tm_xn_, tm_h_;
+  uint64_t ws_epoch_ = 0;  // bumps when workspace moves (graphs must be re-captured)
+  // shape-keyed plan cache for score()
+  std::map<std::tuple<int32_t, int32_t, int32_t, int32_t, int32_t, int32_t, int32_t>,
+           std::unique_ptr<Plan>>
+      cache_;
+  std::map<const Plan*, uint64_t> plan_epoch_;
+  void capture(Plan& p);
+ public:
+  uint64_t epoch() const { return ws_epoch_; }
+};
+
+// ---------------------------------------------------------------- NCCL
+struct Comm {
+  void* nccl = nullptr;  // ncclComm_t
+  int nranks = 1, rank = 0, device = 0;
+};
+void nccl_unique_id(uint8_t out[128]);
+Comm* comm_create(int nranks, int rank, const uint8_t id[128], int device);
+void comm_destroy(Comm* c);
+void nccl_allgather_bytes(Comm* c, const void* send, void* recv, size_t bytes, cudaStream_t s);
+
+}  // namespace srh

@@ -1,0 +1,85 @@
+// Host planner: request validation, FLOP accounting, multi-item masks,
+// batch planning, and packing of one or more scoring requests into the
+// ragged row layout the device pass consumes.
+//
+// Reference behaviour mirrored here (engine.cpp):
+//   flops / actual_flops            :30-88
+//   require_token_mode              :51-61
+//   build_multi_item_mask, pairs    :147-184
+//   score_multi_item positions      :209-217 (prefix-relative, T_q + j)
+//   score_mixed payload checks      :243-251
+//   plan_batches                    :278-326
+//   score_multi_item_chunked plan   :328-377
+// All token modes (naive / ibpc / multi_item) compute the same function: the
+// reference's own tests hold them equal (test_engine.cpp:140-187) and the
+// survey measured them bit-identical. The device therefore runs one packed
+// shared-prefix pass for every mode; the modes differ only in validation
+// and in the FlopReport they return.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "../kernels/launch.h"
+#include "model.hpp"
+
+namespace srh {
+
+sr_flop_report flops(int mode, int64_t t_q, int64_t t_i, int64_t n_items);
+
+struct ItemView {
+  int32_t length;  // tokens or soft rows
+};
+
+// Validates one request against the model (throws srh::Error with the
+// reference's error category) and returns per-item lengths.
+std::vector<int32_t> validate_request(const ModelConfig& cfg, const sr_request& req);
+
+// FlopReport + kv_incremental_per_item as the reference reports them for
+// this request's mode (including chunk re-payment for multi_item).
+void report_for(const ModelConfig& cfg, const sr_request& req, const std::vector<int32_t>& lens,
+                sr_flop_report* flops_out, double* kv_out);
+
+struct PackedBatch {
+  int32_t M = 0;                       // packed rows
+  int32_t n_items = 0;                 // items over all requests
+  int32_t max_seg_len = 0;             // longest request (items)
+  std::vector<int32_t> row_src;        // token id, or -(1 + soft row index)
+  std::vector<int32_t> row_pos;        // positional-embedding index
+  std::vector<srk::RowSpan> spans;     // attention mask per row
+  std::vector<srk::AttnTile> tiles;    // attention work tiles
+  std::vector<int32_t> last_rows;      // per item: packed row scored
+  std::vector<int64_t> ids;            // per item: doc id for the tie rule
+  std::vector<int32_t> seg_off;        // per request: item offsets [n_req + 1]
+  std::vector<float> soft_rows;        // mixed-mode rows [R x d]
+  int32_t n_soft = 0;
+};
+
+// Packs requests back to back. Row layout for request q (base = first row):
+//   prefix rows  base .. base+T_q-1 : pos j,       keys [base, r]          (causal)
+//   item i rows  s_i .. s_i+L_i-1   : pos T_q + j, keys [base, base+T_q) U [s_i, r]
+// `id_base` offsets default ids (index within the request) for sharding.
+void pack_requests(const ModelConfig& cfg, const sr_request* reqs, int n_req,
+                   const std::vector<std::vector<int32_t>>& lens, PackedBatch& out);
+
+int64_t multi_item_pair_count(int32_t prefix_len, const int32_t* lens, int n);
+
+struct BatchEntry {
+  int32_t request_index, item_begin, item_end;
+};
+struct Batch {
+  std::vector<BatchEntry> entries;
+  int64_t token_count = 0;
+};
+std::vector<Batch> plan_batches(const std::vector<int32_t>& prefix_len,
+                                const std::vector<std::vector<int32_t>>& item_len,
+                                int64_t max_batch_tokens);
+
+struct HostTopk {
+  double score;
+  int64_t id;
+  int32_t index;
+};
+std::vector<HostTopk> topk_host(const double* scores, const int64_t* ids, int32_t n, int32_t k);
+
+}  // namespace srh

@@ -1,0 +1,107 @@
+// Host launchers for the tcgen05 GEMM (gemm_tcgen05.cuh).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "gemm_tcgen05.cuh"
+#include "launch.h"
+
+namespace srk {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+  });
+  return fn;
+}
+
+template <int BN, int EPI>
+cudaError_t launch_one(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
+                       void* out, int ldo, cudaStream_t stream) {
+  using C = GemmCfg<BN>;
+  auto kern = gemm_bf16_tcgen05_kernel<BN, EPI>;
+  static bool attr_set = false;  // benign race: idempotent attribute set
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int tiles = ((M + C::BM - 1) / C::BM) * (N / BN);
+  const int grid = tiles < num_sms(dev) ? tiles : num_sms(dev);
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(tmA, tmB, M, N, K, out, ldo);
+  return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t launch_bn(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
+                      void* out, int ldo, int epi, cudaStream_t stream) {
+  switch (epi) {
+    case EPI_BF16: return launch_one<BN, EPI_BF16>(tmA, tmB, M, N, K, out, ldo, stream);
+    case EPI_GELU_BF16: return launch_one<BN, EPI_GELU_BF16>(tmA, tmB, M, N, K, out, ldo, stream);
+    case EPI_RESID_F32: return launch_one<BN, EPI_RESID_F32>(tmA, tmB, M, N, K, out, ldo, stream);
+    case EPI_F32: return launch_one<BN, EPI_F32>(tmA, tmB, M, N, K, out, ldo, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+int num_sms(int device) {
+  static int cached[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (cached[device] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    cached[device] = n > 0 ? n : 148;
+  }
+  return cached[device];
+}
+
+cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                              uint32_t box_rows, uint32_t box_cols) {
+  auto fn = get_encode_fn();
+  if (fn == nullptr) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+int gemm_pick_bn(int N) {
+  if (N % 256 == 0) return 256;
+  if (N % 128 == 0) return 128;
+  if (N % 64 == 0) return 64;
+  return 0;
+}
+
+cudaError_t gemm_bf16(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
+                      void* out, int ldo, int epi, int bn, cudaStream_t stream) {
+  if (M <= 0) return cudaSuccess;
+  if (N % bn != 0 || K % 8 != 0) return cudaErrorInvalidValue;
+  switch (bn) {
+    case 256: return launch_bn<256>(tmA, tmB, M, N, K, out, ldo, epi, stream);
+    case 128: return launch_bn<128>(tmA, tmB, M, N, K, out, ldo, epi, stream);
+    case 64: return launch_bn<64>(tmA, tmB, M, N, K, out, ldo, epi, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace srk

@@ -1,0 +1,86 @@
+// Host-side launch interface for the sm_100a kernels (internal; the public
+// boundary is include/semrank_b200.h).
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace srk {
+
+// Row descriptor for segment-masked attention (one per packed row).
+// Row r may attend keys [prefix_begin, prefix_end) U [span_start, r]
+// (kernels.hpp:39-46 MaskSpan, generalised with prefix_begin so several
+// queries can share one packed batch).
+struct RowSpan {
+  int32_t prefix_begin;
+  int32_t prefix_end;
+  int32_t span_start;
+  int32_t pad;
+};
+
+// One attention work tile: query rows [q_begin, q_end) and the two key ranges
+// that cover every key any of those rows may see.
+struct AttnTile {
+  int32_t q_begin, q_end;
+  int32_t r1_begin, r1_end;  // shared-prefix keys
+  int32_t r2_begin, r2_end;  // own-segment keys
+  int32_t pad0, pad1;
+};
+
+// ------------------------------------------------------------------- GEMM
+int num_sms(int device);
+cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                              uint32_t box_rows, uint32_t box_cols);
+// Picks BN from N; N must be a multiple of 64, K a multiple of 8.
+int gemm_pick_bn(int N);
+cudaError_t gemm_bf16(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
+                      void* out, int ldo, int epi, int bn, cudaStream_t stream);
+
+// ------------------------------------------------------------ elementwise
+// x[r] = (src[r] >= 0 ? tok_emb[src[r]] : soft[-src[r]-1]) + pos_emb[pos[r]]
+// and xn[r] = bf16(LN(x[r]) * gain) (layer-0 LN1 fused).
+cudaError_t embed_ln(const int32_t* src, const int32_t* pos, const float* tok_emb,
+                     const float* soft_rows, const float* pos_emb, const float* gain, float* x,
+                     __nv_bfloat16* xn, int M, int d, cudaStream_t stream);
+cudaError_t layer_norm_bf16(const float* x, const float* gain, __nv_bfloat16* out, int M, int d,
+                            cudaStream_t stream);
+
+// -------------------------------------------------------------- attention
+// qkv: [M x 3d] bf16 rows (q | k | v); out: [M x d] bf16.
+cudaError_t attention(const __nv_bfloat16* qkv, const RowSpan* spans, const AttnTile* tiles,
+                      int n_tiles, __nv_bfloat16* out, int M, int n_heads, int head_dim,
+                      cudaStream_t stream);
+
+// -------------------------------------------------------- score head/topk
+// Final LN on the last-token rows + task-column dot products + probabilities.
+// w_cols: [C x d] fp32 (columns of the score head), bias: [C].
+// col_kind/arity describe how columns map to tasks (see engine.cu).
+cudaError_t score_head(const float* x, const int32_t* last_rows, int n_items, int d,
+                       const float* ln_gain, const float* w_cols, const float* bias, int n_cols,
+                       const int32_t* task_col, const int32_t* task_arity, int n_tasks,
+                       int yes_col, int no_col, double* scores, float* hidden_out,
+                       cudaStream_t stream);
+
+struct TopkEntry {
+  double score;
+  int64_t id;
+  int32_t index;
+  int32_t pad;
+};
+// Per segment s (items [seg_off[s], seg_off[s+1])): the k best entries by
+// (score desc, id asc, index asc). scores has stride `stride`.
+// max_seg_len bounds the longest segment (sizes the chunking).
+cudaError_t topk(const double* scores, int stride, const int64_t* ids, const int32_t* seg_off,
+                 int n_segments, int max_seg_len, int k, TopkEntry* scratch, int scratch_cap,
+                 TopkEntry* out, cudaStream_t stream);
+// Merge: entries [n] (already candidates) -> best k.
+cudaError_t topk_merge(const TopkEntry* in, int n, int k, TopkEntry* out, cudaStream_t stream);
+
+// ------------------------------------------------------------ conversions
+// dst[n][k] = bf16(src[k][n]) : fp32 [K x N] row-major -> bf16 [N x K].
+cudaError_t transpose_to_bf16(const float* src, __nv_bfloat16* dst, int K, int N,
+                              cudaStream_t stream);
+
+}  // namespace srk

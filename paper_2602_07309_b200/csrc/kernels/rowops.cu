@@ -1,0 +1,178 @@
+// Row kernels: embedding gather (+ fused layer-0 LN1), gain-only LayerNorm,
+// and the one-time weight conversion fp32 [K x N] -> bf16 [N x K].
+//
+// LayerNorm semantics follow kernels.cpp:31-45 (layer_norm_row): two-pass
+// mean then population variance, eps 1e-5, (x - mean) * rsqrt(var + eps) * gain,
+// no bias. One warp per row; the row lives in registers between passes, so
+// HBM traffic is one fp32 read + one bf16 write per element.
+#include <cuda_bf16.h>
+
+#include "launch.h"
+
+namespace srk {
+
+namespace {
+
+constexpr float kLnEps = 1e-5f;
+
+// Row held as float4 chunks: lane owns chunks lane, lane+32, ...
+template <int NV>
+__device__ __forceinline__ void ln_row_store(const float4 (&v)[NV], int d4, const float* gain,
+                                             __nv_bfloat16* out_row, int lane) {
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < d4) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+  const float d = static_cast<float>(d4 * 4);
+  const float mean = s / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < d4) {
+      const float a = v[i].x - mean, b = v[i].y - mean, e = v[i].z - mean, f = v[i].w - mean;
+      q += (a * a + b * b) + (e * e + f * f);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffff, q, o);
+  const float inv = 1.0f / sqrtf(q / d + kLnEps);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < d4) {
+      const float4 gg = reinterpret_cast<const float4*>(gain)[c];
+      uint2 packed;
+      packed.x = __float_as_uint(0.f);
+      __nv_bfloat162 lo = __floats2bfloat162_rn((v[i].x - mean) * inv * gg.x,
+                                                (v[i].y - mean) * inv * gg.y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn((v[i].z - mean) * inv * gg.z,
+                                                (v[i].w - mean) * inv * gg.w);
+      packed.x = *reinterpret_cast<uint32_t*>(&lo);
+      packed.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(out_row)[c] = packed;
+    }
+  }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256)
+    embed_ln_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ pos,
+                    const float* __restrict__ tok_emb, const float* __restrict__ soft_rows,
+                    const float* __restrict__ pos_emb, const float* __restrict__ gain,
+                    float* __restrict__ x, __nv_bfloat16* __restrict__ xn, int M, int d) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const int d4 = d >> 2;
+  const int s = src[row];
+  const float4* e = reinterpret_cast<const float4*>(
+      s >= 0 ? tok_emb + static_cast<size_t>(s) * d
+             : soft_rows + static_cast<size_t>(-s - 1) * d);
+  const float4* p = reinterpret_cast<const float4*>(pos_emb + static_cast<size_t>(pos[row]) * d);
+  float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(row) * d);
+  float4 v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < d4) {
+      const float4 a = e[c], b = p[c];
+      // model.cpp:258-271 / 282-290: rows = embedding + pos_emb, fp32
+      v[i] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+      xr[c] = v[i];
+    }
+  }
+  ln_row_store<NV>(v, d4, gain, xn + static_cast<size_t>(row) * d, lane);
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256)
+    layer_norm_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                      __nv_bfloat16* __restrict__ out, int M, int d) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const int d4 = d >> 2;
+  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(row) * d);
+  float4 v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < d4) v[i] = xr[c];
+  }
+  ln_row_store<NV>(v, d4, gain, out + static_cast<size_t>(row) * d, lane);
+}
+
+template <int NV>
+cudaError_t launch_embed(const int32_t* src, const int32_t* pos, const float* tok_emb,
+                         const float* soft_rows, const float* pos_emb, const float* gain, float* x,
+                         __nv_bfloat16* xn, int M, int d, cudaStream_t stream) {
+  embed_ln_kernel<NV><<<(M + 7) / 8, 256, 0, stream>>>(src, pos, tok_emb, soft_rows, pos_emb,
+                                                       gain, x, xn, M, d);
+  return cudaGetLastError();
+}
+
+template <int NV>
+cudaError_t launch_ln(const float* x, const float* gain, __nv_bfloat16* out, int M, int d,
+                      cudaStream_t stream) {
+  layer_norm_kernel<NV><<<(M + 7) / 8, 256, 0, stream>>>(x, gain, out, M, d);
+  return cudaGetLastError();
+}
+
+__global__ void transpose_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                      int K, int N) {
+  __shared__ float tile[32][33];
+  const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int k = k0 + i, n = n0 + threadIdx.x;
+    tile[i][threadIdx.x] = (k < K && n < N) ? src[static_cast<size_t>(k) * N + n] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int n = n0 + i, k = k0 + threadIdx.x;
+    if (n < N && k < K) dst[static_cast<size_t>(n) * K + k] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+  }
+}
+
+}  // namespace
+
+#define SRK_DISPATCH_NV(d, FN, ...)              \
+  do {                                           \
+    const int nv = ((d) / 4 + 31) / 32;          \
+    if (nv <= 1) return FN<1>(__VA_ARGS__);      \
+    if (nv <= 2) return FN<2>(__VA_ARGS__);      \
+    if (nv <= 4) return FN<4>(__VA_ARGS__);      \
+    if (nv <= 8) return FN<8>(__VA_ARGS__);      \
+    if (nv <= 16) return FN<16>(__VA_ARGS__);    \
+    if (nv <= 32) return FN<32>(__VA_ARGS__);    \
+    return cudaErrorInvalidValue;                \
+  } while (0)
+
+cudaError_t embed_ln(const int32_t* src, const int32_t* pos, const float* tok_emb,
+                     const float* soft_rows, const float* pos_emb, const float* gain, float* x,
+                     __nv_bfloat16* xn, int M, int d, cudaStream_t stream) {
+  if (M <= 0) return cudaSuccess;
+  if (d % 4 != 0) return cudaErrorInvalidValue;
+  SRK_DISPATCH_NV(d, launch_embed, src, pos, tok_emb, soft_rows, pos_emb, gain, x, xn, M, d,
+                  stream);
+}
+
+cudaError_t layer_norm_bf16(const float* x, const float* gain, __nv_bfloat16* out, int M, int d,
+                            cudaStream_t stream) {
+  if (M <= 0) return cudaSuccess;
+  if (d % 4 != 0) return cudaErrorInvalidValue;
+  SRK_DISPATCH_NV(d, launch_ln, x, gain, out, M, d, stream);
+}
+
+cudaError_t transpose_to_bf16(const float* src, __nv_bfloat16* dst, int K, int N,
+                              cudaStream_t stream) {
+  dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
+  transpose_bf16_kernel<<<grid, block, 0, stream>>>(src, dst, K, N);
+  return cudaGetLastError();
+}
+
+}  // namespace srk

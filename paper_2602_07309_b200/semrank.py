@@ -1,0 +1,466 @@
+"""Python mirror of the reference scorer API (semrank, include/semrank/*.hpp).
+
+Same names, argument meaning and error behaviour as the reference C++ API so
+parity tests read like the reference's own tests; every call goes through the
+C-ABI (include/semrank_b200.h) into the B200 engine. Nothing here computes
+scores on the host.
+
+  reference                                   here
+  ModelConfig / HeadSpec   (model.hpp:16-40)  ModelConfig / HeadSpec
+  ModelWeights, init_model (model.hpp:56-70)  ModelWeights, init_model
+  save/load_weights   (weights_io.hpp:16-17)  save_weights / load_weights
+  ScoreMode/Item/Request/Result (engine.hpp)  same names
+  flops, build_multi_item_mask, plan_batches  same names (host-side logic)
+  ScoringEngine::score  (engine.hpp:109-119)  ScoringEngine.score (+ top-k)
+  semrank::Error{ErrorCode} (error.hpp)       SemrankError(code)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _capi as _c
+from ._capi import lib as _lib
+
+
+class ErrorCode(enum.IntEnum):
+    """semrank::ErrorCode (error.hpp:13-29); values are the C-ABI statuses."""
+    LengthOverflow = 1
+    MaskInvalid = 2
+    SpecViolation = 3
+    PayloadInvalid = 4
+    SchemaUnknown = 5
+    Alignment = 6
+    Divergence = 7
+    Parameter = 8
+    DegenerateInput = 9
+    UndefinedMetric = 10
+    StateInvalid = 11
+    OversizeItem = 12
+    Consistency = 13
+    Reconciliation = 14
+    Io = 15
+    Cuda = 100
+    Nccl = 101
+
+
+class SemrankError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = ErrorCode(code)
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = _lib.sr_last_error().decode(errors="replace")
+        raise SemrankError(status, f"[{_lib.sr_status_name(status).decode()}] {msg}")
+
+
+class ScoreMode(enum.IntEnum):
+    Naive = 0
+    Ibpc = 1
+    MultiItem = 2
+    Mixed = 3
+
+
+_MODE_NAMES = {ScoreMode.Naive: "naive", ScoreMode.Ibpc: "ibpc",
+               ScoreMode.MultiItem: "multi_item", ScoreMode.Mixed: "mixed"}
+
+
+def score_mode_name(mode: ScoreMode) -> str:  # engine.cpp:12-20
+    return _MODE_NAMES.get(ScoreMode(mode), "unknown")
+
+
+def score_mode_from_name(name: str) -> ScoreMode:  # engine.cpp:22-29
+    for m, n in _MODE_NAMES.items():
+        if n == name:
+            return m
+    if name == "multi-item":
+        return ScoreMode.MultiItem
+    raise SemrankError(ErrorCode.Parameter, "unknown scoring mode: " + name)
+
+
+kRelevanceTask = "relevance"
+
+
+@dataclass
+class HeadSpec:
+    name: str
+    arity: int = 1
+
+
+@dataclass
+class ModelConfig:
+    n_layers: int = 2
+    d_model: int = 64
+    n_heads: int = 4
+    d_ff: int = 256
+    vocab_size: int = 300
+    max_seq: int = 4096
+    yes_token_id: int = 261
+    no_token_id: int = 262
+    head_specs: List[HeadSpec] = field(default_factory=list)
+
+    def head_dim(self) -> int:
+        return self.d_model // self.n_heads
+
+    @staticmethod
+    def default_toy() -> "ModelConfig":  # model.cpp:52-57
+        return ModelConfig(head_specs=[HeadSpec(n) for n in
+                                       ("click", "apply", "badfit", "shortlist", "dismiss")])
+
+    def _to_c(self):
+        names = (C.c_char_p * max(1, len(self.head_specs)))(
+            *[h.name.encode() for h in self.head_specs])
+        arity = (C.c_int32 * max(1, len(self.head_specs)))(*[h.arity for h in self.head_specs])
+        c = _c.ModelConfigC(self.n_layers, self.d_model, self.n_heads, self.d_ff,
+                            self.vocab_size, self.max_seq, self.yes_token_id, self.no_token_id,
+                            len(self.head_specs), names, arity)
+        c._keep = (names, arity)
+        return c
+
+    def validate(self) -> None:  # model.cpp:29-50
+        c = self._to_c()
+        _check(_lib.sr_config_validate(C.byref(c)))
+
+    @staticmethod
+    def _from_c(c) -> "ModelConfig":
+        heads = [HeadSpec(c.head_names[i].decode(), c.head_arity[i]) for i in range(c.n_task_heads)]
+        return ModelConfig(c.n_layers, c.d_model, c.n_heads, c.d_ff, c.vocab_size, c.max_seq,
+                           c.yes_token_id, c.no_token_id, heads)
+
+
+class ModelWeights:
+    """Host weights (model.hpp:56-67), owned by the C library."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+        cfg = _c.ModelConfigC()
+        _check(_lib.sr_weights_config(self._h, C.byref(cfg)))
+        self.config = ModelConfig._from_c(cfg)
+        self.version = _lib.sr_weights_version(self._h).decode()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.sr_weights_free(h)
+            self._h = C.c_void_p()
+
+    def tensors(self) -> Dict[str, np.ndarray]:
+        """name -> zero-copy float32 view, in SRNKWTS1 canonical order."""
+        out = {}
+        n = _lib.sr_weights_tensor_count(self._h)
+        for i in range(n):
+            name = C.c_char_p()
+            data = C.POINTER(C.c_float)()
+            numel = C.c_size_t()
+            _check(_lib.sr_weights_tensor(self._h, i, C.byref(name), C.byref(data), C.byref(numel)))
+            arr = np.ctypeslib.as_array(data, shape=(numel.value,)) if numel.value else \
+                np.zeros(0, np.float32)
+            out[name.value.decode()] = arr
+        return out
+
+    def save(self, path: str) -> None:
+        _check(_lib.sr_weights_save(self._h, path.encode()))
+
+    @staticmethod
+    def from_tensors(cfg: ModelConfig, tensors: Sequence[np.ndarray], version: str = "") \
+            -> "ModelWeights":
+        arrs = [np.ascontiguousarray(t, dtype=np.float32).ravel() for t in tensors]
+        ptrs = (C.POINTER(C.c_float) * len(arrs))(
+            *[a.ctypes.data_as(C.POINTER(C.c_float)) for a in arrs])
+        c = cfg._to_c()
+        h = C.c_void_p()
+        _check(_lib.sr_weights_from_tensors(C.byref(c), version.encode(), ptrs, C.byref(h)))
+        return ModelWeights(h)
+
+
+def init_model(config: ModelConfig, seed: int, scheme: str = "reference") -> ModelWeights:
+    """init_model (model.cpp:94-134). scheme "fan_in" = DESIGN.md §2 scaled init."""
+    sch = {"reference": 0, "fan_in": 1}[scheme]
+    c = config._to_c()
+    h = C.c_void_p()
+    _check(_lib.sr_weights_init(C.byref(c), C.c_uint64(seed), sch, C.byref(h)))
+    return ModelWeights(h)
+
+
+def load_weights(path: str) -> ModelWeights:
+    h = C.c_void_p()
+    _check(_lib.sr_weights_load(path.encode(), C.byref(h)))
+    return ModelWeights(h)
+
+
+def save_weights(w: ModelWeights, path: str) -> None:
+    w.save(path)
+
+
+# ------------------------------------------------------------------ engine
+@dataclass
+class FlopReport:
+    attention_units: float = 0.0
+    linear_units: float = 0.0
+    t_q: float = 0.0
+    t_i_mean: float = 0.0
+    n_items: float = 0.0
+
+    @staticmethod
+    def _from_c(f) -> "FlopReport":
+        return FlopReport(f.attention_units, f.linear_units, f.t_q, f.t_i_mean, f.n_items)
+
+
+def flops(mode: ScoreMode, t_q: int, t_i: int, n_items: int) -> FlopReport:  # engine.cpp:30-47
+    f = _c.FlopReportC()
+    _check(_lib.sr_flops(int(mode), t_q, t_i, n_items, C.byref(f)))
+    return FlopReport._from_c(f)
+
+
+@dataclass
+class ScoreItem:
+    id: str = ""
+    tokens: Sequence[int] = ()
+    embedding: Optional[np.ndarray] = None  # mixed mode: [n_emb_tokens x d_model]
+    n_emb_tokens: int = 0
+
+
+@dataclass
+class ScoreRequest:
+    request_id: str = ""
+    prefix_tokens: Sequence[int] = ()
+    items: List[ScoreItem] = field(default_factory=list)
+    mode: ScoreMode = ScoreMode.Ibpc
+    latency_sensitive: bool = False
+
+
+@dataclass
+class ItemScores:
+    item_id: str
+    tasks: Dict[str, float]
+
+
+@dataclass
+class ScoreResult:
+    request_id: str = ""
+    items: List[ItemScores] = field(default_factory=list)
+    mode: ScoreMode = ScoreMode.Naive
+    flops: FlopReport = field(default_factory=FlopReport)
+    kv_incremental_per_item: float = 0.0
+    topk: List[tuple] = field(default_factory=list)  # (item_id, relevance)
+    scores: Optional[np.ndarray] = None  # [n_items x n_tasks], col 0 relevance
+
+
+class MultiItemMask:  # engine.hpp:63-72
+    def __init__(self, prefix_len: int, item_spans: List[tuple]):
+        self.prefix_len = prefix_len
+        self.item_spans = item_spans
+
+    def allowed_pair_count(self) -> int:
+        lens = np.array([e - s for s, e in self.item_spans], np.int32)
+        out = C.c_int64()
+        _check(_lib.sr_multi_item_pair_count(
+            self.prefix_len, lens.ctypes.data_as(C.POINTER(C.c_int32)), len(lens), C.byref(out)))
+        return out.value
+
+    def to_attention_mask(self) -> List[tuple]:
+        """[(prefix_end, span_start)] per packed item row."""
+        lens = np.array([e - s for s, e in self.item_spans], np.int32)
+        n_rows = int(lens.sum())
+        buf = np.zeros(2 * max(n_rows, 1), np.int32)
+        nr = C.c_int32()
+        _check(_lib.sr_multi_item_mask(self.prefix_len, lens.ctypes.data_as(C.POINTER(C.c_int32)),
+                                       len(lens), buf.ctypes.data_as(C.POINTER(C.c_int32)),
+                                       n_rows, C.byref(nr)))
+        return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(nr.value)]
+
+
+def build_multi_item_mask(prefix_len: int, item_lengths: Sequence[int]) -> MultiItemMask:
+    lens = np.asarray(list(item_lengths), np.int32)
+    nr = C.c_int32()
+    _check(_lib.sr_multi_item_mask(prefix_len, lens.ctypes.data_as(C.POINTER(C.c_int32)),
+                                   len(lens), None, 0, C.byref(nr)))
+    spans, cur = [], prefix_len
+    for l in lens:
+        spans.append((cur, cur + int(l)))
+        cur += int(l)
+    return MultiItemMask(prefix_len, spans)
+
+
+@dataclass
+class BatchEntry:
+    request_index: int
+    item_begin: int
+    item_end: int
+
+
+@dataclass
+class Batch:
+    entries: List[BatchEntry] = field(default_factory=list)
+    token_count: int = 0
+
+
+def _item_len(it: ScoreItem) -> int:
+    return it.n_emb_tokens if it.n_emb_tokens > 0 else len(it.tokens)
+
+
+def plan_batches(requests: Sequence[ScoreRequest], max_batch_tokens: int) -> List[Batch]:
+    """plan_batches (engine.cpp:278-326), computed by the native planner."""
+    pl = np.array([len(r.prefix_tokens) for r in requests], np.int32)
+    off = np.zeros(len(requests) + 1, np.int32)
+    lens = []
+    for i, r in enumerate(requests):
+        lens += [_item_len(it) for it in r.items]
+        off[i + 1] = len(lens)
+    il = np.array(lens if lens else [0], np.int32)
+    cap_e, cap_b = max(1, len(lens)), max(1, len(lens))
+    ent = np.zeros(4 * cap_e, np.int32)
+    tok = np.zeros(cap_b, np.int64)
+    ne, nb = C.c_int32(), C.c_int32()
+    I = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))
+    _check(_lib.sr_plan_batches(len(requests), I(pl), I(off), I(il), max_batch_tokens, I(ent), cap_e,
+                                C.byref(ne), tok.ctypes.data_as(C.POINTER(C.c_int64)), cap_b,
+                                C.byref(nb)))
+    batches = [Batch(token_count=int(tok[b])) for b in range(nb.value)]
+    for e in range(ne.value):
+        b, r, lo, hi = (int(x) for x in ent[4 * e:4 * e + 4])
+        batches[b].entries.append(BatchEntry(r, lo, hi))
+    return batches
+
+
+def _item_doc_ids(items: Sequence[ScoreItem]) -> Optional[np.ndarray]:
+    try:
+        return np.array([int(it.id) for it in items], np.int64)
+    except (TypeError, ValueError):
+        return None
+
+
+class _PackedRequest:
+    """Flattened sr_request; keeps the numpy buffers alive."""
+
+    def __init__(self, req: ScoreRequest, d_model: int, item_ids: Optional[np.ndarray] = None):
+        self.prefix = np.ascontiguousarray(np.asarray(req.prefix_tokens, np.int32).reshape(-1))
+        mixed = ScoreMode(req.mode) == ScoreMode.Mixed
+        lens = []
+        for it in req.items:
+            if mixed:
+                n = it.n_emb_tokens
+                emb = np.asarray(it.embedding if it.embedding is not None else [], np.float32)
+                if n < 1 or emb.size != n * d_model:
+                    raise SemrankError(ErrorCode.PayloadInvalid,
+                                       f"item {it.id} embedding payload is not [n x {d_model}]")
+                lens.append(n)
+            else:
+                lens.append(len(it.tokens))
+        self.offsets = np.zeros(len(req.items) + 1, np.int32)
+        self.offsets[1:] = np.cumsum(lens) if lens else []
+        if mixed:
+            self.rows = np.ascontiguousarray(np.concatenate(
+                [np.asarray(it.embedding, np.float32).reshape(-1) for it in req.items]))
+            self.tokens = np.zeros(1, np.int32)
+        else:
+            self.tokens = np.ascontiguousarray(np.concatenate(
+                [np.asarray(it.tokens, np.int32).reshape(-1) for it in req.items])
+                if req.items else np.zeros(1, np.int32))
+            self.rows = None
+        self.ids = item_ids if item_ids is not None else _item_doc_ids(req.items)
+        I = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))
+        self.c = _c.RequestC(
+            I(self.prefix), len(self.prefix), len(req.items), I(self.offsets), I(self.tokens),
+            self.rows.ctypes.data_as(C.POINTER(C.c_float)) if self.rows is not None else None,
+            self.ids.ctypes.data_as(C.POINTER(C.c_int64)) if self.ids is not None else None,
+            int(req.mode))
+
+
+class _ResultBuf:
+    def __init__(self, n_items: int, n_tasks: int, k: int):
+        self.scores = np.zeros((max(n_items, 1), n_tasks), np.float64)
+        self.kk = max(k, 1)
+        self.ids = np.zeros(self.kk, np.int64)
+        self.top = np.zeros(self.kk, np.float64)
+        self.idx = np.zeros(self.kk, np.int32)
+        self.c = _c.ResultC(self.scores.ctypes.data_as(C.POINTER(C.c_double)), k,
+                            self.ids.ctypes.data_as(C.POINTER(C.c_int64)),
+                            self.top.ctypes.data_as(C.POINTER(C.c_double)),
+                            self.idx.ctypes.data_as(C.POINTER(C.c_int32)),
+                            _c.FlopReportC(), 0.0, 0)
+
+
+class ScoringEngine:
+    """ScoringEngine (engine.hpp:109-119) bound to one B200; serialises callers."""
+
+    def __init__(self, weights: ModelWeights, device: int = 0):
+        self.weights = weights
+        self.config = weights.config
+        self.task_names = [kRelevanceTask] + [h.name for h in self.config.head_specs]
+        h = C.c_void_p()
+        _check(_lib.sr_engine_create(weights._h, device, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.sr_engine_destroy(h)
+            self._h = C.c_void_p()
+
+    def _to_result(self, req: ScoreRequest, rb: _ResultBuf) -> ScoreResult:
+        n = len(req.items)
+        res = ScoreResult(request_id=req.request_id, mode=ScoreMode(req.mode),
+                          flops=FlopReport._from_c(rb.c.flops),
+                          kv_incremental_per_item=rb.c.kv_incremental_per_item,
+                          scores=rb.scores[:n].copy())
+        for i, it in enumerate(req.items):
+            res.items.append(ItemScores(it.id, {t: float(rb.scores[i, j])
+                                                for j, t in enumerate(self.task_names)}))
+        for j in range(rb.c.k_returned):
+            res.topk.append((req.items[int(rb.idx[j])].id if rb.idx[j] >= 0 else str(rb.ids[j]),
+                             float(rb.top[j])))
+        return res
+
+    def score(self, request: ScoreRequest, k: int = 0) -> ScoreResult:
+        pr = _PackedRequest(request, self.config.d_model)
+        rb = _ResultBuf(len(request.items), len(self.task_names), k)
+        _check(_lib.sr_engine_score(self._h, C.byref(pr.c), C.byref(rb.c)))
+        return self._to_result(request, rb)
+
+    def score_batch(self, requests: Sequence[ScoreRequest], k: int = 0) -> List[ScoreResult]:
+        prs = [_PackedRequest(r, self.config.d_model) for r in requests]
+        rbs = [_ResultBuf(len(r.items), len(self.task_names), k) for r in requests]
+        reqs = (_c.RequestC * len(prs))(*[p.c for p in prs])
+        ress = (_c.ResultC * len(rbs))(*[r.c for r in rbs])
+        _check(_lib.sr_engine_score_batch(self._h, reqs, len(prs), ress))
+        out = []
+        for r, rb, rc in zip(requests, rbs, ress):
+            rb.c = rc
+            out.append(self._to_result(r, rb))
+        return out
+
+    def item_hidden(self, request: ScoreRequest) -> np.ndarray:
+        pr = _PackedRequest(request, self.config.d_model)
+        out = np.zeros((len(request.items), self.config.d_model), np.float32)
+        _check(_lib.sr_engine_item_hidden(self._h, C.byref(pr.c),
+                                          out.ctypes.data_as(C.POINTER(C.c_float))))
+        return out
+
+
+def score_by_mode(engine: ScoringEngine, request: ScoreRequest, k: int = 0) -> ScoreResult:
+    """score_by_mode (engine.cpp:379-387): dispatch on request.mode."""
+    return engine.score(request, k)
+
+
+def topk_host(scores: np.ndarray, ids: Optional[np.ndarray], k: int):
+    """Caller-side ordering (semrank_main.cpp:393-398) via the native comparator."""
+    s = np.ascontiguousarray(scores, np.float64)
+    n = len(s)
+    kk = min(k, n)
+    oi, os_, ox = np.zeros(max(kk, 1), np.int64), np.zeros(max(kk, 1)), np.zeros(max(kk, 1), np.int32)
+    idp = None
+    if ids is not None:
+        ids = np.ascontiguousarray(ids, np.int64)
+        idp = ids.ctypes.data_as(C.POINTER(C.c_int64))
+    _check(_lib.sr_topk_host(s.ctypes.data_as(C.POINTER(C.c_double)), idp, n, k,
+                             oi.ctypes.data_as(C.POINTER(C.c_int64)),
+                             os_.ctypes.data_as(C.POINTER(C.c_double)),
+                             ox.ctypes.data_as(C.POINTER(C.c_int32))))
+    return oi[:kk], os_[:kk], ox[:kk]
