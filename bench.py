@@ -1,0 +1,410 @@
+#!/usr/bin/env python3
+"""Benchmark: query-item pairs scored per second (BASELINE.json metric).
+
+Workload (N=1): BASELINE.json configs[1] — 0.6B-class pruned SLM (L20 d1024 H8
+ff1536, V300, fan-in random init, seed 2026), 1 query x 256 candidates,
+256-token shared prefix, 96-token item segments, synthetic uniform token ids.
+A step = one full pass of the hot path over one query: packed shared-prefix
+prefill through all 20 layers, final-LN score head, top-k.
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling by candidate sharding —
+the query has 256 x N candidates, rank r scores its contiguous shard of 256
+(prefix recomputed per rank) and the per-rank top-k lists are merged with one
+NCCL all-gather inside the step. value = all pairs / max-over-ranks time.
+
+  value : device-resident inputs, CUDA-graph replay + NCCL merge, CUDA events
+          on the engine stream
+  e2e   : the public API call ScoringEngine.score (ctypes -> C-ABI): host
+          token arrays in, host scores + top-k out, every copy inside the step
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref: reference sources compiled in place; else the C port) on
+bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (n_layers, d_model, n_heads, d_ff, t_q, t_i, n_items per GPU, soft_tokens)
+    "c2": (20, 1024, 8, 1536, 256, 96, 256, False),
+    "c3": (20, 1024, 8, 1536, 256, 8, 1024, True),
+    "c1": (2, 64, 4, 256, 500, 50, 64, False),
+}
+WORKLOAD_DESC = {
+    "c2": "0.6B-class pruned SLM (L20 d1024 H8 ff1536), 1 query x 256 candidates, "
+          "256-token shared prefix, 96-token items",
+    "c3": "0.6B-class pruned SLM, 1 query x 1024 candidates, 256-token prefix, "
+          "8 soft-token rows per item (context compression)",
+    "c1": "reference default toy ranker (L2 d64 H4 ff256), 1 query x 64 candidates, "
+          "T_q 500, T_i 50 (cmd_bench shape)",
+}
+TOPK = 10  # service page size (service.hpp:24)
+
+
+def model_flops_per_query(L, d, ff, t_q, lens):
+    """linear 2L(T)(4d^2+2d ff) + attention 4dL[pairs] + head."""
+    T = t_q + sum(lens)
+    lin = 2.0 * L * T * (4 * d * d + 2 * d * ff)
+    pairs = t_q * (t_q + 1) / 2 + sum(t_q * l + l * (l + 1) / 2 for l in lens)
+    att = 4.0 * d * L * pairs
+    return lin, att, 2.0 * d * 7 * len(lens)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def load_traffic():
+    """dram bytes per GEMM launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(prefix="clk_", suffix=".csv")
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) < 9:
+                    continue
+                try:
+                    sm.append(float(p[1]))
+                    smax = float(p[2])
+                except ValueError:
+                    continue
+                for n, v in zip(names, p[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        os.unlink(self.path)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_request(sr, wl, world, rank, seed=7):
+    L, d, H, ff, t_q, t_i, n_loc, soft = WORKLOADS[wl]
+    rng = np.random.default_rng(seed)
+    prefix = rng.integers(0, 256, t_q).astype(np.int32)
+    n_all = n_loc * world
+    lo = rank * n_loc
+    req = sr.ScoreRequest(request_id=f"bench-{wl}", prefix_tokens=prefix,
+                          mode=sr.ScoreMode.Mixed if soft else sr.ScoreMode.MultiItem)
+    if soft:
+        # soft-token rows ~ N(0, 0.08^2) (the reference's embedding scale)
+        rows = rng.standard_normal((n_all, t_i, d)).astype(np.float32) * np.float32(0.08)
+        for i in range(lo, lo + n_loc):
+            req.items.append(sr.ScoreItem(id=str(i), embedding=rows[i], n_emb_tokens=t_i))
+    else:
+        toks = rng.integers(0, 256, (n_all, t_i)).astype(np.int32)
+        for i in range(lo, lo + n_loc):
+            req.items.append(sr.ScoreItem(id=str(i), tokens=toks[i]))
+    ids = np.arange(lo, lo + n_loc, dtype=np.int64)
+    return req, ids
+
+
+# ------------------------------------------------------------- CPU baseline
+def cpu_reference_run(wl, n_items, weights_path, fan_in, threads):
+    """One bounded sample on the host: prefix + n_items items, reference
+    multi_item (or mixed) mode; returns seconds. Test infrastructure only."""
+    from oracle import oracle as O
+    L, d, H, ff, t_q, t_i, _, soft = WORKLOADS[wl]
+    rng = np.random.default_rng(7)
+    prefix = rng.integers(0, 256, t_q).astype(np.int32)
+    if soft:
+        rows = [rng.standard_normal((t_i, d)).astype(np.float32) * np.float32(0.08)
+                for _ in range(n_items)]
+        items = None
+    else:
+        items = [rng.integers(0, 256, t_i).astype(np.int32) for _ in range(n_items)]
+        rows = None
+    if O.ref_available():
+        O.ref().ref_set_parallel(1)
+        t0 = time.perf_counter()
+        O.ref_score(weights_path, 3 if soft else 2, prefix, items=items, rows=rows)
+        return time.perf_counter() - t0, "reference"
+    w = O.OracleWeights.load(weights_path)
+    t0 = time.perf_counter()
+    w.score(prefix, items=items, rows=rows, threads=threads)
+    return time.perf_counter() - t0, "port"
+
+
+def cpu_baseline(sr, wl, weights, budget_s=20.0):
+    """Times the reference CPU path on a bounded sample sized to ~budget_s."""
+    L, d, H, ff, t_q, t_i, n_loc, soft = WORKLOADS[wl]
+    path = os.path.join(tempfile.gettempdir(), f"bench_{wl}_weights.srnk")
+    weights.save(path)
+    threads = os.cpu_count() or 1
+    probe_n = 1 if wl != "c1" else 8
+    t_probe, kind = cpu_reference_run(wl, probe_n, path, True, threads)
+    # model: t(n) = t_prefix + n * t_item with t_prefix ~ (t_q / t_i) * t_item
+    per_item = t_probe / (probe_n + t_q / t_i)
+    n = int(max(probe_n, min(n_loc, (budget_s / per_item) - t_q / t_i)))
+    t, kind = cpu_reference_run(wl, n, path, True, threads)
+    return {"value": n / t, "unit": "pairs/s", "cores": threads, "kind": kind,
+            "sample": f"1 query: {t_q}-token prefix + {n} x {t_i}-token items of the {wl} "
+                      f"workload, reference {'mixed' if soft else 'multi_item'} mode, "
+                      f"OpenMP on all host threads, prefix time included ({t:.1f} s)"}, path
+
+
+# ---------------------------------------------------------------- main arms
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import paper_2602_07309_b200 as sr  # host-side init only (no GPU work)
+    wl = args.workload
+    L, d, H, ff, t_q, t_i, n_loc, soft = WORKLOADS[wl]
+    cfg = sr.ModelConfig(n_layers=L, d_model=d, n_heads=H, d_ff=ff,
+                         head_specs=sr.ModelConfig.default_toy().head_specs)
+    w = sr.init_model(cfg, 2026 if wl != "c1" else 1, "fan_in" if wl != "c1" else "reference")
+    path = os.path.join(tempfile.gettempdir(), f"bench_{wl}_weights.srnk")
+    w.save(path)
+    threads = os.cpu_count() or 1
+    steps = args.steps + args.warmup
+    budget = max(2.0, 150.0 / max(steps, 1))
+    probe_n = 1 if wl != "c1" else 8
+    t_probe, kind = cpu_reference_run(wl, probe_n, path, True, threads)
+    per_item = t_probe / (probe_n + t_q / t_i)
+    n = int(max(probe_n, min(n_loc, budget / per_item - t_q / t_i)))
+    times = []
+    for s in range(steps):
+        t, kind = cpu_reference_run(wl, n, path, True, threads)
+        if s >= args.warmup:
+            times.append(t)
+    value = n * len(times) / sum(times)
+    sample = (f"per step 1 query: {t_q}-token prefix + {n} x {t_i}-token items "
+              f"({'mixed' if soft else 'multi_item'} mode), prefix included")
+    line = {"metric": "query-item pairs scored/sec", "value": value, "unit": "pairs/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * statistics.mean(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD_DESC[wl], "model": f"semrank-{wl}",
+                       "global_batch": n, "seq_len": t_q + t_i, "parallelism": "cpu-openmp"},
+            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2602_07309_b200 as sr
+
+    wl = args.workload
+    L, d, H, ff, t_q, t_i, n_loc, soft = WORKLOADS[wl]
+    cfg = sr.ModelConfig(n_layers=L, d_model=d, n_heads=H, d_ff=ff,
+                         head_specs=sr.ModelConfig.default_toy().head_specs)
+    weights = sr.init_model(cfg, 2026 if wl != "c1" else 1, "fan_in" if wl != "c1" else "reference")
+    eng = sr.ScoringEngine(weights, device=local)
+    req, ids = make_request(sr, wl, world, rank)
+    k = TOPK
+    comm = None
+    if world > 1:
+        uid = sr.Comm.unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        comm = sr.Comm(world, rank, obj[0], local)
+    plan = eng.plan(req, k=k, item_ids=ids)
+    stream = torch.cuda.ExternalStream(eng.stream_ptr)
+
+    def step():
+        if comm is not None:
+            plan.run_sharded(comm)
+        else:
+            plan.run()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    plan.sync()
+
+    # -------------------------------------------------- device-resident value
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    plan.sync()
+    barrier()
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = ev[0][0].elapsed_time(ev[-1][1])
+    t = torch.tensor([total_ms], device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    pairs = n_loc * world * args.steps
+    value = pairs / (total_ms / 1000.0)
+    lat_sorted = sorted(step_ms)
+    p99 = lat_sorted[max(0, int(np.ceil(0.99 * len(lat_sorted))) - 1)]  # service.cpp:28-34
+    result = plan.fetch()
+
+    # ----------------------------------------------------------- e2e (public API)
+    shape = plan.shape()
+    for _ in range(max(1, args.warmup)):
+        (eng.score_sharded(comm, req, k, ids) if comm else eng.score(req, k))
+    barrier()
+    e2e_times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        (eng.score_sharded(comm, req, k, ids) if comm else eng.score(req, k))
+        e2e_times.append(time.perf_counter() - t0)
+    barrier()
+    te = torch.tensor([sum(e2e_times)], device="cuda")
+    if dist is not None:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = pairs / float(te.item())
+    h2d = shape["h2d_bytes"]  # packed rows/spans/tiles/ids (+ soft rows), per call
+    d2h = shape["d2h_bytes"]  # scores [N x tasks] f64 + top-k entries
+
+    # -------------------------------------------------- per-kernel roofline
+    prof = plan.profile(reps=3)
+    lens = [t_i] * n_loc
+    lin, att, head = model_flops_per_query(L, d, ff, t_q, lens)
+    gemm_ms = sum(prof[c][0] for c in ("gemm_qkv", "gemm_o", "gemm_in", "gemm_out"))
+    gemm_launches = sum(prof[c][1] for c in ("gemm_qkv", "gemm_o", "gemm_in", "gemm_out"))
+    peaks, peak_kind = load_peaks()
+    achieved = lin / (gemm_ms / 1000.0) / 1e12
+    peak = peaks.get("bf16_tflops_sustained", 1391.8)
+    traffic = load_traffic().get(f"{wl}_gemm_dram_bytes_per_launch")
+    M = shape["rows"]
+    attn_bytes = 8.0 * d * M * L  # §8(d): read Q,K,V + write O, bf16, per layer
+    attn_ms = prof["attention"][0]
+    roofline = {"bound": "tensor", "kernel": "tcgen05 GEMMs (QKV/O/W_in/W_out)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_source": f"{peak_kind} bf16_tflops_sustained",
+                "algorithmic_flops_per_launch": lin / max(gemm_launches, 1),
+                "gemm_share_of_step": gemm_ms / max(sum(v[0] for v in prof.values()), 1e-9),
+                "attention": {"bound": "hbm", "achieved_gbs": attn_bytes / (attn_ms / 1000) / 1e9,
+                              "peak_gbs": peaks.get("hbm_gbs"),
+                              "frac": attn_bytes / (attn_ms / 1000) / 1e9 / peaks.get("hbm_gbs", 1),
+                              "achieved_tflops": att / (attn_ms / 1000) / 1e12},
+                "per_class_ms": {c: round(v[0], 4) for c, v in prof.items()}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu, _ = cpu_baseline(sr, wl, weights)
+        except Exception as e:  # oracle missing on the box -> reported, not fatal
+            cpu = {"value": None, "unit": "pairs/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"unavailable: {e}"}
+
+    line = {
+        "metric": "query-item pairs scored/sec", "value": value, "unit": "pairs/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": WORKLOAD_DESC[wl], "model": f"semrank-{wl}-L{L}-d{d}",
+                   "global_batch": n_loc * world, "seq_len": t_q + t_i,
+                   "parallelism": f"candidate-shard x{world}" if world > 1 else "single-gpu",
+                   "tokens_per_query_per_gpu": M, "top_k": k,
+                   "p99_query_ms": p99, "p50_query_ms": statistics.median(step_ms),
+                   "latency_budget_ms": 500, "meets_p99_budget": p99 <= 500,
+                   "prefill_tokens_per_s_per_gpu": M / (total_ms / args.steps / 1000.0),
+                   "l2": "inputs+weights+activations per step > 126 MB L2 (no flush)"},
+        "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "path": "ScoringEngine.score -> sr_engine_score (host arrays in/out)"},
+        "gpu_launches": plan.kernel_count() * args.steps,
+        "clocks": clk, "roofline": roofline, "cpu_baseline": cpu,
+        "topk_head": [(iid, round(s, 6)) for iid, s in result.topk[:3]],
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -174,6 +174,11 @@ int32_t sr_plan_batches(int32_t n_requests, const int32_t* prefix_len,
                         int64_t max_batch_tokens, int32_t* entries_out, int32_t cap_entries,
                         int32_t* n_entries_out, int64_t* batch_tokens_out, int32_t cap_batches,
                         int32_t* n_batches_out);
+/* Validates a request against a config exactly as scoring would (same error
+ * categories: engine.cpp:51-61, 243-251; model.cpp:222-264) and returns the
+ * FlopReport / kv_incremental_per_item the reference reports for its mode. */
+int32_t sr_request_report(const sr_model_config* cfg, const sr_request* req,
+                          sr_flop_report* flops_out, double* kv_out);
 /* Host top-k with the caller comparator (score desc, id asc, index asc). */
 int32_t sr_topk_host(const double* scores, const int64_t* ids, int32_t n, int32_t k,
                      int64_t* ids_out, double* scores_out, int32_t* index_out);
@@ -204,6 +209,15 @@ int32_t sr_plan_sync(sr_plan* p);
 int32_t sr_plan_fetch(sr_plan* p, sr_result* res); /* D2H of scores + top-k */
 int32_t sr_plan_kernel_count(const sr_plan* p, int32_t* launches);
 void sr_plan_destroy(sr_plan* p);
+/* Live per-kernel-class timing: eager forward with CUDA events around each
+ * launch on the engine stream. Classes: 0 embed+LN1, 1 QKV GEMM, 2 attention,
+ * 3 O GEMM, 4 LayerNorm, 5 W_in GEMM, 6 W_out GEMM, 7 score head, 8 top-k.
+ * ms_out[9] = mean ms per forward; launches_out[9] = launches per forward. */
+#define SR_PROF_CLASSES 9
+int32_t sr_plan_profile(sr_plan* p, int32_t reps, float* ms_out, int32_t* launches_out);
+/* Shape of a plan: {rows M, items, attention tiles, soft rows, H2D bytes per
+ * call, D2H bytes per call, k, tasks}. */
+int32_t sr_plan_shape(const sr_plan* p, int64_t* out8);
 
 /* ------------------------------------------------------- multi-GPU (NCCL) */
 /* Candidate sharding: every rank holds the full weights, scores its shard

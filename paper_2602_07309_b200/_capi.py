@@ -75,6 +75,7 @@ _sig("sr_multi_item_pair_count", i32, i32, P(i32), i32, P(i64))
 _sig("sr_multi_item_mask", i32, i32, P(i32), i32, P(i32), i32, P(i32))
 _sig("sr_plan_batches", i32, i32, P(i32), P(i32), P(i32), i64, P(i32), i32, P(i32), P(i64),
      i32, P(i32))
+_sig("sr_request_report", i32, P(ModelConfigC), P(RequestC), P(FlopReportC), P(f64))
 _sig("sr_topk_host", i32, P(f64), P(i64), i32, i32, P(i64), P(f64), P(i32))
 _sig("sr_engine_create", i32, vp, i32, P(vp))
 _sig("sr_engine_destroy", None, vp)
@@ -89,6 +90,8 @@ _sig("sr_plan_sync", i32, vp)
 _sig("sr_plan_fetch", i32, vp, P(ResultC))
 _sig("sr_plan_kernel_count", i32, vp, P(i32))
 _sig("sr_plan_destroy", None, vp)
+_sig("sr_plan_profile", i32, vp, i32, P(f32), P(i32))
+_sig("sr_plan_shape", i32, vp, P(i64))
 _sig("sr_nccl_unique_id", i32, P(C.c_uint8))
 _sig("sr_comm_create", i32, i32, i32, P(C.c_uint8), i32, P(vp))
 _sig("sr_comm_destroy", None, vp)
@@ -105,10 +108,12 @@ HEADER_SYMBOLS = [
     "sr_config_default_toy", "sr_task_count", "sr_weights_init", "sr_weights_load",
     "sr_weights_save", "sr_weights_from_tensors", "sr_weights_free", "sr_weights_config",
     "sr_weights_version", "sr_weights_tensor_count", "sr_weights_tensor", "sr_flops",
-    "sr_multi_item_pair_count", "sr_multi_item_mask", "sr_plan_batches", "sr_topk_host",
+    "sr_multi_item_pair_count", "sr_multi_item_mask", "sr_plan_batches", "sr_request_report",
+    "sr_topk_host",
     "sr_engine_create", "sr_engine_destroy", "sr_engine_score", "sr_engine_score_batch",
     "sr_engine_item_hidden", "sr_engine_device", "sr_engine_stream", "sr_plan_create",
     "sr_plan_run", "sr_plan_sync", "sr_plan_fetch", "sr_plan_kernel_count", "sr_plan_destroy",
+    "sr_plan_profile", "sr_plan_shape",
     "sr_nccl_unique_id", "sr_comm_create", "sr_comm_destroy", "sr_engine_score_sharded",
     "sr_plan_run_sharded", "sr_kernel_gemm", "sr_kernel_attention", "sr_kernel_layernorm",
     "sr_kernel_topk",

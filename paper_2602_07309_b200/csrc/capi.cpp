@@ -282,6 +282,17 @@ int32_t sr_plan_batches(int32_t n_requests, const int32_t* prefix_len,
   });
 }
 
+int32_t sr_request_report(const sr_model_config* cfg, const sr_request* req,
+                          sr_flop_report* flops_out, double* kv_out) {
+  return guard([&] {
+    if (!cfg || !req) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    const auto c = srh::ModelConfig::from_c(*cfg);
+    c.validate();
+    const auto lens = srh::validate_request(c, *req);
+    srh::report_for(c, *req, lens, flops_out, kv_out);
+  });
+}
+
 int32_t sr_topk_host(const double* scores, const int64_t* ids, int32_t n, int32_t k,
                      int64_t* ids_out, double* scores_out, int32_t* index_out) {
   return guard([&] {
@@ -372,6 +383,36 @@ int32_t sr_plan_kernel_count(const sr_plan* p, int32_t* launches) {
   return guard([&] {
     if (!p || !launches) srh::fail(SR_SPEC_VIOLATION, "null argument");
     *launches = p->p->launches;
+  });
+}
+
+int32_t sr_plan_profile(sr_plan* p, int32_t reps, float* ms_out, int32_t* launches_out) {
+  return guard([&] {
+    if (!p) srh::fail(SR_SPEC_VIOLATION, "null plan");
+    std::lock_guard<std::mutex> lock(p->owner->e->mutex());
+    p->owner->e->profile(*p->p, reps, ms_out, launches_out);
+  });
+}
+
+int32_t sr_plan_shape(const sr_plan* p, int64_t* out8) {
+  return guard([&] {
+    if (!p || !out8) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    const auto& pk = p->p->pack;
+    out8[0] = pk.M;
+    out8[1] = pk.n_items;
+    out8[2] = static_cast<int64_t>(pk.tiles.size());
+    out8[3] = pk.n_soft;
+    int64_t h2d = 0;
+    h2d += static_cast<int64_t>(pk.row_src.size()) * 4 + static_cast<int64_t>(pk.row_pos.size()) * 4;
+    h2d += static_cast<int64_t>(pk.spans.size()) * sizeof(srk::RowSpan);
+    h2d += static_cast<int64_t>(pk.tiles.size()) * sizeof(srk::AttnTile);
+    h2d += static_cast<int64_t>(pk.last_rows.size()) * 4 + static_cast<int64_t>(pk.ids.size()) * 8;
+    h2d += static_cast<int64_t>(pk.seg_off.size()) * 4 + static_cast<int64_t>(pk.soft_rows.size()) * 4;
+    out8[4] = h2d;
+    out8[5] = static_cast<int64_t>(pk.n_items) * p->p->n_tasks * 8 +
+              static_cast<int64_t>(pk.seg_off.size() - 1) * p->p->k * sizeof(srk::TopkEntry);
+    out8[6] = p->p->k;
+    out8[7] = p->p->n_tasks;
   });
 }
 

@@ -169,43 +169,112 @@ void Engine::ensure_workspace(int32_t M) {
   ++ws_epoch_;
 }
 
-int32_t Engine::enqueue_forward(Plan& p, float* hidden_out) {
+void Profiler::begin(int cls) {
+  cudaEvent_t a;
+  SR_CUDA_CHECK(cudaEventCreate(&a));
+  SR_CUDA_CHECK(cudaEventRecord(a, stream));
+  cur = cls;
+  cur_start = a;
+}
+void Profiler::end() {
+  cudaEvent_t b;
+  SR_CUDA_CHECK(cudaEventCreate(&b));
+  SR_CUDA_CHECK(cudaEventRecord(b, stream));
+  marks.push_back({cur, {cur_start, b}});
+}
+Profiler::~Profiler() {
+  for (auto& m : marks) {
+    cudaEventDestroy(m.second.first);
+    cudaEventDestroy(m.second.second);
+  }
+}
+
+int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
   const int M = p.pack.M, d = cfg_.d_model, F = cfg_.d_ff, H = cfg_.n_heads;
   const int hd = cfg_.head_dim();
   cudaStream_t s = stream_;
   int32_t n = 0;
+  auto B = [&](int c) {
+    if (prof) prof->begin(c);
+  };
+  auto E = [&]() {
+    if (prof) prof->end();
+  };
+  B(PROF_EMBED_LN);
   SR_CUDA_CHECK(srk::embed_ln(p.src.ptr, p.pos.ptr, tok_emb_, p.pack.n_soft ? p.soft.ptr : nullptr,
                               pos_emb_, layers_[0].ln1, x_.ptr, xn_.ptr, M, d, s));
+  E();
   ++n;
   const int bn_qkv = srk::gemm_pick_bn(3 * d), bn_d = srk::gemm_pick_bn(d),
             bn_f = srk::gemm_pick_bn(F);
   for (int l = 0; l < cfg_.n_layers; ++l) {
     const auto& L = layers_[l];
+    B(PROF_GEMM_QKV);
     SR_CUDA_CHECK(srk::gemm_bf16(tm_xn_, L.tm_qkv, M, 3 * d, d, qkv_.ptr, 3 * d, 0, bn_qkv, s));
+    E();
+    B(PROF_ATTENTION);
     SR_CUDA_CHECK(srk::attention(qkv_.ptr, p.spans.ptr, p.tiles.ptr,
                                  static_cast<int>(p.pack.tiles.size()), xn_.ptr, M, H, hd, s));
+    E();
+    B(PROF_GEMM_O);
     SR_CUDA_CHECK(srk::gemm_bf16(tm_xn_, L.tm_o, M, d, d, x_.ptr, d, 2, bn_d, s));
+    E();
+    B(PROF_LAYERNORM);
     SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, L.ln2, xn_.ptr, M, d, s));
+    E();
+    B(PROF_GEMM_IN);
     SR_CUDA_CHECK(srk::gemm_bf16(tm_xn_, L.tm_in, M, F, d, h_.ptr, F, 1, bn_f, s));
+    E();
+    B(PROF_GEMM_OUT);
     SR_CUDA_CHECK(srk::gemm_bf16(tm_h_, L.tm_out, M, d, F, x_.ptr, d, 2, bn_d, s));
+    E();
     n += 6;
     if (l + 1 < cfg_.n_layers) {
+      B(PROF_LAYERNORM);
       SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, layers_[l + 1].ln1, xn_.ptr, M, d, s));
+      E();
       ++n;
     }
   }
+  B(PROF_SCORE_HEAD);
   SR_CUDA_CHECK(srk::score_head(x_.ptr, p.last_rows.ptr, p.pack.n_items, d, ln_f_, head_w_,
                                 head_b_, n_cols_, task_col_, task_arity_, n_tasks(), yes_col_,
                                 no_col_, p.scores.ptr, hidden_out, s));
+  E();
   ++n;
   if (p.k > 0) {
     const int n_seg = static_cast<int>(p.pack.seg_off.size()) - 1;
+    B(PROF_TOPK);
     SR_CUDA_CHECK(srk::topk(p.scores.ptr, n_tasks(), p.ids.ptr, p.seg_off.ptr, n_seg,
                             p.pack.max_seg_len, p.k, p.topk_scratch.ptr,
                             static_cast<int>(p.topk_scratch.cap), p.topk_out.ptr, s));
+    E();
     n += p.pack.max_seg_len > 4096 ? 2 : 1;
   }
   return n;
+}
+
+void Engine::profile(Plan& p, int reps, float* ms_out, int32_t* launches_out) {
+  SR_CUDA_CHECK(cudaSetDevice(device_));
+  std::vector<double> acc(PROF_N, 0.0);
+  std::vector<int32_t> cnt(PROF_N, 0);
+  reps = std::max(reps, 1);
+  for (int r = 0; r < reps; ++r) {
+    Profiler prof;
+    prof.stream = stream_;
+    enqueue_forward(p, nullptr, &prof);
+    SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    for (auto& m : prof.marks) {
+      float ms = 0.f;
+      SR_CUDA_CHECK(cudaEventElapsedTime(&ms, m.second.first, m.second.second));
+      acc[m.first] += ms;
+      if (r == 0) cnt[m.first] += 1;
+    }
+  }
+  for (int c = 0; c < PROF_N; ++c) {
+    if (ms_out) ms_out[c] = static_cast<float>(acc[c] / reps);
+    if (launches_out) launches_out[c] = cnt[c];
+  }
 }
 
 namespace {

@@ -70,6 +70,23 @@ struct LayerDev {
 
 class Engine;
 
+// Kernel classes for live per-class timing (sr_plan_profile).
+enum ProfClass : int {
+  PROF_EMBED_LN = 0, PROF_GEMM_QKV, PROF_ATTENTION, PROF_GEMM_O, PROF_LAYERNORM, PROF_GEMM_IN,
+  PROF_GEMM_OUT, PROF_SCORE_HEAD, PROF_TOPK, PROF_N
+};
+
+// Records a CUDA event pair around every launch of a profiled forward.
+struct Profiler {
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  cudaStream_t stream = nullptr;
+  int cur = -1;
+  cudaEvent_t cur_start = nullptr;
+  void begin(int cls);
+  void end();
+  ~Profiler();
+};
+
 // One request shape, resident on the device, replayed through a CUDA graph.
 struct Plan {
   Engine* eng = nullptr;
@@ -121,7 +138,10 @@ class Engine {
   void run_plan_sharded(Plan& p, struct Comm* comm);
 
   // Enqueue the full forward for the plan's packed batch on stream_.
-  int32_t enqueue_forward(Plan& p, float* hidden_out);
+  int32_t enqueue_forward(Plan& p, float* hidden_out, Profiler* prof = nullptr);
+  // Eager forward with an event pair around every launch; per-class mean ms
+  // and launch counts per forward, averaged over `reps` runs.
+  void profile(Plan& p, int reps, float* ms_out, int32_t* launches_out);
 
  private:
   void ensure_workspace(int32_t M);

@@ -329,6 +329,16 @@ def plan_batches(requests: Sequence[ScoreRequest], max_batch_tokens: int) -> Lis
     return batches
 
 
+def request_report(config: ModelConfig, request: ScoreRequest):
+    """Host-side validation + the reference FlopReport for the request's mode."""
+    pr = _PackedRequest(request, config.d_model)
+    c = config._to_c()
+    f = _c.FlopReportC()
+    kv = C.c_double()
+    _check(_lib.sr_request_report(C.byref(c), C.byref(pr.c), C.byref(f), C.byref(kv)))
+    return FlopReport._from_c(f), kv.value
+
+
 def _item_doc_ids(items: Sequence[ScoreItem]) -> Optional[np.ndarray]:
     try:
         return np.array([int(it.id) for it in items], np.int64)
@@ -357,7 +367,8 @@ class _PackedRequest:
         self.offsets[1:] = np.cumsum(lens) if lens else []
         if mixed:
             self.rows = np.ascontiguousarray(np.concatenate(
-                [np.asarray(it.embedding, np.float32).reshape(-1) for it in req.items]))
+                [np.asarray(it.embedding, np.float32).reshape(-1) for it in req.items])
+                if req.items else np.zeros(1, np.float32))
             self.tokens = np.zeros(1, np.int32)
         else:
             self.tokens = np.ascontiguousarray(np.concatenate(
@@ -436,12 +447,105 @@ class ScoringEngine:
             out.append(self._to_result(r, rb))
         return out
 
+    def plan(self, request: ScoreRequest, k: int = 0, item_ids=None) -> "Plan":
+        return Plan(self, request, k, item_ids)
+
+    def score_sharded(self, comm: "Comm", request: ScoreRequest, k: int,
+                      item_ids: Optional[np.ndarray] = None) -> ScoreResult:
+        """Score this rank's shard; top-k is merged across ranks (NCCL)."""
+        pr = _PackedRequest(request, self.config.d_model, item_ids)
+        rb = _ResultBuf(len(request.items), len(self.task_names), k)
+        _check(_lib.sr_engine_score_sharded(self._h, comm._h, C.byref(pr.c), C.byref(rb.c)))
+        return self._to_result(request, rb)
+
+    @property
+    def stream_ptr(self) -> int:
+        return _lib.sr_engine_stream(self._h) or 0
+
     def item_hidden(self, request: ScoreRequest) -> np.ndarray:
         pr = _PackedRequest(request, self.config.d_model)
         out = np.zeros((len(request.items), self.config.d_model), np.float32)
         _check(_lib.sr_engine_item_hidden(self._h, C.byref(pr.c),
                                           out.ctypes.data_as(C.POINTER(C.c_float))))
         return out
+
+
+PROF_CLASSES = ["embed_ln", "gemm_qkv", "attention", "gemm_o", "layernorm", "gemm_in",
+                "gemm_out", "score_head", "topk"]
+
+
+class Comm:
+    """NCCL communicator for candidate-sharded scoring (one rank per GPU)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(_lib.sr_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, nranks: int, rank: int, uid: bytes, device: int):
+        buf = (C.c_uint8 * 128)(*uid)
+        h = C.c_void_p()
+        _check(_lib.sr_comm_create(nranks, rank, buf, device, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.sr_comm_destroy(h)
+            self._h = C.c_void_p()
+
+
+class Plan:
+    """Resident request (packed inputs on the device + captured CUDA graph)."""
+
+    def __init__(self, engine: "ScoringEngine", request: ScoreRequest, k: int = 0,
+                 item_ids: Optional[np.ndarray] = None):
+        self.engine = engine
+        self.request = request
+        self._pr = _PackedRequest(request, engine.config.d_model, item_ids)
+        h = C.c_void_p()
+        _check(_lib.sr_plan_create(engine._h, C.byref(self._pr.c), k, C.byref(h)))
+        self._h = h
+        self.k = k
+        self._rb = _ResultBuf(len(request.items), len(engine.task_names), k)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.sr_plan_destroy(h)
+            self._h = C.c_void_p()
+
+    def run(self) -> None:
+        _check(_lib.sr_plan_run(self._h))
+
+    def run_sharded(self, comm: Comm) -> None:
+        _check(_lib.sr_plan_run_sharded(self._h, comm._h))
+
+    def sync(self) -> None:
+        _check(_lib.sr_plan_sync(self._h))
+
+    def fetch(self) -> ScoreResult:
+        _check(_lib.sr_plan_fetch(self._h, C.byref(self._rb.c)))
+        return self.engine._to_result(self.request, self._rb)
+
+    def kernel_count(self) -> int:
+        n = C.c_int32()
+        _check(_lib.sr_plan_kernel_count(self._h, C.byref(n)))
+        return n.value
+
+    def shape(self) -> dict:
+        o = np.zeros(8, np.int64)
+        _check(_lib.sr_plan_shape(self._h, o.ctypes.data_as(C.POINTER(C.c_int64))))
+        keys = ["rows", "items", "attn_tiles", "soft_rows", "h2d_bytes", "d2h_bytes", "k", "tasks"]
+        return {k: int(v) for k, v in zip(keys, o)}
+
+    def profile(self, reps: int = 3) -> dict:
+        ms = np.zeros(len(PROF_CLASSES), np.float32)
+        cnt = np.zeros(len(PROF_CLASSES), np.int32)
+        _check(_lib.sr_plan_profile(self._h, reps, ms.ctypes.data_as(C.POINTER(C.c_float)),
+                                    cnt.ctypes.data_as(C.POINTER(C.c_int32))))
+        return {c: (float(m), int(n)) for c, m, n in zip(PROF_CLASSES, ms, cnt)}
 
 
 def score_by_mode(engine: ScoringEngine, request: ScoreRequest, k: int = 0) -> ScoreResult:

@@ -1,0 +1,14 @@
+#!/bin/bash
+# One GPU measurement pass: smoke, bench, launch list, ncu --set full captures.
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv
+nproc; lscpu | grep "Model name"
+timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
+timeout -s KILL 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err
+cat gpurun_out/bench.json
+timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+wc -l gpurun_out/launches.csv
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:gemm_bf16 -s 4 -c 4 -o gpurun_out/prof_gemm python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_gemm.log 2>&1; tail -3 gpurun_out/ncu_gemm.log
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:attn_segment -s 1 -c 1 -o gpurun_out/prof_attn python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_attn.log 2>&1; tail -3 gpurun_out/ncu_attn.log
+ls -la gpurun_out
