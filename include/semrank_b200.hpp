@@ -1,0 +1,243 @@
+// semrank_b200.hpp — header-only C++ facade over the C-ABI with the
+// reference's own type names (namespace semrank; engine.hpp / model.hpp /
+// weights_io.hpp / error.hpp), so a caller such as the reference's
+// service.cpp (service.cpp:224 `engine_.score(score_request)`) relinks against
+// libsemrank_b200.so instead of the CPU scorer. Differences from the
+// reference API, all additive:
+//   * ModelWeights is an owning handle (weights live in the library);
+//   * ScoringEngine takes a device index and owns device copies;
+//   * ScoringEngine::score takes an optional top-k length and fills
+//     ScoreResult::topk (caller-side ordering, semrank_main.cpp:393-398).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "semrank_b200.h"
+
+namespace semrank {
+
+enum class ErrorCode {  // error.hpp:13-29 (same order)
+  LengthOverflow, MaskInvalid, SpecViolation, PayloadInvalid, SchemaUnknown, Alignment,
+  Divergence, Parameter, DegenerateInput, UndefinedMetric, StateInvalid, OversizeItem,
+  Consistency, Reconciliation, Io
+};
+
+class Error : public std::runtime_error {
+ public:
+  Error(ErrorCode code, const std::string& m) : std::runtime_error(m), code_(code) {}
+  ErrorCode code() const { return code_; }
+
+ private:
+  ErrorCode code_;
+};
+
+// Device-side failures (CUDA / NCCL) have no reference equivalent.
+class DeviceError : public std::runtime_error {
+ public:
+  explicit DeviceError(const std::string& m) : std::runtime_error(m) {}
+};
+
+inline void check(int32_t st) {
+  if (st == SR_OK) return;
+  const std::string msg = sr_last_error();
+  if (st >= 1 && st <= 15) throw Error(static_cast<ErrorCode>(st - 1), msg);
+  throw DeviceError(std::string(sr_status_name(st)) + ": " + msg);
+}
+
+enum class ScoreMode { Naive, Ibpc, MultiItem, Mixed };  // engine.hpp:15
+
+struct HeadSpec {
+  std::string name;
+  int arity = 1;
+};
+
+struct ModelConfig {  // model.hpp:24-40
+  int n_layers = 2, d_model = 64, n_heads = 4, d_ff = 256, vocab_size = 300, max_seq = 4096;
+  int yes_token_id = 261, no_token_id = 262;
+  std::vector<HeadSpec> head_specs;
+  int head_dim() const { return d_model / n_heads; }
+  static ModelConfig default_toy() {
+    ModelConfig c;
+    c.head_specs = {{"click", 1}, {"apply", 1}, {"badfit", 1}, {"shortlist", 1}, {"dismiss", 1}};
+    return c;
+  }
+  void validate() const { with_c([](const sr_model_config& c) { check(sr_config_validate(&c)); }); }
+
+  template <typename F>
+  void with_c(F&& f) const {
+    std::vector<const char*> names;
+    std::vector<int32_t> ar;
+    for (const auto& h : head_specs) {
+      names.push_back(h.name.c_str());
+      ar.push_back(h.arity);
+    }
+    sr_model_config c{n_layers, d_model, n_heads, d_ff, vocab_size, max_seq, yes_token_id,
+                      no_token_id, static_cast<int32_t>(head_specs.size()), names.data(),
+                      ar.data()};
+    f(c);
+  }
+};
+
+class ModelWeights {  // model.hpp:56-67, owning handle
+ public:
+  explicit ModelWeights(sr_weights* w) : w_(w, &sr_weights_free) {
+    sr_model_config c{};
+    check(sr_weights_config(w, &c));
+    config.n_layers = c.n_layers;
+    config.d_model = c.d_model;
+    config.n_heads = c.n_heads;
+    config.d_ff = c.d_ff;
+    config.vocab_size = c.vocab_size;
+    config.max_seq = c.max_seq;
+    config.yes_token_id = c.yes_token_id;
+    config.no_token_id = c.no_token_id;
+    for (int i = 0; i < c.n_task_heads; ++i)
+      config.head_specs.push_back({c.head_names[i], c.head_arity[i]});
+    version = sr_weights_version(w);
+  }
+  ModelConfig config;
+  std::string version;
+  const sr_weights* handle() const { return w_.get(); }
+
+ private:
+  std::shared_ptr<sr_weights> w_;
+};
+
+inline ModelWeights init_model(const ModelConfig& cfg, std::uint64_t seed,
+                               sr_init_scheme scheme = SR_INIT_REFERENCE) {  // model.cpp:94-134
+  sr_weights* w = nullptr;
+  cfg.with_c([&](const sr_model_config& c) { check(sr_weights_init(&c, seed, scheme, &w)); });
+  return ModelWeights(w);
+}
+inline ModelWeights load_weights(const std::string& path) {  // weights_io.cpp:137-196
+  sr_weights* w = nullptr;
+  check(sr_weights_load(path.c_str(), &w));
+  return ModelWeights(w);
+}
+inline void save_weights(const ModelWeights& w, const std::string& path) {
+  check(sr_weights_save(w.handle(), path.c_str()));
+}
+
+struct ScoreItem {  // engine.hpp:20-25
+  std::string id;
+  std::vector<int> tokens;
+  std::vector<float> embedding;  // mixed: [n_emb_tokens x d_model]
+  int n_emb_tokens = 0;
+};
+
+struct ScoreRequest {  // engine.hpp:27-33
+  std::string request_id;
+  std::vector<int> prefix_tokens;
+  std::vector<ScoreItem> items;
+  ScoreMode mode = ScoreMode::Ibpc;
+  bool latency_sensitive = false;
+};
+
+struct FlopReport {  // engine.hpp:38-44
+  double attention_units = 0, linear_units = 0, t_q = 0, t_i_mean = 0, n_items = 0;
+};
+
+inline FlopReport flops(ScoreMode mode, long t_q, long t_i, long n_items) {  // engine.cpp:30-47
+  sr_flop_report r{};
+  check(sr_flops(static_cast<int32_t>(mode), t_q, t_i, n_items, &r));
+  return {r.attention_units, r.linear_units, r.t_q, r.t_i_mean, r.n_items};
+}
+
+struct ItemScores {  // engine.hpp:46-49
+  std::string item_id;
+  std::map<std::string, double> tasks;
+};
+
+struct ScoreResult {  // engine.hpp:53-59 (+ topk)
+  std::string request_id;
+  std::vector<ItemScores> items;
+  ScoreMode mode = ScoreMode::Naive;
+  FlopReport flops;
+  double kv_incremental_per_item = 0;
+  std::vector<std::pair<std::string, double>> topk;  // (item id, relevance), best first
+};
+
+inline constexpr const char* kRelevanceTask = "relevance";
+
+class ScoringEngine {  // engine.hpp:109-119
+ public:
+  explicit ScoringEngine(const ModelWeights& weights, int device = 0) : weights_(weights) {
+    sr_engine* e = nullptr;
+    check(sr_engine_create(weights.handle(), device, &e));
+    e_.reset(e);
+  }
+  const ModelWeights& weights() const { return weights_; }
+
+  ScoreResult score(const ScoreRequest& request, int k = 0) {
+    const int d = weights_.config.d_model;
+    const bool mixed = request.mode == ScoreMode::Mixed;
+    std::vector<int32_t> prefix(request.prefix_tokens.begin(), request.prefix_tokens.end());
+    std::vector<int32_t> off{0}, toks;
+    std::vector<float> rows;
+    std::vector<int64_t> ids;
+    bool numeric_ids = true;
+    for (const auto& it : request.items) {
+      if (mixed) {
+        if (it.n_emb_tokens < 1 || it.embedding.size() != static_cast<size_t>(it.n_emb_tokens) * d)
+          throw Error(ErrorCode::PayloadInvalid,
+                      "item " + it.id + " embedding payload is not [n x " + std::to_string(d) + "]");
+        rows.insert(rows.end(), it.embedding.begin(), it.embedding.end());
+        off.push_back(off.back() + it.n_emb_tokens);
+      } else {
+        toks.insert(toks.end(), it.tokens.begin(), it.tokens.end());
+        off.push_back(off.back() + static_cast<int32_t>(it.tokens.size()));
+      }
+      try {
+        size_t pos = 0;
+        ids.push_back(std::stoll(it.id, &pos));
+        numeric_ids = numeric_ids && pos == it.id.size();
+      } catch (...) {
+        numeric_ids = false;
+      }
+    }
+    sr_request req{prefix.data(), static_cast<int32_t>(prefix.size()),
+                   static_cast<int32_t>(request.items.size()), off.data(),
+                   toks.empty() ? nullptr : toks.data(), rows.empty() ? nullptr : rows.data(),
+                   numeric_ids ? ids.data() : nullptr, static_cast<int32_t>(request.mode)};
+    const int T = 1 + static_cast<int>(weights_.config.head_specs.size());
+    std::vector<double> scores(request.items.size() * T);
+    std::vector<int64_t> tid(k > 0 ? k : 1);
+    std::vector<double> tsc(k > 0 ? k : 1);
+    std::vector<int32_t> tix(k > 0 ? k : 1);
+    sr_result res{scores.data(), k, tid.data(), tsc.data(), tix.data(), {}, 0, 0};
+    check(sr_engine_score(e_.get(), &req, &res));
+    ScoreResult out;
+    out.request_id = request.request_id;
+    out.mode = request.mode;
+    out.flops = {res.flops.attention_units, res.flops.linear_units, res.flops.t_q,
+                 res.flops.t_i_mean, res.flops.n_items};
+    out.kv_incremental_per_item = res.kv_incremental_per_item;
+    for (size_t i = 0; i < request.items.size(); ++i) {
+      ItemScores s{request.items[i].id, {}};
+      s.tasks[kRelevanceTask] = scores[i * T];
+      for (int h = 1; h < T; ++h) s.tasks[weights_.config.head_specs[h - 1].name] = scores[i * T + h];
+      out.items.push_back(std::move(s));
+    }
+    for (int j = 0; j < res.k_returned; ++j) out.topk.push_back({request.items[tix[j]].id, tsc[j]});
+    return out;
+  }
+
+ private:
+  struct Del {
+    void operator()(sr_engine* e) const { sr_engine_destroy(e); }
+  };
+  ModelWeights weights_;
+  std::unique_ptr<sr_engine, Del> e_;
+};
+
+inline ScoreResult score_by_mode(ScoringEngine& engine, const ScoreRequest& request) {
+  return engine.score(request);  // engine.cpp:379-387
+}
+
+}  // namespace semrank
