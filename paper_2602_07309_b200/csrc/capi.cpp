@@ -480,8 +480,9 @@ int32_t sr_kernel_attention(const void* qkv, const int32_t* spans_host, int32_t 
     std::vector<srk::RowSpan> spans(M);
     std::memcpy(spans.data(), spans_host, sizeof(srk::RowSpan) * M);
     std::vector<srk::AttnTile> tiles;
-    for (int r0 = 0; r0 < M; r0 += 64) {
-      const int r1 = std::min(M, r0 + 64);
+    const int tr = srk::attention_tile_rows(head_dim);
+    for (int r0 = 0; r0 < M; r0 += tr) {
+      const int r1 = std::min(M, r0 + tr);
       int pb = INT32_MAX, pe = 0, ss = INT32_MAX;
       for (int r = r0; r < r1; ++r) {
         const auto& s = spans[r];
@@ -513,9 +514,18 @@ int32_t sr_kernel_attention(const void* qkv, const int32_t* spans_host, int32_t 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaMemcpy(dsp, spans.data(), sizeof(srk::RowSpan) * M, cudaMemcpyHostToDevice);
     cudaMemcpy(dt, tiles.data(), sizeof(srk::AttnTile) * tiles.size(), cudaMemcpyHostToDevice);
-    cudaError_t err = srk::attention(static_cast<const __nv_bfloat16*>(qkv), dsp, dt,
-                                     static_cast<int>(tiles.size()),
-                                     static_cast<__nv_bfloat16*>(out), M, n_heads, head_dim, s);
+    cudaError_t err;
+    if (head_dim >= 64) {
+      CUtensorMap tm;
+      err = srk::make_tmap_bf16_2d(&tm, qkv, M, 3 * n_heads * head_dim, 128, 64);
+      if (err == cudaSuccess)
+        err = srk::attention_tc(tm, dsp, dt, static_cast<int>(tiles.size()),
+                                static_cast<__nv_bfloat16*>(out), n_heads, head_dim, s);
+    } else {
+      err = srk::attention(static_cast<const __nv_bfloat16*>(qkv), dsp, dt,
+                           static_cast<int>(tiles.size()), static_cast<__nv_bfloat16*>(out), M,
+                           n_heads, head_dim, s);
+    }
     if (err == cudaSuccess) err = cudaStreamSynchronize(s);
     cudaFree(dsp);
     cudaFree(dt);

@@ -160,11 +160,15 @@ void Engine::ensure_workspace(int32_t M) {
   qkv_.cap = rows * 3 * d;
   SR_CUDA_CHECK(cudaMalloc(&h_.ptr, rows * F * sizeof(__nv_bfloat16)));
   h_.cap = rows * F;
-  // Rows past M hold stale data; GEMM tiles read them but never store them.
+  // Rows past M hold stale (always finite) data: GEMM tiles and attention key
+  // blocks may read them, their results are masked or clipped, never stored.
+  SR_CUDA_CHECK(cudaMemset(x_.ptr, 0, rows * d * sizeof(float)));
+  SR_CUDA_CHECK(cudaMemset(qkv_.ptr, 0, rows * 3 * d * sizeof(__nv_bfloat16)));
   SR_CUDA_CHECK(cudaMemset(xn_.ptr, 0, rows * d * sizeof(__nv_bfloat16)));
   SR_CUDA_CHECK(cudaMemset(h_.ptr, 0, rows * F * sizeof(__nv_bfloat16)));
   SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tm_xn_, xn_.ptr, rows, d, 128, 64));
   SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tm_h_, h_.ptr, rows, F, 128, 64));
+  SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tm_qkv_, qkv_.ptr, rows, 3 * d, 128, 64));
   ws_rows_ = rows;
   ++ws_epoch_;
 }
@@ -213,8 +217,12 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
     SR_CUDA_CHECK(srk::gemm_bf16(tm_xn_, L.tm_qkv, M, 3 * d, d, qkv_.ptr, 3 * d, 0, bn_qkv, s));
     E();
     B(PROF_ATTENTION);
-    SR_CUDA_CHECK(srk::attention(qkv_.ptr, p.spans.ptr, p.tiles.ptr,
-                                 static_cast<int>(p.pack.tiles.size()), xn_.ptr, M, H, hd, s));
+    if (hd >= 64)
+      SR_CUDA_CHECK(srk::attention_tc(tm_qkv_, p.spans.ptr, p.tiles.ptr,
+                                      static_cast<int>(p.pack.tiles.size()), xn_.ptr, H, hd, s));
+    else  // toy head sizes (16/32): the 64-row mma.sync kernel
+      SR_CUDA_CHECK(srk::attention(qkv_.ptr, p.spans.ptr, p.tiles.ptr,
+                                   static_cast<int>(p.pack.tiles.size()), xn_.ptr, M, H, hd, s));
     E();
     B(PROF_GEMM_O);
     SR_CUDA_CHECK(srk::gemm_bf16(tm_xn_, L.tm_o, M, d, d, x_.ptr, d, 2, bn_d, s));
@@ -400,7 +408,8 @@ void Engine::score(const sr_request* reqs, int n_req, sr_result* res) {
     for (int32_t l : lens[q]) items += l;
     M += reqs[q].t_q + items;
     N += reqs[q].n_items;
-    tiles += (reqs[q].t_q + 63) / 64 + (items + 63) / 64;
+    const int tr = srk::attention_tile_rows(cfg_.head_dim());
+    tiles += (reqs[q].t_q + tr - 1) / tr + (items + tr - 1) / tr;
     if (reqs[q].mode == SR_MODE_MIXED) soft += items;
     maxseg = std::max(maxseg, reqs[q].n_items);
   }

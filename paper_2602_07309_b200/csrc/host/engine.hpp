@@ -165,7 +165,7 @@ class Engine {
   int32_t ws_rows_ = 0;
   DevBuf<float> x_;
   DevBuf<__nv_bfloat16> xn_, qkv_, h_;
-  CUtensorMap tm_xn_, tm_h_;
+  CUtensorMap tm_xn_, tm_h_, tm_qkv_;
   uint64_t ws_epoch_ = 0;  // bumps when workspace moves (graphs must be re-captured)
   // shape-keyed plan cache for score()
   std::map<std::tuple<int32_t, int32_t, int32_t, int32_t, int32_t, int32_t, int32_t>,

@@ -7,7 +7,6 @@
 namespace srh {
 
 namespace {
-constexpr int kTileRows = 64;  // attention query tile (kernels/attention.cu kBlockM)
 
 sr_flop_report actual_flops(bool amortized, double tq, const std::vector<int32_t>& lens) {
   // engine.cpp:63-88
@@ -158,6 +157,7 @@ void report_for(const ModelConfig& cfg, const sr_request& req, const std::vector
 void pack_requests(const ModelConfig& cfg, const sr_request* reqs, int n_req,
                    const std::vector<std::vector<int32_t>>& lens, PackedBatch& out) {
   const int d = cfg.d_model;
+  const int kTileRows = srk::attention_tile_rows(cfg.head_dim());
   int64_t M = 0, N = 0, R = 0;
   for (int q = 0; q < n_req; ++q) {
     M += reqs[q].t_q;

@@ -1,0 +1,362 @@
+// Segment-masked shared-prefix attention on 5th-generation tensor cores.
+//
+// Same semantics as kernels/attention.cu (reference kernels.cpp:51-95 with the
+// multi-item mask of engine.cpp:147-184): query row r attends keys
+// [prefix_begin, prefix_end) U [span_start, r]; softmax(q.k/sqrt(hd)) V.
+//
+// One CTA = 128 packed query rows x one head; keys stream in blocks of 128
+// over the tile's two ranges (R1 = shared prefix, R2 = own segments).
+//   warp 0     TMA: Q once, K_j (single buffer), V_j (2-stage ring), 128 B swizzle
+//   warp 1     TMEM alloc + single-thread tcgen05.mma issuer:
+//                S_j = Q K_j^T        -> TMEM (double-buffered, 2 x 128 cols)
+//                O  += P_j V_j        -> TMEM (HD cols), V used MN-major
+//   warps 2-9  softmax: two threads per query row (keys 0-63 / 64-127 of a
+//              block); tcgen05.ld of the row slice of S_j, mask (skipped when
+//              the slice is fully visible), pair max exchange in smem,
+//              P_j = ex2(..) as bf16 into a double-buffered swizzled smem tile
+//              (A operand of the PV MMA).
+// Lazy rescaling (as FlashAttention-4): the exponent base m_used only moves
+// when the block max exceeds it by more than 2^8, so O (in TMEM) is rescaled
+// rarely and the softmax of block j+1 normally runs while PV_j executes.
+// Intermediate P <= 2^8 is exact enough in bf16 and the fp32 row sum l uses
+// the same base, so the result is the reference softmax up to rounding.
+#include <cuda_bf16.h>
+
+#include "launch.h"
+#include "ptx.cuh"
+
+namespace srk {
+
+namespace {
+
+constexpr int kTM = 128;     // query rows per tile (UMMA M)
+constexpr int kBK = 128;     // keys per block (UMMA N of S, K of PV)
+constexpr int kHalf = 64;    // keys per softmax thread per block
+constexpr int kBox = 16384;  // 128 rows x 128 B swizzle box
+constexpr int kThreads = 320;
+constexpr int kSoftmaxThreads = 256;
+constexpr float kRescaleLog2 = 8.0f;  // rescale O only when the max grows by > 2^8
+
+template <int HD>
+struct AttnCfg {
+  static constexpr int NB = HD / 64;        // 64-wide boxes per row
+  static constexpr int TILE = NB * kBox;    // Q / K / V tile bytes
+  static constexpr int P_BYTES = 2 * kBox;  // 128 x 128 bf16
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = Q_OFF + TILE;
+  static constexpr int V_OFF = K_OFF + TILE;        // 2 stages
+  static constexpr int P_OFF = V_OFF + 2 * TILE;    // 2 buffers
+  static constexpr int RED_OFF = P_OFF + 2 * P_BYTES;
+  static constexpr int BAR_OFF = RED_OFF + 3 * 2 * 128 * 4;  // slots: parity 0/1, final sum
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int O_COL = 2 * kBK;  // TMEM: S0 [0,128) S1 [128,256) O [256, 256+HD)
+  static constexpr int TMEM_COLS = 512;
+};
+
+__device__ __forceinline__ void block_range(const AttnTile& t, int nb1, int j, int& k0, int& kbeg,
+                                            int& kend) {
+  if (j < nb1) {
+    k0 = t.r1_begin + j * kBK;
+    kbeg = t.r1_begin;
+    kend = t.r1_end;
+  } else {
+    k0 = t.r2_begin + (j - nb1) * kBK;
+    kbeg = t.r2_begin;
+    kend = t.r2_end;
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const RowSpan* __restrict__ spans,
+                   const AttnTile* __restrict__ tiles, __nv_bfloat16* __restrict__ out,
+                   int n_heads) {
+  using C = AttnCfg<HD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // Align inside the shared window without leaving the shared address space.
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sQ = smem + C::Q_OFF;
+  uint8_t* sK = smem + C::K_OFF;
+  uint8_t* sV = smem + C::V_OFF;
+  uint8_t* sP = smem + C::P_OFF;
+  float* red = reinterpret_cast<float*>(smem + C::RED_OFF);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = bars + 2;
+  uint64_t* v_full = bars + 3;   // [2]
+  uint64_t* v_empty = bars + 5;  // [2]
+  uint64_t* s_full = bars + 7;   // [2]
+  uint64_t* s_free = bars + 9;   // [2]
+  uint64_t* p_full = bars + 11;  // [2]
+  uint64_t* pv_done = bars + 13; // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const AttnTile tile = tiles[blockIdx.x];
+  const int h = blockIdx.y;
+  const int d = n_heads * HD;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb1 = (tile.r1_end - tile.r1_begin + kBK - 1) / kBK;
+  const int nb2 = (tile.r2_end - tile.r2_begin + kBK - 1) / kBK;
+  const int nblk = nb1 + nb2;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    mbar_init(q_full, 1);
+    mbar_init(k_full, 1);
+    mbar_init(k_empty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_free[s], kSoftmaxThreads);
+      mbar_init(&p_full[s], kSoftmaxThreads);
+      mbar_init(&pv_done[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, C::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------- TMA
+    if (lane == 0) {
+      const uint64_t keep = policy_evict_last();  // prefix K/V: re-read by every item tile
+      mbar_arrive_expect_tx(q_full, C::TILE);
+      for (int b = 0; b < C::NB; ++b)
+        tma_load_2d(&tm_qkv, q_full, sQ + b * kBox, h * HD + b * 64, tile.q_begin);
+      for (int j = 0; j < nblk; ++j) {
+        int k0, kb, ke;
+        block_range(tile, nb1, j, k0, kb, ke);
+        mbar_wait(k_empty, (j & 1) ^ 1);
+        mbar_arrive_expect_tx(k_full, C::TILE);
+        for (int b = 0; b < C::NB; ++b)
+          tma_load_2d_hint(&tm_qkv, k_full, sK + b * kBox, d + h * HD + b * 64, k0, keep);
+        const int st = j & 1;
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&v_full[st], C::TILE);
+        for (int b = 0; b < C::NB; ++b)
+          tma_load_2d_hint(&tm_qkv, &v_full[st], sV + st * C::TILE + b * kBox,
+                           2 * d + h * HD + b * 64, k0, keep);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(kTM, kBK);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32_bmn(kTM, HD);
+      const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(k_full, j & 1);
+        mbar_wait(&s_free[st], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int s = 0; s < HD / 16; ++s) {
+          const uint32_t off = (s >> 2) * kBox + (s & 3) * 32;
+          umma_bf16(tmem + st * kBK, sw128_kmajor_desc(q_addr + off),
+                    sw128_kmajor_desc(k_addr + off), idesc_s, s > 0 ? 1u : 0u);
+        }
+        umma_commit(k_empty);
+        umma_commit(&s_full[st]);
+      };
+      if (nblk > 0) issue_s(0);
+      for (int j = 0; j < nblk; ++j) {
+        if (j + 1 < nblk) issue_s(j + 1);
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(&p_full[st], ph);
+        mbar_wait(&v_full[st], ph);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sV + st * C::TILE);
+        const uint32_t p_addr = smem_u32(sP + st * C::P_BYTES);
+#pragma unroll
+        for (int s = 0; s < kBK / 16; ++s) {
+          const uint32_t a_off = (s >> 2) * kBox + (s & 3) * 32;
+          umma_bf16(tmem + C::O_COL, sw128_kmajor_desc(p_addr + a_off),
+                    sw128_mnmajor_desc(v_addr + s * 16 * 128, kBox, 1024), idesc_pv,
+                    (j > 0 || s > 0) ? 1u : 0u);
+        }
+        umma_commit(&v_empty[st]);
+        umma_commit(&pv_done[st]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------------------------------------------------- softmax
+    const int quad = warp & 3;         // TMEM lane quadrant of this warp
+    const int half = (warp - 2) >> 2;  // 0: keys 0-63, 1: keys 64-127 of a block
+    const int r = quad * 32 + lane;    // tile row owned by this thread (shared with a partner)
+    const int row = tile.q_begin + r;
+    const bool live = row < tile.q_end;
+    RowSpan sp = {0, 0, 0, 0};
+    if (live) sp = spans[row];
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const float scale_log2 = 1.4426950408889634f * rsqrtf(static_cast<float>(HD));
+    float m_used = -INFINITY;  // exponent base (raw score units), shared by the pair
+    float l = 0.f;             // this thread's partial row sum
+
+    for (int j = 0; j < nblk; ++j) {
+      int k0, kb, ke;
+      block_range(tile, nb1, j, k0, kb, ke);
+      const int sb = j & 1;
+      const int kh = k0 + half * kHalf;  // first key of this thread's slice
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      float s[kHalf];
+#pragma unroll
+      for (int c = 0; c < kHalf / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + sb * kBK + half * kHalf + c * 32, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
+      }
+      tc_fence_before();
+      mbar_arrive(&s_free[sb]);
+
+      // Visible iff in [kb, ke) and in ([pb, pe) U [ss, row]). Fast path when
+      // the whole 64-key slice is visible to every row of the warp.
+      const int a_lo = max(kb, sp.prefix_begin), a_hi = min(ke, sp.prefix_end);
+      const int b_lo = max(kb, sp.span_start), b_hi = min(ke, row + 1);
+      const bool full = live && ((kh >= a_lo && kh + kHalf <= a_hi) ||
+                                 (kh >= b_lo && kh + kHalf <= b_hi));
+      float mx = -INFINITY;
+      if (__all_sync(0xffffffff, full)) {
+#pragma unroll
+        for (int i = 0; i < kHalf; ++i) mx = fmaxf(mx, s[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < kHalf; ++i) {
+          const int key = kh + i;
+          const bool ok = live && ((key >= a_lo && key < a_hi) || (key >= b_lo && key < b_hi));
+          s[i] = ok ? s[i] : -INFINITY;
+          mx = fmaxf(mx, s[i]);
+        }
+      }
+      // pair max exchange (double-buffered by block parity)
+      float* slot = red + (j & 1) * 256;
+      slot[half * 128 + r] = mx;
+      named_bar_sync(1, kSoftmaxThreads);
+      mx = fmaxf(mx, slot[(half ^ 1) * 128 + r]);
+
+      // Move the base only on a large increase (or from -inf).
+      const bool move = mx > m_used && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2);
+      const float m_new = move ? mx : m_used;
+      if (j > 0 && __any_sync(0xffffffff, move)) {
+        // All PV up to j-1 accumulated with the old base: rescale O rows.
+        mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        tc_fence_after();
+        const float corr = move ? ex2_approx((m_used - m_new) * scale_log2) : 1.f;
+        l *= corr;
+#pragma unroll 1
+        for (int c = 0; c < HD / 64; ++c) {
+          uint32_t v[32];
+          const uint32_t a = tmem + lane_off + C::O_COL + half * (HD / 2) + c * 32;
+          tmem_ld_32x32b_x32(a, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+          tmem_st_32x32b_x32(a, v);
+        }
+        tmem_st_wait();
+      }
+      m_used = m_new;
+      const float base = m_used == -INFINITY ? 0.f : m_used * scale_log2;
+      float rs = 0.f;
+#pragma unroll
+      for (int i = 0; i < kHalf; ++i) {
+        s[i] = ex2_approx(fmaf(s[i], scale_log2, -base));
+        rs += s[i];
+      }
+      l += rs;
+      // P buffer sb was last read by PV_{j-2}.
+      if (j >= 2) mbar_wait(&pv_done[sb], ((j - 2) >> 1) & 1);
+      uint8_t* pbuf = sP + sb * C::P_BYTES + half * kBox + r * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float* f = &s[c * 8];
+        const uint4 pk = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                                    pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+        *reinterpret_cast<uint4*>(pbuf + ((c ^ (r & 7)) * 16)) = pk;
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&p_full[sb]);
+    }
+
+    // Row sum = both halves' partial sums (same base sequence).
+    float* fin = red + 2 * 256;
+    fin[half * 128 + r] = l;
+    named_bar_sync(1, kSoftmaxThreads);
+    l += fin[(half ^ 1) * 128 + r];
+
+    // Epilogue: O / l -> bf16 -> out[row, h*HD + half*HD/2 ...]
+    if (nblk > 0) {
+      mbar_wait(&pv_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
+      tc_fence_after();
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < HD / 64; ++c) {
+      uint32_t v[32];
+      const int col = half * (HD / 2) + c * 32;
+      tmem_ld_32x32b_x32(tmem + lane_off + C::O_COL + col, v);
+      tmem_ld_wait();
+      if (live) {
+        uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * d + h * HD + col);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float* f = reinterpret_cast<const float*>(&v[q * 8]);
+          dst[q] = make_uint4(pack_bf16x2(f[0] * inv, f[1] * inv), pack_bf16x2(f[2] * inv, f[3] * inv),
+                              pack_bf16x2(f[4] * inv, f[5] * inv), pack_bf16x2(f[6] * inv, f[7] * inv));
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+template <int HD>
+cudaError_t launch_tc(const CUtensorMap& tm, const RowSpan* spans, const AttnTile* tiles,
+                      int n_tiles, __nv_bfloat16* out, int n_heads, cudaStream_t stream) {
+  using C = AttnCfg<HD>;
+  auto kern = attn_tc_kernel<HD>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  kern<<<dim3(n_tiles, n_heads), kThreads, C::SMEM, stream>>>(tm, spans, tiles, out, n_heads);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int attention_tile_rows(int head_dim) { return head_dim >= 64 ? kTM : 64; }
+
+cudaError_t attention_tc(const CUtensorMap& tm_qkv, const RowSpan* spans, const AttnTile* tiles,
+                         int n_tiles, __nv_bfloat16* out, int n_heads, int head_dim,
+                         cudaStream_t stream) {
+  if (n_tiles <= 0) return cudaSuccess;
+  switch (head_dim) {
+    case 64: return launch_tc<64>(tm_qkv, spans, tiles, n_tiles, out, n_heads, stream);
+    case 128: return launch_tc<128>(tm_qkv, spans, tiles, n_tiles, out, n_heads, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace srk

@@ -25,6 +25,25 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
+// Output map for the epilogue's TMA store / add-reduce: [M x N] with row
+// pitch ldo, 32-row x 128-byte boxes, 128 B swizzle (matches the staging
+// layout written by the epilogue warps). Rows >= M are clipped by TMA.
+template <int EPI>
+cudaError_t make_out_map(CUtensorMap* map, void* out, int M, int N, int ldo) {
+  auto fn = get_encode_fn();
+  if (fn == nullptr) return cudaErrorNotSupported;
+  constexpr bool f32 = EpiOut<EPI>::F32;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldo) * (f32 ? 4 : 2)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(EpiOut<EPI>::CW), 32};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int BN, int EPI>
 cudaError_t launch_one(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
                        void* out, int ldo, cudaStream_t stream) {
@@ -42,7 +61,10 @@ cudaError_t launch_one(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, in
   const int tiles = ((M + C::BM - 1) / C::BM) * (N / BN);
   const int grid = tiles < num_sms(dev) ? tiles : num_sms(dev);
   if (grid <= 0) return cudaSuccess;
-  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(tmA, tmB, M, N, K, out, ldo);
+  CUtensorMap tmC;
+  cudaError_t e = make_out_map<EPI>(&tmC, out, M, N, ldo);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(tmA, tmB, tmC, M, N, K);
   return cudaGetLastError();
 }
 

@@ -10,10 +10,14 @@
 //   EPI_RESID_F32 x += acc, fp32 residual stream (model.cpp:199-202, 210-213)
 //   EPI_F32       plain fp32 store (tests)
 //
-// Roles (192 threads, one CTA per SM, persistent over output tiles):
+// Roles (320 threads, one CTA per SM, persistent over output tiles):
 //   warp 0      TMA producer: A/B k-blocks into a STAGES-deep smem ring
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused op -> HBM
+//   warps 2..9  epilogue, two warps per TMEM lane quadrant (column halves):
+//               tcgen05.ld -> registers -> fused op -> 32-row x 128 B chunk in
+//               a swizzled smem staging buffer -> TMA bulk store, or for the
+//               residual a TMA bulk add-reduction (the L2 performs x += acc in
+//               fp32, so the SM never reads x and every access is a full line).
 // The accumulator is double-buffered in TMEM (2 x BN fp32 columns) so the
 // epilogue of tile i overlaps the main loop of tile i+1.
 #pragma once
@@ -33,22 +37,31 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
   static constexpr int TMEM_COLS = 2 * BN;  // power of two for BN in {64,128,256}
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 1024;
-  static constexpr int THREADS = 192;
+  static constexpr int EPI_WARPS = 8;       // two per TMEM lane quadrant (column halves)
+  static constexpr int STG_BYTES = 32 * 128;  // per epilogue warp: 32 rows x 128 B
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_WARPS * STG_BYTES + 256 + 1024;
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+};
+
+// Output tensor map box for an epilogue: 32 rows x 128 B (32 fp32 or 64 bf16).
+template <int EPI>
+struct EpiOut {
+  static constexpr bool F32 = (EPI == EPI_RESID_F32 || EPI == EPI_F32);
+  static constexpr int CW = F32 ? 32 : 64;  // columns per staged chunk
 };
 
 template <int BN, int EPI>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     gemm_bf16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA,
-                             const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-                             void* __restrict__ out, int ldo) {
+                             const __grid_constant__ CUtensorMap tmB,
+                             const __grid_constant__ CUtensorMap tmC, int M, int N, int K) {
   using C = GemmCfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint8_t* sStg = sB + C::STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + C::EPI_WARPS * C::STG_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -64,13 +77,14 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 32 * C::EPI_WARPS);
     }
     fence_barrier_init();
   }
@@ -139,63 +153,75 @@ __global__ void __launch_bounds__(192, 1)
     }
     __syncwarp();
   } else {
-    // Epilogue: warp w may only touch TMEM lanes [32*(w%4), 32*(w%4)+32).
+    // Epilogue: warp w may only touch TMEM lanes [32*(w%4), 32*(w%4)+32);
+    // the two warps of a quadrant split the tile's columns.
+    constexpr int CW = EpiOut<EPI>::CW;
+    constexpr int SPAN = (BN / 2 > CW) ? BN / 2 : CW;  // columns per warp
     const int quad = warp & 3;
+    const int col0 = ((warp - 2) >> 2) * SPAN;
+    uint8_t* stg = sStg + (warp - 2) * C::STG_BYTES;
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       const int m0 = (tile / n_tiles) * C::BM;
       const int n0 = (tile % n_tiles) * BN;
+      const int r0 = m0 + quad * 32;  // first row of this warp's 32-row slab
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m0 + quad * 32 + lane;
-      const bool live = row < M;
+      if (col0 < BN && r0 < M) {
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c,
-                           r);
-        tmem_ld_wait();
-        if (!live) continue;
-        const size_t off = static_cast<size_t>(row) * ldo + n0 + c;
-        if constexpr (EPI == EPI_BF16 || EPI == EPI_GELU_BF16) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + off);
+        for (int c = col0; c < col0 + SPAN; c += CW) {
+          // the staging buffer is free once the previous bulk op read it
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+          uint8_t* row_base = stg + lane * 128;
+          if constexpr (EpiOut<EPI>::F32) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c,
+                               r);
+            tmem_ld_wait();
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            float f[8];
+            for (int k = 0; k < 8; ++k)
+              *reinterpret_cast<uint4*>(row_base + ((k ^ (lane & 7)) * 16)) =
+                  make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+          } else {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              f[j] = __uint_as_float(r[v * 8 + j]);
-              if constexpr (EPI == EPI_GELU_BF16) f[j] = gelu_erf(f[j]);
+            for (int hh = 0; hh < 2; ++hh) {
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(
+                  tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c + hh * 32, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                float f[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  f[j] = __uint_as_float(r[8 * k + j]);
+                  if constexpr (EPI == EPI_GELU_BF16) f[j] = gelu_erf(f[j]);
+                }
+                const int chunk = hh * 4 + k;
+                *reinterpret_cast<uint4*>(row_base + ((chunk ^ (lane & 7)) * 16)) =
+                    make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                               pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+              }
             }
-            dst[v] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
-                                pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
           }
-        } else if constexpr (EPI == EPI_RESID_F32) {
-          float4* x = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + off);
-          float4 cur[8];
-#pragma unroll
-          for (int v = 0; v < 8; ++v) cur[v] = x[v];
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            cur[v].x += __uint_as_float(r[v * 4 + 0]);
-            cur[v].y += __uint_as_float(r[v * 4 + 1]);
-            cur[v].z += __uint_as_float(r[v * 4 + 2]);
-            cur[v].w += __uint_as_float(r[v * 4 + 3]);
-            x[v] = cur[v];
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (EPI == EPI_RESID_F32)
+              tma_reduce_add_2d(&tmC, stg, n0 + c, r0);
+            else
+              tma_store_2d(&tmC, stg, n0 + c, r0);
+            bulk_commit();
           }
-        } else {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + off);
-#pragma unroll
-          for (int v = 0; v < 8; ++v)
-            dst[v] = make_float4(__uint_as_float(r[v * 4 + 0]), __uint_as_float(r[v * 4 + 1]),
-                                 __uint_as_float(r[v * 4 + 2]), __uint_as_float(r[v * 4 + 3]));
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) bulk_wait0();
   }
 
   tc_fence_before();

@@ -52,6 +52,13 @@ cudaError_t layer_norm_bf16(const float* x, const float* gain, __nv_bfloat16* ou
 cudaError_t attention(const __nv_bfloat16* qkv, const RowSpan* spans, const AttnTile* tiles,
                       int n_tiles, __nv_bfloat16* out, int M, int n_heads, int head_dim,
                       cudaStream_t stream);
+// tcgen05/TMEM path for head_dim in {64, 128}; tm_qkv maps the [rows x 3d]
+// bf16 qkv buffer with 64 x 128 boxes (make_tmap_bf16_2d(.., 128, 64)).
+cudaError_t attention_tc(const CUtensorMap& tm_qkv, const RowSpan* spans, const AttnTile* tiles,
+                         int n_tiles, __nv_bfloat16* out, int n_heads, int head_dim,
+                         cudaStream_t stream);
+// Query rows per attention tile for a head size (128 on the tcgen05 path).
+int attention_tile_rows(int head_dim);
 
 // -------------------------------------------------------- score head/topk
 // Final LN on the last-token rows + task-column dot products + probabilities.
