@@ -243,6 +243,9 @@ int32_t sr_kernel_attention(const void* qkv, const int32_t* spans_host, int32_t 
                             int32_t n_heads, int32_t head_dim, void* out, void* stream);
 int32_t sr_kernel_layernorm(const float* x, const float* gain, void* out_bf16, int32_t M,
                             int32_t d, void* stream);
+/* Tuning aid: record a clock64 timeline (64 slots per CTA, first 256 tiles of
+ * head 0) from the tcgen05 attention kernel into dev_buf; NULL disables. */
+int32_t sr_debug_attention_trace(void* dev_buf);
 int32_t sr_kernel_topk(const double* scores, const int64_t* ids, int32_t n, int32_t k,
                        int64_t* ids_out_host, double* scores_out_host, int32_t* index_out_host);
 

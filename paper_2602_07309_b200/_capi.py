@@ -100,6 +100,7 @@ _sig("sr_plan_run_sharded", i32, vp, vp)
 _sig("sr_kernel_gemm", i32, vp, vp, i32, i32, i32, vp, i32, i32, vp)
 _sig("sr_kernel_attention", i32, vp, P(i32), i32, i32, i32, vp, vp)
 _sig("sr_kernel_layernorm", i32, vp, vp, vp, i32, i32, vp)
+_sig("sr_debug_attention_trace", i32, vp)
 _sig("sr_kernel_topk", i32, vp, vp, i32, i32, P(i64), P(f64), P(i32))
 
 # Every symbol the header declares (tests check the library exports them).
@@ -116,5 +117,5 @@ HEADER_SYMBOLS = [
     "sr_plan_profile", "sr_plan_shape",
     "sr_nccl_unique_id", "sr_comm_create", "sr_comm_destroy", "sr_engine_score_sharded",
     "sr_plan_run_sharded", "sr_kernel_gemm", "sr_kernel_attention", "sr_kernel_layernorm",
-    "sr_kernel_topk",
+    "sr_kernel_topk", "sr_debug_attention_trace",
 ]

@@ -542,6 +542,12 @@ int32_t sr_kernel_layernorm(const float* x, const float* gain, void* out_bf16, i
   });
 }
 
+int32_t sr_debug_attention_trace(void* dev_buf) {
+  return guard([&] {
+    SR_CUDA_CHECK(srk::attention_set_trace(static_cast<unsigned long long*>(dev_buf)));
+  });
+}
+
 int32_t sr_kernel_topk(const double* scores, const int64_t* ids, int32_t n, int32_t k,
                        int64_t* ids_out_host, double* scores_out_host, int32_t* index_out_host) {
   return guard([&] {

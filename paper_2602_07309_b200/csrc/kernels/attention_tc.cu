@@ -6,20 +6,19 @@
 //
 // One CTA = 128 packed query rows x one head; keys stream in blocks of 128
 // over the tile's two ranges (R1 = shared prefix, R2 = own segments).
-//   warp 0     TMA: Q once, K_j (single buffer), V_j (2-stage ring), 128 B swizzle
+//   warp 0     TMA: Q once, K_j and V_j into 2-stage rings (128 B swizzle)
 //   warp 1     TMEM alloc + single-thread tcgen05.mma issuer:
-//                S_j = Q K_j^T        -> TMEM (double-buffered, 2 x 128 cols)
-//                O  += P_j V_j        -> TMEM (HD cols), V used MN-major
+//                S_j = Q K_j^T   SS-MMA -> TMEM S buffer (j & 1), 128 fp32 cols
+//                O  += P_j V_j   TS-MMA: P_j read from TMEM (bf16, aliased on the
+//                                consumed S_j buffer), V_j from smem MN-major
 //   warps 2-9  softmax: two threads per query row (keys 0-63 / 64-127 of a
 //              block); tcgen05.ld of the row slice of S_j, mask (skipped when
 //              the slice is fully visible), pair max exchange in smem,
-//              P_j = ex2(..) as bf16 into a double-buffered swizzled smem tile
-//              (A operand of the PV MMA).
-// Lazy rescaling (as FlashAttention-4): the exponent base m_used only moves
-// when the block max exceeds it by more than 2^8, so O (in TMEM) is rescaled
-// rarely and the softmax of block j+1 normally runs while PV_j executes.
-// Intermediate P <= 2^8 is exact enough in bf16 and the fp32 row sum l uses
-// the same base, so the result is the reference softmax up to rounding.
+//              P_j = ex2(..) packed bf16x2, tcgen05.st back into TMEM.
+// Lazy rescaling (as FlashAttention-4): the exponent base only moves when the
+// block max exceeds it by more than 2^8, so O (in TMEM) is rescaled rarely and
+// the softmax of block j+1 runs while PV_j and S_{j+2} execute. P <= 2^8 is
+// exact enough in bf16 and the fp32 row sum uses the same base.
 #include <cuda_bf16.h>
 
 #include "launch.h"
@@ -39,19 +38,26 @@ constexpr float kRescaleLog2 = 8.0f;  // rescale O only when the max grows by > 
 
 template <int HD>
 struct AttnCfg {
-  static constexpr int NB = HD / 64;        // 64-wide boxes per row
-  static constexpr int TILE = NB * kBox;    // Q / K / V tile bytes
-  static constexpr int P_BYTES = 2 * kBox;  // 128 x 128 bf16
+  static constexpr int NB = HD / 64;      // 64-wide boxes per row
+  static constexpr int TILE = NB * kBox;  // Q / K / V tile bytes
   static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = Q_OFF + TILE;
-  static constexpr int V_OFF = K_OFF + TILE;        // 2 stages
-  static constexpr int P_OFF = V_OFF + 2 * TILE;    // 2 buffers
-  static constexpr int RED_OFF = P_OFF + 2 * P_BYTES;
+  static constexpr int K_OFF = Q_OFF + TILE;      // 2 stages
+  static constexpr int V_OFF = K_OFF + 2 * TILE;  // 2 stages
+  static constexpr int RED_OFF = V_OFF + 2 * TILE;
   static constexpr int BAR_OFF = RED_OFF + 3 * 2 * 128 * 4;  // slots: parity 0/1, final sum
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static constexpr int O_COL = 2 * kBK;  // TMEM: S0 [0,128) S1 [128,256) O [256, 256+HD)
   static constexpr int TMEM_COLS = 512;
 };
+
+// Optional per-CTA timeline (clock64 stamps, 64 slots per CTA, first 256
+// tiles of head 0); enabled by attention_set_trace() for kernel tuning only.
+__device__ unsigned long long* g_attn_trace = nullptr;
+#define SRK_TRACE(slot)                                                          \
+  do {                                                                          \
+    if (g_attn_trace != nullptr && blockIdx.y == 0 && blockIdx.x < 256)         \
+      g_attn_trace[blockIdx.x * 64 + (slot)] = static_cast<unsigned long long>(clock64()); \
+  } while (0)
 
 __device__ __forceinline__ void block_range(const AttnTile& t, int nb1, int j, int& k0, int& kbeg,
                                             int& kend) {
@@ -78,20 +84,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sQ = smem + C::Q_OFF;
   uint8_t* sK = smem + C::K_OFF;
   uint8_t* sV = smem + C::V_OFF;
-  uint8_t* sP = smem + C::P_OFF;
   float* red = reinterpret_cast<float*>(smem + C::RED_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;
-  uint64_t* k_empty = bars + 2;
-  uint64_t* v_full = bars + 3;   // [2]
-  uint64_t* v_empty = bars + 5;  // [2]
-  uint64_t* s_full = bars + 7;   // [2]
-  uint64_t* s_free = bars + 9;   // [2]
-  uint64_t* p_full = bars + 11;  // [2]
-  uint64_t* pv_done = bars + 13; // [2]
+  uint64_t* k_full = bars + 1;    // [2]
+  uint64_t* k_empty = bars + 3;   // [2]
+  uint64_t* v_full = bars + 5;    // [2]
+  uint64_t* v_empty = bars + 7;   // [2]
+  uint64_t* s_full = bars + 9;    // [2]
+  uint64_t* p_full = bars + 11;   // [2]
+  uint64_t* pv_done = bars + 13;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
+  if (threadIdx.x == 0) SRK_TRACE(0);
   const AttnTile tile = tiles[blockIdx.x];
   const int h = blockIdx.y;
   const int d = n_heads * HD;
@@ -103,13 +108,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
     mbar_init(q_full, 1);
-    mbar_init(k_full, 1);
-    mbar_init(k_empty, 1);
     for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&s_free[s], kSoftmaxThreads);
       mbar_init(&p_full[s], kSoftmaxThreads);
       mbar_init(&pv_done[s], 1);
     }
@@ -123,6 +127,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) {
+    SRK_TRACE(1);
+    if (g_attn_trace != nullptr && blockIdx.y == 0 && blockIdx.x < 256) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_attn_trace[blockIdx.x * 64 + 30] = nblk;
+      g_attn_trace[blockIdx.x * 64 + 31] = smid;
+    }
+  }
 
   if (warp == 0) {
     // ------------------------------------------------------------- TMA
@@ -134,12 +147,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < nblk; ++j) {
         int k0, kb, ke;
         block_range(tile, nb1, j, k0, kb, ke);
-        mbar_wait(k_empty, (j & 1) ^ 1);
-        mbar_arrive_expect_tx(k_full, C::TILE);
-        for (int b = 0; b < C::NB; ++b)
-          tma_load_2d_hint(&tm_qkv, k_full, sK + b * kBox, d + h * HD + b * 64, k0, keep);
         const int st = j & 1;
-        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        const uint32_t ph = ((j >> 1) & 1) ^ 1;
+        mbar_wait(&k_empty[st], ph);
+        mbar_arrive_expect_tx(&k_full[st], C::TILE);
+        for (int b = 0; b < C::NB; ++b)
+          tma_load_2d_hint(&tm_qkv, &k_full[st], sK + st * C::TILE + b * kBox,
+                           d + h * HD + b * 64, k0, keep);
+        mbar_wait(&v_empty[st], ph);
         mbar_arrive_expect_tx(&v_full[st], C::TILE);
         for (int b = 0; b < C::NB; ++b)
           tma_load_2d_hint(&tm_qkv, &v_full[st], sV + st * C::TILE + b * kBox,
@@ -152,41 +167,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(kTM, kBK);
       constexpr uint32_t idesc_pv = idesc_bf16_f32_bmn(kTM, HD);
-      const uint32_t q_addr = smem_u32(sQ), k_addr = smem_u32(sK);
+      const uint32_t q_addr = smem_u32(sQ);
       mbar_wait(q_full, 0);
+      SRK_TRACE(2);
       auto issue_s = [&](int j) {
         const int st = j & 1;
-        mbar_wait(k_full, j & 1);
-        mbar_wait(&s_free[st], ((j >> 1) & 1) ^ 1);
+        mbar_wait(&k_full[st], (j >> 1) & 1);
         tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + st * C::TILE);
 #pragma unroll
         for (int s = 0; s < HD / 16; ++s) {
           const uint32_t off = (s >> 2) * kBox + (s & 3) * 32;
           umma_bf16(tmem + st * kBK, sw128_kmajor_desc(q_addr + off),
                     sw128_kmajor_desc(k_addr + off), idesc_s, s > 0 ? 1u : 0u);
         }
-        umma_commit(k_empty);
+        umma_commit(&k_empty[st]);
         umma_commit(&s_full[st]);
       };
       if (nblk > 0) issue_s(0);
+      if (nblk > 1) issue_s(1);
       for (int j = 0; j < nblk; ++j) {
-        if (j + 1 < nblk) issue_s(j + 1);
         const int st = j & 1;
         const uint32_t ph = (j >> 1) & 1;
         mbar_wait(&p_full[st], ph);
+        if (j < 8) SRK_TRACE(3 + j);
         mbar_wait(&v_full[st], ph);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sV + st * C::TILE);
-        const uint32_t p_addr = smem_u32(sP + st * C::P_BYTES);
 #pragma unroll
         for (int s = 0; s < kBK / 16; ++s) {
-          const uint32_t a_off = (s >> 2) * kBox + (s & 3) * 32;
-          umma_bf16(tmem + C::O_COL, sw128_kmajor_desc(p_addr + a_off),
-                    sw128_mnmajor_desc(v_addr + s * 16 * 128, kBox, 1024), idesc_pv,
-                    (j > 0 || s > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + C::O_COL, tmem + st * kBK + s * 8,
+                       sw128_mnmajor_desc(v_addr + s * 16 * 128, kBox, 1024), idesc_pv,
+                       (j > 0 || s > 0) ? 1u : 0u);
         }
         umma_commit(&v_empty[st]);
         umma_commit(&pv_done[st]);
+        if (j + 2 < nblk) {
+          // S_{j+2} reuses this TMEM buffer: PV_j must have read P_j first.
+          mbar_wait(&pv_done[st], ph);
+          issue_s(j + 2);
+        }
       }
     }
     __syncwarp();
@@ -210,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int sb = j & 1;
       const int kh = k0 + half * kHalf;  // first key of this thread's slice
       mbar_wait(&s_full[sb], (j >> 1) & 1);
+      if (warp == 2 && lane == 0 && j < 8) SRK_TRACE(11 + j);
       tc_fence_after();
       float s[kHalf];
 #pragma unroll
@@ -220,8 +241,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
       }
-      tc_fence_before();
-      mbar_arrive(&s_free[sb]);
 
       // Visible iff in [kb, ke) and in ([pb, pe) U [ss, row]). Fast path when
       // the whole 64-key slice is visible to every row of the warp.
@@ -234,22 +253,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < kHalf; ++i) mx = fmaxf(mx, s[i]);
       } else {
+        // Visible keys of the slice as a 64-bit mask (two clipped intervals).
+        auto ivl = [&](int lo, int hi) -> uint64_t {
+          lo = max(lo - kh, 0);
+          hi = min(hi - kh, kHalf);
+          if (!live || hi <= lo) return 0ull;
+          const uint64_t upto_hi = hi >= 64 ? ~0ull : ((1ull << hi) - 1ull);
+          return upto_hi & ~((1ull << lo) - 1ull);
+        };
+        const uint64_t vis = ivl(a_lo, a_hi) | ivl(b_lo, b_hi);
+        const uint32_t v0 = static_cast<uint32_t>(vis), v1 = static_cast<uint32_t>(vis >> 32);
 #pragma unroll
         for (int i = 0; i < kHalf; ++i) {
-          const int key = kh + i;
-          const bool ok = live && ((key >= a_lo && key < a_hi) || (key >= b_lo && key < b_hi));
+          const bool ok = ((i < 32 ? v0 : v1) >> (i & 31)) & 1u;
           s[i] = ok ? s[i] : -INFINITY;
           mx = fmaxf(mx, s[i]);
         }
       }
-      // pair max exchange (double-buffered by block parity)
+      // Pair max exchange (double-buffered by block parity). The barrier also
+      // orders both halves' S reads before either writes P over S.
       float* slot = red + (j & 1) * 256;
       slot[half * 128 + r] = mx;
       named_bar_sync(1, kSoftmaxThreads);
       mx = fmaxf(mx, slot[(half ^ 1) * 128 + r]);
 
       // Move the base only on a large increase (or from -inf).
-      const bool move = mx > m_used && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2);
+      const bool move =
+          mx > m_used && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2);
       const float m_new = move ? mx : m_used;
       if (j > 0 && __any_sync(0xffffffff, move)) {
         // All PV up to j-1 accumulated with the old base: rescale O rows.
@@ -267,30 +297,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
           tmem_st_32x32b_x32(a, v);
         }
-        tmem_st_wait();
       }
       m_used = m_new;
       const float base = m_used == -INFINITY ? 0.f : m_used * scale_log2;
       float rs = 0.f;
+      uint32_t pk[32];
 #pragma unroll
-      for (int i = 0; i < kHalf; ++i) {
-        s[i] = ex2_approx(fmaf(s[i], scale_log2, -base));
-        rs += s[i];
+      for (int i = 0; i < kHalf; i += 2) {
+        const float p0 = ex2_approx(fmaf(s[i], scale_log2, -base));
+        const float p1 = ex2_approx(fmaf(s[i + 1], scale_log2, -base));
+        rs += p0 + p1;
+        pk[i >> 1] = pack_bf16x2(p0, p1);
       }
       l += rs;
-      // P buffer sb was last read by PV_{j-2}.
-      if (j >= 2) mbar_wait(&pv_done[sb], ((j - 2) >> 1) & 1);
-      uint8_t* pbuf = sP + sb * C::P_BYTES + half * kBox + r * 128;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float* f = &s[c * 8];
-        const uint4 pk = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
-                                    pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
-        *reinterpret_cast<uint4*>(pbuf + ((c ^ (r & 7)) * 16)) = pk;
-      }
-      fence_proxy_async_smem();
+      // P_j (bf16x2) over this half's 32 columns of the consumed S_j buffer.
+      tmem_st_32x32b_x32(tmem + lane_off + sb * kBK + half * 32, pk);
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[sb]);
+      if (warp == 2 && lane == 0 && j < 8) SRK_TRACE(19 + j);
     }
 
     // Row sum = both halves' partial sums (same base sequence).
@@ -304,6 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&pv_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
       tc_fence_after();
     }
+    if (warp == 2 && lane == 0) SRK_TRACE(27);
     const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll 1
     for (int c = 0; c < HD / 64; ++c) {
@@ -327,6 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+  if (threadIdx.x == 0) SRK_TRACE(29);
 }
 
 template <int HD>
@@ -345,6 +372,10 @@ cudaError_t launch_tc(const CUtensorMap& tm, const RowSpan* spans, const AttnTil
 }
 
 }  // namespace
+
+cudaError_t attention_set_trace(unsigned long long* dev_buf) {
+  return cudaMemcpyToSymbol(g_attn_trace, &dev_buf, sizeof(dev_buf));
+}
 
 int attention_tile_rows(int head_dim) { return head_dim >= 64 ? kTM : 64; }
 

@@ -57,6 +57,8 @@ cudaError_t attention(const __nv_bfloat16* qkv, const RowSpan* spans, const Attn
 cudaError_t attention_tc(const CUtensorMap& tm_qkv, const RowSpan* spans, const AttnTile* tiles,
                          int n_tiles, __nv_bfloat16* out, int n_heads, int head_dim,
                          cudaStream_t stream);
+// Tuning aid: per-CTA clock64 timeline of attention_tc (nullptr disables).
+cudaError_t attention_set_trace(unsigned long long* dev_buf);
 // Query rows per attention tile for a head size (128 on the tcgen05 path).
 int attention_tile_rows(int head_dim);
 
