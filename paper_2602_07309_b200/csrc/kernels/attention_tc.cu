@@ -4,21 +4,27 @@
 // multi-item mask of engine.cpp:147-184): query row r attends keys
 // [prefix_begin, prefix_end) U [span_start, r]; softmax(q.k/sqrt(hd)) V.
 //
-// One CTA = 128 packed query rows x one head; keys stream in blocks of 128
-// over the tile's two ranges (R1 = shared prefix, R2 = own segments).
-//   warp 0     TMA: Q once, K_j and V_j into 2-stage rings (128 B swizzle)
+// Persistent: one CTA per SM walks work items (128-row query tile x head);
+// keys stream in blocks of 128 over each tile's two ranges (R1 = shared
+// prefix, R2 = own segments). The block sequence is continuous across items,
+// so the Q load and the O epilogue of one item overlap the next item's MMAs.
+//   warp 0     TMA: Q (2 buffers, one per item parity), K_j / V_j 2-stage rings
 //   warp 1     TMEM alloc + single-thread tcgen05.mma issuer:
 //                S_j = Q K_j^T   SS-MMA -> TMEM S buffer (j & 1), 128 fp32 cols
-//                O  += P_j V_j   TS-MMA: P_j read from TMEM (bf16, aliased on the
-//                                consumed S_j buffer), V_j from smem MN-major
+//                O  += P_j V_j   TS-MMA: P_j from TMEM (bf16, aliased on the
+//                                consumed S_j buffer), V_j from smem MN-major;
+//                                O double-buffered by item parity
 //   warps 2-9  softmax: two threads per query row (keys 0-63 / 64-127 of a
-//              block); tcgen05.ld of the row slice of S_j, mask (skipped when
-//              the slice is fully visible), pair max exchange in smem,
-//              P_j = ex2(..) packed bf16x2, tcgen05.st back into TMEM.
+//              block): tcgen05.ld of the row slice, visibility bitmask (skipped
+//              when the slice is fully visible), pair max exchange in smem,
+//              P = ex2(..) as packed bf16x2 via tcgen05.st; per item epilogue
+//              O / l -> bf16 -> HBM.
 // Lazy rescaling (as FlashAttention-4): the exponent base only moves when the
-// block max exceeds it by more than 2^8, so O (in TMEM) is rescaled rarely and
-// the softmax of block j+1 runs while PV_j and S_{j+2} execute. P <= 2^8 is
-// exact enough in bf16 and the fp32 row sum uses the same base.
+// block max exceeds it by more than 2^8, so O is rescaled rarely and softmax
+// of block j+1 overlaps PV_j and S_{j+2}. P <= 2^8 is exact enough in bf16 and
+// the fp32 row sum uses the same base.
+//
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+HD) O1 [384,384+HD).
 #include <cuda_bf16.h>
 
 #include "launch.h"
@@ -40,42 +46,76 @@ template <int HD>
 struct AttnCfg {
   static constexpr int NB = HD / 64;      // 64-wide boxes per row
   static constexpr int TILE = NB * kBox;  // Q / K / V tile bytes
-  static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = Q_OFF + TILE;      // 2 stages
+  static constexpr int Q_OFF = 0;                 // 2 buffers
+  static constexpr int K_OFF = Q_OFF + 2 * TILE;  // 2 stages
   static constexpr int V_OFF = K_OFF + 2 * TILE;  // 2 stages
   static constexpr int RED_OFF = V_OFF + 2 * TILE;
   static constexpr int BAR_OFF = RED_OFF + 3 * 2 * 128 * 4;  // slots: parity 0/1, final sum
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
-  static constexpr int O_COL = 2 * kBK;  // TMEM: S0 [0,128) S1 [128,256) O [256, 256+HD)
+  static constexpr int O_COL = 2 * kBK;  // O buffer b at O_COL + b * 128
   static constexpr int TMEM_COLS = 512;
 };
 
 // Optional per-CTA timeline (clock64 stamps, 64 slots per CTA, first 256
-// tiles of head 0); enabled by attention_set_trace() for kernel tuning only.
+// CTAs); enabled by attention_set_trace() for kernel tuning only.
 __device__ unsigned long long* g_attn_trace = nullptr;
-#define SRK_TRACE(slot)                                                          \
-  do {                                                                          \
-    if (g_attn_trace != nullptr && blockIdx.y == 0 && blockIdx.x < 256)         \
+#define SRK_TRACE(slot)                                                                     \
+  do {                                                                                      \
+    if (g_attn_trace != nullptr && blockIdx.x < 256)                                        \
       g_attn_trace[blockIdx.x * 64 + (slot)] = static_cast<unsigned long long>(clock64()); \
   } while (0)
 
-__device__ __forceinline__ void block_range(const AttnTile& t, int nb1, int j, int& k0, int& kbeg,
-                                            int& kend) {
-  if (j < nb1) {
-    k0 = t.r1_begin + j * kBK;
-    kbeg = t.r1_begin;
-    kend = t.r1_end;
-  } else {
-    k0 = t.r2_begin + (j - nb1) * kBK;
-    kbeg = t.r2_begin;
-    kend = t.r2_end;
+// Walks the (item, block) sequence of one CTA.
+struct Cursor {
+  int li = -1;      // local item counter
+  int item = 0;     // global work-item index
+  int j = 0, nblk = 0, nb1 = 0;
+  AttnTile t;
+  int h = 0;
+  bool valid = false;
+
+  __device__ void load_item(const AttnTile* tiles, int n_tiles, int n_items, int item_) {
+    item = item_;
+    valid = item < n_items;
+    if (!valid) return;
+    t = tiles[item % n_tiles];
+    h = item / n_tiles;
+    nb1 = (t.r1_end - t.r1_begin + kBK - 1) / kBK;
+    nblk = nb1 + (t.r2_end - t.r2_begin + kBK - 1) / kBK;
+    j = 0;
   }
-}
+  // First item with at least one block at or after `item_`.
+  __device__ void next_item(const AttnTile* tiles, int n_tiles, int n_items, int item_) {
+    do {
+      ++li;
+      load_item(tiles, n_tiles, n_items, item_);
+      item_ += gridDim.x;
+    } while (valid && nblk == 0);
+  }
+  __device__ void range(int& k0, int& kbeg, int& kend) const {
+    if (j < nb1) {
+      k0 = t.r1_begin + j * kBK;
+      kbeg = t.r1_begin;
+      kend = t.r1_end;
+    } else {
+      k0 = t.r2_begin + (j - nb1) * kBK;
+      kbeg = t.r2_begin;
+      kend = t.r2_end;
+    }
+  }
+  // Advance one block; returns true when a new item started.
+  __device__ bool advance(const AttnTile* tiles, int n_tiles, int n_items) {
+    if (++j < nblk) return false;
+    next_item(tiles, n_tiles, n_items, item + gridDim.x);
+    return true;
+  }
+};
 
 template <int HD>
 __global__ void __launch_bounds__(kThreads, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const RowSpan* __restrict__ spans,
-                   const AttnTile* __restrict__ tiles, __nv_bfloat16* __restrict__ out,
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                   const __grid_constant__ CUtensorMap tm_out, const RowSpan* __restrict__ spans,
+                   const AttnTile* __restrict__ tiles, int n_tiles, __nv_bfloat16* __restrict__ out,
                    int n_heads) {
   using C = AttnCfg<HD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -86,29 +126,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sV = smem + C::V_OFF;
   float* red = reinterpret_cast<float*>(smem + C::RED_OFF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;    // [2]
-  uint64_t* k_empty = bars + 3;   // [2]
-  uint64_t* v_full = bars + 5;    // [2]
-  uint64_t* v_empty = bars + 7;   // [2]
-  uint64_t* s_full = bars + 9;    // [2]
-  uint64_t* p_full = bars + 11;   // [2]
-  uint64_t* pv_done = bars + 13;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* q_full = bars + 0;    // [2] by item parity
+  uint64_t* q_empty = bars + 2;   // [2]
+  uint64_t* k_full = bars + 4;    // [2] by block parity
+  uint64_t* k_empty = bars + 6;   // [2]
+  uint64_t* v_full = bars + 8;    // [2]
+  uint64_t* v_empty = bars + 10;  // [2]
+  uint64_t* s_full = bars + 12;   // [2]
+  uint64_t* p_full = bars + 14;   // [2]
+  uint64_t* pv_done = bars + 16;  // [2]
+  uint64_t* o_empty = bars + 18;  // [2] by item parity
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
-  if (threadIdx.x == 0) SRK_TRACE(0);
-  const AttnTile tile = tiles[blockIdx.x];
-  const int h = blockIdx.y;
+  const int n_items = n_tiles * n_heads;
   const int d = n_heads * HD;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nb1 = (tile.r1_end - tile.r1_begin + kBK - 1) / kBK;
-  const int nb2 = (tile.r2_end - tile.r2_begin + kBK - 1) / kBK;
-  const int nblk = nb1 + nb2;
+  if (threadIdx.x == 0) SRK_TRACE(0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
-    mbar_init(q_full, 1);
     for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 8);  // one arrival per softmax warp after its O store
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
       mbar_init(&v_full[s], 1);
@@ -116,6 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], kSoftmaxThreads);
       mbar_init(&pv_done[s], 1);
+      mbar_init(&o_empty[s], kSoftmaxThreads);
     }
     fence_barrier_init();
   }
@@ -127,38 +167,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) {
-    SRK_TRACE(1);
-    if (g_attn_trace != nullptr && blockIdx.y == 0 && blockIdx.x < 256) {
-      uint32_t smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      g_attn_trace[blockIdx.x * 64 + 30] = nblk;
-      g_attn_trace[blockIdx.x * 64 + 31] = smid;
-    }
-  }
 
   if (warp == 0) {
     // ------------------------------------------------------------- TMA
     if (lane == 0) {
       const uint64_t keep = policy_evict_last();  // prefix K/V: re-read by every item tile
-      mbar_arrive_expect_tx(q_full, C::TILE);
-      for (int b = 0; b < C::NB; ++b)
-        tma_load_2d(&tm_qkv, q_full, sQ + b * kBox, h * HD + b * 64, tile.q_begin);
-      for (int j = 0; j < nblk; ++j) {
+      Cursor c;
+      c.next_item(tiles, n_tiles, n_items, blockIdx.x);
+      int g = 0;
+      while (c.valid) {
+        if (c.j == 0) {
+          const int qb = c.li & 1;
+          mbar_wait(&q_empty[qb], ((c.li >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&q_full[qb], C::TILE);
+          for (int b = 0; b < C::NB; ++b)
+            tma_load_2d(&tm_qkv, &q_full[qb], sQ + qb * C::TILE + b * kBox, c.h * HD + b * 64,
+                        c.t.q_begin);
+        }
         int k0, kb, ke;
-        block_range(tile, nb1, j, k0, kb, ke);
-        const int st = j & 1;
-        const uint32_t ph = ((j >> 1) & 1) ^ 1;
+        c.range(k0, kb, ke);
+        const int st = g & 1;
+        const uint32_t ph = ((g >> 1) & 1) ^ 1;
         mbar_wait(&k_empty[st], ph);
         mbar_arrive_expect_tx(&k_full[st], C::TILE);
         for (int b = 0; b < C::NB; ++b)
           tma_load_2d_hint(&tm_qkv, &k_full[st], sK + st * C::TILE + b * kBox,
-                           d + h * HD + b * 64, k0, keep);
+                           d + c.h * HD + b * 64, k0, keep);
         mbar_wait(&v_empty[st], ph);
         mbar_arrive_expect_tx(&v_full[st], C::TILE);
         for (int b = 0; b < C::NB; ++b)
           tma_load_2d_hint(&tm_qkv, &v_full[st], sV + st * C::TILE + b * kBox,
-                           2 * d + h * HD + b * 64, k0, keep);
+                           2 * d + c.h * HD + b * 64, k0, keep);
+        ++g;
+        c.advance(tiles, n_tiles, n_items);
       }
     }
     __syncwarp();
@@ -167,13 +208,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(kTM, kBK);
       constexpr uint32_t idesc_pv = idesc_bf16_f32_bmn(kTM, HD);
-      const uint32_t q_addr = smem_u32(sQ);
-      mbar_wait(q_full, 0);
-      SRK_TRACE(2);
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
+      Cursor sc, pc;  // next block to issue S for / next block to issue PV for
+      sc.next_item(tiles, n_tiles, n_items, blockIdx.x);
+      pc = sc;
+      int gs = 0;  // global index of sc
+      auto issue_s = [&]() {
+        const int st = gs & 1;
+        const int qb = sc.li & 1;
+        if (sc.j == 0) mbar_wait(&q_full[qb], (sc.li >> 1) & 1);
+        mbar_wait(&k_full[st], (gs >> 1) & 1);
         tc_fence_after();
+        const uint32_t q_addr = smem_u32(sQ + qb * C::TILE);
         const uint32_t k_addr = smem_u32(sK + st * C::TILE);
 #pragma unroll
         for (int s = 0; s < HD / 16; ++s) {
@@ -183,30 +228,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         umma_commit(&k_empty[st]);
         umma_commit(&s_full[st]);
+        ++gs;
+        sc.advance(tiles, n_tiles, n_items);
       };
-      if (nblk > 0) issue_s(0);
-      if (nblk > 1) issue_s(1);
-      for (int j = 0; j < nblk; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
+      if (sc.valid) issue_s();
+      if (sc.valid) issue_s();
+      int g = 0;
+      while (pc.valid) {
+        const int st = g & 1;
+        const uint32_t ph = (g >> 1) & 1;
+        const int ob = pc.li & 1;
+        if (pc.j == 0) mbar_wait(&o_empty[ob], ((pc.li >> 1) & 1) ^ 1);
         mbar_wait(&p_full[st], ph);
-        if (j < 8) SRK_TRACE(3 + j);
         mbar_wait(&v_full[st], ph);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sV + st * C::TILE);
 #pragma unroll
         for (int s = 0; s < kBK / 16; ++s) {
-          umma_bf16_ts(tmem + C::O_COL, tmem + st * kBK + s * 8,
+          umma_bf16_ts(tmem + C::O_COL + ob * 128, tmem + st * kBK + s * 8,
                        sw128_mnmajor_desc(v_addr + s * 16 * 128, kBox, 1024), idesc_pv,
-                       (j > 0 || s > 0) ? 1u : 0u);
+                       (pc.j > 0 || s > 0) ? 1u : 0u);
         }
         umma_commit(&v_empty[st]);
         umma_commit(&pv_done[st]);
-        if (j + 2 < nblk) {
-          // S_{j+2} reuses this TMEM buffer: PV_j must have read P_j first.
+        if (sc.valid) {
+          // S_{g+2} reuses this TMEM buffer: PV_g must have read P_g first.
           mbar_wait(&pv_done[st], ph);
-          issue_s(j + 2);
+          issue_s();
         }
+        ++g;
+        pc.advance(tiles, n_tiles, n_items);
       }
     }
     __syncwarp();
@@ -215,138 +266,171 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;         // TMEM lane quadrant of this warp
     const int half = (warp - 2) >> 2;  // 0: keys 0-63, 1: keys 64-127 of a block
     const int r = quad * 32 + lane;    // tile row owned by this thread (shared with a partner)
-    const int row = tile.q_begin + r;
-    const bool live = row < tile.q_end;
-    RowSpan sp = {0, 0, 0, 0};
-    if (live) sp = spans[row];
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const float scale_log2 = 1.4426950408889634f * rsqrtf(static_cast<float>(HD));
-    float m_used = -INFINITY;  // exponent base (raw score units), shared by the pair
-    float l = 0.f;             // this thread's partial row sum
-
-    for (int j = 0; j < nblk; ++j) {
-      int k0, kb, ke;
-      block_range(tile, nb1, j, k0, kb, ke);
-      const int sb = j & 1;
-      const int kh = k0 + half * kHalf;  // first key of this thread's slice
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
-      if (warp == 2 && lane == 0 && j < 8) SRK_TRACE(11 + j);
-      tc_fence_after();
-      float s[kHalf];
-#pragma unroll
-      for (int c = 0; c < kHalf / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem + lane_off + sb * kBK + half * kHalf + c * 32, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
-      }
-
-      // Visible iff in [kb, ke) and in ([pb, pe) U [ss, row]). Fast path when
-      // the whole 64-key slice is visible to every row of the warp.
-      const int a_lo = max(kb, sp.prefix_begin), a_hi = min(ke, sp.prefix_end);
-      const int b_lo = max(kb, sp.span_start), b_hi = min(ke, row + 1);
-      const bool full = live && ((kh >= a_lo && kh + kHalf <= a_hi) ||
-                                 (kh >= b_lo && kh + kHalf <= b_hi));
-      float mx = -INFINITY;
-      if (__all_sync(0xffffffff, full)) {
-#pragma unroll
-        for (int i = 0; i < kHalf; ++i) mx = fmaxf(mx, s[i]);
-      } else {
-        // Visible keys of the slice as a 64-bit mask (two clipped intervals).
-        auto ivl = [&](int lo, int hi) -> uint64_t {
-          lo = max(lo - kh, 0);
-          hi = min(hi - kh, kHalf);
-          if (!live || hi <= lo) return 0ull;
-          const uint64_t upto_hi = hi >= 64 ? ~0ull : ((1ull << hi) - 1ull);
-          return upto_hi & ~((1ull << lo) - 1ull);
-        };
-        const uint64_t vis = ivl(a_lo, a_hi) | ivl(b_lo, b_hi);
-        const uint32_t v0 = static_cast<uint32_t>(vis), v1 = static_cast<uint32_t>(vis >> 32);
-#pragma unroll
-        for (int i = 0; i < kHalf; ++i) {
-          const bool ok = ((i < 32 ? v0 : v1) >> (i & 31)) & 1u;
-          s[i] = ok ? s[i] : -INFINITY;
-          mx = fmaxf(mx, s[i]);
-        }
-      }
-      // Pair max exchange (double-buffered by block parity). The barrier also
-      // orders both halves' S reads before either writes P over S.
-      float* slot = red + (j & 1) * 256;
-      slot[half * 128 + r] = mx;
-      named_bar_sync(1, kSoftmaxThreads);
-      mx = fmaxf(mx, slot[(half ^ 1) * 128 + r]);
-
-      // Move the base only on a large increase (or from -inf).
-      const bool move =
-          mx > m_used && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2);
-      const float m_new = move ? mx : m_used;
-      if (j > 0 && __any_sync(0xffffffff, move)) {
-        // All PV up to j-1 accumulated with the old base: rescale O rows.
-        mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+    float* fin = red + 2 * 256;
+    Cursor c;
+    c.next_item(tiles, n_tiles, n_items, blockIdx.x);
+    int g = 0;
+    while (c.valid) {
+      const int c_row0 = c.t.q_begin;
+      const int row = c_row0 + r;
+      const bool live = row < c.t.q_end;
+      RowSpan sp = {0, 0, 0, 0};
+      if (live) sp = spans[row];
+      float m_used = -INFINITY;  // exponent base (raw score units), shared by the pair
+      float l = 0.f;             // this thread's partial row sum
+      const int li = c.li, h = c.h;
+      bool item_done = false;
+      while (!item_done) {
+        int k0, kb, ke;
+        c.range(k0, kb, ke);
+        const int sb = g & 1;
+        const int kh = k0 + half * kHalf;  // first key of this thread's slice
+        mbar_wait(&s_full[sb], (g >> 1) & 1);
+        if (warp == 2 && lane == 0 && g < 24) SRK_TRACE(1 + g);
         tc_fence_after();
-        const float corr = move ? ex2_approx((m_used - m_new) * scale_log2) : 1.f;
-        l *= corr;
-#pragma unroll 1
-        for (int c = 0; c < HD / 64; ++c) {
+        float s[kHalf];
+#pragma unroll
+        for (int cc = 0; cc < kHalf / 32; ++cc) {
           uint32_t v[32];
-          const uint32_t a = tmem + lane_off + C::O_COL + half * (HD / 2) + c * 32;
-          tmem_ld_32x32b_x32(a, v);
+          tmem_ld_32x32b_x32(tmem + lane_off + sb * kBK + half * kHalf + cc * 32, v);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
-          tmem_st_32x32b_x32(a, v);
+          for (int i = 0; i < 32; ++i) s[cc * 32 + i] = __uint_as_float(v[i]);
         }
-      }
-      m_used = m_new;
-      const float base = m_used == -INFINITY ? 0.f : m_used * scale_log2;
-      float rs = 0.f;
-      uint32_t pk[32];
+        // Visible iff in [kb, ke) and in ([pb, pe) U [ss, row]).
+        const int a_lo = max(kb, sp.prefix_begin), a_hi = min(ke, sp.prefix_end);
+        const int b_lo = max(kb, sp.span_start), b_hi = min(ke, row + 1);
+        const bool full = live && ((kh >= a_lo && kh + kHalf <= a_hi) ||
+                                   (kh >= b_lo && kh + kHalf <= b_hi));
+        float mx = -INFINITY;
+        if (__all_sync(0xffffffff, full)) {
 #pragma unroll
-      for (int i = 0; i < kHalf; i += 2) {
-        const float p0 = ex2_approx(fmaf(s[i], scale_log2, -base));
-        const float p1 = ex2_approx(fmaf(s[i + 1], scale_log2, -base));
-        rs += p0 + p1;
-        pk[i >> 1] = pack_bf16x2(p0, p1);
-      }
-      l += rs;
-      // P_j (bf16x2) over this half's 32 columns of the consumed S_j buffer.
-      tmem_st_32x32b_x32(tmem + lane_off + sb * kBK + half * 32, pk);
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(&p_full[sb]);
-      if (warp == 2 && lane == 0 && j < 8) SRK_TRACE(19 + j);
-    }
+          for (int i = 0; i < kHalf; ++i) mx = fmaxf(mx, s[i]);
+        } else {
+          auto ivl = [&](int lo, int hi) -> uint64_t {
+            lo = max(lo - kh, 0);
+            hi = min(hi - kh, kHalf);
+            if (!live || hi <= lo) return 0ull;
+            const uint64_t upto_hi = hi >= 64 ? ~0ull : ((1ull << hi) - 1ull);
+            return upto_hi & ~((1ull << lo) - 1ull);
+          };
+          const uint64_t vis = ivl(a_lo, a_hi) | ivl(b_lo, b_hi);
+          const uint32_t v0 = static_cast<uint32_t>(vis), v1 = static_cast<uint32_t>(vis >> 32);
+#pragma unroll
+          for (int i = 0; i < kHalf; ++i) {
+            const bool ok = ((i < 32 ? v0 : v1) >> (i & 31)) & 1u;
+            s[i] = ok ? s[i] : -INFINITY;
+            mx = fmaxf(mx, s[i]);
+          }
+        }
+        // Pair max exchange (double-buffered by block parity). The barrier also
+        // orders both halves' S reads before either writes P over S.
+        float* slot = red + (g & 1) * 256;
+        slot[half * 128 + r] = mx;
+        named_bar_sync(1, kSoftmaxThreads);
+        mx = fmaxf(mx, slot[(half ^ 1) * 128 + r]);
 
-    // Row sum = both halves' partial sums (same base sequence).
-    float* fin = red + 2 * 256;
-    fin[half * 128 + r] = l;
-    named_bar_sync(1, kSoftmaxThreads);
-    l += fin[(half ^ 1) * 128 + r];
-
-    // Epilogue: O / l -> bf16 -> out[row, h*HD + half*HD/2 ...]
-    if (nblk > 0) {
-      mbar_wait(&pv_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
-      tc_fence_after();
-    }
-    if (warp == 2 && lane == 0) SRK_TRACE(27);
-    const float inv = l > 0.f ? 1.f / l : 0.f;
+        const bool move =
+            mx > m_used && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2);
+        const float m_new = move ? mx : m_used;
+        if (c.j > 0 && __any_sync(0xffffffff, move)) {
+          // Every PV of this item so far used the old base: rescale O rows.
+          mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+          tc_fence_after();
+          const float corr = move ? ex2_approx((m_used - m_new) * scale_log2) : 1.f;
+          l *= corr;
 #pragma unroll 1
-    for (int c = 0; c < HD / 64; ++c) {
-      uint32_t v[32];
-      const int col = half * (HD / 2) + c * 32;
-      tmem_ld_32x32b_x32(tmem + lane_off + C::O_COL + col, v);
-      tmem_ld_wait();
-      if (live) {
-        uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * d + h * HD + col);
+          for (int cc = 0; cc < HD / 64; ++cc) {
+            uint32_t v[32];
+            const uint32_t a = tmem + lane_off + C::O_COL + (li & 1) * 128 + half * (HD / 2) + cc * 32;
+            tmem_ld_32x32b_x32(a, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
+            tmem_st_32x32b_x32(a, v);
+          }
+        }
+        m_used = m_new;
+        const float base = m_used == -INFINITY ? 0.f : m_used * scale_log2;
+        float rs = 0.f;
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < kHalf; i += 2) {
+          const float p0 = ex2_approx(fmaf(s[i], scale_log2, -base));
+          const float p1 = ex2_approx(fmaf(s[i + 1], scale_log2, -base));
+          rs += p0 + p1;
+          pk[i >> 1] = pack_bf16x2(p0, p1);
+        }
+        l += rs;
+        // P (bf16x2) over this half's 32 columns of the consumed S buffer.
+        tmem_st_32x32b_x32(tmem + lane_off + sb * kBK + half * 32, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[sb]);
+        if (warp == 2 && lane == 0 && g < 24) SRK_TRACE(32 + g);
+        ++g;
+        item_done = c.advance(tiles, n_tiles, n_items);
+      }
+
+      // Item epilogue: row sum of both halves, O / l -> bf16 -> HBM.
+      fin[half * 128 + r] = l;
+      named_bar_sync(1, kSoftmaxThreads);
+      l += fin[(half ^ 1) * 128 + r];
+      mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+      tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      // Stage O (bf16) in this item's Q buffer — every S of the item has
+      // completed — in the Q tile's own swizzled layout, then TMA-store each
+      // fully-live 32-row slab; partially-live slabs (request tails) store
+      // their live rows directly so neighbouring tiles are never touched.
+      uint8_t* qbuf = sQ + (li & 1) * C::TILE;
+      const bool slab_live = __all_sync(0xffffffff, live);
+#pragma unroll 1
+      for (int cc = 0; cc < HD / 64; ++cc) {
+        uint32_t v[32];
+        const int col = half * (HD / 2) + cc * 32;
+        tmem_ld_32x32b_x32(tmem + lane_off + C::O_COL + (li & 1) * 128 + col, v);
+        tmem_ld_wait();
+        uint4 pk[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float* f = reinterpret_cast<const float*>(&v[q * 8]);
-          dst[q] = make_uint4(pack_bf16x2(f[0] * inv, f[1] * inv), pack_bf16x2(f[2] * inv, f[3] * inv),
-                              pack_bf16x2(f[4] * inv, f[5] * inv), pack_bf16x2(f[6] * inv, f[7] * inv));
+          pk[q] = make_uint4(pack_bf16x2(f[0] * inv, f[1] * inv), pack_bf16x2(f[2] * inv, f[3] * inv),
+                             pack_bf16x2(f[4] * inv, f[5] * inv), pack_bf16x2(f[6] * inv, f[7] * inv));
+        }
+        if (slab_live) {
+          uint8_t* rowp = qbuf + (col >> 6) * kBox + r * 128;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int chunk = ((col & 63) >> 3) + q;
+            *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) * 16)) = pk[q];
+          }
+        } else if (live) {
+          uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * d + h * HD + col);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dst[q] = pk[q];
         }
       }
+      fence_proxy_async_smem();
+      if constexpr (HD < 128) named_bar_sync(1, kSoftmaxThreads);  // halves share a box
+      else __syncwarp();
+      tc_fence_before();
+      mbar_arrive(&o_empty[li & 1]);
+      if (lane == 0) {
+        // HD=128: warp (quad, half) owns box `half` rows [32 quad, +32).
+        // HD=64 : both halves wrote box 0; the half-0 warp stores it.
+        if (slab_live && (HD == 128 || half == 0))
+          tma_store_2d(&tm_out, qbuf + (HD == 128 ? half : 0) * kBox + quad * 32 * 128,
+                       h * HD + (HD == 128 ? half : 0) * 64, c_row0 + quad * 32);
+        bulk_commit();
+        bulk_wait_read0();
+        mbar_arrive(&q_empty[li & 1]);  // the producer may now reuse this Q buffer
+      }
+      if (warp == 2 && lane == 0 && li < 8) SRK_TRACE(56 + li);
     }
+    if (lane == 0) bulk_wait0();  // O stores complete before exit
   }
 
   tc_fence_before();
@@ -358,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int HD>
 cudaError_t launch_tc(const CUtensorMap& tm, const RowSpan* spans, const AttnTile* tiles,
-                      int n_tiles, __nv_bfloat16* out, int n_heads, cudaStream_t stream) {
+                      int n_tiles, __nv_bfloat16* out, int M, int n_heads, cudaStream_t stream) {
   using C = AttnCfg<HD>;
   auto kern = attn_tc_kernel<HD>;
   static bool attr = false;
@@ -367,7 +451,15 @@ cudaError_t launch_tc(const CUtensorMap& tm, const RowSpan* spans, const AttnTil
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<dim3(n_tiles, n_heads), kThreads, C::SMEM, stream>>>(tm, spans, tiles, out, n_heads);
+  // out [M x d] bf16, 64-column x 32-row boxes in the Q tile's swizzle.
+  CUtensorMap tm_out;
+  cudaError_t e = make_tmap_bf16_2d(&tm_out, out, M, static_cast<uint64_t>(n_heads) * HD, 32, 64);
+  if (e != cudaSuccess) return e;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int items = n_tiles * n_heads;
+  const int grid = items < num_sms(dev) ? items : num_sms(dev);
+  kern<<<grid, kThreads, C::SMEM, stream>>>(tm, tm_out, spans, tiles, n_tiles, out, n_heads);
   return cudaGetLastError();
 }
 
@@ -380,12 +472,12 @@ cudaError_t attention_set_trace(unsigned long long* dev_buf) {
 int attention_tile_rows(int head_dim) { return head_dim >= 64 ? kTM : 64; }
 
 cudaError_t attention_tc(const CUtensorMap& tm_qkv, const RowSpan* spans, const AttnTile* tiles,
-                         int n_tiles, __nv_bfloat16* out, int n_heads, int head_dim,
+                         int n_tiles, __nv_bfloat16* out, int M, int n_heads, int head_dim,
                          cudaStream_t stream) {
   if (n_tiles <= 0) return cudaSuccess;
   switch (head_dim) {
-    case 64: return launch_tc<64>(tm_qkv, spans, tiles, n_tiles, out, n_heads, stream);
-    case 128: return launch_tc<128>(tm_qkv, spans, tiles, n_tiles, out, n_heads, stream);
+    case 64: return launch_tc<64>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream);
+    case 128: return launch_tc<128>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream);
   }
   return cudaErrorInvalidValue;
 }
