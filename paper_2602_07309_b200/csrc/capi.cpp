@@ -465,9 +465,8 @@ int32_t sr_kernel_gemm(const void* a_bf16, const void* b_bf16, int32_t M, int32_
     if (K % 8 != 0) srh::fail(SR_SPEC_VIOLATION, "K must be a multiple of 8");
     CUtensorMap ta, tb;
     SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&ta, a_bf16, M, K, 128, 64));
-    SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tb, b_bf16, N, K, bn, 64));
-    SR_CUDA_CHECK(srk::gemm_bf16(ta, tb, M, N, K, c, ldc, epi, bn,
-                                 static_cast<cudaStream_t>(stream)));
+    SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tb, b_bf16, N, K, srk::gemm_b_box_rows(N), 64));
+    SR_CUDA_CHECK(srk::gemm_auto(ta, tb, M, N, K, c, ldc, epi, static_cast<cudaStream_t>(stream)));
     SR_CUDA_CHECK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   });
 }

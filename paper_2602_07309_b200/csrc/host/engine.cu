@@ -36,8 +36,7 @@ T* upload(const std::vector<T>& v, std::vector<void*>& allocs) {
 }
 
 void make_weight_map(CUtensorMap* m, const void* w, int rows, int cols) {
-  const int bn = srk::gemm_pick_bn(rows);
-  SR_CUDA_CHECK(srk::make_tmap_bf16_2d(m, w, rows, cols, bn, 64));
+  SR_CUDA_CHECK(srk::make_tmap_bf16_2d(m, w, rows, cols, srk::gemm_b_box_rows(rows), 64));
 }
 
 }  // namespace
@@ -209,12 +208,10 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
                               pos_emb_, layers_[0].ln1, x_.ptr, xn_.ptr, M, d, s));
   E();
   ++n;
-  const int bn_qkv = srk::gemm_pick_bn(3 * d), bn_d = srk::gemm_pick_bn(d),
-            bn_f = srk::gemm_pick_bn(F);
   for (int l = 0; l < cfg_.n_layers; ++l) {
     const auto& L = layers_[l];
     B(PROF_GEMM_QKV);
-    SR_CUDA_CHECK(srk::gemm_bf16(tm_xn_, L.tm_qkv, M, 3 * d, d, qkv_.ptr, 3 * d, 0, bn_qkv, s));
+    SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_qkv, M, 3 * d, d, qkv_.ptr, 3 * d, 0, s));
     E();
     B(PROF_ATTENTION);
     if (hd >= 64)
@@ -225,16 +222,16 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
                                    static_cast<int>(p.pack.tiles.size()), xn_.ptr, M, H, hd, s));
     E();
     B(PROF_GEMM_O);
-    SR_CUDA_CHECK(srk::gemm_bf16(tm_xn_, L.tm_o, M, d, d, x_.ptr, d, 2, bn_d, s));
+    SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_o, M, d, d, x_.ptr, d, 2, s));
     E();
     B(PROF_LAYERNORM);
     SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, L.ln2, xn_.ptr, M, d, s));
     E();
     B(PROF_GEMM_IN);
-    SR_CUDA_CHECK(srk::gemm_bf16(tm_xn_, L.tm_in, M, F, d, h_.ptr, F, 1, bn_f, s));
+    SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_in, M, F, d, h_.ptr, F, 1, s));
     E();
     B(PROF_GEMM_OUT);
-    SR_CUDA_CHECK(srk::gemm_bf16(tm_h_, L.tm_out, M, d, F, x_.ptr, d, 2, bn_d, s));
+    SR_CUDA_CHECK(srk::gemm_auto(tm_h_, L.tm_out, M, d, F, x_.ptr, d, 2, s));
     E();
     n += 6;
     if (l + 1 < cfg_.n_layers) {

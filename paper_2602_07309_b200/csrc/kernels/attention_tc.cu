@@ -272,12 +272,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     Cursor c;
     c.next_item(tiles, n_tiles, n_items, blockIdx.x);
     int g = 0;
+    // Row descriptor of the current item, fetched one item ahead.
+    RowSpan sp_next = {0, 0, 0, 0};
+    if (c.valid && c.t.q_begin + r < c.t.q_end) sp_next = spans[c.t.q_begin + r];
+    int pending_q = -1;  // Q buffer whose O store may still be reading smem
     while (c.valid) {
       const int c_row0 = c.t.q_begin;
       const int row = c_row0 + r;
       const bool live = row < c.t.q_end;
-      RowSpan sp = {0, 0, 0, 0};
-      if (live) sp = spans[row];
+      const RowSpan sp = sp_next;
       float m_used = -INFINITY;  // exponent base (raw score units), shared by the pair
       float l = 0.f;             // this thread's partial row sum
       const int li = c.li, h = c.h;
@@ -305,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool full = live && ((kh >= a_lo && kh + kHalf <= a_hi) ||
                                    (kh >= b_lo && kh + kHalf <= b_hi));
         float mx = -INFINITY;
+        bool warp_empty = false;  // no visible key in this slice for any row of the warp
         if (__all_sync(0xffffffff, full)) {
 #pragma unroll
           for (int i = 0; i < kHalf; ++i) mx = fmaxf(mx, s[i]);
@@ -317,12 +321,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             return upto_hi & ~((1ull << lo) - 1ull);
           };
           const uint64_t vis = ivl(a_lo, a_hi) | ivl(b_lo, b_hi);
-          const uint32_t v0 = static_cast<uint32_t>(vis), v1 = static_cast<uint32_t>(vis >> 32);
+          warp_empty = !__any_sync(0xffffffff, vis != 0ull);
+          if (!warp_empty) {
+            const uint32_t v0 = static_cast<uint32_t>(vis), v1 = static_cast<uint32_t>(vis >> 32);
 #pragma unroll
-          for (int i = 0; i < kHalf; ++i) {
-            const bool ok = ((i < 32 ? v0 : v1) >> (i & 31)) & 1u;
-            s[i] = ok ? s[i] : -INFINITY;
-            mx = fmaxf(mx, s[i]);
+            for (int i = 0; i < kHalf; ++i) {
+              const bool ok = ((i < 32 ? v0 : v1) >> (i & 31)) & 1u;
+              s[i] = ok ? s[i] : -INFINITY;
+              mx = fmaxf(mx, s[i]);
+            }
           }
         }
         // Pair max exchange (double-buffered by block parity). The barrier also
@@ -356,12 +363,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float base = m_used == -INFINITY ? 0.f : m_used * scale_log2;
         float rs = 0.f;
         uint32_t pk[32];
+        if (warp_empty) {
 #pragma unroll
-        for (int i = 0; i < kHalf; i += 2) {
-          const float p0 = ex2_approx(fmaf(s[i], scale_log2, -base));
-          const float p1 = ex2_approx(fmaf(s[i + 1], scale_log2, -base));
-          rs += p0 + p1;
-          pk[i >> 1] = pack_bf16x2(p0, p1);
+          for (int i = 0; i < 32; ++i) pk[i] = 0u;
+        } else {
+          // 1 in 4 exponentials on the FMA pipe, the rest on MUFU.
+#pragma unroll
+          for (int i = 0; i < kHalf; i += 2) {
+            const float a0 = fmaf(s[i], scale_log2, -base);
+            const float a1 = fmaf(s[i + 1], scale_log2, -base);
+            const float p0 = ex2_approx(a0);
+            const float p1 = (i & 2) ? ex2_poly(a1) : ex2_approx(a1);
+            rs += p0 + p1;
+            pk[i >> 1] = pack_bf16x2(p0, p1);
+          }
         }
         l += rs;
         // P (bf16x2) over this half's 32 columns of the consumed S buffer.
@@ -370,9 +385,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
         if (warp == 2 && lane == 0 && g < 24) SRK_TRACE(32 + g);
+        if (pending_q >= 0 && lane == 0) {
+          // The previous item's O store has long finished reading its Q
+          // buffer: hand it back to the producer (needed two items later).
+          bulk_wait_read0();
+          mbar_arrive(&q_empty[pending_q]);
+        }
+        pending_q = -1;
         ++g;
         item_done = c.advance(tiles, n_tiles, n_items);
       }
+      // Next item's row descriptor: its latency overlaps this epilogue.
+      if (c.valid && c.t.q_begin + r < c.t.q_end) sp_next = spans[c.t.q_begin + r];
 
       // Item epilogue: row sum of both halves, O / l -> bf16 -> HBM.
       fin[half * 128 + r] = l;
@@ -425,9 +449,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_store_2d(&tm_out, qbuf + (HD == 128 ? half : 0) * kBox + quad * 32 * 128,
                        h * HD + (HD == 128 ? half : 0) * 64, c_row0 + quad * 32);
         bulk_commit();
-        bulk_wait_read0();
-        mbar_arrive(&q_empty[li & 1]);  // the producer may now reuse this Q buffer
       }
+      pending_q = li & 1;  // released after the next item's first block
       if (warp == 2 && lane == 0 && li < 8) SRK_TRACE(56 + li);
     }
     if (lane == 0) bulk_wait0();  // O stores complete before exit

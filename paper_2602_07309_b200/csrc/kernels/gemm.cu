@@ -82,6 +82,43 @@ cudaError_t launch_bn(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int
 
 }  // namespace
 
+template <int EPI>
+cudaError_t launch_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
+                        void* out, int ldo, cudaStream_t stream) {
+  using C = GemmPairCfg;
+  auto kern = gemm_bf16_tcgen05_pair_kernel<EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int tiles = ((M + 2 * C::BM - 1) / (2 * C::BM)) * (N / C::BN);
+  const int pairs = tiles < num_sms(dev) / 2 ? tiles : num_sms(dev) / 2;
+  if (pairs <= 0) return cudaSuccess;
+  CUtensorMap tmC;
+  cudaError_t e = make_out_map<EPI>(&tmC, out, M, N, ldo);
+  if (e != cudaSuccess) return e;
+  kern<<<2 * pairs, C::THREADS, C::SMEM_BYTES, stream>>>(tmA, tmB, tmC, M, N, K);
+  return cudaGetLastError();
+}
+
+cudaError_t gemm_bf16_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
+                           void* out, int ldo, int epi, cudaStream_t stream) {
+  if (M <= 0) return cudaSuccess;
+  if (N % GemmPairCfg::BN != 0 || K % 8 != 0) return cudaErrorInvalidValue;
+  switch (epi) {
+    case EPI_BF16: return launch_pair<EPI_BF16>(tmA, tmB, M, N, K, out, ldo, stream);
+    case EPI_GELU_BF16: return launch_pair<EPI_GELU_BF16>(tmA, tmB, M, N, K, out, ldo, stream);
+    case EPI_RESID_F32: return launch_pair<EPI_RESID_F32>(tmA, tmB, M, N, K, out, ldo, stream);
+    case EPI_F32: return launch_pair<EPI_F32>(tmA, tmB, M, N, K, out, ldo, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
 int num_sms(int device) {
   static int cached[64] = {0};
   if (device < 0 || device >= 64) return 148;

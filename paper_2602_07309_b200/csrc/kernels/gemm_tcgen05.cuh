@@ -230,4 +230,213 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 1) tmem_dealloc(tmem_base, C::TMEM_COLS);
 }
 
+// ----------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes a
+// 256 x 256 tile; CTA r loads rows [128 r, +128) of A and of B (= 128 of the
+// 256 output columns) per k-block, the leader issues
+// tcgen05.mma.cta_group::2 (M = 256) which reads both CTAs' smem and writes
+// each CTA's 128 accumulator rows into its own TMEM. Per SM this halves the
+// B operand traffic through shared memory relative to the 1-CTA 128 x 256
+// tile (the 1-CTA kernel is smem-bandwidth bound at ~64% tensor-pipe).
+struct GemmPairCfg {
+  static constexpr int BM = 128;  // rows per CTA (pair: 256)
+  static constexpr int BN = 256;  // output columns per pair tile
+  static constexpr int BK = 64;
+  static constexpr int A_BYTES = BM * BK * 2;        // 16 KB
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;  // 16 KB (this CTA's half of B)
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = 6;
+  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered 128 x 256 fp32
+  static constexpr int EPI_WARPS = 8;
+  static constexpr int STG_BYTES = 32 * 128;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_WARPS * STG_BYTES + 256 + 1024;
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+};
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
+    gemm_bf16_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                                  const __grid_constant__ CUtensorMap tmB,
+                                  const __grid_constant__ CUtensorMap tmC, int M, int N, int K) {
+  using C = GemmPairCfg;
+  constexpr int BN = C::BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint8_t* sStg = sB + C::STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + C::EPI_WARPS * C::STG_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = static_cast<int>(cluster_id_x());
+  const int n_pairs = static_cast<int>(nclusters_x());
+  const int m_tiles = (M + 2 * C::BM - 1) / (2 * C::BM);
+  const int n_tiles = N / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int nk = (K + C::BK - 1) / C::BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 2);  // leader: own expect_tx arrival + the peer's arrival
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * C::EPI_WARPS);  // one per epilogue warp of both CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_b = policy_evict_last();
+      const uint64_t pol_a = policy_evict_first();
+      const uint32_t peer_full0 = mapa_shared(smem_u32(&full[0]), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair; tile < num_tiles; tile += n_pairs) {
+        const int m0 = (tile / n_tiles) * 2 * C::BM + static_cast<int>(rank) * C::BM;
+        const int n0 = (tile % n_tiles) * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader)
+            mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+          else
+            mbar_arrive_cluster(peer_full0 + stage * 8);
+          tma_load_2d_pair(&tmA, &full[stage], sA + stage * C::A_BYTES, kb * C::BK, m0, pol_a);
+          tma_load_2d_pair(&tmB, &full[stage], sB + stage * C::B_BYTES, kb * C::BK, n0, pol_b);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(2 * C::BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < C::BK / 16; ++k)
+            umma_bf16_pair(d_tmem, sw128_kmajor_desc(a_addr + k * 32),
+                           sw128_kmajor_desc(b_addr + k * 32), idesc, (kb | k) != 0 ? 1u : 0u);
+          umma_commit_pair(&empty[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    constexpr int CW = EpiOut<EPI>::CW;
+    constexpr int SPAN = BN / 2;  // columns per epilogue warp
+    const int quad = warp & 3;
+    const int col0 = ((warp - 2) >> 2) * SPAN;
+    uint8_t* stg = sStg + (warp - 2) * C::STG_BYTES;
+    const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+    int local = 0;
+    for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      const int m0 = (tile / n_tiles) * 2 * C::BM + static_cast<int>(rank) * C::BM;
+      const int n0 = (tile % n_tiles) * BN;
+      const int r0 = m0 + quad * 32;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      if (r0 < M) {
+#pragma unroll 1
+        for (int c = col0; c < col0 + SPAN; c += CW) {
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+          uint8_t* row_base = stg + lane * 128;
+          if constexpr (EpiOut<EPI>::F32) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c,
+                               r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              *reinterpret_cast<uint4*>(row_base + ((k ^ (lane & 7)) * 16)) =
+                  make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+          } else {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(
+                  tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c + hh * 32, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                float f[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  f[j] = __uint_as_float(r[8 * k + j]);
+                  if constexpr (EPI == EPI_GELU_BF16) f[j] = gelu_erf(f[j]);
+                }
+                const int chunk = hh * 4 + k;
+                *reinterpret_cast<uint4*>(row_base + ((chunk ^ (lane & 7)) * 16)) =
+                    make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                               pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+              }
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (EPI == EPI_RESID_F32)
+              tma_reduce_add_2d(&tmC, stg, n0 + c, r0);
+            else
+              tma_store_2d(&tmC, stg, n0 + c, r0);
+            bulk_commit();
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+    }
+    if (lane == 0) bulk_wait0();
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+}
+
 }  // namespace srk

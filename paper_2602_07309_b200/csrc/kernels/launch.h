@@ -37,6 +37,20 @@ cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows,
 int gemm_pick_bn(int N);
 cudaError_t gemm_bf16(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
                       void* out, int ldo, int epi, int bn, cudaStream_t stream);
+// CTA-pair (cta_group::2) 256 x 256 tiles; N % 256 == 0; tmA and tmB both use
+// 128-row x 64-column boxes.
+cudaError_t gemm_bf16_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
+                           void* out, int ldo, int epi, cudaStream_t stream);
+// The projection GEMMs take the pair path when N is a multiple of 256.
+inline bool gemm_use_pair(int N) { return N % 256 == 0; }
+// B-operand box rows for a weight [N x K] map on the chosen path.
+inline int gemm_b_box_rows(int N) { return gemm_use_pair(N) ? 128 : gemm_pick_bn(N); }
+// Dispatch: pair kernel when N % 256 == 0, else the 1-CTA kernel.
+inline cudaError_t gemm_auto(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
+                             void* out, int ldo, int epi, cudaStream_t stream) {
+  if (gemm_use_pair(N)) return gemm_bf16_pair(tmA, tmB, M, N, K, out, ldo, epi, stream);
+  return gemm_bf16(tmA, tmB, M, N, K, out, ldo, epi, gemm_pick_bn(N), stream);
+}
 
 // ------------------------------------------------------------ elementwise
 // x[r] = (src[r] >= 0 ? tok_emb[src[r]] : soft[-src[r]-1]) + pos_emb[pos[r]]
