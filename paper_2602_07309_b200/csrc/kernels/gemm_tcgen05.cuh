@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(320, 1)
     const int quad = warp & 3;
     const int col0 = ((warp - 2) >> 2) * SPAN;
     uint8_t* stg = sStg + (warp - 2) * C::STG_BYTES;
+    const uint64_t pol_keep = policy_evict_last();
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int acc = local & 1;
@@ -210,8 +211,8 @@ __global__ void __launch_bounds__(320, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            if constexpr (EPI == EPI_RESID_F32)
-              tma_reduce_add_2d(&tmC, stg, n0 + c, r0);
+            if constexpr (EPI == EPI_RESID_F32)  // x is re-read next by the LayerNorm
+              tma_reduce_add_2d_hint(&tmC, stg, n0 + c, r0, pol_keep);
             else
               tma_store_2d(&tmC, stg, n0 + c, r0);
             bulk_commit();
@@ -369,6 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     const int col0 = ((warp - 2) >> 2) * SPAN;
     uint8_t* stg = sStg + (warp - 2) * C::STG_BYTES;
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint64_t pol_keep = policy_evict_last();
     int local = 0;
     for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
       const int acc = local & 1;
@@ -418,8 +420,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            if constexpr (EPI == EPI_RESID_F32)
-              tma_reduce_add_2d(&tmC, stg, n0 + c, r0);
+            if constexpr (EPI == EPI_RESID_F32)  // x is re-read next by the LayerNorm
+              tma_reduce_add_2d_hint(&tmC, stg, n0 + c, r0, pol_keep);
             else
               tma_store_2d(&tmC, stg, n0 + c, r0);
             bulk_commit();

@@ -134,6 +134,15 @@ class ModelConfig:
                            c.yes_token_id, c.no_token_id, heads)
 
 
+class _OwnedBuffer:
+    """float32 array interface over library memory that pins its owner."""
+
+    def __init__(self, owner, addr: int, n: int):
+        self._owner = owner
+        self.__array_interface__ = {"data": (addr, False), "shape": (n,), "typestr": "<f4",
+                                    "version": 3}
+
+
 class ModelWeights:
     """Host weights (model.hpp:56-67), owned by the C library."""
 
@@ -151,7 +160,10 @@ class ModelWeights:
             self._h = C.c_void_p()
 
     def tensors(self) -> Dict[str, np.ndarray]:
-        """name -> zero-copy float32 view, in SRNKWTS1 canonical order."""
+        """name -> zero-copy float32 view, in SRNKWTS1 canonical order.
+
+        Each view keeps this ModelWeights alive (its base holds a reference),
+        so views may outlive the Python handle they came from."""
         out = {}
         n = _lib.sr_weights_tensor_count(self._h)
         for i in range(n):
@@ -159,8 +171,10 @@ class ModelWeights:
             data = C.POINTER(C.c_float)()
             numel = C.c_size_t()
             _check(_lib.sr_weights_tensor(self._h, i, C.byref(name), C.byref(data), C.byref(numel)))
-            arr = np.ctypeslib.as_array(data, shape=(numel.value,)) if numel.value else \
-                np.zeros(0, np.float32)
+            if numel.value:
+                arr = np.asarray(_OwnedBuffer(self, C.cast(data, C.c_void_p).value, numel.value))
+            else:
+                arr = np.zeros(0, np.float32)
             out[name.value.decode()] = arr
         return out
 
