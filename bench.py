@@ -42,8 +42,13 @@ WORKLOADS = {
     "c2": (20, 1024, 8, 1536, 256, 96, 256, False),
     "c3": (20, 1024, 8, 1536, 256, 8, 1024, True),
     "c1": (2, 64, 4, 256, 500, 50, 64, False),
+    "c4": (28, 2048, 16, 6144, 256, 96, 250, False),
 }
+# queries packed into one device pass per step (per GPU)
+QUERIES = {"c4": 32}
 WORKLOAD_DESC = {
+    "c4": "1.7B-class unpruned teacher-shaped ranker (L28 d2048 H16 ff6144), 32 queries x 250 "
+          "candidates per step in one packed pass, 256-token prefixes, 96-token items",
     "c2": "0.6B-class pruned SLM (L20 d1024 H8 ff1536), 1 query x 256 candidates, "
           "256-token shared prefix, 96-token items",
     "c3": "0.6B-class pruned SLM, 1 query x 1024 candidates, 256-token prefix, "
@@ -155,6 +160,16 @@ def make_request(sr, wl, world, rank, seed=7):
     return req, ids
 
 
+def make_queries(sr, wl, n_queries, rank):
+    """n_queries independent requests (own prefixes and items) for batched workloads."""
+    out = []
+    for q in range(n_queries):
+        req, _ = make_request(sr, wl, 1, 0, seed=1000 * (rank + 1) + q)
+        req.request_id = f"bench-{wl}-{q}"
+        out.append(req)
+    return out
+
+
 # ------------------------------------------------------------- CPU baseline
 def cpu_reference_run(wl, n_items, weights_path, fan_in, threads):
     """One bounded sample on the host: prefix + n_items items, reference
@@ -259,15 +274,23 @@ def run_ours(args):
                          head_specs=sr.ModelConfig.default_toy().head_specs)
     weights = sr.init_model(cfg, 2026 if wl != "c1" else 1, "fan_in" if wl != "c1" else "reference")
     eng = sr.ScoringEngine(weights, device=local)
-    req, ids = make_request(sr, wl, world, rank)
+    nq = QUERIES.get(wl, 1)
     k = TOPK
     comm = None
-    if world > 1:
-        uid = sr.Comm.unique_id() if rank == 0 else bytes(128)
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        comm = sr.Comm(world, rank, obj[0], local)
-    plan = eng.plan(req, k=k, item_ids=ids)
+    reqs = None
+    if nq > 1:
+        # batched queries: independent per rank (replicas), one packed pass per step
+        reqs = make_queries(sr, wl, nq, rank)
+        req, ids = reqs[0], None
+        plan = sr.BatchPlan(eng, reqs, k)
+    else:
+        req, ids = make_request(sr, wl, world, rank)
+        if world > 1:
+            uid = sr.Comm.unique_id() if rank == 0 else bytes(128)
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            comm = sr.Comm(world, rank, obj[0], local)
+        plan = eng.plan(req, k=k, item_ids=ids)
     stream = torch.cuda.ExternalStream(eng.stream_ptr)
 
     def step():
@@ -305,21 +328,30 @@ def run_ours(args):
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    pairs = n_loc * world * args.steps
+    pairs = n_loc * nq * world * args.steps
     value = pairs / (total_ms / 1000.0)
     lat_sorted = sorted(step_ms)
     p99 = lat_sorted[max(0, int(np.ceil(0.99 * len(lat_sorted))) - 1)]  # service.cpp:28-34
-    result = plan.fetch()
+    result = plan.fetch_all()[0] if nq > 1 else plan.fetch()
 
     # ----------------------------------------------------------- e2e (public API)
     shape = plan.shape()
+
+    def e2e_call():
+        if nq > 1:
+            eng.score_batch(reqs, k)
+        elif comm is not None:
+            eng.score_sharded(comm, req, k, ids)
+        else:
+            eng.score(req, k)
+
     for _ in range(max(1, args.warmup)):
-        (eng.score_sharded(comm, req, k, ids) if comm else eng.score(req, k))
+        e2e_call()
     barrier()
     e2e_times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        (eng.score_sharded(comm, req, k, ids) if comm else eng.score(req, k))
+        e2e_call()
         e2e_times.append(time.perf_counter() - t0)
     barrier()
     te = torch.tensor([sum(e2e_times)], device="cuda")
@@ -332,7 +364,26 @@ def run_ours(args):
     # -------------------------------------------------- per-kernel roofline
     prof = plan.profile(reps=3)
     lens = [t_i] * n_loc
-    lin, att, head = model_flops_per_query(L, d, ff, t_q, lens)
+    lin, att, head = (nq * v for v in model_flops_per_query(L, d, ff, t_q, lens))
+
+    # latency-bounded throughput sweep over queries per pass (batched workloads)
+    sweep = []
+    if nq > 1:
+        for b in sorted({1, max(1, nq // 4), nq}):
+            bp = sr.BatchPlan(eng, reqs[:b], k)
+            bp.run()
+            bp.sync()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(3):
+                bp.run()
+            e1.record(stream)
+            bp.sync()
+            ms = e0.elapsed_time(e1) / 3
+            sweep.append({"queries_per_pass": b, "latency_ms": round(ms, 3),
+                          "pairs_per_s": round(b * n_loc / (ms / 1000.0), 1),
+                          "meets_500ms": ms <= 500})
+            del bp
     gemm_ms = sum(prof[c][0] for c in ("gemm_qkv", "gemm_o", "gemm_in", "gemm_out"))
     gemm_launches = sum(prof[c][1] for c in ("gemm_qkv", "gemm_o", "gemm_in", "gemm_out"))
     peaks, peak_kind = load_peaks()
@@ -368,8 +419,12 @@ def run_ours(args):
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": WORKLOAD_DESC[wl], "model": f"semrank-{wl}-L{L}-d{d}",
-                   "global_batch": n_loc * world, "seq_len": t_q + t_i,
-                   "parallelism": f"candidate-shard x{world}" if world > 1 else "single-gpu",
+                   "global_batch": n_loc * nq * world, "seq_len": t_q + t_i,
+                   "queries_per_step_per_gpu": nq,
+                   "parallelism": ("single-gpu" if world == 1 else
+                                   f"query-batch replicas x{world}" if nq > 1 else
+                                   f"candidate-shard x{world}"),
+                   "sweep": sweep or None,
                    "tokens_per_query_per_gpu": M, "top_k": k,
                    "p99_query_ms": p99, "p50_query_ms": statistics.median(step_ms),
                    "latency_budget_ms": 500, "meets_p99_budget": p99 <= 500,

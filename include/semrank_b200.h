@@ -204,6 +204,11 @@ void* sr_engine_stream(const sr_engine* e);
 /* Resident-input path (benchmarking / serving loops): a plan owns packed
  * device inputs and a captured CUDA graph for one request shape. */
 int32_t sr_plan_create(sr_engine* e, const sr_request* req, int32_t k, sr_plan** out);
+/* Several requests packed into one resident pass (per-request top-k). */
+int32_t sr_plan_create_batch(sr_engine* e, const sr_request* reqs, int32_t n_req, int32_t k,
+                             sr_plan** out);
+/* Results of a batch plan: res[i] receives request i. */
+int32_t sr_plan_fetch_batch(sr_plan* p, sr_result* res, int32_t n_req);
 int32_t sr_plan_run(sr_plan* p);         /* enqueue on the engine stream; async */
 int32_t sr_plan_sync(sr_plan* p);
 int32_t sr_plan_fetch(sr_plan* p, sr_result* res); /* D2H of scores + top-k */

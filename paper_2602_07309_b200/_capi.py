@@ -85,6 +85,8 @@ _sig("sr_engine_item_hidden", i32, vp, P(RequestC), P(f32))
 _sig("sr_engine_device", i32, vp)
 _sig("sr_engine_stream", vp, vp)
 _sig("sr_plan_create", i32, vp, P(RequestC), i32, P(vp))
+_sig("sr_plan_create_batch", i32, vp, P(RequestC), i32, i32, P(vp))
+_sig("sr_plan_fetch_batch", i32, vp, P(ResultC), i32)
 _sig("sr_plan_run", i32, vp)
 _sig("sr_plan_sync", i32, vp)
 _sig("sr_plan_fetch", i32, vp, P(ResultC))
@@ -113,7 +115,7 @@ HEADER_SYMBOLS = [
     "sr_topk_host",
     "sr_engine_create", "sr_engine_destroy", "sr_engine_score", "sr_engine_score_batch",
     "sr_engine_item_hidden", "sr_engine_device", "sr_engine_stream", "sr_plan_create",
-    "sr_plan_run", "sr_plan_sync", "sr_plan_fetch", "sr_plan_kernel_count", "sr_plan_destroy",
+    "sr_plan_create_batch", "sr_plan_fetch_batch", "sr_plan_run", "sr_plan_sync", "sr_plan_fetch", "sr_plan_kernel_count", "sr_plan_destroy",
     "sr_plan_profile", "sr_plan_shape",
     "sr_nccl_unique_id", "sr_comm_create", "sr_comm_destroy", "sr_engine_score_sharded",
     "sr_plan_run_sharded", "sr_kernel_gemm", "sr_kernel_attention", "sr_kernel_layernorm",

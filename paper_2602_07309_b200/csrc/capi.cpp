@@ -356,6 +356,27 @@ int32_t sr_plan_create(sr_engine* e, const sr_request* req, int32_t k, sr_plan**
   });
 }
 
+int32_t sr_plan_create_batch(sr_engine* e, const sr_request* reqs, int32_t n_req, int32_t k,
+                             sr_plan** out) {
+  return guard([&] {
+    if (!e || !reqs || !out || n_req <= 0) srh::fail(SR_SPEC_VIOLATION, "bad argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    auto p = std::make_unique<sr_plan>();
+    p->owner = e;
+    p->p = e->e->make_plan(reqs, n_req, k);
+    *out = p.release();
+  });
+}
+
+int32_t sr_plan_fetch_batch(sr_plan* p, sr_result* res, int32_t n_req) {
+  return guard([&] {
+    if (!p || !res) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    if (n_req != static_cast<int32_t>(p->p->reqs.size()))
+      srh::fail(SR_PARAMETER, "result count differs from the plan's request count");
+    p->owner->e->fetch(*p->p, res, n_req);
+  });
+}
+
 int32_t sr_plan_run(sr_plan* p) {
   return guard([&] {
     if (!p) srh::fail(SR_SPEC_VIOLATION, "null plan");

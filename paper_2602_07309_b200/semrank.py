@@ -562,6 +562,32 @@ class Plan:
         return {c: (float(m), int(n)) for c, m, n in zip(PROF_CLASSES, ms, cnt)}
 
 
+class BatchPlan(Plan):
+    """Several requests resident in one packed device pass (plan_batches
+    consumer; BASELINE config C4 runs 32 queries per pass)."""
+
+    def __init__(self, engine: "ScoringEngine", requests: Sequence[ScoreRequest], k: int = 0):
+        self.engine = engine
+        self.requests = list(requests)
+        self.request = self.requests[0]
+        self._prs = [_PackedRequest(r, engine.config.d_model) for r in self.requests]
+        arr = (_c.RequestC * len(self._prs))(*[p.c for p in self._prs])
+        h = C.c_void_p()
+        _check(_lib.sr_plan_create_batch(engine._h, arr, len(self._prs), k, C.byref(h)))
+        self._h = h
+        self.k = k
+        self._rbs = [_ResultBuf(len(r.items), len(engine.task_names), k) for r in self.requests]
+
+    def fetch_all(self) -> List[ScoreResult]:
+        ress = (_c.ResultC * len(self._rbs))(*[rb.c for rb in self._rbs])
+        _check(_lib.sr_plan_fetch_batch(self._h, ress, len(self._rbs)))
+        out = []
+        for r, rb, rc in zip(self.requests, self._rbs, ress):
+            rb.c = rc
+            out.append(self.engine._to_result(r, rb))
+        return out
+
+
 def score_by_mode(engine: ScoringEngine, request: ScoreRequest, k: int = 0) -> ScoreResult:
     """score_by_mode (engine.cpp:379-387): dispatch on request.mode."""
     return engine.score(request, k)
