@@ -238,7 +238,8 @@ int32_t sr_plan_run_sharded(sr_plan* p, sr_comm* c); /* resident variant */
 
 /* --------------------------------------- kernel-level entry points (tests) */
 /* All pointers are device pointers; stream may be NULL (legacy stream). */
-/* C[M x N] = A[M x K] . B[N x K]^T ; epi 0 bf16, 1 gelu->bf16, 2 fp32 C += acc, 3 fp32. */
+/* C[M x N] = A[M x K] . B[N x K]^T ; epi 0 bf16, 1 gelu->bf16, 2 fp32 C += acc, 3 fp32.
+ * Synchronous when stream is NULL, asynchronous on an explicit stream. */
 int32_t sr_kernel_gemm(const void* a_bf16, const void* b_bf16, int32_t M, int32_t N, int32_t K,
                        void* c, int32_t ldc, int32_t epi, void* stream);
 /* Segment-masked attention. qkv [M x 3d] bf16, spans [M x 4] int32
@@ -251,6 +252,8 @@ int32_t sr_kernel_layernorm(const float* x, const float* gain, void* out_bf16, i
 /* Tuning aid: record a clock64 timeline (64 slots per CTA, first 256 tiles of
  * head 0) from the tcgen05 attention kernel into dev_buf; NULL disables. */
 int32_t sr_debug_attention_trace(void* dev_buf);
+/* Tuning aid: %globaltimer timeline of the CTA-pair GEMM (64 slots per CTA). */
+int32_t sr_debug_gemm_trace(void* dev_buf);
 int32_t sr_kernel_topk(const double* scores, const int64_t* ids, int32_t n, int32_t k,
                        int64_t* ids_out_host, double* scores_out_host, int32_t* index_out_host);
 

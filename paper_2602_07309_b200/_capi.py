@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsemrank_b200.so")
+# SEMRANK_LIB selects an alternative in-tree build (kernel tuning variants).
+LIB_PATH = os.environ.get("SEMRANK_LIB") or os.path.join(_HERE, "lib", "libsemrank_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -103,6 +104,7 @@ _sig("sr_kernel_gemm", i32, vp, vp, i32, i32, i32, vp, i32, i32, vp)
 _sig("sr_kernel_attention", i32, vp, P(i32), i32, i32, i32, vp, vp)
 _sig("sr_kernel_layernorm", i32, vp, vp, vp, i32, i32, vp)
 _sig("sr_debug_attention_trace", i32, vp)
+_sig("sr_debug_gemm_trace", i32, vp)
 _sig("sr_kernel_topk", i32, vp, vp, i32, i32, P(i64), P(f64), P(i32))
 
 # Every symbol the header declares (tests check the library exports them).
@@ -119,5 +121,5 @@ HEADER_SYMBOLS = [
     "sr_plan_profile", "sr_plan_shape",
     "sr_nccl_unique_id", "sr_comm_create", "sr_comm_destroy", "sr_engine_score_sharded",
     "sr_plan_run_sharded", "sr_kernel_gemm", "sr_kernel_attention", "sr_kernel_layernorm",
-    "sr_kernel_topk", "sr_debug_attention_trace",
+    "sr_kernel_topk", "sr_debug_attention_trace", "sr_debug_gemm_trace",
 ]

@@ -488,7 +488,8 @@ int32_t sr_kernel_gemm(const void* a_bf16, const void* b_bf16, int32_t M, int32_
     SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&ta, a_bf16, M, K, 128, 64));
     SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tb, b_bf16, N, K, srk::gemm_b_box_rows(N), 64));
     SR_CUDA_CHECK(srk::gemm_auto(ta, tb, M, N, K, c, ldc, epi, static_cast<cudaStream_t>(stream)));
-    SR_CUDA_CHECK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    // NULL stream: synchronous (errors surface here); explicit stream: async.
+    if (stream == nullptr) SR_CUDA_CHECK(cudaStreamSynchronize(nullptr));
   });
 }
 
@@ -566,6 +567,10 @@ int32_t sr_debug_attention_trace(void* dev_buf) {
   return guard([&] {
     SR_CUDA_CHECK(srk::attention_set_trace(static_cast<unsigned long long*>(dev_buf)));
   });
+}
+
+int32_t sr_debug_gemm_trace(void* dev_buf) {
+  return guard([&] { SR_CUDA_CHECK(srk::gemm_set_trace(static_cast<unsigned long long*>(dev_buf))); });
 }
 
 int32_t sr_kernel_topk(const double* scores, const int64_t* ids, int32_t n, int32_t k,

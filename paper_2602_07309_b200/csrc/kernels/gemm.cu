@@ -1,6 +1,7 @@
 // Host launchers for the tcgen05 GEMM (gemm_tcgen05.cuh).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm_tcgen05.cuh"
@@ -82,28 +83,68 @@ cudaError_t launch_bn(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int
 
 }  // namespace
 
-template <int EPI>
+// Pairs per cluster: 1 by default. SRK_GEMM_NP=2 selects the 4-CTA cluster
+// with A multicast (N % 512 == 0). Measured on B200 (C2 shapes): per-tile
+// main-loop time is identical with and without the multicast (the loop is not
+// L2-bandwidth bound at 6 stages), so the 16 SMs a 4-CTA grid leaves idle
+// make it slower; kept for tuning on other shapes / parts.
+int gemm_pairs_per_cluster(int N) {
+  static const int forced = [] {
+    const char* v = std::getenv("SRK_GEMM_NP");
+    return v != nullptr ? std::atoi(v) : 0;
+  }();
+  if (N % (2 * GemmPairCfg::BN) == 0 && forced == 2) return 2;
+  return 1;
+}
+
+template <int EPI, int NP>
 cudaError_t launch_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
                         void* out, int ldo, cudaStream_t stream) {
   using C = GemmPairCfg;
-  auto kern = gemm_bf16_tcgen05_pair_kernel<EPI>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  auto kern = gemm_bf16_tcgen05_pair_kernel<EPI, NP>;
+  static int max_clusters = 0;  // co-resident clusters of 2*NP CTAs (per process, one GPU type)
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2 * NP;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(C::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (max_clusters == 0) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cfg.gridDim = dim3(2 * NP * (num_sms(dev) / (2 * NP)), 1, 1);
+    int n = 0;
+    e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+    if (e != cudaSuccess) return e;
+    if (n <= 0) return cudaErrorInvalidConfiguration;
+    max_clusters = n;
   }
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const int tiles = ((M + 2 * C::BM - 1) / (2 * C::BM)) * (N / C::BN);
-  const int pairs = tiles < num_sms(dev) / 2 ? tiles : num_sms(dev) / 2;
-  if (pairs <= 0) return cudaSuccess;
+  const int tiles = ((M + 2 * C::BM - 1) / (2 * C::BM)) * (N / (NP * C::BN));
+  const int clusters = tiles < max_clusters ? tiles : max_clusters;
+  if (clusters <= 0) return cudaSuccess;
   CUtensorMap tmC;
   cudaError_t e = make_out_map<EPI>(&tmC, out, M, N, ldo);
   if (e != cudaSuccess) return e;
-  kern<<<2 * pairs, C::THREADS, C::SMEM_BYTES, stream>>>(tmA, tmB, tmC, M, N, K);
+  cfg.gridDim = dim3(2 * NP * clusters, 1, 1);
+  e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, M, N, K);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+template <int EPI>
+cudaError_t launch_pair_np(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
+                           void* out, int ldo, cudaStream_t stream) {
+  if (gemm_pairs_per_cluster(N) == 2)
+    return launch_pair<EPI, 2>(tmA, tmB, M, N, K, out, ldo, stream);
+  return launch_pair<EPI, 1>(tmA, tmB, M, N, K, out, ldo, stream);
 }
 
 cudaError_t gemm_bf16_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
@@ -111,10 +152,10 @@ cudaError_t gemm_bf16_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M
   if (M <= 0) return cudaSuccess;
   if (N % GemmPairCfg::BN != 0 || K % 8 != 0) return cudaErrorInvalidValue;
   switch (epi) {
-    case EPI_BF16: return launch_pair<EPI_BF16>(tmA, tmB, M, N, K, out, ldo, stream);
-    case EPI_GELU_BF16: return launch_pair<EPI_GELU_BF16>(tmA, tmB, M, N, K, out, ldo, stream);
-    case EPI_RESID_F32: return launch_pair<EPI_RESID_F32>(tmA, tmB, M, N, K, out, ldo, stream);
-    case EPI_F32: return launch_pair<EPI_F32>(tmA, tmB, M, N, K, out, ldo, stream);
+    case EPI_BF16: return launch_pair_np<EPI_BF16>(tmA, tmB, M, N, K, out, ldo, stream);
+    case EPI_GELU_BF16: return launch_pair_np<EPI_GELU_BF16>(tmA, tmB, M, N, K, out, ldo, stream);
+    case EPI_RESID_F32: return launch_pair_np<EPI_RESID_F32>(tmA, tmB, M, N, K, out, ldo, stream);
+    case EPI_F32: return launch_pair_np<EPI_F32>(tmA, tmB, M, N, K, out, ldo, stream);
   }
   return cudaErrorInvalidValue;
 }
@@ -161,6 +202,10 @@ cudaError_t gemm_bf16(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int
     case 64: return launch_bn<64>(tmA, tmB, M, N, K, out, ldo, epi, stream);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t gemm_set_trace(unsigned long long* dev_buf) {
+  return cudaMemcpyToSymbol(g_gemm_trace, &dev_buf, sizeof(dev_buf));
 }
 
 }  // namespace srk

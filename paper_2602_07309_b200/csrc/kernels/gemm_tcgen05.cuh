@@ -28,6 +28,18 @@ namespace srk {
 
 enum GemmEpilogue : int { EPI_BF16 = 0, EPI_GELU_BF16 = 1, EPI_RESID_F32 = 2, EPI_F32 = 3 };
 
+// Optional per-CTA timeline of the pair kernel (%globaltimer ns, 64 slots per
+// CTA): 0 entry, 1 setup done, 2+i MMA of local tile i issued, 24+i epilogue
+// of tile i done, 63 exit. Kernel tuning only (sr_debug_gemm_trace).
+__device__ unsigned long long* g_gemm_trace = nullptr;
+__device__ __forceinline__ void gemm_trace(int slot) {
+  if (g_gemm_trace != nullptr && blockIdx.x < 256) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gemm_trace[blockIdx.x * 64 + slot] = t;
+  }
+}
+
 template <int BN>
 struct GemmCfg {
   static constexpr int BM = 128;
@@ -239,6 +251,13 @@ __global__ void __launch_bounds__(320, 1)
 // each CTA's 128 accumulator rows into its own TMEM. Per SM this halves the
 // B operand traffic through shared memory relative to the 1-CTA 128 x 256
 // tile (the 1-CTA kernel is smem-bandwidth bound at ~64% tensor-pipe).
+//
+// NP = 2 pairs per cluster (cluster of 4): the two pairs compute adjacent
+// 256-column tiles of the same 256 rows, so each A k-block is fetched once
+// and multicast to both pairs (pair kb % 2 issues it): a quarter less L2 ->
+// SM operand traffic, at the cost of the SMs a 4-CTA cluster grid cannot use
+// (132 of 148 on B200). Opt-in (SRK_GEMM_NP=2): on the C2 shapes the per-tile
+// time did not change, so NP = 1 on all 148 SMs is faster.
 struct GemmPairCfg {
   static constexpr int BM = 128;  // rows per CTA (pair: 256)
   static constexpr int BN = 256;  // output columns per pair tile
@@ -246,27 +265,36 @@ struct GemmPairCfg {
   static constexpr int A_BYTES = BM * BK * 2;        // 16 KB
   static constexpr int B_BYTES = (BN / 2) * BK * 2;  // 16 KB (this CTA's half of B)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = 6;
+#ifndef SRK_PAIR_STAGES
+#define SRK_PAIR_STAGES 6
+#endif
+#ifndef SRK_PAIR_STG_BUFS
+#define SRK_PAIR_STG_BUFS 1
+#endif
+  static constexpr int STAGES = SRK_PAIR_STAGES;
   static constexpr int TMEM_COLS = 2 * BN;  // double-buffered 128 x 256 fp32
   static constexpr int EPI_WARPS = 8;
+  static constexpr int STG_BUFS = SRK_PAIR_STG_BUFS;  // staging buffers per epilogue warp
   static constexpr int STG_BYTES = 32 * 128;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_WARPS * STG_BYTES + 256 + 1024;
+  static constexpr int SMEM_BYTES =
+      STAGES * STAGE_BYTES + EPI_WARPS * STG_BUFS * STG_BYTES + 256 + 1024;
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
 };
 
-template <int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
+template <int EPI, int NP>
+__global__ void __launch_bounds__(320, 1)
     gemm_bf16_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                                   const __grid_constant__ CUtensorMap tmB,
                                   const __grid_constant__ CUtensorMap tmC, int M, int N, int K) {
   using C = GemmPairCfg;
+  static_assert(NP == 1 || NP == 2, "one or two CTA pairs per cluster");
   constexpr int BN = C::BN;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint8_t* sStg = sB + C::STAGES * C::B_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + C::EPI_WARPS * C::STG_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + C::EPI_WARPS * C::STG_BUFS * C::STG_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -275,13 +303,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  const int pair = static_cast<int>(cluster_id_x());
+  const int pr = static_cast<int>(rank >> 1);  // pair within the cluster
+  const int cr = static_cast<int>(rank & 1);   // CTA within the pair
+  const bool leader = cr == 0;
+  const uint32_t lead_rank = rank & ~1u;
+  const int pair = static_cast<int>(cluster_id_x());  // cluster index
   const int n_pairs = static_cast<int>(nclusters_x());
   const int m_tiles = (M + 2 * C::BM - 1) / (2 * C::BM);
-  const int n_tiles = N / BN;
+  const int n_tiles = N / (BN * NP);  // cluster tiles along N
   const int num_tiles = m_tiles * n_tiles;
   const int nk = (K + C::BK - 1) / C::BK;
+  if (threadIdx.x == 0) gemm_trace(0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -289,7 +321,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     tma_prefetch_desc(&tmC);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 2);  // leader: own expect_tx arrival + the peer's arrival
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], NP);  // one commit from every pair that reads the stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -305,24 +337,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) gemm_trace(1);
 
   if (warp == 0) {
     if (lane == 0) {
+#ifndef SRK_PAIR_APOL
+#define SRK_PAIR_APOL 2
+#endif
       const uint64_t pol_b = policy_evict_last();
-      const uint64_t pol_a = policy_evict_first();
-      const uint32_t peer_full0 = mapa_shared(smem_u32(&full[0]), 0);
+      const uint64_t pol_a = SRK_PAIR_APOL == 0   ? policy_evict_first()
+                             : SRK_PAIR_APOL == 1 ? policy_evict_normal()
+                                                  : policy_evict_last();
+      const uint32_t peer_full0 = mapa_shared(smem_u32(&full[0]), lead_rank);
+      const uint16_t a_mask = static_cast<uint16_t>((1u << cr) | (1u << (cr + 2)));
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = pair; tile < num_tiles; tile += n_pairs) {
-        const int m0 = (tile / n_tiles) * 2 * C::BM + static_cast<int>(rank) * C::BM;
-        const int n0 = (tile % n_tiles) * BN + static_cast<int>(rank) * (BN / 2);
+        const int m0 = (tile / n_tiles) * 2 * C::BM + cr * C::BM;
+        const int n0 = ((tile % n_tiles) * NP + pr) * BN + cr * (BN / 2);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader)
             mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
           else
             mbar_arrive_cluster(peer_full0 + stage * 8);
-          tma_load_2d_pair(&tmA, &full[stage], sA + stage * C::A_BYTES, kb * C::BK, m0, pol_a);
+          if constexpr (NP == 1)
+            tma_load_2d_pair(&tmA, &full[stage], sA + stage * C::A_BYTES, kb * C::BK, m0, pol_a);
+          else if ((kb & 1) == pr)  // A is shared by both pairs: one multicast load
+            tma_load_2d_pair_mc(&tmA, &full[stage], sA + stage * C::A_BYTES, kb * C::BK, m0,
+                                a_mask, pol_a);
           tma_load_2d_pair(&tmB, &full[stage], sB + stage * C::B_BYTES, kb * C::BK, n0, pol_b);
           if (++stage == C::STAGES) {
             stage = 0;
@@ -353,13 +396,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           for (int k = 0; k < C::BK / 16; ++k)
             umma_bf16_pair(d_tmem, sw128_kmajor_desc(a_addr + k * 32),
                            sw128_kmajor_desc(b_addr + k * 32), idesc, (kb | k) != 0 ? 1u : 0u);
-          umma_commit_pair(&empty[stage]);
+          umma_commit_pair(&empty[stage], NP == 1 ? 0x3 : 0xF);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair(&tfull[acc]);
+        umma_commit_pair(&tfull[acc], static_cast<uint16_t>(3u << (2 * pr)));
+        if (local < 22) gemm_trace(2 + local);
       }
     }
     __syncwarp();
@@ -368,46 +412,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     constexpr int SPAN = BN / 2;  // columns per epilogue warp
     const int quad = warp & 3;
     const int col0 = ((warp - 2) >> 2) * SPAN;
-    uint8_t* stg = sStg + (warp - 2) * C::STG_BYTES;
-    const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+    uint8_t* stg0 = sStg + (warp - 2) * C::STG_BUFS * C::STG_BYTES;
+    const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), lead_rank);
     const uint64_t pol_keep = policy_evict_last();
     int local = 0;
+    int nstg = 0;  // staging chunks issued by this warp (buffer = nstg % STG_BUFS)
     for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      const int m0 = (tile / n_tiles) * 2 * C::BM + static_cast<int>(rank) * C::BM;
-      const int n0 = (tile % n_tiles) * BN;
+      const int m0 = (tile / n_tiles) * 2 * C::BM + cr * C::BM;
+      const int n0 = ((tile % n_tiles) * NP + pr) * BN;
       const int r0 = m0 + quad * 32;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (r0 < M) {
 #pragma unroll 1
-        for (int c = col0; c < col0 + SPAN; c += CW) {
-          if (lane == 0) bulk_wait_read0();
-          __syncwarp();
+        for (int c = col0; c < col0 + SPAN; c += CW, ++nstg) {
+          uint8_t* stg = stg0 + (nstg % C::STG_BUFS) * C::STG_BYTES;
           uint8_t* row_base = stg + lane * 128;
           if constexpr (EpiOut<EPI>::F32) {
             uint32_t r[32];
             tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c,
                                r);
+            // The TMEM read overlaps the wait for this buffer's previous store.
+            if (lane == 0) bulk_wait_read<C::STG_BUFS - 1>();
+            __syncwarp();
             tmem_ld_wait();
 #pragma unroll
             for (int k = 0; k < 8; ++k)
               *reinterpret_cast<uint4*>(row_base + ((k ^ (lane & 7)) * 16)) =
                   make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
           } else {
+            uint32_t r[2][32];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+              tmem_ld_32x32b_x32(
+                  tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c + hh * 32,
+                  r[hh]);
+            if (lane == 0) bulk_wait_read<C::STG_BUFS - 1>();
+            __syncwarp();
+            tmem_ld_wait();
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-              uint32_t r[32];
-              tmem_ld_32x32b_x32(
-                  tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c + hh * 32, r);
-              tmem_ld_wait();
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 float f[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                  f[j] = __uint_as_float(r[8 * k + j]);
+                  f[j] = __uint_as_float(r[hh][8 * k + j]);
                   if constexpr (EPI == EPI_GELU_BF16) f[j] = gelu_erf(f[j]);
                 }
                 const int chunk = hh * 4 + k;
@@ -431,6 +483,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+      if (warp == 2 && lane == 0 && local < 38) gemm_trace(24 + local);
     }
     if (lane == 0) bulk_wait0();
   }
@@ -439,6 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   cluster_sync();
   tc_fence_after();
   if (warp == 1) tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+  if (threadIdx.x == 0) gemm_trace(63);
 }
 
 }  // namespace srk

@@ -73,6 +73,7 @@ cudaError_t attention_tc(const CUtensorMap& tm_qkv, const RowSpan* spans, const 
                          cudaStream_t stream);
 // Tuning aid: per-CTA clock64 timeline of attention_tc (nullptr disables).
 cudaError_t attention_set_trace(unsigned long long* dev_buf);
+cudaError_t gemm_set_trace(unsigned long long* dev_buf);
 // Query rows per attention tile for a head size (128 on the tcgen05 path).
 int attention_tile_rows(int head_dim);
 

@@ -25,8 +25,11 @@ def _ok(st):
     assert st == 0, lib.sr_last_error().decode()
 
 
+# N % 256 == 0 takes the CTA-pair path (SRK_GEMM_NP=2: 4-CTA clusters with A
+# multicast when N % 512 == 0), other N the 1-CTA kernel.
 GEMM_SHAPES = [(128, 256, 64), (300, 3072, 1024), (1000, 1536, 1024), (257, 1024, 1536),
-               (77, 192, 64), (500, 64, 256), (4096, 1024, 1024), (129, 128, 2048)]
+               (77, 192, 64), (500, 64, 256), (4096, 1024, 1024), (129, 128, 2048),
+               (6000, 3072, 1024), (2000, 512, 64), (700, 768, 512)]
 
 
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
@@ -59,7 +62,8 @@ def test_gemm_bf16_and_gelu_epilogues(cuda, M, N, K):
     assert torch.allclose(c.float(), gref, rtol=8e-3, atol=1e-3)
 
 
-@pytest.mark.parametrize("M,N,K", [(300, 1024, 1024), (257, 1024, 1536), (64, 64, 256)])
+@pytest.mark.parametrize("M,N,K", [(300, 1024, 1024), (257, 1024, 1536), (64, 64, 256),
+                                   (5000, 1024, 1536)])
 def test_gemm_residual_epilogue(cuda, M, N, K):
     import torch
     g = torch.Generator(device="cpu").manual_seed(9)
@@ -181,3 +185,28 @@ def test_topk_matches_stable_sort(cuda, n, k, ties):
     order = sorted(range(n), key=lambda i: (-scores[i], ids[i]))[:kk]
     assert list(oi) == [int(ids[i]) for i in order]
     assert list(ox) == order
+
+
+def test_gemm_single_pair_path_matches_cluster_path(cuda):
+    """SRK_GEMM_NP=2 (4-CTA clusters, A multicast to two pairs) gives the same
+    bits as the default single-pair path: the K order per tile is identical."""
+    import subprocess
+    import sys
+    code = (
+        "import torch, ctypes as C\n"
+        "from paper_2602_07309_b200._capi import lib\n"
+        "g = torch.Generator().manual_seed(3)\n"
+        "a = torch.randn(3000, 1024, generator=g).bfloat16().cuda()\n"
+        "b = torch.randn(1536, 1024, generator=g).bfloat16().cuda()\n"
+        "c = torch.zeros(3000, 1536, device='cuda')\n"
+        "assert lib.sr_kernel_gemm(C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), 3000, 1536,"
+        " 1024, C.c_void_p(c.data_ptr()), 1536, 3, None) == 0\n"
+        "import hashlib, sys; sys.stdout.write(hashlib.sha1(c.cpu().numpy().tobytes()).hexdigest())\n")
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for np_ in ("1", "2"):
+        env = dict(os.environ, SRK_GEMM_NP=np_, PYTHONPATH=root)
+        out[np_] = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                                  text=True, timeout=300, check=True).stdout
+    assert out["1"] == out["2"] and len(out["1"]) == 40
