@@ -242,6 +242,15 @@ int32_t sr_plan_run_sharded(sr_plan* p, sr_comm* c); /* resident variant */
  * Synchronous when stream is NULL, asynchronous on an explicit stream. */
 int32_t sr_kernel_gemm(const void* a_bf16, const void* b_bf16, int32_t M, int32_t N, int32_t K,
                        void* c, int32_t ldc, int32_t epi, void* stream);
+/* LayerNorm folded into the projections. Device pointers.
+ * epi 4: c = x fp32 [M x N] += A.B^T, xb = bf16(x) [M x N],
+ *        stats[N/128][ld] = float2 (mean, M2) of x over each 128-column slice.
+ * epi 5 / 6: c = bf16([gelu](rstd * (A.B^T - mean * colsum))), A = bf16 x,
+ *        B = diag(gain) W, mean/rstd from stats[n_parts][ld] (each part over
+ *        K / n_parts columns), colsum[N]. N % 256 == 0 (CTA-pair kernel). */
+int32_t sr_kernel_gemm_ln(const void* a_bf16, const void* b_bf16, int32_t M, int32_t N, int32_t K,
+                          void* c, int32_t ldc, int32_t epi, void* xb_bf16, void* stats,
+                          int32_t n_parts, const float* colsum, int32_t ld, void* stream);
 /* Segment-masked attention. qkv [M x 3d] bf16, spans [M x 4] int32
  * {prefix_begin, prefix_end, span_start, 0}; out [M x d] bf16. Tiles are
  * planned internally. */

@@ -101,6 +101,7 @@ _sig("sr_comm_destroy", None, vp)
 _sig("sr_engine_score_sharded", i32, vp, vp, P(RequestC), P(ResultC))
 _sig("sr_plan_run_sharded", i32, vp, vp)
 _sig("sr_kernel_gemm", i32, vp, vp, i32, i32, i32, vp, i32, i32, vp)
+_sig("sr_kernel_gemm_ln", i32, vp, vp, i32, i32, i32, vp, i32, i32, vp, vp, i32, vp, i32, vp)
 _sig("sr_kernel_attention", i32, vp, P(i32), i32, i32, i32, vp, vp)
 _sig("sr_kernel_layernorm", i32, vp, vp, vp, i32, i32, vp)
 _sig("sr_debug_attention_trace", i32, vp)
@@ -120,6 +121,6 @@ HEADER_SYMBOLS = [
     "sr_plan_create_batch", "sr_plan_fetch_batch", "sr_plan_run", "sr_plan_sync", "sr_plan_fetch", "sr_plan_kernel_count", "sr_plan_destroy",
     "sr_plan_profile", "sr_plan_shape",
     "sr_nccl_unique_id", "sr_comm_create", "sr_comm_destroy", "sr_engine_score_sharded",
-    "sr_plan_run_sharded", "sr_kernel_gemm", "sr_kernel_attention", "sr_kernel_layernorm",
+    "sr_plan_run_sharded", "sr_kernel_gemm", "sr_kernel_gemm_ln", "sr_kernel_attention", "sr_kernel_layernorm",
     "sr_kernel_topk", "sr_debug_attention_trace", "sr_debug_gemm_trace",
 ]

@@ -493,6 +493,32 @@ int32_t sr_kernel_gemm(const void* a_bf16, const void* b_bf16, int32_t M, int32_
   });
 }
 
+int32_t sr_kernel_gemm_ln(const void* a_bf16, const void* b_bf16, int32_t M, int32_t N, int32_t K,
+                          void* c, int32_t ldc, int32_t epi, void* xb_bf16, void* stats,
+                          int32_t n_parts, const float* colsum, int32_t ld, void* stream) {
+  return guard([&] {
+    if (epi < srk::EPI_RESID_LN || epi > srk::EPI_LN_GELU_BF16)
+      srh::fail(SR_PARAMETER, "epi must be 4, 5 or 6");
+    if (!srk::gemm_use_pair(N)) srh::fail(SR_SPEC_VIOLATION, "N must be a multiple of 256");
+    if (K % 8 != 0) srh::fail(SR_SPEC_VIOLATION, "K must be a multiple of 8");
+    CUtensorMap ta, tb;
+    SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&ta, a_bf16, M, K, 128, 64));
+    SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tb, b_bf16, N, K, srk::gemm_b_box_rows(N), 64));
+    srk::LnFold f{};
+    f.ld = ld;
+    if (epi == srk::EPI_RESID_LN) {
+      f.xb = static_cast<__nv_bfloat16*>(xb_bf16);
+      f.stats_out = static_cast<float*>(stats);
+    } else {
+      f.stats_in = static_cast<const float*>(stats);
+      f.colsum = colsum;
+      f.n_parts = n_parts;
+    }
+    SR_CUDA_CHECK(srk::gemm_auto(ta, tb, M, N, K, c, ldc, epi, static_cast<cudaStream_t>(stream), &f));
+    if (stream == nullptr) SR_CUDA_CHECK(cudaStreamSynchronize(nullptr));
+  });
+}
+
 int32_t sr_kernel_attention(const void* qkv, const int32_t* spans_host, int32_t M,
                             int32_t n_heads, int32_t head_dim, void* out, void* stream) {
   return guard([&] {

@@ -15,6 +15,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.hpp"
@@ -60,6 +61,16 @@ Engine::Engine(const ModelWeights& w, int device) : cfg_(w.config), device_(devi
   if (hd != 16 && hd != 32 && hd != 64 && hd != 128)
     fail(SR_SPEC_VIOLATION, "head_dim must be one of 16/32/64/128");
   SR_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  // Opt-in (SRK_FOLD_LN=1): LN folded into the projections when every GEMM
+  // takes the pair kernel. Measured on B200 at C2 it breaks even with the
+  // separate LayerNorm kernel (the residual epilogue's extra x traffic slows
+  // the main loop as much as the LN launches cost), so it is off by default.
+  {
+    const char* v = std::getenv("SRK_FOLD_LN");
+    const bool allow = v != nullptr && std::atoi(v) != 0;
+    fold_ln_ = allow && srk::gemm_use_pair(d) && srk::gemm_use_pair(3 * d) &&
+               srk::gemm_use_pair(F) && d % 128 == 0 && d / 128 <= 16;
+  }
 
   tok_emb_ = upload(w.tok_emb, allocs_);
   pos_emb_ = upload(w.pos_emb, allocs_);
@@ -69,12 +80,13 @@ Engine::Engine(const ModelWeights& w, int device) : cfg_(w.config), device_(devi
   float* stage = nullptr;
   const size_t stage_elems = static_cast<size_t>(std::max(d, F)) * std::max(d, F);
   SR_CUDA_CHECK(cudaMalloc(&stage, stage_elems * sizeof(float)));
-  auto conv = [&](const std::vector<float>& src, __nv_bfloat16* dst, int K, int N) {
+  auto conv = [&](const std::vector<float>& src, __nv_bfloat16* dst, int K, int N,
+                  const float* scale_k) {
     // Same-stream copy: a pageable cudaMemcpy may return before its DMA lands,
     // and stream_ is non-blocking w.r.t. the legacy stream.
     SR_CUDA_CHECK(cudaMemcpyAsync(stage, src.data(), src.size() * sizeof(float),
                                   cudaMemcpyHostToDevice, stream_));
-    SR_CUDA_CHECK(srk::transpose_to_bf16(stage, dst, K, N, stream_));
+    SR_CUDA_CHECK(srk::transpose_to_bf16(stage, dst, K, N, stream_, scale_k));
     SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
   };
   layers_.resize(cfg_.n_layers);
@@ -91,14 +103,26 @@ Engine::Engine(const ModelWeights& w, int device) : cfg_(w.config), device_(devi
     L.wo = alloc_bf16(static_cast<size_t>(d) * d);
     L.win = alloc_bf16(static_cast<size_t>(F) * d);
     L.wout = alloc_bf16(static_cast<size_t>(d) * F);
-    conv(lw.wq, L.wqkv, d, d);
-    conv(lw.wk, L.wqkv + static_cast<size_t>(d) * d, d, d);
-    conv(lw.wv, L.wqkv + static_cast<size_t>(2) * d * d, d, d);
-    conv(lw.wo, L.wo, d, d);
-    conv(lw.w_mlp_in, L.win, d, F);
-    conv(lw.w_mlp_out, L.wout, F, d);
     L.ln1 = upload(lw.ln1_gain, allocs_);
     L.ln2 = upload(lw.ln2_gain, allocs_);
+    // Folded LN: the gains scale the K rows of the following projection.
+    const float* g1 = fold_ln_ ? L.ln1 : nullptr;
+    const float* g2 = fold_ln_ ? L.ln2 : nullptr;
+    conv(lw.wq, L.wqkv, d, d, g1);
+    conv(lw.wk, L.wqkv + static_cast<size_t>(d) * d, d, d, g1);
+    conv(lw.wv, L.wqkv + static_cast<size_t>(2) * d * d, d, d, g1);
+    conv(lw.wo, L.wo, d, d, nullptr);
+    conv(lw.w_mlp_in, L.win, d, F, g2);
+    conv(lw.w_mlp_out, L.wout, F, d, nullptr);
+    if (fold_ln_) {
+      SR_CUDA_CHECK(cudaMalloc(&L.cs_qkv, sizeof(float) * 3 * d));
+      allocs_.push_back(L.cs_qkv);
+      SR_CUDA_CHECK(cudaMalloc(&L.cs_in, sizeof(float) * F));
+      allocs_.push_back(L.cs_in);
+      SR_CUDA_CHECK(srk::bf16_row_sums(L.wqkv, 3 * d, d, L.cs_qkv, stream_));
+      SR_CUDA_CHECK(srk::bf16_row_sums(L.win, F, d, L.cs_in, stream_));
+      SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    }
     make_weight_map(&L.tm_qkv, L.wqkv, 3 * d, d);
     make_weight_map(&L.tm_o, L.wo, d, d);
     make_weight_map(&L.tm_in, L.win, F, d);
@@ -151,6 +175,8 @@ void Engine::ensure_workspace(int32_t M) {
   xn_.release();
   qkv_.release();
   h_.release();
+  xb_.release();
+  stats_.release();
   SR_CUDA_CHECK(cudaMalloc(&x_.ptr, rows * d * sizeof(float)));
   x_.cap = rows * d;
   SR_CUDA_CHECK(cudaMalloc(&xn_.ptr, rows * d * sizeof(__nv_bfloat16)));
@@ -168,6 +194,16 @@ void Engine::ensure_workspace(int32_t M) {
   SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tm_xn_, xn_.ptr, rows, d, 128, 64));
   SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tm_h_, h_.ptr, rows, F, 128, 64));
   SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tm_qkv_, qkv_.ptr, rows, 3 * d, 128, 64));
+  if (fold_ln_) {
+    SR_CUDA_CHECK(cudaMalloc(&xb_.ptr, rows * d * sizeof(__nv_bfloat16)));
+    xb_.cap = rows * d;
+    SR_CUDA_CHECK(cudaMemset(xb_.ptr, 0, rows * d * sizeof(__nv_bfloat16)));
+    const size_t ns = (d / 128) * static_cast<size_t>(rows) * 2;
+    SR_CUDA_CHECK(cudaMalloc(&stats_.ptr, ns * sizeof(float)));
+    stats_.cap = ns;
+    SR_CUDA_CHECK(cudaMemset(stats_.ptr, 0, ns * sizeof(float)));
+    SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tm_xb_, xb_.ptr, rows, d, 128, 64));
+  }
   ws_rows_ = rows;
   ++ws_epoch_;
 }
@@ -203,42 +239,90 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
   auto E = [&]() {
     if (prof) prof->end();
   };
-  B(PROF_EMBED_LN);
-  SR_CUDA_CHECK(srk::embed_ln(p.src.ptr, p.pos.ptr, tok_emb_, p.pack.n_soft ? p.soft.ptr : nullptr,
-                              pos_emb_, layers_[0].ln1, x_.ptr, xn_.ptr, M, d, s));
-  E();
-  ++n;
-  for (int l = 0; l < cfg_.n_layers; ++l) {
-    const auto& L = layers_[l];
-    B(PROF_GEMM_QKV);
-    SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_qkv, M, 3 * d, d, qkv_.ptr, 3 * d, 0, s));
-    E();
-    B(PROF_ATTENTION);
+  auto attention = [&]() {
     if (hd >= 64)
       SR_CUDA_CHECK(srk::attention_tc(tm_qkv_, p.spans.ptr, p.tiles.ptr,
                                       static_cast<int>(p.pack.tiles.size()), xn_.ptr, M, H, hd, s));
     else  // toy head sizes (16/32): the 64-row mma.sync kernel
       SR_CUDA_CHECK(srk::attention(qkv_.ptr, p.spans.ptr, p.tiles.ptr,
                                    static_cast<int>(p.pack.tiles.size()), xn_.ptr, M, H, hd, s));
+  };
+  if (fold_ln_) {
+    // LN folded into the GEMMs (gemm_tcgen05.cuh GemmLnArgs): no LayerNorm launches.
+    srk::LnFold in{}, out{};
+    in.stats_in = stats_.ptr;
+    in.ld = ws_rows_;
+    out.xb = xb_.ptr;
+    out.stats_out = stats_.ptr;
+    out.ld = ws_rows_;
+    B(PROF_EMBED_LN);
+    SR_CUDA_CHECK(srk::embed_stats(p.src.ptr, p.pos.ptr, tok_emb_,
+                                   p.pack.n_soft ? p.soft.ptr : nullptr, pos_emb_, x_.ptr,
+                                   xb_.ptr, stats_.ptr, M, d, s));
     E();
-    B(PROF_GEMM_O);
-    SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_o, M, d, d, x_.ptr, d, 2, s));
-    E();
-    B(PROF_LAYERNORM);
-    SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, L.ln2, xn_.ptr, M, d, s));
-    E();
-    B(PROF_GEMM_IN);
-    SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_in, M, F, d, h_.ptr, F, 1, s));
-    E();
-    B(PROF_GEMM_OUT);
-    SR_CUDA_CHECK(srk::gemm_auto(tm_h_, L.tm_out, M, d, F, x_.ptr, d, 2, s));
-    E();
-    n += 6;
-    if (l + 1 < cfg_.n_layers) {
-      B(PROF_LAYERNORM);
-      SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, layers_[l + 1].ln1, xn_.ptr, M, d, s));
+    ++n;
+    for (int l = 0; l < cfg_.n_layers; ++l) {
+      const auto& L = layers_[l];
+      const bool last = l + 1 == cfg_.n_layers;
+      in.n_parts = l == 0 ? 1 : d / 128;
+      in.colsum = L.cs_qkv;
+      B(PROF_GEMM_QKV);
+      SR_CUDA_CHECK(srk::gemm_auto(tm_xb_, L.tm_qkv, M, 3 * d, d, qkv_.ptr, 3 * d,
+                                   srk::EPI_LN_BF16, s, &in));
       E();
-      ++n;
+      B(PROF_ATTENTION);
+      attention();
+      E();
+      B(PROF_GEMM_O);
+      SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_o, M, d, d, x_.ptr, d, srk::EPI_RESID_LN, s, &out));
+      E();
+      in.n_parts = d / 128;
+      in.colsum = L.cs_in;
+      B(PROF_GEMM_IN);
+      SR_CUDA_CHECK(srk::gemm_auto(tm_xb_, L.tm_in, M, F, d, h_.ptr, F, srk::EPI_LN_GELU_BF16, s,
+                                   &in));
+      E();
+      // The last layer's x goes to the score head (final LN on fp32 rows):
+      // no bf16 copy or statistics needed.
+      B(PROF_GEMM_OUT);
+      SR_CUDA_CHECK(srk::gemm_auto(tm_h_, L.tm_out, M, d, F, x_.ptr, d,
+                                   last ? srk::EPI_RESID_F32 : srk::EPI_RESID_LN, s, &out));
+      E();
+      n += 5;
+    }
+  } else {
+    B(PROF_EMBED_LN);
+    SR_CUDA_CHECK(srk::embed_ln(p.src.ptr, p.pos.ptr, tok_emb_, p.pack.n_soft ? p.soft.ptr : nullptr,
+                                pos_emb_, layers_[0].ln1, x_.ptr, xn_.ptr, M, d, s));
+    E();
+    ++n;
+    for (int l = 0; l < cfg_.n_layers; ++l) {
+      const auto& L = layers_[l];
+      B(PROF_GEMM_QKV);
+      SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_qkv, M, 3 * d, d, qkv_.ptr, 3 * d, 0, s));
+      E();
+      B(PROF_ATTENTION);
+      attention();
+      E();
+      B(PROF_GEMM_O);
+      SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_o, M, d, d, x_.ptr, d, 2, s));
+      E();
+      B(PROF_LAYERNORM);
+      SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, L.ln2, xn_.ptr, M, d, s));
+      E();
+      B(PROF_GEMM_IN);
+      SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_in, M, F, d, h_.ptr, F, 1, s));
+      E();
+      B(PROF_GEMM_OUT);
+      SR_CUDA_CHECK(srk::gemm_auto(tm_h_, L.tm_out, M, d, F, x_.ptr, d, 2, s));
+      E();
+      n += 6;
+      if (l + 1 < cfg_.n_layers) {
+        B(PROF_LAYERNORM);
+        SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, layers_[l + 1].ln1, xn_.ptr, M, d, s));
+        E();
+        ++n;
+      }
     }
   }
   B(PROF_SCORE_HEAD);

@@ -65,6 +65,9 @@ struct LayerDev {
   __nv_bfloat16* wout = nullptr;  // [d x ff]
   float* ln1 = nullptr;
   float* ln2 = nullptr;
+  // folded-LN path: wqkv / win hold diag(gain) W; their column sums
+  float* cs_qkv = nullptr;  // [3d]
+  float* cs_in = nullptr;   // [ff]
   CUtensorMap tm_qkv, tm_o, tm_in, tm_out;
 };
 
@@ -123,6 +126,8 @@ class Engine {
   cudaStream_t stream() const { return stream_; }
   int n_tasks() const { return 1 + static_cast<int>(cfg_.head_specs.size()); }
   std::mutex& mutex() { return mu_; }
+  // LayerNorm folded into the GEMM epilogues (all projections on the pair path).
+  bool fold_ln() const { return fold_ln_; }
 
   // Builds a plan: validates + packs + uploads inputs + captures the graph.
   std::unique_ptr<Plan> make_plan(const sr_request* reqs, int n_req, int32_t k);
@@ -159,13 +164,16 @@ class Engine {
   int32_t* task_col_ = nullptr;
   int32_t* task_arity_ = nullptr;
   int n_cols_ = 0, yes_col_ = 0, no_col_ = 0;
+  bool fold_ln_ = false;
   std::vector<LayerDev> layers_;
   std::vector<void*> allocs_;
   // workspace
   int32_t ws_rows_ = 0;
   DevBuf<float> x_;
   DevBuf<__nv_bfloat16> xn_, qkv_, h_;
-  CUtensorMap tm_xn_, tm_h_, tm_qkv_;
+  DevBuf<__nv_bfloat16> xb_;   // folded LN: bf16 copy of the residual stream (GEMM A operand)
+  DevBuf<float> stats_;        // folded LN: [d/128][ws_rows_] (mean, M2) partials
+  CUtensorMap tm_xn_, tm_h_, tm_qkv_, tm_xb_;
   uint64_t ws_epoch_ = 0;  // bumps when workspace moves (graphs must be re-captured)
   // shape-keyed plan cache for score()
   std::map<std::tuple<int32_t, int32_t, int32_t, int32_t, int32_t, int32_t, int32_t>,

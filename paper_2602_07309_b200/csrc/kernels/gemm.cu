@@ -2,6 +2,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "gemm_tcgen05.cuh"
@@ -93,14 +94,14 @@ int gemm_pairs_per_cluster(int N) {
     const char* v = std::getenv("SRK_GEMM_NP");
     return v != nullptr ? std::atoi(v) : 0;
   }();
-  if (N % (2 * GemmPairCfg::BN) == 0 && forced == 2) return 2;
+  if (N % (2 * GemmPairCfg<EPI_BF16>::BN) == 0 && forced == 2) return 2;
   return 1;
 }
 
 template <int EPI, int NP>
 cudaError_t launch_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
-                        void* out, int ldo, cudaStream_t stream) {
-  using C = GemmPairCfg;
+                        void* out, int ldo, const GemmLnArgs& ln, cudaStream_t stream) {
+  using C = GemmPairCfg<EPI>;
   auto kern = gemm_bf16_tcgen05_pair_kernel<EPI, NP>;
   static int max_clusters = 0;  // co-resident clusters of 2*NP CTAs (per process, one GPU type)
   cudaLaunchConfig_t cfg = {};
@@ -134,28 +135,53 @@ cudaError_t launch_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, i
   cudaError_t e = make_out_map<EPI>(&tmC, out, M, N, ldo);
   if (e != cudaSuccess) return e;
   cfg.gridDim = dim3(2 * NP * clusters, 1, 1);
-  e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, M, N, K);
+  e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, ln, M, N, K);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 template <int EPI>
 cudaError_t launch_pair_np(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
-                           void* out, int ldo, cudaStream_t stream) {
+                           void* out, int ldo, const GemmLnArgs& ln, cudaStream_t stream) {
   if (gemm_pairs_per_cluster(N) == 2)
-    return launch_pair<EPI, 2>(tmA, tmB, M, N, K, out, ldo, stream);
-  return launch_pair<EPI, 1>(tmA, tmB, M, N, K, out, ldo, stream);
+    return launch_pair<EPI, 2>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+  return launch_pair<EPI, 1>(tmA, tmB, M, N, K, out, ldo, ln, stream);
 }
 
 cudaError_t gemm_bf16_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
-                           void* out, int ldo, int epi, cudaStream_t stream) {
+                           void* out, int ldo, int epi, cudaStream_t stream, const LnFold* fold) {
   if (M <= 0) return cudaSuccess;
-  if (N % GemmPairCfg::BN != 0 || K % 8 != 0) return cudaErrorInvalidValue;
+  if (N % GemmPairCfg<EPI_BF16>::BN != 0 || K % 8 != 0) return cudaErrorInvalidValue;
+  GemmLnArgs ln;
+  std::memset(&ln, 0, sizeof(ln));
+  if (epi == EPI_RESID_LN) {
+    if (fold == nullptr || fold->xb == nullptr || fold->stats_out == nullptr || fold->ld < M)
+      return cudaErrorInvalidValue;
+    cudaError_t e = make_out_map<EPI_BF16>(&ln.tm_xb, fold->xb, M, N, ldo);
+    if (e != cudaSuccess) return e;
+    ln.stats_out = reinterpret_cast<float2*>(fold->stats_out);
+    ln.ld = fold->ld;
+  } else if (epi == EPI_LN_BF16 || epi == EPI_LN_GELU_BF16) {
+    if (fold == nullptr || fold->stats_in == nullptr || fold->colsum == nullptr ||
+        fold->n_parts < 1 || fold->n_parts > 16 || K % fold->n_parts != 0 || fold->ld < M)
+      return cudaErrorInvalidValue;
+    ln.stats_in = reinterpret_cast<const float2*>(fold->stats_in);
+    ln.colsum = fold->colsum;
+    ln.n_parts = fold->n_parts;
+    ln.ld = fold->ld;
+  }
   switch (epi) {
-    case EPI_BF16: return launch_pair_np<EPI_BF16>(tmA, tmB, M, N, K, out, ldo, stream);
-    case EPI_GELU_BF16: return launch_pair_np<EPI_GELU_BF16>(tmA, tmB, M, N, K, out, ldo, stream);
-    case EPI_RESID_F32: return launch_pair_np<EPI_RESID_F32>(tmA, tmB, M, N, K, out, ldo, stream);
-    case EPI_F32: return launch_pair_np<EPI_F32>(tmA, tmB, M, N, K, out, ldo, stream);
+    case EPI_BF16: return launch_pair_np<EPI_BF16>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+    case EPI_GELU_BF16:
+      return launch_pair_np<EPI_GELU_BF16>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+    case EPI_RESID_F32:
+      return launch_pair_np<EPI_RESID_F32>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+    case EPI_F32: return launch_pair_np<EPI_F32>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+    case EPI_RESID_LN:
+      return launch_pair_np<EPI_RESID_LN>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+    case EPI_LN_BF16: return launch_pair_np<EPI_LN_BF16>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+    case EPI_LN_GELU_BF16:
+      return launch_pair_np<EPI_LN_GELU_BF16>(tmA, tmB, M, N, K, out, ldo, ln, stream);
   }
   return cudaErrorInvalidValue;
 }

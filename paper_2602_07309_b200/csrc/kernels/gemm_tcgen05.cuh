@@ -22,11 +22,12 @@
 // epilogue of tile i overlaps the main loop of tile i+1.
 #pragma once
 
+#include "launch.h"
 #include "ptx.cuh"
 
 namespace srk {
 
-enum GemmEpilogue : int { EPI_BF16 = 0, EPI_GELU_BF16 = 1, EPI_RESID_F32 = 2, EPI_F32 = 3 };
+// GemmEpilogue (EPI_*) is declared in launch.h.
 
 // Optional per-CTA timeline of the pair kernel (%globaltimer ns, 64 slots per
 // CTA): 0 entry, 1 setup done, 2+i MMA of local tile i issued, 24+i epilogue
@@ -58,7 +59,7 @@ struct GemmCfg {
 // Output tensor map box for an epilogue: 32 rows x 128 B (32 fp32 or 64 bf16).
 template <int EPI>
 struct EpiOut {
-  static constexpr bool F32 = (EPI == EPI_RESID_F32 || EPI == EPI_F32);
+  static constexpr bool F32 = (EPI == EPI_RESID_F32 || EPI == EPI_F32 || EPI == EPI_RESID_LN);
   static constexpr int CW = F32 ? 32 : 64;  // columns per staged chunk
 };
 
@@ -244,6 +245,30 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ----------------------------------------------------------------------------
+// LayerNorm folded into the GEMMs (pair kernel only).
+//
+// The reference normalises the residual stream before each projection
+// (model.cpp:187-188, 204-205: h = LN(x) * gain, then h . W). Here LN never
+// materialises:
+//   * the residual GEMMs (O and W_out, EPI_RESID_LN) load the fp32 x tile,
+//     add the accumulator, store x, store a bf16 copy xb, and write per-row
+//     partial statistics (mean, M2) over each 128-column slice;
+//   * the next projection (QKV / W_in, EPI_LN_BF16 / EPI_LN_GELU_BF16) takes
+//     xb as its A operand against gain-folded weights W' = diag(gain) W and
+//     finishes the normalisation in the epilogue:
+//         LN(x) . W' = rstd * (xb . W' - mean * colsum(W'))
+//     with mean/rstd combined from the partials (Chan et al.), i.e. the
+//     reference's two-pass population variance and eps 1e-5 (kernels.cpp:31-45).
+struct alignas(64) GemmLnArgs {
+  CUtensorMap tm_xb;        // EPI_RESID_LN: bf16 copy of x, 32 x 64 boxes, 128 B swizzle
+  float2* stats_out;        // EPI_RESID_LN: [N / 128][ld] (mean, M2) over 128 columns
+  const float2* stats_in;   // EPI_LN_*: [n_parts][ld], each part over K / n_parts columns
+  const float* colsum;      // EPI_LN_*: [N] column sums of the folded bf16 weights
+  int n_parts;
+  int ld;
+};
+
+// ----------------------------------------------------------------------------
 // CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes a
 // 256 x 256 tile; CTA r loads rows [128 r, +128) of A and of B (= 128 of the
 // 256 output columns) per k-block, the leader issues
@@ -258,6 +283,16 @@ __global__ void __launch_bounds__(320, 1)
 // SM operand traffic, at the cost of the SMs a 4-CTA cluster grid cannot use
 // (132 of 148 on B200). Opt-in (SRK_GEMM_NP=2): on the C2 shapes the per-tile
 // time did not change, so NP = 1 on all 148 SMs is faster.
+#ifndef SRK_PAIR_STAGES
+#define SRK_PAIR_STAGES 6
+#endif
+#ifndef SRK_PAIR_STG_BUFS
+#define SRK_PAIR_STG_BUFS 1
+#endif
+#ifndef SRK_RESID_LN_STAGES
+#define SRK_RESID_LN_STAGES 4
+#endif
+template <int EPI>
 struct GemmPairCfg {
   static constexpr int BM = 128;  // rows per CTA (pair: 256)
   static constexpr int BN = 256;  // output columns per pair tile
@@ -265,30 +300,33 @@ struct GemmPairCfg {
   static constexpr int A_BYTES = BM * BK * 2;        // 16 KB
   static constexpr int B_BYTES = (BN / 2) * BK * 2;  // 16 KB (this CTA's half of B)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-#ifndef SRK_PAIR_STAGES
-#define SRK_PAIR_STAGES 6
-#endif
-#ifndef SRK_PAIR_STG_BUFS
-#define SRK_PAIR_STG_BUFS 1
-#endif
-  static constexpr int STAGES = SRK_PAIR_STAGES;
+  // The residual+LN epilogue stages x in and out (2 fp32 chunks + 1 bf16
+  // chunk per warp), paid for with two ring stages. (A register -> global
+  // variant with 16x256b TMEM loads was measured slower: 8 rows x 32 B per
+  // store instruction made the epilogue LSU-bound, 2-3x the staged time.)
+  static constexpr bool RESID_LN = EPI == EPI_RESID_LN;
+  static constexpr int STAGES = RESID_LN ? SRK_RESID_LN_STAGES : SRK_PAIR_STAGES;
   static constexpr int TMEM_COLS = 2 * BN;  // double-buffered 128 x 256 fp32
   static constexpr int EPI_WARPS = 8;
-  static constexpr int STG_BUFS = SRK_PAIR_STG_BUFS;  // staging buffers per epilogue warp
+  static constexpr int STG_BUFS = RESID_LN ? 3 : SRK_PAIR_STG_BUFS;  // per epilogue warp
   static constexpr int STG_BYTES = 32 * 128;
+  static constexpr int BAR_BYTES = 512;
   static constexpr int SMEM_BYTES =
-      STAGES * STAGE_BYTES + EPI_WARPS * STG_BUFS * STG_BYTES + 256 + 1024;
+      STAGES * STAGE_BYTES + EPI_WARPS * STG_BUFS * STG_BYTES + BAR_BYTES + 1024;
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
 template <int EPI, int NP>
 __global__ void __launch_bounds__(320, 1)
     gemm_bf16_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                                   const __grid_constant__ CUtensorMap tmB,
-                                  const __grid_constant__ CUtensorMap tmC, int M, int N, int K) {
-  using C = GemmPairCfg;
+                                  const __grid_constant__ CUtensorMap tmC,
+                                  const __grid_constant__ GemmLnArgs ln, int M, int N, int K) {
+  using C = GemmPairCfg<EPI>;
   static_assert(NP == 1 || NP == 2, "one or two CTA pairs per cluster");
   constexpr int BN = C::BN;
+  constexpr bool LN_IN = EPI == EPI_LN_BF16 || EPI == EPI_LN_GELU_BF16;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
@@ -298,7 +336,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xbar = tempty + 2;  // EPI_RESID_LN: 2 per epilogue warp (x chunk loads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 2 * C::EPI_WARPS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -319,6 +358,7 @@ __global__ void __launch_bounds__(320, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmC);
+    if constexpr (C::RESID_LN) tma_prefetch_desc(&ln.tm_xb);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 2);  // leader: own expect_tx arrival + the peer's arrival
       mbar_init(&empty[s], NP);  // one commit from every pair that reads the stage
@@ -327,6 +367,8 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * C::EPI_WARPS);  // one per epilogue warp of both CTAs
     }
+    if constexpr (C::RESID_LN)
+      for (int b = 0; b < 2 * C::EPI_WARPS; ++b) mbar_init(&xbar[b], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -355,6 +397,13 @@ __global__ void __launch_bounds__(320, 1)
       for (int tile = pair; tile < num_tiles; tile += n_pairs) {
         const int m0 = (tile / n_tiles) * 2 * C::BM + cr * C::BM;
         const int n0 = ((tile % n_tiles) * NP + pr) * BN + cr * (BN / 2);
+        if constexpr (C::RESID_LN) {
+          // The epilogue reads this CTA's 128 x 256 fp32 slab of x after the
+          // main loop: pull it into L2 now so those loads are L2 hits.
+          const int xc = ((tile % n_tiles) * NP + pr) * BN;
+          for (int rr = 0; rr < C::BM; rr += 32)
+            for (int cc = 0; cc < BN; cc += 32) tma_prefetch_2d_l2(&tmC, xc + cc, m0 + rr);
+        }
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader)
@@ -417,66 +466,197 @@ __global__ void __launch_bounds__(320, 1)
     const uint64_t pol_keep = policy_evict_last();
     int local = 0;
     int nstg = 0;  // staging chunks issued by this warp (buffer = nstg % STG_BUFS)
+    uint32_t xph = 0;  // EPI_RESID_LN: parity of the two x-chunk barriers (bit b)
     for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       const int m0 = (tile / n_tiles) * 2 * C::BM + cr * C::BM;
       const int n0 = ((tile % n_tiles) * NP + pr) * BN;
       const int r0 = m0 + quad * 32;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      if (r0 < M) {
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN;
+      if constexpr (C::RESID_LN) {
+        // x chunks 0 and 1 of this warp's 32 x 128 slab load while the MMA
+        // runs (the producer already pulled the slab into L2).
+        uint8_t* F0 = stg0;
+        uint64_t* xb_bar = xbar + 2 * (warp - 2);
+        if (r0 < M && lane == 0) {
+          bulk_wait_read0();  // previous tile's stores have left both buffers
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            mbar_arrive_expect_tx(&xb_bar[b], C::STG_BYTES);
+            tma_load_2d(&tmC, &xb_bar[b], F0 + b * C::STG_BYTES, n0 + col0 + 32 * b, r0);
+          }
+        }
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        if (r0 < M) {
+          uint8_t* Bb = stg0 + 2 * C::STG_BYTES;
+          float s_mean = 0.f, s_m2 = 0.f;
 #pragma unroll 1
-        for (int c = col0; c < col0 + SPAN; c += CW, ++nstg) {
-          uint8_t* stg = stg0 + (nstg % C::STG_BUFS) * C::STG_BYTES;
-          uint8_t* row_base = stg + lane * 128;
-          if constexpr (EpiOut<EPI>::F32) {
+          for (int c = 0; c < SPAN / 32; ++c) {
+            const int b = c & 1;
+            uint8_t* Fb = F0 + b * C::STG_BYTES;
+            __syncwarp();  // lane 0's buffer waits of the previous chunk come first
             uint32_t r[32];
-            tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c,
-                               r);
-            // The TMEM read overlaps the wait for this buffer's previous store.
-            if (lane == 0) bulk_wait_read<C::STG_BUFS - 1>();
-            __syncwarp();
+            tmem_ld_32x32b_x32(t_row + col0 + 32 * c, r);
+            mbar_wait(&xb_bar[b], (xph >> b) & 1u);
+            xph ^= 1u << b;
             tmem_ld_wait();
+            uint8_t* row = Fb + lane * 128;
+            float v[32];
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-              *reinterpret_cast<uint4*>(row_base + ((k ^ (lane & 7)) * 16)) =
-                  make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
-          } else {
-            uint32_t r[2][32];
+            for (int k = 0; k < 8; ++k) {
+              uint4* qp = reinterpret_cast<uint4*>(row + ((k ^ (lane & 7)) * 16));
+              const uint4 xv = *qp;
+              v[4 * k + 0] = __uint_as_float(xv.x) + __uint_as_float(r[4 * k + 0]);
+              v[4 * k + 1] = __uint_as_float(xv.y) + __uint_as_float(r[4 * k + 1]);
+              v[4 * k + 2] = __uint_as_float(xv.z) + __uint_as_float(r[4 * k + 2]);
+              v[4 * k + 3] = __uint_as_float(xv.w) + __uint_as_float(r[4 * k + 3]);
+              *qp = make_uint4(__float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
+                               __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
+            }
+            // chunk mean / M2 (two-pass over registers), merged into the running
+            // pair (Chan et al.)
+            float cs = 0.f;
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh)
-              tmem_ld_32x32b_x32(
-                  tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN + c + hh * 32,
-                  r[hh]);
-            if (lane == 0) bulk_wait_read<C::STG_BUFS - 1>();
+            for (int j = 0; j < 32; ++j) cs += v[j];
+            const float cm = cs * (1.f / 32.f);
+            float cq = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) cq = fmaf(v[j] - cm, v[j] - cm, cq);
+            if (c == 0) {
+              s_mean = cm;
+              s_m2 = cq;
+            } else {
+              const float na = 32.f * c, n = na + 32.f;
+              const float dl = cm - s_mean;
+              s_mean = fmaf(dl, 32.f / n, s_mean);
+              s_m2 += cq + dl * dl * (na * 32.f / n);
+            }
+            uint8_t* brow = Bb + lane * 128;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              *reinterpret_cast<uint4*>(brow + ((((c & 1) * 4 + k) ^ (lane & 7)) * 16)) =
+                  make_uint4(pack_bf16x2(v[8 * k], v[8 * k + 1]),
+                             pack_bf16x2(v[8 * k + 2], v[8 * k + 3]),
+                             pack_bf16x2(v[8 * k + 4], v[8 * k + 5]),
+                             pack_bf16x2(v[8 * k + 6], v[8 * k + 7]));
+            fence_proxy_async_smem();
             __syncwarp();
-            tmem_ld_wait();
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                float f[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  f[j] = __uint_as_float(r[hh][8 * k + j]);
-                  if constexpr (EPI == EPI_GELU_BF16) f[j] = gelu_erf(f[j]);
-                }
-                const int chunk = hh * 4 + k;
-                *reinterpret_cast<uint4*>(row_base + ((chunk ^ (lane & 7)) * 16)) =
-                    make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
-                               pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+            if (lane == 0) {
+              tma_store_2d(&tmC, Fb, n0 + col0 + 32 * c, r0);
+              bulk_commit();
+              if (c & 1) {  // the bf16 copy is read next by QKV / W_in: keep it in L2
+                tma_store_2d_hint(&ln.tm_xb, Bb, n0 + col0 + 32 * (c - 1), r0, pol_keep);
+                bulk_commit();
+              }
+              if (c + 2 < SPAN / 32) {
+                bulk_wait_read0();  // Fb (and Bb) have been read out
+                mbar_arrive_expect_tx(&xb_bar[b], C::STG_BYTES);
+                tma_load_2d(&tmC, &xb_bar[b], Fb, n0 + col0 + 32 * (c + 2), r0);
               }
             }
           }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            if constexpr (EPI == EPI_RESID_F32)  // x is re-read next by the LayerNorm
-              tma_reduce_add_2d_hint(&tmC, stg, n0 + c, r0, pol_keep);
-            else
-              tma_store_2d(&tmC, stg, n0 + c, r0);
-            bulk_commit();
+          const int row = r0 + lane;
+          if (row < M)
+            ln.stats_out[static_cast<size_t>((n0 + col0) >> 7) * ln.ld + row] =
+                make_float2(s_mean, s_m2);
+        }
+      } else {
+        // EPI_LN_*: out = acc * rstd - mean * rstd * colsum (row stats per
+        // lane); the partials are fetched before the accumulator wait.
+        float ln_scale = 0.f, ln_shift = 0.f;
+        float2 part[16];
+        if constexpr (LN_IN) {
+          const int row = r0 + lane;
+          if (row < M) {
+#pragma unroll
+            for (int p = 0; p < 16; ++p)
+              if (p < ln.n_parts) part[p] = ln.stats_in[static_cast<size_t>(p) * ln.ld + row];
+          }
+        }
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        if constexpr (LN_IN) {
+          if (r0 + lane < M) {
+            const int P = ln.n_parts;
+            float mean = 0.f;
+#pragma unroll
+            for (int p = 0; p < 16; ++p)
+              if (p < P) mean += part[p].x;
+            mean /= static_cast<float>(P);
+            const float cnt = static_cast<float>(K / P);
+            float m2 = 0.f;
+#pragma unroll
+            for (int p = 0; p < 16; ++p)
+              if (p < P) {
+                const float dl = part[p].x - mean;
+                m2 += fmaf(dl * dl, cnt, part[p].y);
+              }
+            ln_scale = 1.0f / sqrtf(m2 / static_cast<float>(K) + 1e-5f);
+            ln_shift = -mean * ln_scale;
+          }
+        }
+        if (r0 < M) {
+#pragma unroll 1
+          for (int c = col0; c < col0 + SPAN; c += CW, ++nstg) {
+            uint8_t* stg = stg0 + (nstg % C::STG_BUFS) * C::STG_BYTES;
+            uint8_t* row_base = stg + lane * 128;
+            if constexpr (EpiOut<EPI>::F32) {
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(t_row + c, r);
+              // The TMEM read overlaps the wait for this buffer's previous store.
+              if (lane == 0) bulk_wait_read<C::STG_BUFS - 1>();
+              __syncwarp();
+              tmem_ld_wait();
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                *reinterpret_cast<uint4*>(row_base + ((k ^ (lane & 7)) * 16)) =
+                    make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+            } else {
+              uint32_t r[2][32];
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) tmem_ld_32x32b_x32(t_row + c + hh * 32, r[hh]);
+              if (lane == 0) bulk_wait_read<C::STG_BUFS - 1>();
+              __syncwarp();
+              tmem_ld_wait();
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  float f[8];
+                  if constexpr (LN_IN) {
+                    const float4* cp =
+                        reinterpret_cast<const float4*>(ln.colsum + n0 + c + hh * 32 + 8 * k);
+                    const float4 c0v = __ldg(cp), c1v = __ldg(cp + 1);
+                    const float csv[8] = {c0v.x, c0v.y, c0v.z, c0v.w, c1v.x, c1v.y, c1v.z, c1v.w};
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                      f[j] = fmaf(csv[j], ln_shift, __uint_as_float(r[hh][8 * k + j]) * ln_scale);
+                  } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(r[hh][8 * k + j]);
+                  }
+                  if constexpr (EPI == EPI_GELU_BF16 || EPI == EPI_LN_GELU_BF16) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) f[j] = gelu_erf(f[j]);
+                  }
+                  const int chunk = hh * 4 + k;
+                  *reinterpret_cast<uint4*>(row_base + ((chunk ^ (lane & 7)) * 16)) =
+                      make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                                 pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+                }
+              }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (EPI == EPI_RESID_F32)  // x is re-read next by the LayerNorm
+                tma_reduce_add_2d_hint(&tmC, stg, n0 + c, r0, pol_keep);
+              else
+                tma_store_2d(&tmC, stg, n0 + c, r0);
+              bulk_commit();
+            }
           }
         }
       }

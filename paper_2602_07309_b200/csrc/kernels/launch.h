@@ -30,6 +30,17 @@ struct AttnTile {
 };
 
 // ------------------------------------------------------------------- GEMM
+// Fused epilogues (gemm_tcgen05.cuh):
+//   EPI_BF16      Q|K|V projection -> bf16 (model.cpp:189-196)
+//   EPI_GELU_BF16 W_in + exact-erf GELU -> bf16 (model.cpp:206-209, kernels.cpp:47-49)
+//   EPI_RESID_F32 x += acc, fp32 residual stream (model.cpp:199-202, 210-213)
+//   EPI_F32       plain fp32 store (tests)
+//   EPI_RESID_LN / EPI_LN_BF16 / EPI_LN_GELU_BF16: LayerNorm folded into the
+//                 projections (pair kernel only, see LnFold below)
+enum GemmEpilogue : int {
+  EPI_BF16 = 0, EPI_GELU_BF16 = 1, EPI_RESID_F32 = 2, EPI_F32 = 3,
+  EPI_RESID_LN = 4, EPI_LN_BF16 = 5, EPI_LN_GELU_BF16 = 6
+};
 int num_sms(int device);
 cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                               uint32_t box_rows, uint32_t box_cols);
@@ -37,18 +48,35 @@ cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows,
 int gemm_pick_bn(int N);
 cudaError_t gemm_bf16(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
                       void* out, int ldo, int epi, int bn, cudaStream_t stream);
+// LayerNorm folded into the projections (gemm_tcgen05.cuh, GemmLnArgs).
+// epi 4 (residual + LN statistics): out = x fp32 [M x N] += acc, xb = bf16(x),
+//   stats_out[N/128][ld] = per-row (mean, M2) float2 partials over 128 columns.
+// epi 5 / 6 (normalised projection [+ GELU]): A = xb, B = diag(gain) W (bf16),
+//   out = bf16([gelu](rstd * (acc - mean * colsum))), mean/rstd from
+//   stats_in[n_parts][ld] (each part over K / n_parts columns).
+struct LnFold {
+  __nv_bfloat16* xb = nullptr;
+  float* stats_out = nullptr;       // float2 pairs
+  const float* stats_in = nullptr;  // float2 pairs
+  const float* colsum = nullptr;
+  int n_parts = 0;
+  int ld = 0;
+};
 // CTA-pair (cta_group::2) 256 x 256 tiles; N % 256 == 0; tmA and tmB both use
-// 128-row x 64-column boxes.
+// 128-row x 64-column boxes. Epilogues 4-6 need `fold`.
 cudaError_t gemm_bf16_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
-                           void* out, int ldo, int epi, cudaStream_t stream);
+                           void* out, int ldo, int epi, cudaStream_t stream,
+                           const LnFold* fold = nullptr);
 // The projection GEMMs take the pair path when N is a multiple of 256.
 inline bool gemm_use_pair(int N) { return N % 256 == 0; }
 // B-operand box rows for a weight [N x K] map on the chosen path.
 inline int gemm_b_box_rows(int N) { return gemm_use_pair(N) ? 128 : gemm_pick_bn(N); }
 // Dispatch: pair kernel when N % 256 == 0, else the 1-CTA kernel.
 inline cudaError_t gemm_auto(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
-                             void* out, int ldo, int epi, cudaStream_t stream) {
-  if (gemm_use_pair(N)) return gemm_bf16_pair(tmA, tmB, M, N, K, out, ldo, epi, stream);
+                             void* out, int ldo, int epi, cudaStream_t stream,
+                             const LnFold* fold = nullptr) {
+  if (gemm_use_pair(N)) return gemm_bf16_pair(tmA, tmB, M, N, K, out, ldo, epi, stream, fold);
+  if (epi > 3) return cudaErrorInvalidValue;  // LN folding is a pair-kernel epilogue
   return gemm_bf16(tmA, tmB, M, N, K, out, ldo, epi, gemm_pick_bn(N), stream);
 }
 
@@ -58,6 +86,10 @@ inline cudaError_t gemm_auto(const CUtensorMap& tmA, const CUtensorMap& tmB, int
 cudaError_t embed_ln(const int32_t* src, const int32_t* pos, const float* tok_emb,
                      const float* soft_rows, const float* pos_emb, const float* gain, float* x,
                      __nv_bfloat16* xn, int M, int d, cudaStream_t stream);
+// Folded-LN path: x as above, xb = bf16(x), stats[0][row] = (mean, M2) of x.
+cudaError_t embed_stats(const int32_t* src, const int32_t* pos, const float* tok_emb,
+                        const float* soft_rows, const float* pos_emb, float* x,
+                        __nv_bfloat16* xb, float* stats, int M, int d, cudaStream_t stream);
 cudaError_t layer_norm_bf16(const float* x, const float* gain, __nv_bfloat16* out, int M, int d,
                             cudaStream_t stream);
 
@@ -104,7 +136,10 @@ cudaError_t topk_merge(const TopkEntry* in, int n, int k, TopkEntry* out, cudaSt
 
 // ------------------------------------------------------------ conversions
 // dst[n][k] = bf16(src[k][n]) : fp32 [K x N] row-major -> bf16 [N x K].
+// scale_k (device, optional): dst[n][k] = bf16(src[k][n] * scale_k[k]) (LN gain folding).
 cudaError_t transpose_to_bf16(const float* src, __nv_bfloat16* dst, int K, int N,
-                              cudaStream_t stream);
+                              cudaStream_t stream, const float* scale_k = nullptr);
+// out[n] = sum_k float(w[n][k]) for bf16 w [N x K] (folded-LN column sums).
+cudaError_t bf16_row_sums(const __nv_bfloat16* w, int N, int K, float* out, cudaStream_t stream);
 
 }  // namespace srk

@@ -107,6 +107,13 @@ __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const 
       "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// Tensor tile -> L2 only (no smem destination, no completion tracking).
+__device__ __forceinline__ void tma_prefetch_2d_l2(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }

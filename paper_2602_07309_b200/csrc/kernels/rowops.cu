@@ -89,6 +89,81 @@ __global__ void __launch_bounds__(256)
   ln_row_store<NV>(v, d4, gain, xn + static_cast<size_t>(row) * d, lane);
 }
 
+// Folded-LN variant (gemm_tcgen05.cuh GemmLnArgs): the layer-0 LN1 is
+// finished inside the QKV GEMM, so this writes x, xb = bf16(x) and the row's
+// (mean, M2) (two-pass, as kernels.cpp:31-45) as the single statistics part.
+template <int NV>
+__global__ void __launch_bounds__(256)
+    embed_stats_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ pos,
+                       const float* __restrict__ tok_emb, const float* __restrict__ soft_rows,
+                       const float* __restrict__ pos_emb, float* __restrict__ x,
+                       __nv_bfloat16* __restrict__ xb, float2* __restrict__ stats, int M, int d) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const int d4 = d >> 2;
+  const int s = src[row];
+  const float4* e = reinterpret_cast<const float4*>(
+      s >= 0 ? tok_emb + static_cast<size_t>(s) * d
+             : soft_rows + static_cast<size_t>(-s - 1) * d);
+  const float4* p = reinterpret_cast<const float4*>(pos_emb + static_cast<size_t>(pos[row]) * d);
+  float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(row) * d);
+  uint2* br = reinterpret_cast<uint2*>(xb + static_cast<size_t>(row) * d);
+  float4 v[NV];
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < d4) {
+      const float4 a = e[c], b = p[c];
+      v[i] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+      xr[c] = v[i];
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v[i].x, v[i].y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(v[i].z, v[i].w);
+      br[c] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+      sum += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffff, sum, o);
+  const float mean = sum / static_cast<float>(d);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + i * 32;
+    if (c < d4) {
+      const float a = v[i].x - mean, b = v[i].y - mean, g = v[i].z - mean, h = v[i].w - mean;
+      q += (a * a + b * b) + (g * g + h * h);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffff, q, o);
+  if (lane == 0) stats[row] = make_float2(mean, q);
+}
+
+template <int NV>
+cudaError_t launch_embed_stats(const int32_t* src, const int32_t* pos, const float* tok_emb,
+                               const float* soft_rows, const float* pos_emb, float* x,
+                               __nv_bfloat16* xb, float* stats, int M, int d,
+                               cudaStream_t stream) {
+  embed_stats_kernel<NV><<<(M + 7) / 8, 256, 0, stream>>>(
+      src, pos, tok_emb, soft_rows, pos_emb, x, xb, reinterpret_cast<float2*>(stats), M, d);
+  return cudaGetLastError();
+}
+
+// One warp per weight row: out[n] = sum_k float(w[n][k]) (double accumulation).
+__global__ void bf16_row_sums_kernel(const __nv_bfloat16* __restrict__ w, int N, int K,
+                                     float* __restrict__ out) {
+  const int n = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (n >= N) return;
+  double s = 0.0;
+  for (int k = lane; k < K; k += 32) s += static_cast<double>(__bfloat162float(w[static_cast<size_t>(n) * K + k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+  if (lane == 0) out[n] = static_cast<float>(s);
+}
+
 template <int NV>
 __global__ void __launch_bounds__(256)
     layer_norm_kernel(const float* __restrict__ x, const float* __restrict__ gain,
@@ -124,7 +199,7 @@ cudaError_t launch_ln(const float* x, const float* gain, __nv_bfloat16* out, int
 }
 
 __global__ void transpose_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
-                                      int K, int N) {
+                                      int K, int N, const float* __restrict__ scale_k) {
   __shared__ float tile[32][33];
   const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += 8) {
@@ -134,7 +209,9 @@ __global__ void transpose_bf16_kernel(const float* __restrict__ src, __nv_bfloat
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += 8) {
     const int n = n0 + i, k = k0 + threadIdx.x;
-    if (n < N && k < K) dst[static_cast<size_t>(n) * K + k] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+    if (n < N && k < K)
+      dst[static_cast<size_t>(n) * K + k] =
+          __float2bfloat16_rn(scale_k ? tile[threadIdx.x][i] * scale_k[k] : tile[threadIdx.x][i]);
   }
 }
 
@@ -169,10 +246,25 @@ cudaError_t layer_norm_bf16(const float* x, const float* gain, __nv_bfloat16* ou
 }
 
 cudaError_t transpose_to_bf16(const float* src, __nv_bfloat16* dst, int K, int N,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, const float* scale_k) {
   dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
-  transpose_bf16_kernel<<<grid, block, 0, stream>>>(src, dst, K, N);
+  transpose_bf16_kernel<<<grid, block, 0, stream>>>(src, dst, K, N, scale_k);
   return cudaGetLastError();
+}
+
+cudaError_t bf16_row_sums(const __nv_bfloat16* w, int N, int K, float* out, cudaStream_t stream) {
+  if (N <= 0) return cudaSuccess;
+  bf16_row_sums_kernel<<<(N + 7) / 8, 256, 0, stream>>>(w, N, K, out);
+  return cudaGetLastError();
+}
+
+cudaError_t embed_stats(const int32_t* src, const int32_t* pos, const float* tok_emb,
+                        const float* soft_rows, const float* pos_emb, float* x,
+                        __nv_bfloat16* xb, float* stats, int M, int d, cudaStream_t stream) {
+  if (M <= 0) return cudaSuccess;
+  if (d % 4 != 0) return cudaErrorInvalidValue;
+  SRK_DISPATCH_NV(d, launch_embed_stats, src, pos, tok_emb, soft_rows, pos_emb, x, xb, stats, M,
+                  d, stream);
 }
 
 }  // namespace srk

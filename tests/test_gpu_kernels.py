@@ -77,6 +77,64 @@ def test_gemm_residual_epilogue(cuda, M, N, K):
     assert err <= 1e-3 * max(1.0, ref.abs().max().item()), err
 
 
+@pytest.mark.parametrize("M,N,K", [(300, 1024, 1024), (5000, 1024, 1536), (257, 2048, 1024),
+                                   (100, 256, 512)])
+def test_gemm_residual_ln_statistics_epilogue(cuda, M, N, K):
+    """epi 4: x += A.B^T (fp32), xb = bf16(x) exactly, per-128-column (mean, M2)."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(M + N + K)
+    a = (torch.randn(M, K, generator=g) / K ** 0.5).bfloat16().to(cuda)
+    b = torch.randn(N, K, generator=g).bfloat16().to(cuda)
+    x0 = (torch.randn(M, N, generator=g) + torch.randn(M, 1, generator=g)).to(cuda)
+    x = x0.clone()
+    xb = torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
+    ld = M + 7
+    stats = torch.full((N // 128, ld, 2), float("nan"), device=cuda)
+    _ok(_lib().sr_kernel_gemm_ln(_vp(a), _vp(b), M, N, K, _vp(x), N, 4, _vp(xb), _vp(stats), 0,
+                                 None, ld, None))
+    ref = x0 + a.float() @ b.float().T
+    assert (x - ref).abs().max().item() <= 1e-3 * max(1.0, ref.abs().max().item())
+    assert torch.equal(xb, x.bfloat16())
+    parts = x.view(M, N // 128, 128)
+    mean = parts.double().mean(-1)
+    m2 = ((parts.double() - mean[..., None]) ** 2).sum(-1)
+    got = stats[:, :M].permute(1, 0, 2).double()
+    assert torch.allclose(got[..., 0], mean, rtol=1e-5, atol=1e-5)
+    assert torch.allclose(got[..., 1], m2, rtol=1e-4, atol=1e-4)
+
+
+@pytest.mark.parametrize("M,N,K,P", [(300, 3072, 1024, 8), (1000, 1536, 1024, 1),
+                                     (777, 6144, 2048, 16), (64, 256, 256, 2)])
+def test_gemm_folded_layernorm_epilogues(cuda, M, N, K, P):
+    """epi 5/6: bf16([gelu](LN(x)*gain . W)) from xb, partial stats and diag(gain) W."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(M * 3 + N + K)
+    x = (torch.randn(M, K, generator=g) * 0.5 + 0.2 * torch.randn(M, 1, generator=g)).to(cuda)
+    gain = (1 + 0.1 * torch.randn(K, generator=g)).to(cuda)
+    w = (torch.randn(K, N, generator=g) / K ** 0.5).to(cuda)  # reference layout [d_in x d_out]
+    bt = (gain[:, None] * w).T.contiguous().bfloat16()        # folded, K-major [N x K]
+    colsum = bt.float().sum(1).contiguous()
+    xb = x.bfloat16()
+    ld = M + 3
+    parts = x.view(M, P, K // P).double()
+    pm = parts.mean(-1)
+    stats = torch.zeros(P, ld, 2, device=cuda)
+    stats[:, :M, 0] = pm.T.float()
+    stats[:, :M, 1] = ((parts - pm[..., None]) ** 2).sum(-1).T.float()
+    mean = x.double().mean(-1, keepdim=True)
+    rstd = 1 / torch.sqrt(((x.double() - mean) ** 2).mean(-1, keepdim=True) + 1e-5)
+    # Same algebra in fp64 on the same bf16 operands: only accumulation order differs.
+    algebra = (rstd * (xb.double() @ bt.double().T - mean * colsum.double()[None])).float()
+    ln_ref = (((x - mean.float()) * rstd.float() * gain) @ w)  # the reference's LN . W in fp32
+    for epi, fn in ((5, lambda z: z), (6, torch.nn.functional.gelu)):
+        c = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=cuda)
+        _ok(_lib().sr_kernel_gemm_ln(_vp(xb), _vp(bt), M, N, K, _vp(c), N, epi, None, _vp(stats),
+                                     P, _vp(colsum), ld, None))
+        assert torch.allclose(c.float(), fn(algebra), rtol=8e-3, atol=2e-3)
+        # vs the unfused reference: bf16 operand rounding (x and gain*W) on top
+        assert (c.float() - fn(ln_ref)).abs().max().item() < 6e-2
+
+
 def _attention_ref(qkv, spans, H, hd):
     """fp32 reference of kernels.cpp:51-95 with explicit allowed sets."""
     import torch

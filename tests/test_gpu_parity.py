@@ -184,6 +184,24 @@ def test_c2_full_request_parity_and_isolation(cuda):
     assert np.array_equal(res2.scores[slots], got)
 
 
+def test_c2_folded_layernorm_path_parity(cuda, monkeypatch):
+    """The opt-in folded-LN forward (SRK_FOLD_LN=1: statistics from the residual
+    GEMM epilogue, LN finished in the QKV / W_in epilogues) at C2 scale."""
+    g = gold("c2_subset.json")
+    cfg = c2_cfg()
+    monkeypatch.setenv("SRK_FOLD_LN", "1")
+    eng = sr.ScoringEngine(sr.init_model(cfg, 2026, "fan_in"))
+    monkeypatch.delenv("SRK_FOLD_LN")
+    res = eng.score(request(g["prefix"], g["items"]), k=4)
+    ref32 = np.asarray(g["multi_item"])
+    ref16 = oracle_bf16(cfg, 2026, 1).score(g["prefix"], g["items"])
+    d16, d32 = np.abs(res.scores - ref16).max(), np.abs(res.scores - ref32).max()
+    print(f"C2 folded LN: max dev vs oracle(bf16 w) {d16:.2e}, vs reference fp32 {d32:.2e}")
+    assert d16 <= TOL and d32 <= TOL
+    base = engine_for(cfg, 2026, "fan_in").score(request(g["prefix"], g["items"]), k=4)
+    assert np.abs(res.scores - base.scores).max() <= TOL
+
+
 def test_c3_soft_token_items_parity(cuda):
     """BASELINE configs[2]: 1024 items of 8 soft-token rows, C2 model."""
     cfg = c2_cfg()

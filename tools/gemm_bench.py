@@ -13,7 +13,10 @@ from paper_2602_07309_b200._capi import lib  # noqa: E402
 
 M = int(os.environ.get("GB_M", 24832))
 SHAPES = [("qkv", 3072, 1024, 0), ("o", 1024, 1024, 2), ("w_in", 1536, 1024, 1),
-          ("w_out", 1024, 1536, 2)]
+          ("w_out", 1024, 1536, 2),
+          # folded-LN epilogues (4 residual + statistics, 5 LN-projection, 6 + GELU)
+          ("qkv_ln", 3072, 1024, 5), ("o_ln", 1024, 1024, 4), ("w_in_ln", 1536, 1024, 6),
+          ("wout_ln", 1024, 1536, 4)]
 if os.environ.get("GB_SHAPES"):  # name:N:K:epi,...
     SHAPES = [(f[0], int(f[1]), int(f[2]), int(f[3]))
               for f in (x.split(":") for x in os.environ["GB_SHAPES"].split(","))]
@@ -45,15 +48,25 @@ def timed(fn, reps=10):
 for name, N, K, epi in SHAPES:
     A = (torch.randn(M, K, device=dev) * 0.5).bfloat16()
     B = (torch.randn(N, K, device=dev) * 0.05).bfloat16()
-    if epi >= 2:
+    if epi in (2, 3, 4):
         Cm = torch.zeros(M, N, device=dev, dtype=torch.float32)
     else:
         Cm = torch.zeros(M, N, device=dev, dtype=torch.bfloat16)
+    XB = torch.zeros(M, N, device=dev, dtype=torch.bfloat16)
+    P = K // 128
+    ST = torch.zeros(max(N, K) // 128, M, 2, device=dev)
+    ST[..., 1] = 128.0  # unit variance partials
+    CS = torch.randn(N, device=dev)
 
     def ours():
-        rc = lib.sr_kernel_gemm(C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), M, N, K,
-                                C.c_void_p(Cm.data_ptr()), N, epi,
-                                C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        if epi >= 4:
+            rc = lib.sr_kernel_gemm_ln(C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), M, N, K,
+                                       C.c_void_p(Cm.data_ptr()), N, epi, C.c_void_p(XB.data_ptr()),
+                                       C.c_void_p(ST.data_ptr()), P, C.c_void_p(CS.data_ptr()), M, s)
+        else:
+            rc = lib.sr_kernel_gemm(C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()), M, N, K,
+                                    C.c_void_p(Cm.data_ptr()), N, epi, s)
         assert rc == 0, lib.sr_last_error()
 
     def cublas():
