@@ -70,6 +70,8 @@ Engine::Engine(const ModelWeights& w, int device) : cfg_(w.config), device_(devi
     const bool allow = v != nullptr && std::atoi(v) != 0;
     fold_ln_ = allow && srk::gemm_use_pair(d) && srk::gemm_use_pair(3 * d) &&
                srk::gemm_use_pair(F) && d % 128 == 0 && d / 128 <= 16;
+    const char* sv = std::getenv("SRK_SERPENTINE");
+    serpentine_ = sv == nullptr || std::atoi(sv) != 0;
   }
 
   tok_emb_ = upload(w.tok_emb, allocs_);
@@ -247,6 +249,10 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
       SR_CUDA_CHECK(srk::attention(qkv_.ptr, p.spans.ptr, p.tiles.ptr,
                                    static_cast<int>(p.pack.tiles.size()), xn_.ptr, M, H, hd, s));
   };
+  // Serpentine L2 order (SRK_SERPENTINE=0 disables): each kernel of the chain
+  // O -> LN2 -> W_in -> W_out -> LN1 -> QKV walks its rows opposite to its
+  // producer, so it starts on the rows still resident in L2.
+  const bool serp = serpentine_;
   if (fold_ln_) {
     // LN folded into the GEMMs (gemm_tcgen05.cuh GemmLnArgs): no LayerNorm launches.
     srk::LnFold in{}, out{};
@@ -299,7 +305,8 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
     for (int l = 0; l < cfg_.n_layers; ++l) {
       const auto& L = layers_[l];
       B(PROF_GEMM_QKV);
-      SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_qkv, M, 3 * d, d, qkv_.ptr, 3 * d, 0, s));
+      SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_qkv, M, 3 * d, d, qkv_.ptr, 3 * d, 0, s, nullptr,
+                                   serp));
       E();
       B(PROF_ATTENTION);
       attention();
@@ -308,13 +315,13 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
       SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_o, M, d, d, x_.ptr, d, 2, s));
       E();
       B(PROF_LAYERNORM);
-      SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, L.ln2, xn_.ptr, M, d, s));
+      SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, L.ln2, xn_.ptr, M, d, s, serp));
       E();
       B(PROF_GEMM_IN);
       SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_in, M, F, d, h_.ptr, F, 1, s));
       E();
       B(PROF_GEMM_OUT);
-      SR_CUDA_CHECK(srk::gemm_auto(tm_h_, L.tm_out, M, d, F, x_.ptr, d, 2, s));
+      SR_CUDA_CHECK(srk::gemm_auto(tm_h_, L.tm_out, M, d, F, x_.ptr, d, 2, s, nullptr, serp));
       E();
       n += 6;
       if (l + 1 < cfg_.n_layers) {

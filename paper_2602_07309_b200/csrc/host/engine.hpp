@@ -165,6 +165,7 @@ class Engine {
   int32_t* task_arity_ = nullptr;
   int n_cols_ = 0, yes_col_ = 0, no_col_ = 0;
   bool fold_ln_ = false;
+  bool serpentine_ = false;
   std::vector<LayerDev> layers_;
   std::vector<void*> allocs_;
   // workspace

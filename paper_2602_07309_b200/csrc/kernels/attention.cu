@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kThreads)
     attn_segment_kernel(const __nv_bfloat16* __restrict__ qkv, const RowSpan* __restrict__ spans,
                         const AttnTile* __restrict__ tiles, __nv_bfloat16* __restrict__ out,
                         int M, int n_heads) {
+  pdl_wait();
   using T = Tile<HD>;
   constexpr int TILE_BYTES = kBlockM * HD * 2;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -305,8 +306,7 @@ cudaError_t launch_attn(const __nv_bfloat16* qkv, const RowSpan* spans, const At
     attr = true;
   }
   dim3 grid(n_tiles, n_heads);
-  kern<<<grid, kThreads, smem, stream>>>(qkv, spans, tiles, out, M, n_heads);
-  return cudaGetLastError();
+  return launch_k(kern, grid, dim3(kThreads), smem, stream, qkv, spans, tiles, out, M, n_heads);
 }
 
 }  // namespace

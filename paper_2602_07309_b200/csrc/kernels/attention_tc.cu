@@ -18,6 +18,7 @@
 //              block): tcgen05.ld of the row slice, visibility bitmask (skipped
 //              when the slice is fully visible), pair max exchange in smem,
 //              P = ex2(..) as packed bf16x2 via tcgen05.st; per item epilogue
+//              (deferred behind the next item's first block)
 //              O / l -> bf16 -> HBM.
 // Lazy rescaling (as FlashAttention-4): the exponent base only moves when the
 // block max exceeds it by more than 2^8, so O is rescaled rarely and softmax
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
 
   if (warp == 0) {
     // ------------------------------------------------------------- TMA
@@ -275,7 +277,77 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Row descriptor of the current item, fetched one item ahead.
     RowSpan sp_next = {0, 0, 0, 0};
     if (c.valid && c.t.q_begin + r < c.t.q_end) sp_next = spans[c.t.q_begin + r];
-    int pending_q = -1;  // Q buffer whose O store may still be reading smem
+    // The O epilogue of item i is deferred until P of item i+1's first block
+    // has been handed to the MMA warp, so the tensor core runs PV / S of the
+    // next item while this warpgroup drains O (it used to sit idle for the
+    // whole epilogue at every item boundary).
+    struct Pending {
+      bool on = false;
+      int li = 0, h = 0, row0 = 0, g_last = 0;
+      bool live = false;
+      float l = 0.f;
+    } pend;
+    auto epilogue = [&](const Pending& e) {
+      // Row sum of both halves, O / l -> bf16 -> HBM.
+      fin[half * 128 + r] = e.l;
+      named_bar_sync(1, kSoftmaxThreads);
+      const float lsum = e.l + fin[(half ^ 1) * 128 + r];
+      mbar_wait(&pv_done[e.g_last & 1], (e.g_last >> 1) & 1);
+      tc_fence_after();
+      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+      const int row = e.row0 + r;
+      // Stage O (bf16) in this item's Q buffer — every S of the item has
+      // completed — in the Q tile's own swizzled layout, then TMA-store each
+      // fully-live 32-row slab; partially-live slabs (request tails) store
+      // their live rows directly so neighbouring tiles are never touched.
+      uint8_t* qbuf = sQ + (e.li & 1) * C::TILE;
+      const bool slab_live = __all_sync(0xffffffff, e.live);
+#pragma unroll 1
+      for (int cc = 0; cc < HD / 64; ++cc) {
+        uint32_t v[32];
+        const int col = half * (HD / 2) + cc * 32;
+        tmem_ld_32x32b_x32(tmem + lane_off + C::O_COL + (e.li & 1) * 128 + col, v);
+        tmem_ld_wait();
+        uint4 pk[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float* f = reinterpret_cast<const float*>(&v[q * 8]);
+          pk[q] = make_uint4(pack_bf16x2(f[0] * inv, f[1] * inv), pack_bf16x2(f[2] * inv, f[3] * inv),
+                             pack_bf16x2(f[4] * inv, f[5] * inv), pack_bf16x2(f[6] * inv, f[7] * inv));
+        }
+        if (slab_live) {
+          uint8_t* rowp = qbuf + (col >> 6) * kBox + r * 128;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int chunk = ((col & 63) >> 3) + q;
+            *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) * 16)) = pk[q];
+          }
+        } else if (e.live) {
+          uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * d + e.h * HD + col);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dst[q] = pk[q];
+        }
+      }
+      fence_proxy_async_smem();
+      if constexpr (HD < 128) named_bar_sync(1, kSoftmaxThreads);  // halves share a box
+      else __syncwarp();
+      tc_fence_before();
+      mbar_arrive(&o_empty[e.li & 1]);
+      if (lane == 0) {
+        // HD=128: warp (quad, half) owns box `half` rows [32 quad, +32).
+        // HD=64 : both halves wrote box 0; the half-0 warp stores it.
+        if (slab_live && (HD == 128 || half == 0))
+          tma_store_2d(&tm_out, qbuf + (HD == 128 ? half : 0) * kBox + quad * 32 * 128,
+                       e.h * HD + (HD == 128 ? half : 0) * 64, e.row0 + quad * 32);
+        bulk_commit();
+        // Hand the Q buffer back once the store has read it: the producer
+        // needs it for item li + 2, which may be the very next block (an
+        // item of one block), so it cannot wait for a later hand-off.
+        bulk_wait_read0();
+        mbar_arrive(&q_empty[e.li & 1]);
+      }
+      if (warp == 2 && lane == 0 && e.li < 8) SRK_TRACE(56 + e.li);
+    };
     while (c.valid) {
       const int c_row0 = c.t.q_begin;
       const int row = c_row0 + r;
@@ -285,6 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float l = 0.f;             // this thread's partial row sum
       const int li = c.li, h = c.h;
       bool item_done = false;
+      bool first = true;
       while (!item_done) {
         int k0, kb, ke;
         c.range(k0, kb, ke);
@@ -310,8 +383,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         float mx = -INFINITY;
         bool warp_empty = false;  // no visible key in this slice for any row of the warp
         if (__all_sync(0xffffffff, full)) {
+          // two independent FMNMX3 chains
+          float ma = -INFINITY, mb = -INFINITY;
 #pragma unroll
-          for (int i = 0; i < kHalf; ++i) mx = fmaxf(mx, s[i]);
+          for (int i = 0; i < kHalf; i += 4) {
+            ma = fmax3f(ma, s[i], s[i + 1]);
+            mb = fmax3f(mb, s[i + 2], s[i + 3]);
+          }
+          mx = fmaxf(ma, mb);
         } else {
           auto ivl = [&](int lo, int hi) -> uint64_t {
             lo = max(lo - kh, 0);
@@ -328,8 +407,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < kHalf; ++i) {
               const bool ok = ((i < 32 ? v0 : v1) >> (i & 31)) & 1u;
               s[i] = ok ? s[i] : -INFINITY;
-              mx = fmaxf(mx, s[i]);
             }
+            float ma = -INFINITY, mb = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < kHalf; i += 4) {
+              ma = fmax3f(ma, s[i], s[i + 1]);
+              mb = fmax3f(mb, s[i + 2], s[i + 3]);
+            }
+            mx = fmaxf(ma, mb);
           }
         }
         // Pair max exchange (double-buffered by block parity). The barrier also
@@ -367,16 +452,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) pk[i] = 0u;
         } else {
-          // 1 in 4 exponentials on the FMA pipe, the rest on MUFU.
+          // Packed fp32x2 scale-subtract and row sums (FFMA2 / FADD2), MUFU
+          // exponentials: the softmax is issue-bound (ncu: 41% issue active,
+          // XU 19%), so the FMA-pipe exp2 emulation of earlier rounds cost
+          // more issue slots than the MUFU time it saved.
+          const uint64_t sc2 = f32x2(scale_log2, scale_log2), nb2 = f32x2(-base, -base);
+          uint64_t acc0 = f32x2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
           for (int i = 0; i < kHalf; i += 2) {
-            const float a0 = fmaf(s[i], scale_log2, -base);
-            const float a1 = fmaf(s[i + 1], scale_log2, -base);
+            float a0, a1;
+            f32x2_split(fma_f32x2(f32x2(s[i], s[i + 1]), sc2, nb2), a0, a1);
             const float p0 = ex2_approx(a0);
-            const float p1 = (i & 2) ? ex2_poly(a1) : ex2_approx(a1);
-            rs += p0 + p1;
+            const float p1 = ex2_approx(a1);
+            if (i & 2) acc1 = add_f32x2(acc1, f32x2(p0, p1));
+            else acc0 = add_f32x2(acc0, f32x2(p0, p1));
             pk[i >> 1] = pack_bf16x2(p0, p1);
           }
+          float r0, r1, r2, r3;
+          f32x2_split(acc0, r0, r1);
+          f32x2_split(acc1, r2, r3);
+          rs = (r0 + r1) + (r2 + r3);
         }
         l += rs;
         // P (bf16x2) over this half's 32 columns of the consumed S buffer.
@@ -385,77 +480,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
         if (warp == 2 && lane == 0 && g < 24) SRK_TRACE(32 + g);
-        if (pending_q >= 0 && lane == 0) {
-          // The previous item's O store has long finished reading its Q
-          // buffer: hand it back to the producer (needed two items later).
-          bulk_wait_read0();
-          mbar_arrive(&q_empty[pending_q]);
-        }
-        pending_q = -1;
         ++g;
         item_done = c.advance(tiles, n_tiles, n_items);
+        if (first) {
+          first = false;
+          if (pend.on) epilogue(pend);  // previous item, overlapping this item's MMAs
+          pend.on = false;
+        }
       }
-      // Next item's row descriptor: its latency overlaps this epilogue.
+      // Next item's row descriptor: its latency overlaps the deferred epilogue.
       if (c.valid && c.t.q_begin + r < c.t.q_end) sp_next = spans[c.t.q_begin + r];
-
-      // Item epilogue: row sum of both halves, O / l -> bf16 -> HBM.
-      fin[half * 128 + r] = l;
-      named_bar_sync(1, kSoftmaxThreads);
-      l += fin[(half ^ 1) * 128 + r];
-      mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
-      tc_fence_after();
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      // Stage O (bf16) in this item's Q buffer — every S of the item has
-      // completed — in the Q tile's own swizzled layout, then TMA-store each
-      // fully-live 32-row slab; partially-live slabs (request tails) store
-      // their live rows directly so neighbouring tiles are never touched.
-      uint8_t* qbuf = sQ + (li & 1) * C::TILE;
-      const bool slab_live = __all_sync(0xffffffff, live);
-#pragma unroll 1
-      for (int cc = 0; cc < HD / 64; ++cc) {
-        uint32_t v[32];
-        const int col = half * (HD / 2) + cc * 32;
-        tmem_ld_32x32b_x32(tmem + lane_off + C::O_COL + (li & 1) * 128 + col, v);
-        tmem_ld_wait();
-        uint4 pk[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float* f = reinterpret_cast<const float*>(&v[q * 8]);
-          pk[q] = make_uint4(pack_bf16x2(f[0] * inv, f[1] * inv), pack_bf16x2(f[2] * inv, f[3] * inv),
-                             pack_bf16x2(f[4] * inv, f[5] * inv), pack_bf16x2(f[6] * inv, f[7] * inv));
-        }
-        if (slab_live) {
-          uint8_t* rowp = qbuf + (col >> 6) * kBox + r * 128;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int chunk = ((col & 63) >> 3) + q;
-            *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) * 16)) = pk[q];
-          }
-        } else if (live) {
-          uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * d + h * HD + col);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) dst[q] = pk[q];
-        }
-      }
-      fence_proxy_async_smem();
-      if constexpr (HD < 128) named_bar_sync(1, kSoftmaxThreads);  // halves share a box
-      else __syncwarp();
-      tc_fence_before();
-      mbar_arrive(&o_empty[li & 1]);
-      if (lane == 0) {
-        // HD=128: warp (quad, half) owns box `half` rows [32 quad, +32).
-        // HD=64 : both halves wrote box 0; the half-0 warp stores it.
-        if (slab_live && (HD == 128 || half == 0))
-          tma_store_2d(&tm_out, qbuf + (HD == 128 ? half : 0) * kBox + quad * 32 * 128,
-                       h * HD + (HD == 128 ? half : 0) * 64, c_row0 + quad * 32);
-        bulk_commit();
-      }
-      pending_q = li & 1;  // released after the next item's first block
-      if (warp == 2 && lane == 0 && li < 8) SRK_TRACE(56 + li);
+      pend.on = true;
+      pend.li = li;
+      pend.h = h;
+      pend.row0 = c_row0;
+      pend.g_last = g - 1;
+      pend.live = live;
+      pend.l = l;
     }
+    if (pend.on) epilogue(pend);
     if (lane == 0) bulk_wait0();  // O stores complete before exit
   }
 
+  pdl_trigger();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -482,8 +529,8 @@ cudaError_t launch_tc(const CUtensorMap& tm, const RowSpan* spans, const AttnTil
   cudaGetDevice(&dev);
   const int items = n_tiles * n_heads;
   const int grid = items < num_sms(dev) ? items : num_sms(dev);
-  kern<<<grid, kThreads, C::SMEM, stream>>>(tm, tm_out, spans, tiles, n_tiles, out, n_heads);
-  return cudaGetLastError();
+  return launch_k(kern, dim3(grid), dim3(kThreads), C::SMEM, stream, tm, tm_out, spans, tiles,
+                  n_tiles, out, n_heads);
 }
 
 }  // namespace

@@ -66,8 +66,7 @@ cudaError_t launch_one(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, in
   CUtensorMap tmC;
   cudaError_t e = make_out_map<EPI>(&tmC, out, M, N, ldo);
   if (e != cudaSuccess) return e;
-  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(tmA, tmB, tmC, M, N, K);
-  return cudaGetLastError();
+  return launch_k(kern, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES, stream, tmA, tmB, tmC, M, N, K);
 }
 
 template <int BN>
@@ -100,16 +99,18 @@ int gemm_pairs_per_cluster(int N) {
 
 template <int EPI, int NP>
 cudaError_t launch_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
-                        void* out, int ldo, const GemmLnArgs& ln, cudaStream_t stream) {
+                        void* out, int ldo, const GemmLnArgs& ln, int rev, cudaStream_t stream) {
   using C = GemmPairCfg<EPI>;
   auto kern = gemm_bf16_tcgen05_pair_kernel<EPI, NP>;
   static int max_clusters = 0;  // co-resident clusters of 2*NP CTAs (per process, one GPU type)
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2 * NP;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.blockDim = dim3(C::THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = stream;
@@ -135,21 +136,23 @@ cudaError_t launch_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, i
   cudaError_t e = make_out_map<EPI>(&tmC, out, M, N, ldo);
   if (e != cudaSuccess) return e;
   cfg.gridDim = dim3(2 * NP * clusters, 1, 1);
-  e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, ln, M, N, K);
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, ln, M, N, K, rev);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 template <int EPI>
 cudaError_t launch_pair_np(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
-                           void* out, int ldo, const GemmLnArgs& ln, cudaStream_t stream) {
+                           void* out, int ldo, const GemmLnArgs& ln, int rev, cudaStream_t stream) {
   if (gemm_pairs_per_cluster(N) == 2)
-    return launch_pair<EPI, 2>(tmA, tmB, M, N, K, out, ldo, ln, stream);
-  return launch_pair<EPI, 1>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+    return launch_pair<EPI, 2>(tmA, tmB, M, N, K, out, ldo, ln, rev, stream);
+  return launch_pair<EPI, 1>(tmA, tmB, M, N, K, out, ldo, ln, rev, stream);
 }
 
 cudaError_t gemm_bf16_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
-                           void* out, int ldo, int epi, cudaStream_t stream, const LnFold* fold) {
+                           void* out, int ldo, int epi, cudaStream_t stream, const LnFold* fold,
+                           bool rev) {
   if (M <= 0) return cudaSuccess;
   if (N % GemmPairCfg<EPI_BF16>::BN != 0 || K % 8 != 0) return cudaErrorInvalidValue;
   GemmLnArgs ln;
@@ -171,19 +174,27 @@ cudaError_t gemm_bf16_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M
     ln.ld = fold->ld;
   }
   switch (epi) {
-    case EPI_BF16: return launch_pair_np<EPI_BF16>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+    case EPI_BF16: return launch_pair_np<EPI_BF16>(tmA, tmB, M, N, K, out, ldo, ln, rev ? 1 : 0, stream);
     case EPI_GELU_BF16:
-      return launch_pair_np<EPI_GELU_BF16>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+      return launch_pair_np<EPI_GELU_BF16>(tmA, tmB, M, N, K, out, ldo, ln, rev ? 1 : 0, stream);
     case EPI_RESID_F32:
-      return launch_pair_np<EPI_RESID_F32>(tmA, tmB, M, N, K, out, ldo, ln, stream);
-    case EPI_F32: return launch_pair_np<EPI_F32>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+      return launch_pair_np<EPI_RESID_F32>(tmA, tmB, M, N, K, out, ldo, ln, rev ? 1 : 0, stream);
+    case EPI_F32: return launch_pair_np<EPI_F32>(tmA, tmB, M, N, K, out, ldo, ln, rev ? 1 : 0, stream);
     case EPI_RESID_LN:
-      return launch_pair_np<EPI_RESID_LN>(tmA, tmB, M, N, K, out, ldo, ln, stream);
-    case EPI_LN_BF16: return launch_pair_np<EPI_LN_BF16>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+      return launch_pair_np<EPI_RESID_LN>(tmA, tmB, M, N, K, out, ldo, ln, rev ? 1 : 0, stream);
+    case EPI_LN_BF16: return launch_pair_np<EPI_LN_BF16>(tmA, tmB, M, N, K, out, ldo, ln, rev ? 1 : 0, stream);
     case EPI_LN_GELU_BF16:
-      return launch_pair_np<EPI_LN_GELU_BF16>(tmA, tmB, M, N, K, out, ldo, ln, stream);
+      return launch_pair_np<EPI_LN_GELU_BF16>(tmA, tmB, M, N, K, out, ldo, ln, rev ? 1 : 0, stream);
   }
   return cudaErrorInvalidValue;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("SRK_PDL");
+    return v == nullptr || std::atoi(v) != 0;
+  }();
+  return on;
 }
 
 int num_sms(int device) {

@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // inputs of the previous kernel (and its reads of our outputs) are done
 
   if (warp == 0) {
     if (lane == 0) {
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) bulk_wait0();
   }
 
+  pdl_trigger();  // this CTA's work is issued: the next kernel may start launching
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -322,7 +324,8 @@ __global__ void __launch_bounds__(320, 1)
     gemm_bf16_tcgen05_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                                   const __grid_constant__ CUtensorMap tmB,
                                   const __grid_constant__ CUtensorMap tmC,
-                                  const __grid_constant__ GemmLnArgs ln, int M, int N, int K) {
+                                  const __grid_constant__ GemmLnArgs ln, int M, int N, int K,
+                                  int rev) {
   using C = GemmPairCfg<EPI>;
   static_assert(NP == 1 || NP == 2, "one or two CTA pairs per cluster");
   constexpr int BN = C::BN;
@@ -352,6 +355,12 @@ __global__ void __launch_bounds__(320, 1)
   const int n_tiles = N / (BN * NP);  // cluster tiles along N
   const int num_tiles = m_tiles * n_tiles;
   const int nk = (K + C::BK - 1) / C::BK;
+  // rev: walk the 256-row blocks from the last to the first, so the rows the
+  // previous kernel wrote last (still in L2) are read first (serpentine order).
+  auto m_block = [&](int tile) {
+    const int mb = tile / n_tiles;
+    return rev ? m_tiles - 1 - mb : mb;
+  };
   if (threadIdx.x == 0) gemm_trace(0);
 
   if (warp == 0 && lane == 0) {
@@ -379,6 +388,7 @@ __global__ void __launch_bounds__(320, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // inputs of the previous kernel (and its reads of our outputs) are done
   if (threadIdx.x == 0) gemm_trace(1);
 
   if (warp == 0) {
@@ -395,7 +405,7 @@ __global__ void __launch_bounds__(320, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = pair; tile < num_tiles; tile += n_pairs) {
-        const int m0 = (tile / n_tiles) * 2 * C::BM + cr * C::BM;
+        const int m0 = m_block(tile) * 2 * C::BM + cr * C::BM;
         const int n0 = ((tile % n_tiles) * NP + pr) * BN + cr * (BN / 2);
         if constexpr (C::RESID_LN) {
           // The epilogue reads this CTA's 128 x 256 fp32 slab of x after the
@@ -470,7 +480,7 @@ __global__ void __launch_bounds__(320, 1)
     for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      const int m0 = (tile / n_tiles) * 2 * C::BM + cr * C::BM;
+      const int m0 = m_block(tile) * 2 * C::BM + cr * C::BM;
       const int n0 = ((tile % n_tiles) * NP + pr) * BN;
       const int r0 = m0 + quad * 32;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN;
@@ -639,7 +649,7 @@ __global__ void __launch_bounds__(320, 1)
                   }
                   if constexpr (EPI == EPI_GELU_BF16 || EPI == EPI_LN_GELU_BF16) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) f[j] = gelu_erf(f[j]);
+                    for (int j = 0; j < 8; j += 2) gelu_erf_x2(f[j], f[j + 1]);
                   }
                   const int chunk = hh * 4 + k;
                   *reinterpret_cast<uint4*>(row_base + ((chunk ^ (lane & 7)) * 16)) =
@@ -668,6 +678,7 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) bulk_wait0();
   }
 
+  pdl_trigger();  // this CTA's work is issued: the next kernel may start launching
   tc_fence_before();
   cluster_sync();
   tc_fence_after();

@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(256)
                       int n_cols, const int32_t* __restrict__ task_col,
                       const int32_t* __restrict__ task_arity, int n_tasks, int yes_col,
                       int no_col, double* __restrict__ scores, float* __restrict__ hidden_out) {
+  pdl_wait();
   extern __shared__ float s_logits[];  // [8 warps][n_cols]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * 8 + warp;
@@ -132,10 +133,9 @@ cudaError_t launch_head(const float* x, const int32_t* last_rows, int n_items, i
                         int yes_col, int no_col, double* scores, float* hidden_out,
                         cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(8) * n_cols * sizeof(float);
-  score_head_kernel<NV><<<(n_items + 7) / 8, 256, smem, stream>>>(
-      x, last_rows, n_items, d, gain, w_cols, bias, n_cols, task_col, task_arity, n_tasks,
-      yes_col, no_col, scores, hidden_out);
-  return cudaGetLastError();
+  return launch_k(score_head_kernel<NV>, dim3((n_items + 7) / 8), dim3(256), smem, stream, x,
+                  last_rows, n_items, d, gain, w_cols, bias, n_cols, task_col, task_arity, n_tasks,
+                  yes_col, no_col, scores, hidden_out);
 }
 
 // ------------------------------------------------------------------ top-k
@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(kSortThreads)
     topk_scores_kernel(const double* __restrict__ scores, int stride,
                        const int64_t* __restrict__ ids, const int32_t* __restrict__ seg_off,
                        int n_segments, int k, TopkEntry* __restrict__ out, int chunks_per_seg) {
+  pdl_wait();
   extern __shared__ TopkEntry buf[];
   const int seg = blockIdx.x / chunks_per_seg;
   const int chunk = blockIdx.x % chunks_per_seg;
@@ -224,6 +225,7 @@ __global__ void __launch_bounds__(kSortThreads)
 __global__ void __launch_bounds__(kSortThreads)
     topk_entries_kernel(const TopkEntry* __restrict__ in, int per_seg, int k,
                         TopkEntry* __restrict__ out) {
+  pdl_wait();
   extern __shared__ TopkEntry buf[];
   const TopkEntry* src = in + static_cast<size_t>(blockIdx.x) * per_seg;
   const int P = pow2_at_least(per_seg);
@@ -272,16 +274,16 @@ cudaError_t topk(const double* scores, int stride, const int64_t* ids, const int
     attr = true;
   }
   if (chunks <= 1) {
-    topk_scores_kernel<<<n_segments, kSortThreads, smem, stream>>>(scores, stride, ids, seg_off,
-                                                                   n_segments, k, out, 1);
-    return cudaGetLastError();
+    return launch_k(topk_scores_kernel, dim3(n_segments), dim3(kSortThreads), smem, stream, scores,
+                    stride, ids, seg_off, n_segments, k, out, 1);
   }
   if (static_cast<long>(chunks) * k > kSortCap) return cudaErrorInvalidValue;
   if (static_cast<long>(n_segments) * chunks * k > scratch_cap) return cudaErrorInvalidValue;
-  topk_scores_kernel<<<n_segments * chunks, kSortThreads, smem, stream>>>(
-      scores, stride, ids, seg_off, n_segments, k, scratch, chunks);
-  topk_entries_kernel<<<n_segments, kSortThreads, smem, stream>>>(scratch, chunks * k, k, out);
-  return cudaGetLastError();
+  cudaError_t e = launch_k(topk_scores_kernel, dim3(n_segments * chunks), dim3(kSortThreads), smem,
+                           stream, scores, stride, ids, seg_off, n_segments, k, scratch, chunks);
+  if (e != cudaSuccess) return e;
+  return launch_k(topk_entries_kernel, dim3(n_segments), dim3(kSortThreads), smem, stream,
+                  static_cast<const TopkEntry*>(scratch), chunks * k, k, out);
 }
 
 cudaError_t topk_merge(const TopkEntry* in, int n, int k, TopkEntry* out, cudaStream_t stream) {
@@ -290,8 +292,7 @@ cudaError_t topk_merge(const TopkEntry* in, int n, int k, TopkEntry* out, cudaSt
   const size_t smem = sizeof(TopkEntry) * kSortCap;
   cudaFuncSetAttribute(topk_entries_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem));
-  topk_entries_kernel<<<1, kSortThreads, smem, stream>>>(in, n, k, out);
-  return cudaGetLastError();
+  return launch_k(topk_entries_kernel, dim3(1), dim3(kSortThreads), smem, stream, in, n, k, out);
 }
 
 }  // namespace srk

@@ -7,7 +7,38 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
+#include <utility>
+
 namespace srk {
+
+// Programmatic dependent launch for the forward's kernels (SRK_PDL=0 turns it
+// off): a kernel may be scheduled while its predecessor drains, and must pass
+// pdl_wait() before touching anything the predecessor wrote (or still reads);
+// pdl_trigger() lets its own successor launch; every kernel triggers once its
+// own work is done (successors then overlap only the teardown + launch).
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#endif
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
 
 // Row descriptor for segment-masked attention (one per packed row).
 // Row r may attend keys [prefix_begin, prefix_end) U [span_start, r]
@@ -66,7 +97,7 @@ struct LnFold {
 // 128-row x 64-column boxes. Epilogues 4-6 need `fold`.
 cudaError_t gemm_bf16_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
                            void* out, int ldo, int epi, cudaStream_t stream,
-                           const LnFold* fold = nullptr);
+                           const LnFold* fold = nullptr, bool rev = false);
 // The projection GEMMs take the pair path when N is a multiple of 256.
 inline bool gemm_use_pair(int N) { return N % 256 == 0; }
 // B-operand box rows for a weight [N x K] map on the chosen path.
@@ -74,8 +105,9 @@ inline int gemm_b_box_rows(int N) { return gemm_use_pair(N) ? 128 : gemm_pick_bn
 // Dispatch: pair kernel when N % 256 == 0, else the 1-CTA kernel.
 inline cudaError_t gemm_auto(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int N, int K,
                              void* out, int ldo, int epi, cudaStream_t stream,
-                             const LnFold* fold = nullptr) {
-  if (gemm_use_pair(N)) return gemm_bf16_pair(tmA, tmB, M, N, K, out, ldo, epi, stream, fold);
+                             const LnFold* fold = nullptr, bool rev = false) {
+  // rev: 256-row blocks in reverse order (L2 serpentine; pair kernel only)
+  if (gemm_use_pair(N)) return gemm_bf16_pair(tmA, tmB, M, N, K, out, ldo, epi, stream, fold, rev);
   if (epi > 3) return cudaErrorInvalidValue;  // LN folding is a pair-kernel epilogue
   return gemm_bf16(tmA, tmB, M, N, K, out, ldo, epi, gemm_pick_bn(N), stream);
 }
@@ -90,8 +122,9 @@ cudaError_t embed_ln(const int32_t* src, const int32_t* pos, const float* tok_em
 cudaError_t embed_stats(const int32_t* src, const int32_t* pos, const float* tok_emb,
                         const float* soft_rows, const float* pos_emb, float* x,
                         __nv_bfloat16* xb, float* stats, int M, int d, cudaStream_t stream);
+// rev: rows walked from the last block to the first (L2 serpentine order).
 cudaError_t layer_norm_bf16(const float* x, const float* gain, __nv_bfloat16* out, int M, int d,
-                            cudaStream_t stream);
+                            cudaStream_t stream, bool rev = false);
 
 // -------------------------------------------------------------- attention
 // qkv: [M x 3d] bf16 rows (q | k | v); out: [M x d] bf16.

@@ -410,6 +410,31 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n_threads) 
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n_threads) : "memory");
 }
 
+// Blackwell 3-input max (FMNMX3) and packed fp32x2 FMA / add (FFMA2, FADD2).
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f32x2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f32x2_split(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fma_f32x2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t add_f32x2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 __device__ __forceinline__ float gelu_erf(float v) {
   // kernels.cpp:47-49 (reference): 0.5 v (1 + erf(v / sqrt 2)), exact erf.
   // 1 + erf(z) = 2 - erfc(z) for z >= 0 and erfc(|z|) for z < 0, with the
@@ -432,6 +457,46 @@ __device__ __forceinline__ float gelu_erf(float v) {
   const float erfc = t * __expf(fmaf(-z, z, p));
   const float one_plus_erf = v >= 0.0f ? 2.0f - erfc : erfc;
   return 0.5f * v * one_plus_erf;
+}
+
+__device__ __forceinline__ uint64_t mul_f32x2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// gelu_erf on a pair of values with packed fp32x2 arithmetic (FFMA2/FMUL2):
+// the same Chebyshev erfc and operation order per lane as gelu_erf, half the
+// FMA-pipe instructions (the W_in epilogue is issue-bound).
+__device__ __forceinline__ void gelu_erf_x2(float& v0, float& v1) {
+  const uint64_t z = mul_f32x2(f32x2(fabsf(v0), fabsf(v1)),
+                               f32x2(0.70710678118654752f, 0.70710678118654752f));
+  float z0, z1;
+  f32x2_split(z, z0, z1);
+  float d0, d1;
+  f32x2_split(fma_f32x2(f32x2(0.5f, 0.5f), z, f32x2(1.0f, 1.0f)), d0, d1);
+  float t0, t1;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t0) : "f"(d0));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t1) : "f"(d1));
+  const uint64_t t = f32x2(t0, t1);
+  uint64_t p = f32x2(0.17087277f, 0.17087277f);
+  p = fma_f32x2(p, t, f32x2(-0.82215223f, -0.82215223f));
+  p = fma_f32x2(p, t, f32x2(1.48851587f, 1.48851587f));
+  p = fma_f32x2(p, t, f32x2(-1.13520398f, -1.13520398f));
+  p = fma_f32x2(p, t, f32x2(0.27886807f, 0.27886807f));
+  p = fma_f32x2(p, t, f32x2(-0.18628806f, -0.18628806f));
+  p = fma_f32x2(p, t, f32x2(0.09678418f, 0.09678418f));
+  p = fma_f32x2(p, t, f32x2(0.37409196f, 0.37409196f));
+  p = fma_f32x2(p, t, f32x2(1.00002368f, 1.00002368f));
+  p = fma_f32x2(p, t, f32x2(-1.26551223f, -1.26551223f));
+  const uint64_t arg = fma_f32x2(f32x2(-z0, -z1), z, p);
+  float a0, a1;
+  f32x2_split(arg, a0, a1);
+  float e0, e1;
+  f32x2_split(mul_f32x2(t, f32x2(__expf(a0), __expf(a1))), e0, e1);
+  const float o0 = v0 >= 0.0f ? 2.0f - e0 : e0;
+  const float o1 = v1 >= 0.0f ? 2.0f - e1 : e1;
+  f32x2_split(mul_f32x2(mul_f32x2(f32x2(0.5f, 0.5f), f32x2(v0, v1)), f32x2(o0, o1)), v0, v1);
 }
 
 }  // namespace srk

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(256)
                     const float* __restrict__ tok_emb, const float* __restrict__ soft_rows,
                     const float* __restrict__ pos_emb, const float* __restrict__ gain,
                     float* __restrict__ x, __nv_bfloat16* __restrict__ xn, int M, int d) {
+  pdl_wait();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -87,6 +88,7 @@ __global__ void __launch_bounds__(256)
     }
   }
   ln_row_store<NV>(v, d4, gain, xn + static_cast<size_t>(row) * d, lane);
+  pdl_trigger();
 }
 
 // Folded-LN variant (gemm_tcgen05.cuh GemmLnArgs): the layer-0 LN1 is
@@ -98,6 +100,7 @@ __global__ void __launch_bounds__(256)
                        const float* __restrict__ tok_emb, const float* __restrict__ soft_rows,
                        const float* __restrict__ pos_emb, float* __restrict__ x,
                        __nv_bfloat16* __restrict__ xb, float2* __restrict__ stats, int M, int d) {
+  pdl_wait();
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -139,6 +142,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffff, q, o);
   if (lane == 0) stats[row] = make_float2(mean, q);
+  pdl_trigger();
 }
 
 template <int NV>
@@ -146,9 +150,8 @@ cudaError_t launch_embed_stats(const int32_t* src, const int32_t* pos, const flo
                                const float* soft_rows, const float* pos_emb, float* x,
                                __nv_bfloat16* xb, float* stats, int M, int d,
                                cudaStream_t stream) {
-  embed_stats_kernel<NV><<<(M + 7) / 8, 256, 0, stream>>>(
-      src, pos, tok_emb, soft_rows, pos_emb, x, xb, reinterpret_cast<float2*>(stats), M, d);
-  return cudaGetLastError();
+  return launch_k(embed_stats_kernel<NV>, dim3((M + 7) / 8), dim3(256), 0, stream, src, pos,
+                  tok_emb, soft_rows, pos_emb, x, xb, reinterpret_cast<float2*>(stats), M, d);
 }
 
 // One warp per weight row: out[n] = sum_k float(w[n][k]) (double accumulation).
@@ -167,8 +170,10 @@ __global__ void bf16_row_sums_kernel(const __nv_bfloat16* __restrict__ w, int N,
 template <int NV>
 __global__ void __launch_bounds__(256)
     layer_norm_kernel(const float* __restrict__ x, const float* __restrict__ gain,
-                      __nv_bfloat16* __restrict__ out, int M, int d) {
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+                      __nv_bfloat16* __restrict__ out, int M, int d, int rev) {
+  pdl_wait();
+  const int blk = rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+  const int row = blk * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
   const int d4 = d >> 2;
@@ -180,22 +185,22 @@ __global__ void __launch_bounds__(256)
     if (c < d4) v[i] = xr[c];
   }
   ln_row_store<NV>(v, d4, gain, out + static_cast<size_t>(row) * d, lane);
+  pdl_trigger();
 }
 
 template <int NV>
 cudaError_t launch_embed(const int32_t* src, const int32_t* pos, const float* tok_emb,
                          const float* soft_rows, const float* pos_emb, const float* gain, float* x,
                          __nv_bfloat16* xn, int M, int d, cudaStream_t stream) {
-  embed_ln_kernel<NV><<<(M + 7) / 8, 256, 0, stream>>>(src, pos, tok_emb, soft_rows, pos_emb,
-                                                       gain, x, xn, M, d);
-  return cudaGetLastError();
+  return launch_k(embed_ln_kernel<NV>, dim3((M + 7) / 8), dim3(256), 0, stream, src, pos, tok_emb,
+                  soft_rows, pos_emb, gain, x, xn, M, d);
 }
 
 template <int NV>
 cudaError_t launch_ln(const float* x, const float* gain, __nv_bfloat16* out, int M, int d,
-                      cudaStream_t stream) {
-  layer_norm_kernel<NV><<<(M + 7) / 8, 256, 0, stream>>>(x, gain, out, M, d);
-  return cudaGetLastError();
+                      cudaStream_t stream, int rev) {
+  return launch_k(layer_norm_kernel<NV>, dim3((M + 7) / 8), dim3(256), 0, stream, x, gain, out, M,
+                  d, rev);
 }
 
 __global__ void transpose_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
@@ -239,10 +244,10 @@ cudaError_t embed_ln(const int32_t* src, const int32_t* pos, const float* tok_em
 }
 
 cudaError_t layer_norm_bf16(const float* x, const float* gain, __nv_bfloat16* out, int M, int d,
-                            cudaStream_t stream) {
+                            cudaStream_t stream, bool rev) {
   if (M <= 0) return cudaSuccess;
   if (d % 4 != 0) return cudaErrorInvalidValue;
-  SRK_DISPATCH_NV(d, launch_ln, x, gain, out, M, d, stream);
+  SRK_DISPATCH_NV(d, launch_ln, x, gain, out, M, d, stream, rev ? 1 : 0);
 }
 
 cudaError_t transpose_to_bf16(const float* src, __nv_bfloat16* dst, int K, int N,
