@@ -28,6 +28,9 @@
 // TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+HD) O1 [384,384+HD).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+#include <string>
+
 #include "launch.h"
 #include "ptx.cuh"
 
@@ -533,6 +536,452 @@ cudaError_t launch_tc(const CUtensorMap& tm, const RowSpan* spans, const AttnTil
                   n_tiles, out, n_heads);
 }
 
+
+// ----------------------------------------------------------------------------
+// Ping-pong variant (opt-in, see attn_use_pp): two query tiles ("slots") in flight per CTA,
+// as FlashAttention-4. Each slot has its own Q / K / V buffers, S/P and O
+// TMEM regions and a 4-warp softmax group in which every thread owns one
+// query row end to end (no cross-warp max exchange, no per-block CTA-wide
+// barrier). The MMA warp issues whichever slot's next S or PV is ready, so
+// the tensor core computes one slot's QK^T / PV while the other slot's
+// softmax (and its item epilogue) runs.
+//   warp 0 / 10  TMA producer of slot 0 / 1: K_j, V_j (single-stage per slot)
+//   warp 1       TMEM alloc + event-driven tcgen05.mma issuer for both slots
+//   warps 2-5    softmax + epilogue of slot 0 (rows = TMEM lanes, 128 threads)
+//   warps 6-9    softmax + epilogue of slot 1
+// The softmax group itself reloads its slot's Q once the item's O has been
+// staged (in the Q buffer) and stored.
+// TMEM (512 cols): S/P slot x at [128 x, +128), O slot x at [256 + 128 x, +HD).
+constexpr int kPPThreads = 352;
+
+template <int HD>
+struct PPCfg {
+  static constexpr int NB = HD / 64;
+  static constexpr int TILE = NB * kBox;
+  static constexpr int Q_OFF = 0;         // [slot]
+  static constexpr int K_OFF = 2 * TILE;  // [slot]
+  static constexpr int V_OFF = 4 * TILE;  // [slot]
+  static constexpr int BAR_OFF = 6 * TILE;
+  static constexpr int SMEM = BAR_OFF + 512 + 1024;
+  static constexpr int O_COL = 256;
+};
+
+enum PPBar : int { PB_Q_FULL = 0, PB_K_FULL, PB_K_EMPTY, PB_V_FULL, PB_V_EMPTY, PB_S_FULL,
+                   PB_P_FULL, PB_PV_DONE, PB_N };
+
+// One slot's (item, block) sequence: items first, first + stride, ...
+struct SlotCursor {
+  int item = 0, stride = 1, n_items = 0, n_tiles = 1;
+  int j = 0, nblk = 0, nb1 = 0, h = 0;
+  AttnTile t;
+  bool valid = false;
+  __device__ void init(const AttnTile* tiles, int n_tiles_, int n_items_, int first, int stride_) {
+    n_tiles = n_tiles_;
+    n_items = n_items_;
+    stride = stride_;
+    seek(tiles, first);
+  }
+  __device__ void seek(const AttnTile* tiles, int it) {
+    for (;; it += stride) {
+      item = it;
+      valid = it < n_items;
+      if (!valid) return;
+      t = tiles[it % n_tiles];
+      h = it / n_tiles;
+      nb1 = (t.r1_end - t.r1_begin + kBK - 1) / kBK;
+      nblk = nb1 + (t.r2_end - t.r2_begin + kBK - 1) / kBK;
+      j = 0;
+      if (nblk > 0) return;
+    }
+  }
+  __device__ void range(int& k0, int& kbeg, int& kend) const {
+    if (j < nb1) {
+      k0 = t.r1_begin + j * kBK;
+      kbeg = t.r1_begin;
+      kend = t.r1_end;
+    } else {
+      k0 = t.r2_begin + (j - nb1) * kBK;
+      kbeg = t.r2_begin;
+      kend = t.r2_end;
+    }
+  }
+  // Advance one block; true when the item finished.
+  __device__ bool advance(const AttnTile* tiles) {
+    if (++j < nblk) return false;
+    seek(tiles, item + stride);
+    return true;
+  }
+};
+
+// Visible keys [lo, hi) (relative to the chunk start) as a 32-bit mask.
+__device__ __forceinline__ uint32_t chunk_bits(int lo, int hi) {
+  lo = max(lo, 0);
+  hi = min(hi, 32);
+  if (hi <= lo) return 0u;
+  const uint32_t upto = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+  return upto & ~((1u << lo) - 1u);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kPPThreads, 1)
+    attn_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                   const __grid_constant__ CUtensorMap tm_out, const RowSpan* __restrict__ spans,
+                   const AttnTile* __restrict__ tiles, int n_tiles, __nv_bfloat16* __restrict__ out,
+                   int n_heads) {
+  using C = PPCfg<HD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sQ = smem + C::Q_OFF;
+  uint8_t* sK = smem + C::K_OFF;
+  uint8_t* sV = smem + C::V_OFF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  auto bar = [&](int x, int i) { return bars + x * PB_N + i; };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * PB_N);
+
+  const int n_items = n_tiles * n_heads;
+  const int d = n_heads * HD;
+  const int G = static_cast<int>(gridDim.x);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) SRK_TRACE(0);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_out);
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(bar(x, PB_Q_FULL), 1);
+      mbar_init(bar(x, PB_K_FULL), 1);
+      mbar_init(bar(x, PB_K_EMPTY), 1);
+      mbar_init(bar(x, PB_V_FULL), 1);
+      mbar_init(bar(x, PB_V_EMPTY), 1);
+      mbar_init(bar(x, PB_S_FULL), 1);
+      mbar_init(bar(x, PB_P_FULL), 128);
+      mbar_init(bar(x, PB_PV_DONE), 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+
+  if (warp == 0 || warp == 10) {
+    // ------------------------------------------------ K / V of one slot
+    const int x = warp == 0 ? 0 : 1;
+    if (lane == 0) {
+      const uint64_t keep = policy_evict_last();  // prefix K/V: re-read by every item tile
+      SlotCursor c;
+      c.init(tiles, n_tiles, n_items, blockIdx.x + x * G, 2 * G);
+      uint8_t* k_buf = sK + x * C::TILE;
+      uint8_t* v_buf = sV + x * C::TILE;
+      for (int n = 0; c.valid; ++n) {
+        int k0, kb, ke;
+        c.range(k0, kb, ke);
+        const uint32_t ph = (n & 1) ^ 1;
+        mbar_wait(bar(x, PB_K_EMPTY), ph);
+        mbar_arrive_expect_tx(bar(x, PB_K_FULL), C::TILE);
+        for (int b = 0; b < C::NB; ++b)
+          tma_load_2d_hint(&tm_qkv, bar(x, PB_K_FULL), k_buf + b * kBox, d + c.h * HD + b * 64, k0,
+                           keep);
+        mbar_wait(bar(x, PB_V_EMPTY), ph);
+        mbar_arrive_expect_tx(bar(x, PB_V_FULL), C::TILE);
+        for (int b = 0; b < C::NB; ++b)
+          tma_load_2d_hint(&tm_qkv, bar(x, PB_V_FULL), v_buf + b * kBox, 2 * d + c.h * HD + b * 64,
+                           k0, keep);
+        c.advance(tiles);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA (both slots)
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(kTM, kBK);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32_bmn(kTM, HD);
+      SlotCursor c[2];
+      int ns[2] = {0, 0}, np[2] = {0, 0}, nq[2] = {0, 0};
+      bool want_s[2], s_free[2] = {true, true};
+      for (int x = 0; x < 2; ++x) {
+        c[x].init(tiles, n_tiles, n_items, blockIdx.x + x * G, 2 * G);
+        want_s[x] = true;
+      }
+      while (c[0].valid || c[1].valid) {
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {  // unrolled: per-slot state stays in registers
+          if (!c[x].valid) continue;
+          if (want_s[x]) {
+            // S_x = Q_x K^T into the slot's S buffer, free once PV of the
+            // previous block has read P out of it.
+            if (!s_free[x]) {
+              if (!mbar_test(bar(x, PB_PV_DONE), (np[x] - 1) & 1)) continue;
+              s_free[x] = true;
+            }
+            if (c[x].j == 0 && !mbar_test(bar(x, PB_Q_FULL), nq[x] & 1)) continue;
+            if (!mbar_test(bar(x, PB_K_FULL), ns[x] & 1)) continue;
+            tc_fence_after();
+            if (c[x].j == 0) ++nq[x];
+            const uint32_t q_addr = smem_u32(sQ + x * C::TILE);
+            const uint32_t k_addr = smem_u32(sK + x * C::TILE);
+#pragma unroll
+            for (int s = 0; s < HD / 16; ++s) {
+              const uint32_t off = (s >> 2) * kBox + (s & 3) * 32;
+              umma_bf16(tmem + x * kBK, sw128_kmajor_desc(q_addr + off),
+                        sw128_kmajor_desc(k_addr + off), idesc_s, s > 0 ? 1u : 0u);
+            }
+            umma_commit(bar(x, PB_K_EMPTY));
+            umma_commit(bar(x, PB_S_FULL));
+            ++ns[x];
+            want_s[x] = false;
+          } else {
+            // O_x += P_x V (P read from TMEM)
+            if (!mbar_test(bar(x, PB_P_FULL), np[x] & 1)) continue;
+            if (!mbar_test(bar(x, PB_V_FULL), np[x] & 1)) continue;
+            tc_fence_after();
+            const uint32_t v_addr = smem_u32(sV + x * C::TILE);
+#pragma unroll
+            for (int s = 0; s < kBK / 16; ++s)
+              umma_bf16_ts(tmem + C::O_COL + x * 128, tmem + x * kBK + s * 8,
+                           sw128_mnmajor_desc(v_addr + s * 16 * 128, kBox, 1024), idesc_pv,
+                           (c[x].j > 0 || s > 0) ? 1u : 0u);
+            umma_commit(bar(x, PB_V_EMPTY));
+            umma_commit(bar(x, PB_PV_DONE));
+            ++np[x];
+            s_free[x] = false;
+            want_s[x] = true;
+            c[x].advance(tiles);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ softmax + epilogue
+    const int x = (warp - 2) >> 2;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;  // query row of the tile = TMEM lane
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + x * kBK;
+    const uint32_t t_o = tmem + lane_off + C::O_COL + x * 128;
+    uint8_t* qbuf = sQ + x * C::TILE;
+    const bool elected = warp == 2 + 4 * x && lane == 0;
+    const float scale_log2 = 1.4426950408889634f * rsqrtf(static_cast<float>(HD));
+    SlotCursor c;
+    c.init(tiles, n_tiles, n_items, blockIdx.x + x * G, 2 * G);
+    auto load_q = [&]() {
+      mbar_arrive_expect_tx(bar(x, PB_Q_FULL), C::TILE);
+      for (int b = 0; b < C::NB; ++b)
+        tma_load_2d(&tm_qkv, bar(x, PB_Q_FULL), qbuf + b * kBox, c.h * HD + b * 64, c.t.q_begin);
+    };
+    if (elected && c.valid) load_q();
+    int g = 0;  // blocks of this slot so far
+    while (c.valid) {
+      const int row0 = c.t.q_begin;
+      const int row = row0 + r;
+      const bool live = row < c.t.q_end;
+      const int h = c.h;
+      RowSpan sp = {0, 0, 0, 0};
+      if (live) sp = spans[row];
+      float m_used = -INFINITY;  // exponent base (raw score units)
+      float l = 0.f;
+      bool item_done = false;
+      while (!item_done) {
+        int k0, kb, ke;
+        c.range(k0, kb, ke);
+        // visible keys of this row in the block, relative to k0
+        const int a_lo = max(kb, sp.prefix_begin) - k0, a_hi = min(ke, sp.prefix_end) - k0;
+        const int b_lo = max(kb, sp.span_start) - k0, b_hi = min(ke, row + 1) - k0;
+        const bool full = live && ((a_lo <= 0 && a_hi >= kBK) || (b_lo <= 0 && b_hi >= kBK));
+        const bool all_full = __all_sync(0xffffffff, full);
+        mbar_wait(bar(x, PB_S_FULL), g & 1);
+        if (warp == 2 && lane == 0 && g < 24) SRK_TRACE(40 + g);
+        tc_fence_after();
+        // The whole 128-key row of S in registers: one TMEM round trip.
+        uint32_t v[kBK];
+#pragma unroll
+        for (int cc = 0; cc < kBK / 32; ++cc)
+          tmem_ld_32x32b_x32(t_s + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[cc * 32]));
+        uint32_t bits[kBK / 32];
+#pragma unroll
+        for (int cc = 0; cc < kBK / 32; ++cc)
+          bits[cc] = all_full ? 0xffffffffu
+                              : (live ? (chunk_bits(a_lo - 32 * cc, a_hi - 32 * cc) |
+                                         chunk_bits(b_lo - 32 * cc, b_hi - 32 * cc))
+                                      : 0u);
+        tmem_ld_wait();
+        float ma = -INFINITY, mb = -INFINITY;
+        if (all_full) {
+#pragma unroll
+          for (int i = 0; i < kBK; i += 4) {
+            ma = fmax3f(ma, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+            mb = fmax3f(mb, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < kBK; i += 2) {
+            if (!((bits[i >> 5] >> (i & 31)) & 1u)) v[i] = __float_as_uint(-INFINITY);
+            if (!((bits[i >> 5] >> ((i + 1) & 31)) & 1u)) v[i + 1] = __float_as_uint(-INFINITY);
+            if (i & 2) mb = fmax3f(mb, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+            else ma = fmax3f(ma, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+          }
+        }
+        const float mx = fmaxf(ma, mb);
+        // Lazy rescale (FlashAttention-4): move the base only when the max
+        // grows by more than 2^8; O is rescaled in TMEM by its own row's thread.
+        const bool move =
+            mx > m_used && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2);
+        const float m_new = move ? mx : m_used;
+        if (c.j > 0 && __any_sync(0xffffffff, move)) {
+          mbar_wait(bar(x, PB_PV_DONE), (g - 1) & 1);  // every PV so far used the old base
+          tc_fence_after();
+          const float corr = move ? ex2_approx((m_used - m_new) * scale_log2) : 1.f;
+          l *= corr;
+#pragma unroll 1
+          for (int cc = 0; cc < HD / 32; ++cc) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(t_o + cc * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+            tmem_st_32x32b_x32(t_o + cc * 32, o);
+          }
+        }
+        m_used = m_new;
+        const float base = m_used == -INFINITY ? 0.f : m_used * scale_log2;
+        const uint64_t sc2 = f32x2(scale_log2, scale_log2), nb2 = f32x2(-base, -base);
+        uint64_t acc0 = f32x2(0.f, 0.f), acc1 = acc0;
+        // P = 2^(s * scale - base) as bf16x2 over the consumed S columns
+        // (keys 32 cc .. 32 cc + 31 -> columns [16 cc, 16 cc + 16)), packed in
+        // place into v[32 cc .. 32 cc + 15]; masked keys hold -inf -> 0.
+#pragma unroll
+        for (int cc = 0; cc < kBK / 32; ++cc) {
+          uint32_t* w = &v[32 * cc];
+          if (!__any_sync(0xffffffff, bits[cc] != 0u)) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[i] = 0u;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              float a0, a1;
+              f32x2_split(fma_f32x2(f32x2(__uint_as_float(w[i]), __uint_as_float(w[i + 1])), sc2,
+                                    nb2),
+                          a0, a1);
+              const float p0 = ex2_approx(a0);
+              const float p1 = ex2_approx(a1);
+              if (i & 2) acc1 = add_f32x2(acc1, f32x2(p0, p1));
+              else acc0 = add_f32x2(acc0, f32x2(p0, p1));
+              w[i >> 1] = pack_bf16x2(p0, p1);
+            }
+          }
+          tmem_st_32x32b_x16(t_s + cc * 16, *reinterpret_cast<uint32_t(*)[16]>(w));
+        }
+        float r0, r1, r2, r3;
+        f32x2_split(acc0, r0, r1);
+        f32x2_split(acc1, r2, r3);
+        l += (r0 + r1) + (r2 + r3);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(bar(x, PB_P_FULL));
+        if (warp == 2 && lane == 0 && g < 24) SRK_TRACE(1 + g);
+        ++g;
+        item_done = c.advance(tiles);
+      }
+      // ---- item epilogue: O / l -> bf16, staged in this slot's Q buffer
+      // (every S of the item has completed), TMA-stored per 32-row slab;
+      // partially-live slabs (request tails) store their live rows directly.
+      mbar_wait(bar(x, PB_PV_DONE), (g - 1) & 1);
+      tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      const bool slab_live = __all_sync(0xffffffff, live);
+#pragma unroll 1
+      for (int cc = 0; cc < HD / 32; ++cc) {
+        uint32_t v[32];
+        const int col = cc * 32;
+        tmem_ld_32x32b_x32(t_o + col, v);
+        tmem_ld_wait();
+        uint4 pk[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float* f = reinterpret_cast<const float*>(&v[q * 8]);
+          pk[q] = make_uint4(pack_bf16x2(f[0] * inv, f[1] * inv), pack_bf16x2(f[2] * inv, f[3] * inv),
+                             pack_bf16x2(f[4] * inv, f[5] * inv), pack_bf16x2(f[6] * inv, f[7] * inv));
+        }
+        if (slab_live) {
+          uint8_t* rowp = qbuf + (col >> 6) * kBox + r * 128;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int chunk = ((col & 63) >> 3) + q;
+            *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) * 16)) = pk[q];
+          }
+        } else if (live) {
+          uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * d + h * HD + col);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dst[q] = pk[q];
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (slab_live)
+          for (int b = 0; b < C::NB; ++b)
+            tma_store_2d(&tm_out, qbuf + b * kBox + quad * 32 * 128, h * HD + b * 64, row0 + quad * 32);
+        bulk_commit();
+        bulk_wait_read0();  // the Q buffer is reloaded next
+      }
+      tc_fence_before();
+      named_bar_sync(2 + x, 128);  // all four slabs have left the Q buffer
+      if (elected && c.valid) load_q();
+      if (warp == 2 && lane == 0 && g < 256) SRK_TRACE(30);
+    }
+    if (lane == 0) bulk_wait0();  // O stores complete before exit
+  }
+
+  pdl_trigger();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (threadIdx.x == 0) SRK_TRACE(29);
+}
+
+template <int HD>
+cudaError_t launch_pp(const CUtensorMap& tm, const RowSpan* spans, const AttnTile* tiles,
+                      int n_tiles, __nv_bfloat16* out, int M, int n_heads, cudaStream_t stream) {
+  using C = PPCfg<HD>;
+  auto kern = attn_pp_kernel<HD>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap tm_out;
+  cudaError_t e = make_tmap_bf16_2d(&tm_out, out, M, static_cast<uint64_t>(n_heads) * HD, 32, 64);
+  if (e != cudaSuccess) return e;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int items = n_tiles * n_heads;
+  // two items in flight per CTA
+  const int want = (items + 1) / 2;
+  const int grid = want < num_sms(dev) ? want : num_sms(dev);
+  return launch_k(kern, dim3(grid), dim3(kPPThreads), C::SMEM, stream, tm, tm_out, spans, tiles,
+                  n_tiles, out, n_heads);
+}
+
+// Opt-in (SRK_ATTN=pp). Measured on B200 at C2 (tools/attn_pp_trace.py):
+// 132k cycles per CTA vs 116k for attn_tc_kernel — with one K/V stage per
+// slot (smem: 2 Q + 2 K + 2 V tiles of 32 KB) each slot waits ~2.5k cycles
+// per block for its next S, and a thread owning a full 128-key row spends
+// ~2.5k cycles per block in softmax, so the two slots do not hide each other.
+bool attn_use_pp() {
+  static const bool pp = [] {
+    const char* v = std::getenv("SRK_ATTN");
+    return v != nullptr && std::string(v) == "pp";
+  }();
+  return pp;
+}
 }  // namespace
 
 cudaError_t attention_set_trace(unsigned long long* dev_buf) {
@@ -545,9 +994,15 @@ cudaError_t attention_tc(const CUtensorMap& tm_qkv, const RowSpan* spans, const 
                          int n_tiles, __nv_bfloat16* out, int M, int n_heads, int head_dim,
                          cudaStream_t stream) {
   if (n_tiles <= 0) return cudaSuccess;
+  // SRK_ATTN=pp selects the two-slot ping-pong kernel (A/B runs).
+  const bool pp = attn_use_pp();
   switch (head_dim) {
-    case 64: return launch_tc<64>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream);
-    case 128: return launch_tc<128>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream);
+    case 64:
+      return pp ? launch_pp<64>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream)
+                : launch_tc<64>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream);
+    case 128:
+      return pp ? launch_pp<128>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream)
+                : launch_tc<128>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream);
   }
   return cudaErrorInvalidValue;
 }

@@ -292,7 +292,7 @@ struct alignas(64) GemmLnArgs {
 #define SRK_PAIR_STG_BUFS 1
 #endif
 #ifndef SRK_RESID_LN_STAGES
-#define SRK_RESID_LN_STAGES 4
+#define SRK_RESID_LN_STAGES 5
 #endif
 template <int EPI>
 struct GemmPairCfg {
@@ -302,15 +302,15 @@ struct GemmPairCfg {
   static constexpr int A_BYTES = BM * BK * 2;        // 16 KB
   static constexpr int B_BYTES = (BN / 2) * BK * 2;  // 16 KB (this CTA's half of B)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // The residual+LN epilogue stages x in and out (2 fp32 chunks + 1 bf16
-  // chunk per warp), paid for with two ring stages. (A register -> global
+  // The residual+LN epilogue stages x in and out (1 fp32 chunk + 1 bf16
+  // chunk per warp), paid for with one ring stage. (A register -> global
   // variant with 16x256b TMEM loads was measured slower: 8 rows x 32 B per
   // store instruction made the epilogue LSU-bound, 2-3x the staged time.)
   static constexpr bool RESID_LN = EPI == EPI_RESID_LN;
   static constexpr int STAGES = RESID_LN ? SRK_RESID_LN_STAGES : SRK_PAIR_STAGES;
   static constexpr int TMEM_COLS = 2 * BN;  // double-buffered 128 x 256 fp32
   static constexpr int EPI_WARPS = 8;
-  static constexpr int STG_BUFS = RESID_LN ? 3 : SRK_PAIR_STG_BUFS;  // per epilogue warp
+  static constexpr int STG_BUFS = RESID_LN ? 2 : SRK_PAIR_STG_BUFS;  // per epilogue warp
   static constexpr int STG_BYTES = 32 * 128;
   static constexpr int BAR_BYTES = 512;
   static constexpr int SMEM_BYTES =
@@ -339,8 +339,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* xbar = tempty + 2;  // EPI_RESID_LN: 2 per epilogue warp (x chunk loads)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 2 * C::EPI_WARPS);
+  uint64_t* xbar = tempty + 2;  // EPI_RESID_LN: 1 per epilogue warp (x chunk loads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + C::EPI_WARPS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&tempty[a], 2 * C::EPI_WARPS);  // one per epilogue warp of both CTAs
     }
     if constexpr (C::RESID_LN)
-      for (int b = 0; b < 2 * C::EPI_WARPS; ++b) mbar_init(&xbar[b], 1);
+      for (int b = 0; b < C::EPI_WARPS; ++b) mbar_init(&xbar[b], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(320, 1)
     const uint64_t pol_keep = policy_evict_last();
     int local = 0;
     int nstg = 0;  // staging chunks issued by this warp (buffer = nstg % STG_BUFS)
-    uint32_t xph = 0;  // EPI_RESID_LN: parity of the two x-chunk barriers (bit b)
+    uint32_t xph = 0;  // EPI_RESID_LN: parity of this warp's x-chunk barrier
     for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
@@ -485,34 +485,30 @@ __global__ void __launch_bounds__(320, 1)
       const int r0 = m0 + quad * 32;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN;
       if constexpr (C::RESID_LN) {
-        // x chunks 0 and 1 of this warp's 32 x 128 slab load while the MMA
-        // runs (the producer already pulled the slab into L2).
-        uint8_t* F0 = stg0;
-        uint64_t* xb_bar = xbar + 2 * (warp - 2);
+        // One fp32 staging chunk F (x in, x + acc out) and one bf16 chunk Bb
+        // per warp; x chunk c+1 is loaded (an L2 hit: the producer prefetched
+        // the slab) as soon as chunk c's store has read F.
+        uint8_t* F = stg0;
+        uint8_t* Bb = stg0 + C::STG_BYTES;
+        uint64_t* xb_bar = xbar + (warp - 2);
         if (r0 < M && lane == 0) {
-          bulk_wait_read0();  // previous tile's stores have left both buffers
-#pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            mbar_arrive_expect_tx(&xb_bar[b], C::STG_BYTES);
-            tma_load_2d(&tmC, &xb_bar[b], F0 + b * C::STG_BYTES, n0 + col0 + 32 * b, r0);
-          }
+          bulk_wait_read0();  // previous tile's stores have left F and Bb
+          mbar_arrive_expect_tx(xb_bar, C::STG_BYTES);
+          tma_load_2d(&tmC, xb_bar, F, n0 + col0, r0);
         }
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         if (r0 < M) {
-          uint8_t* Bb = stg0 + 2 * C::STG_BYTES;
           float s_mean = 0.f, s_m2 = 0.f;
 #pragma unroll 1
           for (int c = 0; c < SPAN / 32; ++c) {
-            const int b = c & 1;
-            uint8_t* Fb = F0 + b * C::STG_BYTES;
             __syncwarp();  // lane 0's buffer waits of the previous chunk come first
             uint32_t r[32];
             tmem_ld_32x32b_x32(t_row + col0 + 32 * c, r);
-            mbar_wait(&xb_bar[b], (xph >> b) & 1u);
-            xph ^= 1u << b;
+            mbar_wait(xb_bar, xph & 1u);
+            xph ^= 1u;
             tmem_ld_wait();
-            uint8_t* row = Fb + lane * 128;
+            uint8_t* row = F + lane * 128;
             float v[32];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -525,24 +521,6 @@ __global__ void __launch_bounds__(320, 1)
               *qp = make_uint4(__float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
                                __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
             }
-            // chunk mean / M2 (two-pass over registers), merged into the running
-            // pair (Chan et al.)
-            float cs = 0.f;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) cs += v[j];
-            const float cm = cs * (1.f / 32.f);
-            float cq = 0.f;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) cq = fmaf(v[j] - cm, v[j] - cm, cq);
-            if (c == 0) {
-              s_mean = cm;
-              s_m2 = cq;
-            } else {
-              const float na = 32.f * c, n = na + 32.f;
-              const float dl = cm - s_mean;
-              s_mean = fmaf(dl, 32.f / n, s_mean);
-              s_m2 += cq + dl * dl * (na * 32.f / n);
-            }
             uint8_t* brow = Bb + lane * 128;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
@@ -554,17 +532,44 @@ __global__ void __launch_bounds__(320, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmC, Fb, n0 + col0 + 32 * c, r0);
+              tma_store_2d(&tmC, F, n0 + col0 + 32 * c, r0);
               bulk_commit();
               if (c & 1) {  // the bf16 copy is read next by QKV / W_in: keep it in L2
                 tma_store_2d_hint(&ln.tm_xb, Bb, n0 + col0 + 32 * (c - 1), r0, pol_keep);
                 bulk_commit();
               }
-              if (c + 2 < SPAN / 32) {
-                bulk_wait_read0();  // Fb (and Bb) have been read out
-                mbar_arrive_expect_tx(&xb_bar[b], C::STG_BYTES);
-                tma_load_2d(&tmC, &xb_bar[b], Fb, n0 + col0 + 32 * (c + 2), r0);
+              if (c + 1 < SPAN / 32) {
+                bulk_wait_read0();  // F (and Bb) have been read out
+                mbar_arrive_expect_tx(xb_bar, C::STG_BYTES);
+                tma_load_2d(&tmC, xb_bar, F, n0 + col0 + 32 * (c + 1), r0);
               }
+            }
+            // chunk mean / M2 (two-pass over registers, FFMA2), merged into the
+            // running pair (Chan et al.); overlaps the next chunk's load
+            uint64_t s2 = f32x2(0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) s2 = add_f32x2(s2, f32x2(v[j], v[j + 1]));
+            float sa, sb;
+            f32x2_split(s2, sa, sb);
+            const float cm = (sa + sb) * (1.f / 32.f);
+            const uint64_t ncm = f32x2(-cm, -cm);
+            uint64_t q2 = f32x2(0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const uint64_t dv = add_f32x2(f32x2(v[j], v[j + 1]), ncm);
+              q2 = fma_f32x2(dv, dv, q2);
+            }
+            float qa, qb;
+            f32x2_split(q2, qa, qb);
+            const float cq = qa + qb;
+            if (c == 0) {
+              s_mean = cm;
+              s_m2 = cq;
+            } else {
+              const float na = 32.f * c, n = na + 32.f;
+              const float dl = cm - s_mean;
+              s_mean = fmaf(dl, 32.f / n, s_mean);
+              s_m2 += cq + dl * dl * (na * 32.f / n);
             }
           }
           const int row = r0 + lane;
@@ -661,10 +666,14 @@ __global__ void __launch_bounds__(320, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
+#ifdef SRK_EXP_RESID_STORE  // timing experiment only: plain store instead of add-reduce
+              tma_store_2d(&tmC, stg, n0 + c, r0);
+#else
               if constexpr (EPI == EPI_RESID_F32)  // x is re-read next by the LayerNorm
                 tma_reduce_add_2d_hint(&tmC, stg, n0 + c, r0, pol_keep);
               else
                 tma_store_2d(&tmC, stg, n0 + c, r0);
+#endif
               bulk_commit();
             }
           }

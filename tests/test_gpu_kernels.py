@@ -268,3 +268,16 @@ def test_gemm_single_pair_path_matches_cluster_path(cuda):
         out[np_] = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
                                   text=True, timeout=300, check=True).stdout
     assert out["1"] == out["2"] and len(out["1"]) == 40
+
+
+def test_pingpong_attention_variant_matches_torch(cuda):
+    """The opt-in two-slot attention kernel (SRK_ATTN=pp, read once per
+    process) against the same fp32 references, in a child process."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, SRK_ATTN="pp")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.abspath(__file__), "-k", "attention_segment_mask"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

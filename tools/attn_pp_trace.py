@@ -1,0 +1,46 @@
+"""GPU tuning aid for the ping-pong attention kernel: per-CTA clock64 stamps
+(slot 1+g = slot-0 softmax handed P of block g to the MMA; 40+g = slot-0
+softmax saw S of block g; 29 = CTA end)."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_07309_b200._capi import lib  # noqa: E402
+
+H, hd, tq, L, n = 8, 128, 256, 96, 256
+spans = [[0, 0, 0, 0]] * tq
+cur = tq
+for _ in range(n):
+    spans += [[0, tq, cur, 0]] * L
+    cur += L
+M = len(spans)
+d = H * hd
+dev = torch.device("cuda:0")
+qkv = (torch.randn(M, 3 * d, device=dev) * 0.5).bfloat16()
+out = torch.zeros(M, d, dtype=torch.bfloat16, device=dev)
+sp = np.asarray(spans, np.int32).reshape(-1)
+trace = torch.zeros(256 * 64, dtype=torch.int64, device=dev)
+for it in range(3):
+    if it == 2:
+        assert lib.sr_debug_attention_trace(C.c_void_p(trace.data_ptr())) == 0
+    assert lib.sr_kernel_attention(C.c_void_p(qkv.data_ptr()),
+                                   sp.ctypes.data_as(C.POINTER(C.c_int32)), M, H, hd,
+                                   C.c_void_p(out.data_ptr()), None) == 0, lib.sr_last_error()
+torch.cuda.synchronize()
+lib.sr_debug_attention_trace(None)
+t = trace.view(256, 64).cpu().numpy().astype(np.int64)
+for b in [0, 1, 77, 147]:
+    row = t[b]
+    t0 = row[0]
+    p = [int(row[1 + g] - t0) for g in range(24) if row[1 + g]]
+    print(f"cta {b}: end {int(row[29] - t0)}  P handoffs (slot 0): {p}")
+    print("   intervals:", list(np.diff(p)))
+    sd = [int(row[40 + g] - t0) for g in range(24) if row[40 + g]]
+    print("   softmax (S seen -> P):", [pp - ss for ss, pp in zip(sd, p)])
+    print("   wait for S (P -> next S):", [sd[i + 1] - p[i] for i in range(min(len(sd) - 1, len(p)))])
+ends = t[:148, 29] - t[:148, 0]
+print("cta cycles: mean", ends.mean(), "min", ends.min(), "max", ends.max())
