@@ -213,14 +213,15 @@ void Engine::ensure_workspace(int32_t M) {
 void Profiler::begin(int cls) {
   cudaEvent_t a;
   SR_CUDA_CHECK(cudaEventCreate(&a));
-  SR_CUDA_CHECK(cudaEventRecord(a, stream));
+  // External record nodes: the events keep their timestamps inside a graph.
+  SR_CUDA_CHECK(cudaEventRecordWithFlags(a, stream, in_graph ? cudaEventRecordExternal : 0));
   cur = cls;
   cur_start = a;
 }
 void Profiler::end() {
   cudaEvent_t b;
   SR_CUDA_CHECK(cudaEventCreate(&b));
-  SR_CUDA_CHECK(cudaEventRecord(b, stream));
+  SR_CUDA_CHECK(cudaEventRecordWithFlags(b, stream, in_graph ? cudaEventRecordExternal : 0));
   marks.push_back({cur, {cur_start, b}});
 }
 Profiler::~Profiler() {
@@ -351,14 +352,33 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
 }
 
 void Engine::profile(Plan& p, int reps, float* ms_out, int32_t* launches_out) {
+  // Per-kernel-class device time as the plan's graph sees it: the forward is
+  // captured once more with an event record node around every launch and
+  // replayed (eager launches would add host launch gaps to every interval).
   SR_CUDA_CHECK(cudaSetDevice(device_));
   std::vector<double> acc(PROF_N, 0.0);
   std::vector<int32_t> cnt(PROF_N, 0);
   reps = std::max(reps, 1);
-  for (int r = 0; r < reps; ++r) {
-    Profiler prof;
-    prof.stream = stream_;
+  Profiler prof;
+  prof.stream = stream_;
+  prof.in_graph = true;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  SR_CUDA_CHECK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+  try {
     enqueue_forward(p, nullptr, &prof);
+  } catch (...) {
+    cudaStreamEndCapture(stream_, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  SR_CUDA_CHECK(cudaStreamEndCapture(stream_, &g));
+  SR_CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
+  cudaGraphDestroy(g);
+  SR_CUDA_CHECK(cudaGraphLaunch(ge, stream_));  // warm-up
+  SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  for (int r = 0; r < reps; ++r) {
+    SR_CUDA_CHECK(cudaGraphLaunch(ge, stream_));
     SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
     for (auto& m : prof.marks) {
       float ms = 0.f;
@@ -367,6 +387,7 @@ void Engine::profile(Plan& p, int reps, float* ms_out, int32_t* launches_out) {
       if (r == 0) cnt[m.first] += 1;
     }
   }
+  cudaGraphExecDestroy(ge);
   for (int c = 0; c < PROF_N; ++c) {
     if (ms_out) ms_out[c] = static_cast<float>(acc[c] / reps);
     if (launches_out) launches_out[c] = cnt[c];

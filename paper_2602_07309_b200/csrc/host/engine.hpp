@@ -83,6 +83,7 @@ enum ProfClass : int {
 struct Profiler {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
   cudaStream_t stream = nullptr;
+  bool in_graph = false;  // events recorded as external nodes of a captured graph
   int cur = -1;
   cudaEvent_t cur_start = nullptr;
   void begin(int cls);
@@ -144,8 +145,8 @@ class Engine {
 
   // Enqueue the full forward for the plan's packed batch on stream_.
   int32_t enqueue_forward(Plan& p, float* hidden_out, Profiler* prof = nullptr);
-  // Eager forward with an event pair around every launch; per-class mean ms
-  // and launch counts per forward, averaged over `reps` runs.
+  // Graph replay of the forward with an event pair around every launch;
+  // per-class mean ms and launch counts per forward, averaged over `reps`.
   void profile(Plan& p, int reps, float* ms_out, int32_t* launches_out);
 
  private:

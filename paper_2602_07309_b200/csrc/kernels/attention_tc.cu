@@ -78,11 +78,21 @@ struct Cursor {
   int h = 0;
   bool valid = false;
 
+  // Descriptor of the next item of this CTA, fetched one item ahead so the
+  // global-load latency stays off the item boundary.
+  AttnTile t_pre;
+  int item_pre = -1;
+
   __device__ void load_item(const AttnTile* tiles, int n_tiles, int n_items, int item_) {
     item = item_;
     valid = item < n_items;
     if (!valid) return;
-    t = tiles[item % n_tiles];
+    t = item == item_pre ? t_pre : tiles[item % n_tiles];
+    const int nx = item + static_cast<int>(gridDim.x);
+    if (nx < n_items) {
+      t_pre = tiles[nx % n_tiles];
+      item_pre = nx;
+    }
     h = item / n_tiles;
     nb1 = (t.r1_end - t.r1_begin + kBK - 1) / kBK;
     nblk = nb1 + (t.r2_end - t.r2_begin + kBK - 1) / kBK;
@@ -356,6 +366,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = c_row0 + r;
       const bool live = row < c.t.q_end;
       const RowSpan sp = sp_next;
+      // the next item's row descriptor, loaded while this item runs
+      if (c.item_pre >= 0 && c.t_pre.q_begin + r < c.t_pre.q_end)
+        sp_next = spans[c.t_pre.q_begin + r];
       float m_used = -INFINITY;  // exponent base (raw score units), shared by the pair
       float l = 0.f;             // this thread's partial row sum
       const int li = c.li, h = c.h;
@@ -491,8 +504,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           pend.on = false;
         }
       }
-      // Next item's row descriptor: its latency overlaps the deferred epilogue.
-      if (c.valid && c.t.q_begin + r < c.t.q_end) sp_next = spans[c.t.q_begin + r];
       pend.on = true;
       pend.li = li;
       pend.h = h;
