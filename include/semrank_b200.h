@@ -126,6 +126,7 @@ typedef struct sr_weights sr_weights;
 typedef struct sr_engine sr_engine;
 typedef struct sr_comm sr_comm;
 typedef struct sr_plan sr_plan;
+typedef struct sr_corpus sr_corpus;
 
 /* ------------------------------------------------------------ diagnostics */
 const char* sr_last_error(void);
@@ -235,6 +236,37 @@ void sr_comm_destroy(sr_comm* c);
 int32_t sr_engine_score_sharded(sr_engine* e, sr_comm* c, const sr_request* local_shard,
                                 sr_result* res);
 int32_t sr_plan_run_sharded(sr_plan* p, sr_comm* c); /* resident variant */
+
+/* ------------------------------- exhaustive retrieval top-K
+ * The candidate generator upstream of the ranker. Replaces
+ *   std::vector<RankedDoc> exhaustive_topk(const Corpus&, const QuerySpec&,
+ *                                          const RARWeights&, kernels::Exec)
+ * (retrieval.hpp:60-70, retrieval.cpp:134-173) with rar_score (:60-71) and
+ * cosine (:44-58): S = w0 cos(q, e_d) + sum_i w_i f_i(d), exact top-K by
+ * (score desc, doc_id asc), scores bit-identical to the reference's doubles.
+ * Corpus (retrieval.hpp:21-33) is passed columnar: embeddings [n x d_emb],
+ * features [n x n_features] in feature_names order, doc ids [n]; it is
+ * copied to the device once. QuerySpec.filters are applied by the caller as
+ * a keep mask (filter_candidates, retrieval.cpp:79-97; NULL = all docs).
+ * Errors as the reference: SR_SPEC_VIOLATION (k < 1), SR_ALIGNMENT (weight
+ * count or query dimension mismatch), SR_DEGENERATE_INPUT (zero query or
+ * document vector among the candidates); no checks run without candidates. */
+int32_t sr_corpus_create(const float* embeddings, const float* features, const int64_t* doc_ids,
+                         int64_t n_docs, int32_t d_emb, int32_t n_features, int32_t device,
+                         sr_corpus** out);
+void sr_corpus_destroy(sr_corpus* c);
+/* Writes min(k, #candidates) entries; *n_out = that count. */
+int32_t sr_corpus_topk(sr_corpus* c, const float* query, int32_t d_query, double w0,
+                       const double* w, int32_t n_w, const uint8_t* keep, int32_t k,
+                       int64_t* ids_out, double* scores_out, int32_t* n_out);
+/* This rank holds a shard of the corpus (global doc ids); one NCCL
+ * all-gather of k entries per rank + the comparator merge (the reference's
+ * shard merge, retrieval.cpp:144-165) gives every rank the global top-K. */
+int32_t sr_corpus_topk_sharded(sr_corpus* c, sr_comm* comm, const float* query, int32_t d_query,
+                               double w0, const double* w, int32_t n_w, const uint8_t* keep,
+                               int32_t k, int64_t* ids_out, double* scores_out, int32_t* n_out);
+/* Docs rescored in double by the last call (the fp32 pass's candidate set). */
+int64_t sr_corpus_last_candidates(const sr_corpus* c);
 
 /* --------------------------------------- kernel-level entry points (tests) */
 /* All pointers are device pointers; stream may be NULL (legacy stream). */

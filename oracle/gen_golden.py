@@ -219,5 +219,52 @@ def main():
                             "prefix": prefix, "items": items, "multi_item": s.tolist()})
 
 
+def _b64(a):
+    import base64
+    return base64.b64encode(np.ascontiguousarray(a).tobytes()).decode()
+
+
+def retrieval():
+    """exhaustive_topk cases (retrieval.cpp:134-173) from the reference, shaped
+    like test_retrieval.cpp:170-255: random unit corpora with a colour
+    attribute, random k and filters; tied scores; K above the corpus size."""
+    rng = np.random.default_rng(20261017)
+    cases = []
+    for t in range(6):
+        n, d, f = (400, 16, 2) if t < 4 else (257, 32, 1)
+        emb = rng.standard_normal((n, d)).astype(np.float32)
+        emb /= np.linalg.norm(emb, axis=1, keepdims=True).astype(np.float32)
+        feat = rng.random((n, f)).astype(np.float32)
+        ids = rng.permutation(n * 3)[:n].astype(np.int64)
+        color = rng.integers(0, 3, n).astype(np.int32)
+        q = rng.standard_normal(d).astype(np.float32)
+        q /= np.float32(np.linalg.norm(q))
+        k = int(rng.integers(1, 41))
+        allowed = [0, 1] if t % 2 else None
+        w = [0.2, -0.1][:f]
+        oi, osc = O.ref_topk(emb, feat, ids, color, q, 1.0, w, allowed, k)
+        cases.append({"n": n, "d": d, "f": f, "emb": _b64(emb), "feat": _b64(feat),
+                      "ids": ids.tolist(), "color": color.tolist(), "query": _b64(q),
+                      "w0": 1.0, "w": w, "allowed": allowed, "k": k,
+                      "ref_ids": oi.tolist(), "ref_scores": [repr(float(x)) for x in osc]})
+    # ties: equal scores everywhere -> ascending doc_id (test_retrieval.cpp:223-240)
+    emb = np.tile(np.array([[1.0, 0.0]], np.float32), (4, 1))
+    ids = np.array([3, 2, 1, 0], np.int64)
+    oi, osc = O.ref_topk(emb, np.zeros((4, 0), np.float32), ids, None, np.array([1, 0], np.float32),
+                         1.0, [], None, 10)
+    cases.append({"n": 4, "d": 2, "f": 0, "emb": _b64(emb), "feat": "", "ids": ids.tolist(),
+                  "color": None, "query": _b64(np.array([1, 0], np.float32)), "w0": 1.0, "w": [],
+                  "allowed": None, "k": 10, "ref_ids": oi.tolist(),
+                  "ref_scores": [repr(float(x)) for x in osc]})
+    dump("retrieval.json", {"source": "exhaustive_topk retrieval.cpp:134-173 via oracle/_ref",
+                            "cases": cases})
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "retrieval":
+        if not O.ref_available():
+            sys.exit("oracle/_ref not built")
+        retrieval()
+    else:
+        main()
+        retrieval()

@@ -227,3 +227,64 @@ def ref_init_save(cfg, seed: int, path: str, fan_in: bool = False) -> None:
     st = fn(_p(dims, i32p), len(cfg.head_specs), names, _p(ar, i32p), seed, path.encode())
     if st != 0:
         raise RuntimeError(lib.ref_last_error().decode())
+
+
+# ---------------------------------------------------------------- retrieval
+class RetrievalError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code  # semrank ErrorCode value (3 SpecViolation, 6 Alignment, 9 Degenerate)
+
+
+def oracle_topk(emb, feat, ids, keep, query, w0, w, k):
+    """C restatement of exhaustive_topk (retrieval.cpp:134-173) -> (ids, scores)."""
+    lib = port()
+    emb = np.ascontiguousarray(emb, np.float32)
+    n, d = emb.shape
+    feat = np.ascontiguousarray(feat, np.float32).reshape(n, -1)
+    ids = np.ascontiguousarray(ids, np.int64)
+    q = np.ascontiguousarray(query, np.float32)
+    wv = np.ascontiguousarray(w, np.float64)
+    kp = None if keep is None else np.ascontiguousarray(keep, np.uint8)
+    kk = max(int(k), 1)
+    oi = np.zeros(kk, np.int64)
+    os_ = np.zeros(kk, np.float64)
+    fn = lib.or_exhaustive_topk
+    fn.restype = C.c_int
+    fn.argtypes = [f32p, f32p, i64p, C.POINTER(C.c_uint8), C.c_int64, C.c_int, C.c_int, f32p,
+                   C.c_int, C.c_double, f64p, C.c_int, C.c_int, i64p, f64p]
+    r = fn(_p(emb, f32p), _p(feat, f32p), _p(ids, i64p),
+           kp.ctypes.data_as(C.POINTER(C.c_uint8)) if kp is not None else None, n, d,
+           feat.shape[1], _p(q, f32p), q.shape[0], float(w0), _p(wv, f64p), wv.shape[0], int(k),
+           _p(oi, i64p), _p(os_, f64p))
+    if r < 0:
+        raise RetrievalError(-r, "oracle error")
+    return oi[:r], os_[:r]
+
+
+def ref_topk(emb, feat, ids, color, query, w0, w, allowed, k):
+    """The reference's own exhaustive_topk through oracle/_ref (attribute
+    "color" per doc from color codes; allowed=None -> no filter)."""
+    lib = ref()
+    emb = np.ascontiguousarray(emb, np.float32)
+    n, d = emb.shape
+    feat = np.ascontiguousarray(feat, np.float32).reshape(n, -1)
+    ids = np.ascontiguousarray(ids, np.int64)
+    col = None if color is None else np.ascontiguousarray(color, np.int32)
+    q = np.ascontiguousarray(query, np.float32)
+    wv = np.ascontiguousarray(w, np.float64)
+    al = np.ascontiguousarray(allowed if allowed is not None else [0], np.int32)
+    kk = max(int(k), 1)
+    oi = np.zeros(kk, np.int64)
+    os_ = np.zeros(kk, np.float64)
+    cnt = np.zeros(1, np.int32)
+    fn = lib.ref_exhaustive_topk
+    fn.argtypes = [f32p, f32p, i64p, i32p, C.c_int64, C.c_int32, C.c_int32, f32p, C.c_int32,
+                   C.c_double, f64p, C.c_int32, i32p, C.c_int32, C.c_int32, i64p, f64p, i32p]
+    st = fn(_p(emb, f32p), _p(feat, f32p), _p(ids, i64p), _p(col, i32p), n, d, feat.shape[1],
+            _p(q, f32p), q.shape[0], float(w0), _p(wv, f64p), wv.shape[0], _p(al, i32p),
+            -1 if allowed is None else len(allowed), int(k), _p(oi, i64p), _p(os_, f64p),
+            _p(cnt, i32p))
+    if st != 0:
+        raise RetrievalError(st - 1, lib.ref_last_error().decode())
+    return oi[:cnt[0]], os_[:cnt[0]]

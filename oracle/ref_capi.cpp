@@ -21,6 +21,7 @@
 #include "semrank/error.hpp"
 #include "semrank/kernels.hpp"
 #include "semrank/model.hpp"
+#include "semrank/retrieval.hpp"
 #include "semrank/rng.hpp"
 #include "semrank/weights_io.hpp"
 
@@ -251,6 +252,47 @@ int ref_plan_batches(int32_t n_req, const int32_t* prefix_len, const int32_t* re
 void ref_uniform_ints(uint64_t seed, int64_t lo, int64_t hi, int32_t n, int64_t* out) {
   Rng r(seed);
   for (int i = 0; i < n; ++i) out[i] = r.uniform_int(lo, hi);
+}
+
+// exhaustive_topk (retrieval.cpp:134-173) on a columnar corpus. Each doc gets
+// attribute "color" = kColors[color[i]]; allowed >= 0 colors form the query's
+// filter (QuerySpec.filters["color"]), n_allowed < 0 means no filter, so the
+// reference's own filter_candidates runs. Results: min(k, #candidates).
+int ref_exhaustive_topk(const float* emb, const float* feat, const int64_t* ids,
+                        const int32_t* color, int64_t n, int32_t d, int32_t f,
+                        const float* query, int32_t d_query, double w0, const double* w,
+                        int32_t n_w, const int32_t* allowed, int32_t n_allowed, int32_t k,
+                        int64_t* ids_out, double* scores_out, int32_t* n_out) {
+  static const char* kColors[] = {"red", "blue", "green", "black", "white", "grey", "pink",
+                                  "teal"};
+  return run([&] {
+    Corpus corpus;
+    for (int j = 0; j < f; ++j) corpus.feature_names.push_back("f" + std::to_string(j));
+    corpus.docs.resize(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      DocumentRecord& doc = corpus.docs[static_cast<size_t>(i)];
+      doc.doc_id = ids[i];
+      if (color != nullptr) doc.attributes["color"] = kColors[color[i] & 7];
+      doc.embedding.assign(emb + i * d, emb + (i + 1) * d);
+      doc.features.assign(feat + i * f, feat + (i + 1) * f);
+    }
+    QuerySpec q;
+    q.embedding.assign(query, query + d_query);
+    q.k = k;
+    if (n_allowed >= 0) {
+      auto& v = q.filters["color"];
+      for (int j = 0; j < n_allowed; ++j) v.push_back(kColors[allowed[j] & 7]);
+    }
+    RARWeights rw;
+    rw.w0 = w0;
+    rw.w.assign(w, w + n_w);
+    const auto top = exhaustive_topk(corpus, q, rw, kernels::default_exec());
+    for (size_t j = 0; j < top.size(); ++j) {
+      ids_out[j] = top[j].doc_id;
+      scores_out[j] = top[j].score;
+    }
+    *n_out = static_cast<int32_t>(top.size());
+  });
 }
 
 }  // extern "C"

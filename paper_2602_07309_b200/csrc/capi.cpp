@@ -7,6 +7,7 @@
 #include <string>
 
 #include "host/engine.hpp"
+#include "host/retrieval.hpp"
 #include "host/model.hpp"
 #include "host/planner.hpp"
 #include "kernels/launch.h"
@@ -46,6 +47,11 @@ struct sr_engine {
 
 struct sr_comm {
   srh::Comm* c = nullptr;
+};
+
+struct sr_corpus {
+  std::unique_ptr<srh::Corpus> c;
+  std::mutex mu;  // one scan at a time per corpus (one stream)
 };
 
 struct sr_plan {
@@ -475,6 +481,48 @@ int32_t sr_plan_run_sharded(sr_plan* p, sr_comm* c) {
     p->owner->e->run_plan_sharded(*p->p, c->c);
     p->sharded_valid = c->c->nranks > 1;
   });
+}
+
+// ------------------------------------------------------------ retrieval
+int32_t sr_corpus_create(const float* embeddings, const float* features, const int64_t* doc_ids,
+                         int64_t n_docs, int32_t d_emb, int32_t n_features, int32_t device,
+                         sr_corpus** out) {
+  return guard([&] {
+    if (!out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    if (n_docs > 0 && (!embeddings || !doc_ids || (n_features > 0 && !features)))
+      srh::fail(SR_SPEC_VIOLATION, "null corpus array");
+    auto c = std::make_unique<sr_corpus>();
+    c->c = std::make_unique<srh::Corpus>(embeddings, features, doc_ids, n_docs, d_emb, n_features,
+                                         device);
+    *out = c.release();
+  });
+}
+
+void sr_corpus_destroy(sr_corpus* c) { delete c; }
+
+int32_t sr_corpus_topk(sr_corpus* c, const float* query, int32_t d_query, double w0,
+                       const double* w, int32_t n_w, const uint8_t* keep, int32_t k,
+                       int64_t* ids_out, double* scores_out, int32_t* n_out) {
+  return guard([&] {
+    if (!c || !query || !n_out || (n_w > 0 && !w)) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(c->mu);
+    *n_out = c->c->topk_host(query, d_query, w0, w, n_w, keep, k, ids_out, scores_out);
+  });
+}
+
+int32_t sr_corpus_topk_sharded(sr_corpus* c, sr_comm* comm, const float* query, int32_t d_query,
+                               double w0, const double* w, int32_t n_w, const uint8_t* keep,
+                               int32_t k, int64_t* ids_out, double* scores_out, int32_t* n_out) {
+  return guard([&] {
+    if (!c || !comm || !query || !n_out || (n_w > 0 && !w))
+      srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(c->mu);
+    *n_out = c->c->topk_sharded(comm->c, query, d_query, w0, w, n_w, keep, k, ids_out, scores_out);
+  });
+}
+
+int64_t sr_corpus_last_candidates(const sr_corpus* c) {
+  return c ? c->c->last_candidates() : 0;
 }
 
 // ------------------------------------------------------------ kernel tests

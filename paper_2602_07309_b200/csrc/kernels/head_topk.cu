@@ -221,15 +221,18 @@ __global__ void __launch_bounds__(kSortThreads)
   for (int j = threadIdx.x; j < k; j += blockDim.x) dst[j] = j < P ? buf[j] : sentinel();
 }
 
-// Stage 2 / merge: segment s owns entries in[s*per_seg .. (s+1)*per_seg).
+// Stage 2 / merge: segment s owns entries in[s*per_seg .. (s+1)*per_seg),
+// entries at or past n_total (a partial last segment) read as sentinels.
 __global__ void __launch_bounds__(kSortThreads)
     topk_entries_kernel(const TopkEntry* __restrict__ in, int per_seg, int k,
-                        TopkEntry* __restrict__ out) {
+                        TopkEntry* __restrict__ out, long long n_total) {
   pdl_wait();
   extern __shared__ TopkEntry buf[];
-  const TopkEntry* src = in + static_cast<size_t>(blockIdx.x) * per_seg;
+  const long long seg0 = static_cast<long long>(blockIdx.x) * per_seg;
+  const TopkEntry* src = in + seg0;
   const int P = pow2_at_least(per_seg);
-  for (int i = threadIdx.x; i < P; i += blockDim.x) buf[i] = i < per_seg ? src[i] : sentinel();
+  for (int i = threadIdx.x; i < P; i += blockDim.x)
+    buf[i] = (i < per_seg && seg0 + i < n_total) ? src[i] : sentinel();
   bitonic_sort(buf, P);
   TopkEntry* dst = out + static_cast<size_t>(blockIdx.x) * k;
   for (int j = threadIdx.x; j < k; j += blockDim.x) dst[j] = j < P ? buf[j] : sentinel();
@@ -283,7 +286,8 @@ cudaError_t topk(const double* scores, int stride, const int64_t* ids, const int
                            stream, scores, stride, ids, seg_off, n_segments, k, scratch, chunks);
   if (e != cudaSuccess) return e;
   return launch_k(topk_entries_kernel, dim3(n_segments), dim3(kSortThreads), smem, stream,
-                  static_cast<const TopkEntry*>(scratch), chunks * k, k, out);
+                  static_cast<const TopkEntry*>(scratch), chunks * k, k, out,
+                  static_cast<long long>(n_segments) * chunks * k);
 }
 
 cudaError_t topk_merge(const TopkEntry* in, int n, int k, TopkEntry* out, cudaStream_t stream) {
@@ -292,7 +296,43 @@ cudaError_t topk_merge(const TopkEntry* in, int n, int k, TopkEntry* out, cudaSt
   const size_t smem = sizeof(TopkEntry) * kSortCap;
   cudaFuncSetAttribute(topk_entries_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem));
-  return launch_k(topk_entries_kernel, dim3(1), dim3(kSortThreads), smem, stream, in, n, k, out);
+  return launch_k(topk_entries_kernel, dim3(1), dim3(kSortThreads), smem, stream, in, n, k, out,
+                  static_cast<long long>(n));
+}
+
+size_t topk_select_scratch(long long n, int k) {
+  // level sizes shrink by >= 2x (groups of kSortCap entries -> k each, k <= kSortCap / 2)
+  size_t total = 0;
+  long long m = n;
+  while (m > kSortCap) {
+    const long long groups = (m + kSortCap - 1) / kSortCap;
+    m = groups * k;
+    total += static_cast<size_t>(m);
+  }
+  return total + 1;
+}
+
+cudaError_t topk_select(const TopkEntry* in, long long n, int k, TopkEntry* scratch,
+                        TopkEntry* out, cudaStream_t stream) {
+  if (n <= 0 || k <= 0) return cudaSuccess;
+  if (k > kSortCap / 2) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(TopkEntry) * kSortCap;
+  cudaFuncSetAttribute(topk_entries_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  const TopkEntry* cur = in;
+  long long m = n;
+  TopkEntry* dst = scratch;
+  while (m > kSortCap) {
+    const long long groups = (m + kSortCap - 1) / kSortCap;
+    cudaError_t e = launch_k(topk_entries_kernel, dim3(static_cast<unsigned>(groups)),
+                             dim3(kSortThreads), smem, stream, cur, kSortCap, k, dst, m);
+    if (e != cudaSuccess) return e;
+    cur = dst;
+    m = groups * k;
+    dst += m;
+  }
+  return launch_k(topk_entries_kernel, dim3(1), dim3(kSortThreads), smem, stream, cur,
+                  static_cast<int>(m), k, out, m);
 }
 
 }  // namespace srk

@@ -166,6 +166,48 @@ cudaError_t topk(const double* scores, int stride, const int64_t* ids, const int
                  TopkEntry* out, cudaStream_t stream);
 // Merge: entries [n] (already candidates) -> best k.
 cudaError_t topk_merge(const TopkEntry* in, int n, int k, TopkEntry* out, cudaStream_t stream);
+// Best k of any number of entries (multi-level: groups of 4096 -> k each);
+// k <= 2048; scratch holds topk_select_scratch(n, k) entries.
+size_t topk_select_scratch(long long n, int k);
+cudaError_t topk_select(const TopkEntry* in, long long n, int k, TopkEntry* scratch,
+                        TopkEntry* out, cudaStream_t stream);
+
+// ------------------------------------------------- exhaustive retrieval scan
+// Reference: exhaustive_topk (retrieval.cpp:134-173) with rar_score
+// (:60-71) = w0 * cosine(q, e_d) (double accumulation, :44-58) + sum w_i f_i.
+// Pass 1 (HBM-bound): fp32 scores with a rigorous error bound eps; each CTA
+// keeps every doc within 2 eps of its running k-th best (a superset of its
+// exact top-k). Pass 2: the candidates are rescored in double in the
+// reference's operation order. Pass 3: exact top-k (score desc, id asc).
+struct RetrievalScan {
+  const float* emb;       // [n x D]
+  const float* feat;      // [n x F] (may be null when F == 0)
+  const int64_t* ids;     // [n]
+  const uint8_t* keep;    // [n] filter mask or null
+  const float* q32;       // [D]
+  const double* qd;       // [D] (query as double)
+  const float* w32;       // [F]
+  const double* wd;       // [F]
+  double w0;
+  double q_norm;          // sqrt(sum double(q_i)^2), the reference's sqrt(na)
+  float eps2;             // 2 * fp32 error bound of a score
+  long long n;
+  int D, F, k;
+};
+// cand: int32 [cand_cap]; counters: int32 [2] = {count, flags} (zeroed by the
+// call); flags bit 0 = a kept doc has a zero embedding, bit 1 = candidate
+// overflow (the exact fallback path must run).
+cudaError_t retrieval_scan(const RetrievalScan& a, int32_t* cand, int cand_cap, int32_t* counters,
+                           int grid, cudaStream_t stream);
+// Large k (> 512): full stable sort of n entries by (score desc, id asc)
+// (device radix sorts), first min(k, n) gathered to out.
+size_t retrieval_sort_scratch(long long n);
+cudaError_t retrieval_sort_topk(const TopkEntry* e, long long n, int k, void* scratch,
+                                size_t scratch_bytes, TopkEntry* out, cudaStream_t stream);
+// Exact double rescoring of cand[0..n_cand) (or of all docs when cand is null
+// and n_cand == n) into entries.
+cudaError_t retrieval_refine(const RetrievalScan& a, const int32_t* cand, long long n_cand,
+                             TopkEntry* out, int32_t* counters, cudaStream_t stream);
 
 // ------------------------------------------------------------ conversions
 // dst[n][k] = bf16(src[k][n]) : fp32 [K x N] row-major -> bf16 [N x K].

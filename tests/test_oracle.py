@@ -148,3 +148,51 @@ def test_port_vs_reference_fuzz(tmp_path):
         for mode in (0, 1, 2):
             want, _, _ = O.ref_score(path, mode, p, items=items, n_tasks=3)
             assert np.array_equal(w.score(p, items, n_tasks=3), want), (trial, mode)
+
+
+# ------------------------------------------------------------ retrieval scan
+def test_retrieval_oracle_matches_reference_golden():
+    """The C restatement of exhaustive_topk is bit-identical to the
+    reference's outputs (tests/golden/retrieval.json)."""
+    from tests.retrieval_cases import golden_cases
+    for c in golden_cases():
+        ids, sc = O.oracle_topk(c["emb"], c["feat"], c["ids"], c["keep"], c["query"], c["w0"],
+                                c["w"], c["k"])
+        assert np.array_equal(ids, c["ref_ids"])
+        assert np.array_equal(sc, c["ref_scores"])
+
+
+def test_retrieval_oracle_error_rules():
+    import pytest as _pt
+    from tests.retrieval_cases import random_corpus
+    emb, feat, ids, _ = random_corpus(3, 50, 8, 2)
+    with _pt.raises(O.RetrievalError) as e:
+        O.oracle_topk(emb, feat, ids, None, emb[0], 1.0, [0.1, 0.2], 0)
+    assert e.value.code == 3  # SpecViolation (retrieval.cpp:138-140)
+    with _pt.raises(O.RetrievalError) as e:
+        O.oracle_topk(emb, feat, ids, None, emb[0], 1.0, [0.1], 5)
+    assert e.value.code == 6  # Alignment (:62-65)
+    with _pt.raises(O.RetrievalError) as e:
+        O.oracle_topk(emb, feat, ids, None, np.zeros(8, np.float32), 1.0, [0.1, 0.2], 5)
+    assert e.value.code == 9  # DegenerateInput (:52-54)
+    # no candidates: no per-candidate checks run, empty result
+    ids_o, _ = O.oracle_topk(emb, feat, ids, np.zeros(50, np.uint8), np.zeros(8, np.float32), 1.0,
+                             [0.1], 5)
+    assert len(ids_o) == 0
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built (no /root/reference)")
+def test_retrieval_oracle_fuzz_against_reference():
+    from tests.retrieval_cases import random_corpus
+    rng = np.random.default_rng(77)
+    for t in range(8):
+        n, d, f = int(rng.integers(1, 3000)), int(rng.integers(1, 40)), int(rng.integers(0, 3))
+        emb, feat, ids, color = random_corpus(100 + t, n, d, f, unit=bool(t % 2))
+        q = rng.standard_normal(d).astype(np.float32)
+        w = list(rng.standard_normal(f))
+        k = int(rng.integers(1, 60))
+        allowed = [int(rng.integers(0, 3))] if t % 3 == 0 else None
+        keep = None if allowed is None else np.isin(color, allowed).astype(np.uint8)
+        a = O.oracle_topk(emb, feat, ids, keep, q, 0.7, w, k)
+        b = O.ref_topk(emb, feat, ids, color, q, 0.7, w, allowed, k)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
