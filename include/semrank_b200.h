@@ -267,6 +267,9 @@ int32_t sr_corpus_topk_sharded(sr_corpus* c, sr_comm* comm, const float* query, 
                                int32_t k, int64_t* ids_out, double* scores_out, int32_t* n_out);
 /* Docs rescored in double by the last call (the fp32 pass's candidate set). */
 int64_t sr_corpus_last_candidates(const sr_corpus* c);
+/* Device time (ms, CUDA events on the corpus stream) of the last call's
+ * fp32 scan kernel (the HBM-bound pass; bench roofline). */
+float sr_corpus_last_scan_ms(const sr_corpus* c);
 
 /* --------------------------------------- kernel-level entry points (tests) */
 /* All pointers are device pointers; stream may be NULL (legacy stream). */

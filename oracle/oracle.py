@@ -262,7 +262,7 @@ def oracle_topk(emb, feat, ids, keep, query, w0, w, k):
     return oi[:r], os_[:r]
 
 
-def ref_topk(emb, feat, ids, color, query, w0, w, allowed, k):
+def ref_topk(emb, feat, ids, color, query, w0, w, allowed, k, timing=None):
     """The reference's own exhaustive_topk through oracle/_ref (attribute
     "color" per doc from color codes; allowed=None -> no filter)."""
     lib = ref()
@@ -280,11 +280,12 @@ def ref_topk(emb, feat, ids, color, query, w0, w, allowed, k):
     cnt = np.zeros(1, np.int32)
     fn = lib.ref_exhaustive_topk
     fn.argtypes = [f32p, f32p, i64p, i32p, C.c_int64, C.c_int32, C.c_int32, f32p, C.c_int32,
-                   C.c_double, f64p, C.c_int32, i32p, C.c_int32, C.c_int32, i64p, f64p, i32p]
+                   C.c_double, f64p, C.c_int32, i32p, C.c_int32, C.c_int32, i64p, f64p, i32p,
+                   f64p]
     st = fn(_p(emb, f32p), _p(feat, f32p), _p(ids, i64p), _p(col, i32p), n, d, feat.shape[1],
             _p(q, f32p), q.shape[0], float(w0), _p(wv, f64p), wv.shape[0], _p(al, i32p),
             -1 if allowed is None else len(allowed), int(k), _p(oi, i64p), _p(os_, f64p),
-            _p(cnt, i32p))
+            _p(cnt, i32p), _p(timing, f64p))
     if st != 0:
         raise RetrievalError(st - 1, lib.ref_last_error().decode())
     return oi[:cnt[0]], os_[:cnt[0]]

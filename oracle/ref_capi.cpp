@@ -8,6 +8,7 @@
 // for bench.py's cpu_baseline / --impl reference arm. Nothing here is
 // shipped or called by the product.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -262,7 +263,7 @@ int ref_exhaustive_topk(const float* emb, const float* feat, const int64_t* ids,
                         const int32_t* color, int64_t n, int32_t d, int32_t f,
                         const float* query, int32_t d_query, double w0, const double* w,
                         int32_t n_w, const int32_t* allowed, int32_t n_allowed, int32_t k,
-                        int64_t* ids_out, double* scores_out, int32_t* n_out) {
+                        int64_t* ids_out, double* scores_out, int32_t* n_out, double* secs_out) {
   static const char* kColors[] = {"red", "blue", "green", "black", "white", "grey", "pink",
                                   "teal"};
   return run([&] {
@@ -286,7 +287,10 @@ int ref_exhaustive_topk(const float* emb, const float* feat, const int64_t* ids,
     RARWeights rw;
     rw.w0 = w0;
     rw.w.assign(w, w + n_w);
+    const auto t0 = std::chrono::steady_clock::now();
     const auto top = exhaustive_topk(corpus, q, rw, kernels::default_exec());
+    if (secs_out)
+      *secs_out = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     for (size_t j = 0; j < top.size(); ++j) {
       ids_out[j] = top[j].doc_id;
       scores_out[j] = top[j].score;

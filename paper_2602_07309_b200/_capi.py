@@ -106,6 +106,7 @@ _sig("sr_corpus_topk", i32, vp, vp, i32, f64, vp, i32, vp, i32, P(i64), P(f64), 
 _sig("sr_corpus_topk_sharded", i32, vp, vp, vp, i32, f64, vp, i32, vp, i32, P(i64), P(f64),
      P(i32))
 _sig("sr_corpus_last_candidates", i64, vp)
+_sig("sr_corpus_last_scan_ms", f32, vp)
 _sig("sr_kernel_gemm", i32, vp, vp, i32, i32, i32, vp, i32, i32, vp)
 _sig("sr_kernel_gemm_ln", i32, vp, vp, i32, i32, i32, vp, i32, i32, vp, vp, i32, vp, i32, vp)
 _sig("sr_kernel_attention", i32, vp, P(i32), i32, i32, i32, vp, vp)
@@ -128,6 +129,7 @@ HEADER_SYMBOLS = [
     "sr_plan_profile", "sr_plan_shape",
     "sr_nccl_unique_id", "sr_comm_create", "sr_comm_destroy", "sr_engine_score_sharded",
     "sr_plan_run_sharded", "sr_corpus_create", "sr_corpus_destroy", "sr_corpus_topk",
-    "sr_corpus_topk_sharded", "sr_corpus_last_candidates", "sr_kernel_gemm", "sr_kernel_gemm_ln", "sr_kernel_attention", "sr_kernel_layernorm",
+    "sr_corpus_topk_sharded", "sr_corpus_last_candidates", "sr_corpus_last_scan_ms",
+    "sr_kernel_gemm", "sr_kernel_gemm_ln", "sr_kernel_attention", "sr_kernel_layernorm",
     "sr_kernel_topk", "sr_debug_attention_trace", "sr_debug_gemm_trace",
 ]

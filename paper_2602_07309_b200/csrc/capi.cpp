@@ -525,6 +525,8 @@ int64_t sr_corpus_last_candidates(const sr_corpus* c) {
   return c ? c->c->last_candidates() : 0;
 }
 
+float sr_corpus_last_scan_ms(const sr_corpus* c) { return c ? c->c->last_scan_ms() : 0.f; }
+
 // ------------------------------------------------------------ kernel tests
 int32_t sr_kernel_gemm(const void* a_bf16, const void* b_bf16, int32_t M, int32_t N, int32_t K,
                        void* c, int32_t ldc, int32_t epi, void* stream) {

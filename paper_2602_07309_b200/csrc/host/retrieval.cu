@@ -56,6 +56,8 @@ Corpus::~Corpus() {
                   static_cast<void*>(keep_), static_cast<void*>(vec_),
                   static_cast<void*>(counters_), static_cast<void*>(cand_)})
     if (p) cudaFree(p);
+  for (auto& e : ev_)
+    if (e) cudaEventDestroy(e);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -141,10 +143,17 @@ int Corpus::topk(const float* query, int d_query, double w0, const double* w, in
     last_candidates_ = n_;
     return static_cast<int>(std::min<long long>(k, n_keep));
   }
+  if (!ev_[0]) {
+    SR_CUDA_CHECK(cudaEventCreate(&ev_[0]));
+    SR_CUDA_CHECK(cudaEventCreate(&ev_[1]));
+  }
+  SR_CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
   SR_CUDA_CHECK(srk::retrieval_scan(a, cand_, cand_cap_, counters_, grid_, stream_));
+  SR_CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
   int32_t cnt[2] = {0, 0};
   SR_CUDA_CHECK(cudaMemcpyAsync(cnt, counters_, sizeof(cnt), cudaMemcpyDeviceToHost, stream_));
   SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  SR_CUDA_CHECK(cudaEventElapsedTime(&last_scan_ms_, ev_[0], ev_[1]));
   if (cnt[1] & 1) fail(SR_DEGENERATE_INPUT, "cosine of a zero vector");
   const bool exact_all = (cnt[1] & 2) != 0;  // near-tie overflow: rescore every doc
   const long long m = exact_all ? n_ : cnt[0];

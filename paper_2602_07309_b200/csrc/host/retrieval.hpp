@@ -32,6 +32,7 @@ class Corpus {
   int topk_sharded(Comm* c, const float* query, int d_query, double w0, const double* w, int n_w,
                    const uint8_t* keep, int k, int64_t* ids_out, double* scores_out);
   long long last_candidates() const { return last_candidates_; }
+  float last_scan_ms() const { return last_scan_ms_; }  // fp32 pass of the last call
   cudaStream_t stream() const { return stream_; }
   long long size() const { return n_; }
 
@@ -52,6 +53,8 @@ class Corpus {
   int grid_ = 0, cand_cap_ = 0;
   std::vector<double> fmax_;
   long long last_candidates_ = 0;
+  float last_scan_ms_ = 0.f;
+  cudaEvent_t ev_[2] = {nullptr, nullptr};
   template <typename T>
   struct Buf {
     T* ptr = nullptr;

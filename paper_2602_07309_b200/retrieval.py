@@ -143,6 +143,10 @@ class DeviceCorpus:
     def last_candidates(self) -> int:
         return int(_lib.sr_corpus_last_candidates(self._h))
 
+    def last_scan_ms(self) -> float:
+        """Device time of the last call's fp32 scan kernel (CUDA events)."""
+        return float(_lib.sr_corpus_last_scan_ms(self._h))
+
 
 def filter_candidates(corpus: Corpus, filters: Dict[str, Sequence[str]]) -> np.ndarray:
     """Boolean keep mask of docs satisfying every predicate (retrieval.cpp:79-97);

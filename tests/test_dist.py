@@ -76,3 +76,47 @@ def test_shards_cover_all_candidates_once():
                 lo, hi = shard(n, world, r)
                 seen += list(range(lo, hi))
             assert seen == list(range(n))
+
+
+def _retrieval_worker(rank, world, port, seed, n, d, k, out_path):
+    """Corpus shard per rank (contiguous, global doc ids), the shard's exact
+    top-k by the C restatement of exhaustive_topk, all-gather, comparator
+    merge (retrieval.cpp:144-165) — the host half of sr_corpus_topk_sharded."""
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from tests.retrieval_cases import random_corpus
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    emb, feat, ids, color = random_corpus(seed, n, d, 1)
+    keep = (color != 1).astype(np.uint8)
+    q = emb[11]
+    lo, hi = shard(n, world, rank)
+    li, ls = O.oracle_topk(emb[lo:hi], feat[lo:hi], ids[lo:hi], keep[lo:hi], q, 1.0, [0.25], k)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (list(map(int, li)), list(map(float, ls))))
+    pool = sorted(((s, i) for g in gathered for i, s in zip(*g)), key=lambda e: (-e[0], e[1]))
+    if rank == 0:
+        with open(out_path, "w") as f:
+            json.dump({"ids": [i for _, i in pool[:k]], "scores": [s for s, _ in pool[:k]]}, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k", [(2, 100), (2, 1), (2, 5000)])
+def test_two_rank_retrieval_merge_equals_single(tmp_path, world, k):
+    import torch.multiprocessing as mp
+
+    from oracle import oracle as O
+    from tests.retrieval_cases import random_corpus
+    n, d, seed = 20_011, 16, 5
+    out = str(tmp_path / "merged.json")
+    mp.spawn(_retrieval_worker, args=(world, _free_port(), seed, n, d, k, out), nprocs=world,
+             join=True)
+    with open(out) as f:
+        merged = json.load(f)
+    emb, feat, ids, color = random_corpus(seed, n, d, 1)
+    want_ids, want_sc = O.oracle_topk(emb, feat, ids, (color != 1).astype(np.uint8), emb[11], 1.0,
+                                      [0.25], k)
+    assert merged["ids"] == list(map(int, want_ids))
+    assert merged["scores"] == list(map(float, want_sc))
