@@ -120,6 +120,17 @@ __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const 
       "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
+// Contiguous global bytes -> smem (1D bulk copy, completes on the mbarrier);
+// 16-byte aligned addresses, size a multiple of 16.
+__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
 // Tensor tile -> L2 only (no smem destination, no completion tracking).
 __device__ __forceinline__ void tma_prefetch_2d_l2(const CUtensorMap* map, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(

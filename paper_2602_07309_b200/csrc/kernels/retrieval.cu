@@ -19,6 +19,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "launch.h"
+#include "ptx.cuh"
 
 namespace srk {
 
@@ -168,6 +169,134 @@ __global__ void __launch_bounds__(kScanThreads)
   pdl_trigger();
 }
 
+
+// TMA-streamed variant (D % 4 == 0): a tile of R docs is R*D*4 contiguous
+// bytes, fetched by one 1D bulk copy into a 3-deep smem ring (no register
+// staging, completion on an mbarrier). Thread t owns doc t of the tile and
+// reads its row as float4s in a rotated order (chunk (j + t) mod D/4), which
+// spreads each quarter-warp over distinct bank groups; the fp32 pass needs
+// only the error bound, not the reference's summation order.
+constexpr int kBulkStages = 3;
+constexpr int kBulkTileBytes = 32768;
+
+__global__ void __launch_bounds__(kScanThreads)
+    retrieval_scan_bulk_kernel(RetrievalScan a, int32_t* __restrict__ g_cand, int g_cap,
+                               int32_t* __restrict__ counters, long long docs_per_cta, int rows) {
+  pdl_wait();
+  // dynamic smem: ring [3][32 KB] | candidates [kCandCap] | query [D] | barriers
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* ring = smem_raw;
+  Cand* cand = reinterpret_cast<Cand*>(smem_raw + kBulkStages * kBulkTileBytes);
+  float* sq = reinterpret_cast<float*>(cand + kCandCap);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sq + ((a.D + 3) & ~3));
+  __shared__ int count;
+  __shared__ float thr;
+  __shared__ int overflow;
+  const int t = threadIdx.x;
+  const long long lo = static_cast<long long>(blockIdx.x) * docs_per_cta;
+  const long long hi = min(a.n, lo + docs_per_cta);
+  const int n_tiles = hi > lo ? static_cast<int>((hi - lo + rows - 1) / rows) : 0;
+  const int D4 = a.D >> 2;
+  for (int i = t; i < a.D; i += kScanThreads) sq[i] = a.q32[i];
+  const uint64_t pol = policy_evict_first();  // streamed once
+  auto issue = [&](int tile) {
+    const long long base = lo + static_cast<long long>(tile) * rows;
+    const int r = static_cast<int>(min(static_cast<long long>(rows), hi - base));
+    const int st = tile % kBulkStages;
+    mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(r) * a.D * 4);
+    bulk_load_1d(ring + st * kBulkTileBytes, a.emb + base * a.D, static_cast<uint32_t>(r) * a.D * 4,
+                 &full[st], pol);
+  };
+  if (t == 0) {
+    count = 0;
+    thr = -INFINITY;
+    overflow = 0;
+    for (int s = 0; s < kBulkStages; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+    for (int s = 0; s < kBulkStages && s < n_tiles; ++s) issue(s);
+  }
+  const float qn = static_cast<float>(a.q_norm);
+  const float w0 = static_cast<float>(a.w0);
+
+  auto compact = [&]() {
+    __syncthreads();
+    const int n = count;
+    int P = 1;
+    while (P < n) P <<= 1;
+    for (int i = n + t; i < P; i += kScanThreads) cand[i] = Cand{-INFINITY, -1};
+    sort_cands(cand, P);
+    if (t == 0) {
+      float th = thr;
+      if (n >= a.k) th = fmaxf(th, cand[a.k - 1].s);
+      thr = th;
+      int l = 0, r = n;
+      while (l < r) {
+        const int m = (l + r) >> 1;
+        if (cand[m].s >= th - a.eps2) l = m + 1;
+        else r = m;
+      }
+      if (l > kCandCap / 2) {
+        l = kCandCap / 2;
+        overflow = 1;
+      }
+      count = l;
+    }
+    __syncthreads();
+  };
+
+  __syncthreads();
+  for (int tile = 0; tile < n_tiles; ++tile) {
+    const long long base = lo + static_cast<long long>(tile) * rows;
+    const int r = static_cast<int>(min(static_cast<long long>(rows), hi - base));
+    const int st = tile % kBulkStages;
+    mbar_wait(&full[st], (tile / kBulkStages) & 1);
+    float dot0 = 0.f, dot1 = 0.f, nb0 = 0.f, nb1 = 0.f;
+    const long long doc = base + t;
+    if (t < r) {
+      const float4* row = reinterpret_cast<const float4*>(ring + st * kBulkTileBytes) + t * D4;
+      int j = t % D4;
+#pragma unroll 4
+      for (int c = 0; c < D4; ++c) {
+        const float4 v = row[j];
+        const float4 qv = reinterpret_cast<const float4*>(sq)[j];
+        dot0 = fmaf(qv.x, v.x, dot0);
+        dot1 = fmaf(qv.y, v.y, dot1);
+        dot0 = fmaf(qv.z, v.z, dot0);
+        dot1 = fmaf(qv.w, v.w, dot1);
+        nb0 = fmaf(v.x, v.x, nb0);
+        nb1 = fmaf(v.y, v.y, nb1);
+        nb0 = fmaf(v.z, v.z, nb0);
+        nb1 = fmaf(v.w, v.w, nb1);
+        j = j + 1 == D4 ? 0 : j + 1;
+      }
+    }
+    __syncthreads();  // every thread is done with this stage
+    if (t == 0 && tile + kBulkStages < n_tiles) issue(tile + kBulkStages);
+    if (t < r && (a.keep == nullptr || a.keep[doc] != 0)) {
+      const float dot = dot0 + dot1, nb = nb0 + nb1;
+      if (nb == 0.f) atomicOr(&counters[1], 1);
+      float s = w0 * (dot / (qn * sqrtf(nb)));
+      for (int f = 0; f < a.F; ++f) s = fmaf(a.w32[f], a.feat[doc * a.F + f], s);
+      if (s >= thr - a.eps2) {
+        const int slot = atomicAdd(&count, 1);
+        cand[slot] = Cand{s, static_cast<int32_t>(doc)};
+      }
+    }
+    __syncthreads();
+    if (count > kCandCap - kScanThreads) compact();
+  }
+  if (count > 0) compact();
+  __shared__ int gbase;
+  if (t == 0) {
+    gbase = count > 0 ? atomicAdd(&counters[0], count) : 0;
+    if (overflow || gbase + count > g_cap) atomicOr(&counters[1], 2);
+  }
+  __syncthreads();
+  if (gbase + count <= g_cap)
+    for (int i = t; i < count; i += kScanThreads) g_cand[gbase + i] = cand[i].idx;
+  pdl_trigger();
+}
+
 // Exact rescoring in the reference's order: dot, na, nb accumulated in
 // double over float products (exact), cos = dot / (sqrt(na) * sqrt(nb)),
 // s = w0 * cos, s += w_i * f_i (retrieval.cpp:44-71). Round-to-nearest
@@ -284,6 +413,23 @@ cudaError_t retrieval_scan(const RetrievalScan& a, int32_t* cand, int cand_cap, 
   cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), stream);
   if (e != cudaSuccess) return e;
   // contiguous doc ranges, a multiple of the tile size
+  if ((a.D & 3) == 0 && a.D <= 128) {
+    // TMA-streamed scan: tiles of `rows` docs (<= 32 KB, <= one per thread)
+    const int rows = min(kScanThreads, kBulkTileBytes / (a.D * 4));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int g2 = min(grid, 2 * num_sms(dev));  // two 100 KB CTAs per SM
+    long long per = (a.n + g2 - 1) / g2;
+    per = (per + rows - 1) / rows * rows;
+    const int blocks = static_cast<int>((a.n + per - 1) / per);
+    const size_t smem = kBulkStages * kBulkTileBytes + kCandCap * sizeof(Cand) +
+                        static_cast<size_t>((a.D + 3) & ~3) * sizeof(float) + 64;
+    e = cudaFuncSetAttribute(retrieval_scan_bulk_kernel,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    return launch_k(retrieval_scan_bulk_kernel, dim3(blocks), dim3(kScanThreads), smem, stream, a,
+                    cand, cand_cap, counters, per, rows);
+  }
   long long per = (a.n + grid - 1) / grid;
   per = (per + kScanThreads - 1) / kScanThreads * kScanThreads;
   const int blocks = static_cast<int>((a.n + per - 1) / per);
