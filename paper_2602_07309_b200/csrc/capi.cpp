@@ -434,7 +434,7 @@ int32_t sr_plan_shape(const sr_plan* p, int64_t* out8) {
     h2d += static_cast<int64_t>(pk.spans.size()) * sizeof(srk::RowSpan);
     h2d += static_cast<int64_t>(pk.tiles.size()) * sizeof(srk::AttnTile);
     h2d += static_cast<int64_t>(pk.last_rows.size()) * 4 + static_cast<int64_t>(pk.ids.size()) * 8;
-    h2d += static_cast<int64_t>(pk.seg_off.size()) * 4 + static_cast<int64_t>(pk.soft_rows.size()) * 4;
+    h2d += static_cast<int64_t>(pk.seg_off.size()) * 4 + static_cast<int64_t>(pk.n_soft) * 4 * p->owner->e->config().d_model;
     out8[4] = h2d;
     out8[5] = static_cast<int64_t>(pk.n_items) * p->p->n_tasks * 8 +
               static_cast<int64_t>(pk.seg_off.size() - 1) * p->p->k * sizeof(srk::TopkEntry);

@@ -417,7 +417,17 @@ void Engine::refill_plan(Plan& p, const sr_request* reqs, int n_req) {
   put(p.last_rows, pk.last_rows, stream_);
   put(p.ids, pk.ids, stream_);
   put(p.seg_off, pk.seg_off, stream_);
-  put(p.soft, pk.soft_rows, stream_);
+  {
+    // soft rows straight from the callers' buffers (one copy per request)
+    const size_t d = cfg_.d_model;
+    p.soft.ensure(std::max<size_t>(static_cast<size_t>(pk.n_soft) * d, 1));
+    size_t off = 0;
+    for (const auto& src : pk.soft_src) {
+      SR_CUDA_CHECK(cudaMemcpyAsync(p.soft.ptr + off * d, src.rows, src.n_rows * d * sizeof(float),
+                                    cudaMemcpyHostToDevice, stream_));
+      off += src.n_rows;
+    }
+  }
   p.scores.ensure(static_cast<size_t>(pk.n_items) * n_tasks());
   const int n_seg = n_req;
   const int chunks = (pk.max_seg_len + 4095) / 4096;

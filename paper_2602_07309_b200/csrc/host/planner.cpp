@@ -175,7 +175,7 @@ void pack_requests(const ModelConfig& cfg, const sr_request* reqs, int n_req,
   out.last_rows.resize(N);
   out.ids.resize(N);
   out.seg_off.assign(n_req + 1, 0);
-  out.soft_rows.resize(static_cast<size_t>(R) * d);
+  out.soft_src.clear();
   out.n_soft = static_cast<int32_t>(R);
   out.max_seg_len = 0;
 
@@ -195,12 +195,14 @@ void pack_requests(const ModelConfig& cfg, const sr_request* reqs, int n_req,
     }
     const int32_t items_begin = row;
     const bool mixed = rq.mode == SR_MODE_MIXED;
+    if (mixed && rq.n_items > 0)
+      out.soft_src.push_back({rq.item_rows, static_cast<size_t>(rq.item_offsets[rq.n_items])});
     for (int i = 0; i < rq.n_items; ++i) {
       const int32_t s = row, L = lens[q][i];
       for (int32_t j = 0; j < L; ++j, ++row) {
         if (mixed) {
-          const float* src = rq.item_rows + (static_cast<size_t>(rq.item_offsets[i]) + j) * d;
-          std::copy(src, src + d, out.soft_rows.begin() + static_cast<size_t>(soft) * d);
+          // soft row index == this request's row index rq.item_offsets[i] + j,
+          // offset by the rows of earlier requests
           out.row_src[row] = -(1 + soft);
           ++soft;
         } else {

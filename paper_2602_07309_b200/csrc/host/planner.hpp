@@ -51,7 +51,14 @@ struct PackedBatch {
   std::vector<int32_t> last_rows;      // per item: packed row scored
   std::vector<int64_t> ids;            // per item: doc id for the tie rule
   std::vector<int32_t> seg_off;        // per request: item offsets [n_req + 1]
-  std::vector<float> soft_rows;        // mixed-mode rows [R x d]
+  // mixed-mode rows [R x d]: not copied on the host — each request's item
+  // rows are already contiguous (item_offsets index them in order), so the
+  // engine copies them straight from the caller's buffer into HBM.
+  struct SoftSrc {
+    const float* rows;
+    size_t n_rows;
+  };
+  std::vector<SoftSrc> soft_src;
   int32_t n_soft = 0;
 };
 

@@ -360,6 +360,34 @@ def _item_doc_ids(items: Sequence[ScoreItem]) -> Optional[np.ndarray]:
         return None
 
 
+def _adjacent_rows(items) -> np.ndarray:
+    """The items' embedding rows as one contiguous float32 array. When they
+    are already consecutive slices of one buffer (a [N x n x d] batch), that
+    buffer is used in place — the engine then copies it straight to HBM —
+    instead of being gathered into a new array."""
+    arrs = [it.embedding for it in items]
+    if all(isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous
+           for a in arrs):
+        base = arrs[0].ctypes.data
+        pos = base
+        for a in arrs:
+            if a.ctypes.data != pos:
+                break
+            pos += a.nbytes
+        else:
+            total = (pos - base) // 4
+            root = arrs[0]
+            while isinstance(root.base, np.ndarray):
+                root = root.base
+            lo = (base - root.ctypes.data) // 4
+            flat = root.reshape(-1) if root.flags.c_contiguous else None
+            if flat is not None and root.dtype == np.float32 and 0 <= lo and \
+                    lo + total <= flat.size:
+                return flat[lo:lo + total]
+    return np.ascontiguousarray(np.concatenate(
+        [np.asarray(a, np.float32).reshape(-1) for a in arrs]))
+
+
 class _PackedRequest:
     """Flattened sr_request; keeps the numpy buffers alive."""
 
@@ -380,9 +408,7 @@ class _PackedRequest:
         self.offsets = np.zeros(len(req.items) + 1, np.int32)
         self.offsets[1:] = np.cumsum(lens) if lens else []
         if mixed:
-            self.rows = np.ascontiguousarray(np.concatenate(
-                [np.asarray(it.embedding, np.float32).reshape(-1) for it in req.items])
-                if req.items else np.zeros(1, np.float32))
+            self.rows = _adjacent_rows(req.items) if req.items else np.zeros(1, np.float32)
             self.tokens = np.zeros(1, np.int32)
         else:
             self.tokens = np.ascontiguousarray(np.concatenate(
