@@ -237,6 +237,24 @@ int32_t sr_engine_score_sharded(sr_engine* e, sr_comm* c, const sr_request* loca
                                 sr_result* res);
 int32_t sr_plan_run_sharded(sr_plan* p, sr_comm* c); /* resident variant */
 
+/* ------------------------------ service post-processing
+ * The step after scoring in SearchService::handle_search (service.cpp:242-277):
+ * calibrate() of the relevance with the fitted isotonic head
+ * (calibration.hpp:17-33, calibration.cpp:65-88: blocks sorted by lo, value
+ * clamped to [0,1], linear ramp across gaps), then the final score is the
+ * calibrated relevance, or sum_j blend_w[j] * calibrated[blend_task[j]] in the
+ * given order (the std::map<string,double> score_blend iterates by task name;
+ * task 0 = relevance, 1.. = heads in config order). The device computes it in
+ * the same double operation order and the top-k (page) orders by it; the
+ * returned topk_scores are then final scores. n_blocks = n_blend = 0 turns
+ * it off. SR_ALIGNMENT for an unknown blend task (service.cpp:258-262). */
+int32_t sr_engine_set_postprocess(sr_engine* e, const double* lo, const double* hi,
+                                  const double* value, int32_t n_blocks,
+                                  const int32_t* blend_task, const double* blend_w,
+                                  int32_t n_blend);
+/* Final scores [n_items] of the last score call (post-processing on). */
+int32_t sr_engine_final_scores(sr_engine* e, double* out, int32_t cap, int32_t* n_out);
+
 /* ------------------------------- exhaustive retrieval top-K
  * The candidate generator upstream of the ranker. Replaces
  *   std::vector<RankedDoc> exhaustive_topk(const Corpus&, const QuerySpec&,

@@ -260,11 +260,30 @@ def retrieval():
                             "cases": cases})
 
 
+def calibration():
+    """fit_isotonic + calibrate (calibration.cpp:13-88) from the reference:
+    a head fitted on random (score, outcome) pairs (with ties) and calibrated
+    values of raw scores below, inside, between and above its blocks."""
+    rng = np.random.default_rng(20261018)
+    raw = np.round(rng.random(300), 3)  # rounding makes equal-score pools
+    oc = (rng.random(300) < raw).astype(np.int32)
+    raws = np.concatenate([rng.random(200), raw[:20], [-0.5, 0.0, 1.0, 1.5]])
+    lo, hi, val, cal = O.ref_fit_calibrate(raw, oc, raws)
+    dump("calibration.json", {"source": "fit_isotonic/calibrate calibration.cpp:13-88 via oracle/_ref",
+                              "lo": [repr(float(x)) for x in lo], "hi": [repr(float(x)) for x in hi],
+                              "value": [repr(float(x)) for x in val],
+                              "raws": [repr(float(x)) for x in raws],
+                              "calibrated": [repr(float(x)) for x in cal]})
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "retrieval":
+    if len(sys.argv) > 1 and sys.argv[1] == "calibration":
+        calibration()
+    elif len(sys.argv) > 1 and sys.argv[1] == "retrieval":
         if not O.ref_available():
             sys.exit("oracle/_ref not built")
         retrieval()
     else:
         main()
         retrieval()
+        calibration()

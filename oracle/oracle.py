@@ -289,3 +289,40 @@ def ref_topk(emb, feat, ids, color, query, w0, w, allowed, k, timing=None):
     if st != 0:
         raise RetrievalError(st - 1, lib.ref_last_error().decode())
     return oi[:cnt[0]], os_[:cnt[0]]
+
+
+# ------------------------------------------------------------- calibration
+def oracle_final_scores(scores, lo, hi, val, blend_task=(), blend_w=()):
+    """C restatement of calibrate + blend (calibration.cpp:65-88, service.cpp:250-266)."""
+    lib = port()
+    sc = np.ascontiguousarray(scores, np.float64)
+    n, stride = sc.shape
+    lo, hi, val = (np.ascontiguousarray(a, np.float64) for a in (lo, hi, val))
+    bt = np.ascontiguousarray(list(blend_task) or [0], np.int32)
+    bw = np.ascontiguousarray(list(blend_w) or [0.0], np.float64)
+    out = np.zeros(n, np.float64)
+    fn = lib.or_final_scores
+    fn.argtypes = [f64p, C.c_int, C.c_int, f64p, f64p, f64p, C.c_int, i32p, f64p, C.c_int, f64p]
+    fn(_p(sc, f64p), stride, n, _p(lo, f64p), _p(hi, f64p), _p(val, f64p), len(lo), _p(bt, i32p),
+       _p(bw, f64p), len(list(blend_task)), _p(out, f64p))
+    return out
+
+
+def ref_fit_calibrate(raw, outcome, raws):
+    """The reference's fit_isotonic + calibrate (oracle/_ref) -> (lo, hi, val, calibrated)."""
+    lib = ref()
+    raw = np.ascontiguousarray(raw, np.float64)
+    oc = np.ascontiguousarray(outcome, np.int32)
+    rs = np.ascontiguousarray(raws, np.float64)
+    cap = len(raw) + 1
+    lo, hi, val = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+    nb = np.zeros(1, np.int32)
+    out = np.zeros(len(rs))
+    fn = lib.ref_fit_calibrate
+    fn.argtypes = [f64p, i32p, C.c_int32, f64p, C.c_int32, f64p, f64p, f64p, C.c_int32, i32p, f64p]
+    st = fn(_p(raw, f64p), _p(oc, i32p), len(raw), _p(rs, f64p), len(rs), _p(lo, f64p),
+            _p(hi, f64p), _p(val, f64p), cap, _p(nb, i32p), _p(out, f64p))
+    if st != 0:
+        raise RuntimeError(lib.ref_last_error().decode())
+    n = int(nb[0])
+    return lo[:n], hi[:n], val[:n], out

@@ -22,6 +22,7 @@
 #include "semrank/error.hpp"
 #include "semrank/kernels.hpp"
 #include "semrank/model.hpp"
+#include "semrank/calibration.hpp"
 #include "semrank/retrieval.hpp"
 #include "semrank/rng.hpp"
 #include "semrank/weights_io.hpp"
@@ -296,6 +297,25 @@ int ref_exhaustive_topk(const float* emb, const float* feat, const int64_t* ids,
       scores_out[j] = top[j].score;
     }
     *n_out = static_cast<int32_t>(top.size());
+  });
+}
+
+// fit_isotonic (calibration.cpp:13-63) on (raw, outcome) pairs, then
+// calibrate (:65-88) of raws[]; blocks written to lo/hi/val (cap entries).
+int ref_fit_calibrate(const double* raw, const int32_t* outcome, int32_t n, const double* raws,
+                      int32_t n_raws, double* lo, double* hi, double* val, int32_t cap,
+                      int32_t* n_blocks, double* out) {
+  return run([&] {
+    std::vector<CalibrationPair> pairs(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) pairs[i] = {raw[i], outcome[i]};
+    const auto head = fit_isotonic(pairs);
+    *n_blocks = static_cast<int32_t>(head.blocks.size());
+    for (size_t b = 0; b < head.blocks.size() && static_cast<int32_t>(b) < cap; ++b) {
+      lo[b] = head.blocks[b].lo;
+      hi[b] = head.blocks[b].hi;
+      val[b] = head.blocks[b].value;
+    }
+    for (int i = 0; i < n_raws; ++i) out[i] = calibrate(head, raws[i]);
   });
 }
 

@@ -5,7 +5,7 @@ sm_100a kernels + C++ host runtime); this package is its Python binding with
 the reference's API names. See DESIGN.md.
 """
 from .semrank import (  # noqa: F401
-    Batch, BatchEntry, ErrorCode, FlopReport, HeadSpec, ItemScores, ModelConfig, ModelWeights,
+    Batch, BatchEntry, CalibrationBlock, CalibrationHead, ErrorCode, FlopReport, HeadSpec, ItemScores, ModelConfig, ModelWeights,
     MultiItemMask, Comm, Plan, BatchPlan, PROF_CLASSES, ScoreItem, ScoreMode, ScoreRequest, ScoreResult, ScoringEngine, SemrankError,
     build_multi_item_mask, flops, init_model, kRelevanceTask, load_weights, plan_batches, request_report,
     save_weights, score_by_mode, score_mode_from_name, score_mode_name, topk_host)

@@ -348,6 +348,30 @@ int32_t sr_engine_item_hidden(sr_engine* e, const sr_request* req, float* hidden
   });
 }
 
+int32_t sr_engine_set_postprocess(sr_engine* e, const double* lo, const double* hi,
+                                  const double* value, int32_t n_blocks,
+                                  const int32_t* blend_task, const double* blend_w,
+                                  int32_t n_blend) {
+  return guard([&] {
+    if (!e || (n_blocks > 0 && (!lo || !hi || !value)) || (n_blend > 0 && (!blend_task || !blend_w)))
+      srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    e->e->set_postprocess(lo, hi, value, n_blocks, blend_task, blend_w, n_blend);
+  });
+}
+
+int32_t sr_engine_final_scores(sr_engine* e, double* out, int32_t cap, int32_t* n_out) {
+  return guard([&] {
+    if (!e || !n_out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    const auto& f = e->e->last_final();
+    const int32_t n = static_cast<int32_t>(f.size());
+    if (out)
+      for (int32_t i = 0; i < std::min(n, cap); ++i) out[i] = f[i];
+    *n_out = n;
+  });
+}
+
 int32_t sr_engine_device(const sr_engine* e) { return e ? e->e->device() : -1; }
 void* sr_engine_stream(const sr_engine* e) { return e ? e->e->stream() : nullptr; }
 

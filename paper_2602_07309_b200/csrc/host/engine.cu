@@ -169,6 +169,42 @@ Plan::~Plan() {
   if (graph) cudaGraphExecDestroy(graph);
 }
 
+void Engine::set_postprocess(const double* lo, const double* hi, const double* value,
+                             int n_blocks, const int32_t* blend_task, const double* blend_w,
+                             int n_blend) {
+  if (n_blocks < 0 || n_blend < 0) fail(SR_PARAMETER, "negative post-processing size");
+  const int T = n_tasks();
+  for (int j = 0; j < n_blend; ++j)
+    if (blend_task[j] < 0 || blend_task[j] >= T)
+      fail(SR_ALIGNMENT, "blend references unknown task");  // service.cpp:258-262
+  for (int b = 0; b + 1 < n_blocks; ++b)
+    if (!(lo[b] <= hi[b] && hi[b] <= lo[b + 1]))
+      fail(SR_PARAMETER, "calibration blocks must be sorted and disjoint");
+  SR_CUDA_CHECK(cudaSetDevice(device_));
+  std::vector<double> blk(static_cast<size_t>(3) * std::max(n_blocks, 1));
+  for (int b = 0; b < n_blocks; ++b) {
+    blk[3 * b] = lo[b];
+    blk[3 * b + 1] = hi[b];
+    blk[3 * b + 2] = value[b];
+  }
+  post_blocks_.ensure(blk.size());
+  post_task_.ensure(static_cast<size_t>(std::max(n_blend, 1)));
+  post_w_.ensure(static_cast<size_t>(std::max(n_blend, 1)));
+  SR_CUDA_CHECK(cudaMemcpy(post_blocks_.ptr, blk.data(), blk.size() * sizeof(double),
+                           cudaMemcpyHostToDevice));
+  if (n_blend > 0) {
+    SR_CUDA_CHECK(cudaMemcpy(post_task_.ptr, blend_task, n_blend * sizeof(int32_t),
+                             cudaMemcpyHostToDevice));
+    SR_CUDA_CHECK(cudaMemcpy(post_w_.ptr, blend_w, n_blend * sizeof(double),
+                             cudaMemcpyHostToDevice));
+  }
+  post_nblocks_ = n_blocks;
+  post_nblend_ = n_blend;
+  post_on_ = n_blocks > 0 || n_blend > 0;
+  last_final_.clear();
+  ++ws_epoch_;  // captured graphs bake the launch list: re-capture
+}
+
 void Engine::ensure_workspace(int32_t M) {
   if (M <= ws_rows_) return;
   const int32_t rows = M + M / 4 + 128;
@@ -339,10 +375,22 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
                                 no_col_, p.scores.ptr, hidden_out, s));
   E();
   ++n;
+  const double* key = p.scores.ptr;
+  int key_stride = n_tasks();
+  if (post_on_) {
+    B(PROF_TOPK);
+    SR_CUDA_CHECK(srk::final_scores(p.scores.ptr, n_tasks(), p.pack.n_items, post_blocks_.ptr,
+                                    post_nblocks_, post_task_.ptr, post_w_.ptr, post_nblend_,
+                                    p.final.ptr, s));
+    E();
+    ++n;
+    key = p.final.ptr;
+    key_stride = 1;
+  }
   if (p.k > 0) {
     const int n_seg = static_cast<int>(p.pack.seg_off.size()) - 1;
     B(PROF_TOPK);
-    SR_CUDA_CHECK(srk::topk(p.scores.ptr, n_tasks(), p.ids.ptr, p.seg_off.ptr, n_seg,
+    SR_CUDA_CHECK(srk::topk(key, key_stride, p.ids.ptr, p.seg_off.ptr, n_seg,
                             p.pack.max_seg_len, p.k, p.topk_scratch.ptr,
                             static_cast<int>(p.topk_scratch.cap), p.topk_out.ptr, s));
     E();
@@ -429,6 +477,7 @@ void Engine::refill_plan(Plan& p, const sr_request* reqs, int n_req) {
     }
   }
   p.scores.ensure(static_cast<size_t>(pk.n_items) * n_tasks());
+  p.final.ensure(static_cast<size_t>(std::max(pk.n_items, 1)));
   const int n_seg = n_req;
   const int chunks = (pk.max_seg_len + 4095) / 4096;
   p.topk_scratch.ensure(static_cast<size_t>(std::max(1, n_seg * chunks * std::max(p.k, 1))));
@@ -489,6 +538,12 @@ void Engine::fetch(Plan& p, sr_result* res, int n_req) {
   std::vector<srk::TopkEntry> top(static_cast<size_t>(n_req) * std::max(p.k, 0));
   SR_CUDA_CHECK(cudaMemcpyAsync(scores.data(), p.scores.ptr, scores.size() * sizeof(double),
                                 cudaMemcpyDeviceToHost, stream_));
+  if (post_on_) {
+    last_final_.resize(static_cast<size_t>(pk.n_items));
+    SR_CUDA_CHECK(cudaMemcpyAsync(last_final_.data(), p.final.ptr,
+                                  last_final_.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                  stream_));
+  }
   if (p.k > 0)
     SR_CUDA_CHECK(cudaMemcpyAsync(top.data(), p.topk_out.ptr, top.size() * sizeof(srk::TopkEntry),
                                   cudaMemcpyDeviceToHost, stream_));

@@ -107,6 +107,7 @@ struct Plan {
   DevBuf<float> soft;
   // outputs
   DevBuf<double> scores;
+  DevBuf<double> final;  // post-processed ranking key (set_postprocess)
   DevBuf<srk::TopkEntry> topk_scratch, topk_out;
   DevBuf<srk::TopkEntry> gathered, merged;  // sharded merge
   // graph
@@ -129,6 +130,14 @@ class Engine {
   std::mutex& mutex() { return mu_; }
   // LayerNorm folded into the GEMM epilogues (all projections on the pair path).
   bool fold_ln() const { return fold_ln_; }
+  // Service post-processing on the device (service.cpp:242-277): calibrated
+  // relevance (isotonic blocks lo/hi/value) and an optional task blend; the
+  // top-k then orders by the final score. n_blocks == 0 and n_blend == 0
+  // turns it off (top-k by raw relevance).
+  void set_postprocess(const double* lo, const double* hi, const double* value, int n_blocks,
+                       const int32_t* blend_task, const double* blend_w, int n_blend);
+  bool postprocess() const { return post_on_; }
+  const std::vector<double>& last_final() const { return last_final_; }
 
   // Builds a plan: validates + packs + uploads inputs + captures the graph.
   std::unique_ptr<Plan> make_plan(const sr_request* reqs, int n_req, int32_t k);
@@ -167,6 +176,11 @@ class Engine {
   int n_cols_ = 0, yes_col_ = 0, no_col_ = 0;
   bool fold_ln_ = false;
   bool serpentine_ = false;
+  bool post_on_ = false;
+  int post_nblocks_ = 0, post_nblend_ = 0;
+  DevBuf<double> post_blocks_, post_w_;
+  DevBuf<int32_t> post_task_;
+  std::vector<double> last_final_;
   std::vector<LayerDev> layers_;
   std::vector<void*> allocs_;
   // workspace

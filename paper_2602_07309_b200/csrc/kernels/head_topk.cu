@@ -238,7 +238,65 @@ __global__ void __launch_bounds__(kSortThreads)
   for (int j = threadIdx.x; j < k; j += blockDim.x) dst[j] = j < P ? buf[j] : sentinel();
 }
 
+// Output side of the service (service.cpp:242-277): calibrate() of the
+// relevance (calibration.cpp:65-88: clamp(value) of the block holding the
+// score, linear ramp across gaps), then the final score = calibrated
+// relevance, or sum_j w_j * calibrated[task_j] in the caller's (std::map)
+// order. Same double operations in the same order as the reference.
+__global__ void final_score_kernel(const double* __restrict__ scores, int stride, int n,
+                                   const double* __restrict__ blk, int n_blocks,
+                                   const int32_t* __restrict__ blend_task,
+                                   const double* __restrict__ blend_w, int n_blend,
+                                   double* __restrict__ out) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double raw = scores[static_cast<size_t>(i) * stride];
+  double cal = raw;
+  if (n_blocks > 0) {
+    auto lo = [&](int b) { return blk[3 * b]; };
+    auto hi = [&](int b) { return blk[3 * b + 1]; };
+    auto val = [&](int b) { return blk[3 * b + 2]; };
+    auto clamp01 = [](double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); };
+    if (raw <= hi(0)) {
+      cal = clamp01(val(0));
+    } else {
+      cal = clamp01(val(n_blocks - 1));
+      for (int b = 0; b + 1 < n_blocks; ++b) {
+        if (raw < lo(b + 1)) {
+          const double t = __ddiv_rn(__dsub_rn(raw, hi(b)), __dsub_rn(lo(b + 1), hi(b)));
+          cal = clamp01(__dadd_rn(val(b), __dmul_rn(t, __dsub_rn(val(b + 1), val(b)))));
+          break;
+        }
+        if (raw <= hi(b + 1)) {
+          cal = clamp01(val(b + 1));
+          break;
+        }
+      }
+    }
+  }
+  double f = cal;
+  if (n_blend > 0) {
+    f = 0.0;
+    for (int j = 0; j < n_blend; ++j) {
+      const int tk = blend_task[j];
+      const double v = tk == 0 ? cal : scores[static_cast<size_t>(i) * stride + tk];
+      f = __dadd_rn(f, __dmul_rn(blend_w[j], v));
+    }
+  }
+  out[i] = f;
+  pdl_trigger();
+}
+
 }  // namespace
+
+cudaError_t final_scores(const double* scores, int stride, int n, const double* blocks,
+                         int n_blocks, const int32_t* blend_task, const double* blend_w,
+                         int n_blend, double* out, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  return launch_k(final_score_kernel, dim3((n + 255) / 256), dim3(256), 0, stream, scores, stride,
+                  n, blocks, n_blocks, blend_task, blend_w, n_blend, out);
+}
 
 cudaError_t score_head(const float* x, const int32_t* last_rows, int n_items, int d,
                        const float* ln_gain, const float* w_cols, const float* bias, int n_cols,

@@ -152,6 +152,13 @@ cudaError_t score_head(const float* x, const int32_t* last_rows, int n_items, in
                        int yes_col, int no_col, double* scores, float* hidden_out,
                        cudaStream_t stream);
 
+// Service post-processing of the raw scores [n x stride] (service.cpp:242-277):
+// calibrated relevance (isotonic blocks, interleaved lo/hi/value) and the
+// optional task blend; out[n] is the key the page top-k sorts by.
+cudaError_t final_scores(const double* scores, int stride, int n, const double* blocks,
+                         int n_blocks, const int32_t* blend_task, const double* blend_w,
+                         int n_blend, double* out, cudaStream_t stream);
+
 struct TopkEntry {
   double score;
   int64_t id;

@@ -262,8 +262,9 @@ class ScoreResult:
     mode: ScoreMode = ScoreMode.Naive
     flops: FlopReport = field(default_factory=FlopReport)
     kv_incremental_per_item: float = 0.0
-    topk: List[tuple] = field(default_factory=list)  # (item_id, relevance)
+    topk: List[tuple] = field(default_factory=list)  # (item_id, relevance or final score)
     scores: Optional[np.ndarray] = None  # [n_items x n_tasks], col 0 relevance
+    final_scores: Optional[np.ndarray] = None  # [n_items] with post-processing on
 
 
 class MultiItemMask:  # engine.hpp:63-72
@@ -438,8 +439,26 @@ class _ResultBuf:
                             _c.FlopReportC(), 0.0, 0)
 
 
+@dataclass
+class CalibrationBlock:  # calibration.hpp:18-23
+    lo: float = 0.0
+    hi: float = 0.0
+    value: float = 0.0
+    count: int = 0
+
+
+@dataclass
+class CalibrationHead:  # calibration.hpp:17-27 (fitted offline by fit_isotonic)
+    blocks: List[CalibrationBlock] = field(default_factory=list)
+
+    def fitted(self) -> bool:
+        return bool(self.blocks)
+
+
 class ScoringEngine:
     """ScoringEngine (engine.hpp:109-119) bound to one B200; serialises callers."""
+
+    _post = False
 
     def __init__(self, weights: ModelWeights, device: int = 0):
         self.weights = weights
@@ -473,7 +492,42 @@ class ScoringEngine:
         pr = _PackedRequest(request, self.config.d_model)
         rb = _ResultBuf(len(request.items), len(self.task_names), k)
         _check(_lib.sr_engine_score(self._h, C.byref(pr.c), C.byref(rb.c)))
-        return self._to_result(request, rb)
+        res = self._to_result(request, rb)
+        if self._post:
+            res.final_scores = self._final(len(request.items))
+        return res
+
+    def set_postprocess(self, calibration: Optional["CalibrationHead"] = None,
+                        score_blend: Optional[Dict[str, float]] = None) -> None:
+        """The service's output side on the device (service.cpp:242-277):
+        calibrated relevance (fitted isotonic head, calibration.cpp:65-88) and
+        the optional ``score_blend`` (task -> weight, summed in task-name order
+        like the reference's std::map); the top-k then ranks by the final score."""
+        blocks = calibration.blocks if calibration is not None else []
+        lo = np.array([b.lo for b in blocks] or [0.0], np.float64)
+        hi = np.array([b.hi for b in blocks] or [0.0], np.float64)
+        val = np.array([b.value for b in blocks] or [0.0], np.float64)
+        names = ["relevance"] + list(self.task_names[1:])
+        tasks, ws = [], []
+        for name, w in sorted((score_blend or {}).items()):
+            if name not in names:
+                raise SemrankError(ErrorCode.Alignment, f"blend references unknown task: {name}")
+            tasks.append(names.index(name))
+            ws.append(float(w))
+        t = np.array(tasks or [0], np.int32)
+        wv = np.array(ws or [0.0], np.float64)
+        D = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+        _check(_lib.sr_engine_set_postprocess(self._h, D(lo), D(hi), D(val), len(blocks),
+                                              t.ctypes.data_as(C.POINTER(C.c_int32)), D(wv),
+                                              len(tasks)))
+        self._post = bool(blocks) or bool(tasks)
+
+    def _final(self, n: int) -> np.ndarray:
+        out = np.zeros(max(n, 1), np.float64)
+        got = C.c_int32(0)
+        _check(_lib.sr_engine_final_scores(self._h, out.ctypes.data_as(C.POINTER(C.c_double)),
+                                           len(out), C.byref(got)))
+        return out[:got.value]
 
     def score_batch(self, requests: Sequence[ScoreRequest], k: int = 0) -> List[ScoreResult]:
         prs = [_PackedRequest(r, self.config.d_model) for r in requests]

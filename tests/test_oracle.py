@@ -196,3 +196,12 @@ def test_retrieval_oracle_fuzz_against_reference():
         a = O.oracle_topk(emb, feat, ids, keep, q, 0.7, w, k)
         b = O.ref_topk(emb, feat, ids, color, q, 0.7, w, allowed, k)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_calibration_oracle_matches_reference_golden():
+    """calibrate (calibration.cpp:65-88) restated in C == the reference's values."""
+    with open(os.path.join(os.path.dirname(__file__), "golden", "calibration.json")) as f:
+        g = json.load(f)
+    F = lambda k: np.array([float(x) for x in g[k]])
+    got = O.oracle_final_scores(F("raws")[:, None], F("lo"), F("hi"), F("value"))
+    assert np.array_equal(got, F("calibrated"))
