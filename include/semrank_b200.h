@@ -237,6 +237,19 @@ int32_t sr_engine_score_sharded(sr_engine* e, sr_comm* c, const sr_request* loca
                                 sr_result* res);
 int32_t sr_plan_run_sharded(sr_plan* p, sr_comm* c); /* resident variant */
 
+/* --------------------------------------- /score wire ingest
+ * parse_score_request_json's embedding_b64 items (service.cpp:361-370):
+ * n_items base64 float32 payloads, concatenated in text with char offsets
+ * char_off[n_items + 1], are copied to HBM and decoded there (base64.cpp:
+ * 60-108 semantics) straight into the soft-token rows, then scored in mixed
+ * mode like sr_engine_score. SR_PAYLOAD_INVALID with the reference's
+ * messages for the first failing item: length not a multiple of 4,
+ * misplaced padding, invalid character, not whole float32 values, not
+ * [n x d_model]. */
+int32_t sr_engine_score_b64(sr_engine* e, const int32_t* prefix, int32_t t_q, const char* text,
+                            const int64_t* char_off, int32_t n_items, const int64_t* item_ids,
+                            sr_result* res);
+
 /* ------------------------------ service post-processing
  * The step after scoring in SearchService::handle_search (service.cpp:242-277):
  * calibrate() of the relevance with the fitted isotonic head

@@ -276,8 +276,33 @@ def calibration():
                               "calibrated": [repr(float(x)) for x in cal]})
 
 
+def wire():
+    """decode_f32_base64 (base64.cpp:60-108) outcomes from the reference on
+    well-formed payloads (every padding length) and each malformation."""
+    import base64 as b64
+    rng = np.random.default_rng(20261019)
+    cases = []
+    for n in (1, 2, 3, 16, 64):
+        v = rng.standard_normal(n).astype(np.float32)
+        t = b64.b64encode(v.tobytes()).decode()
+        out, st, msg = O.ref_decode_f32_base64(t)
+        cases.append({"text": t, "status": st, "message": msg,
+                      "floats": _b64(out) if out is not None else None})
+    good = b64.b64encode(rng.standard_normal(6).astype(np.float32).tobytes()).decode()
+    for t in [good[:-1], "AA=A" + good[4:], good[:8] + "*" + good[9:], good[:-4] + "A=A=",
+              good[:-4] + "AA=B", b64.b64encode(b"\x01\x02\x03").decode(), "", "====",
+              "AAA=AAAA"]:
+        out, st, msg = O.ref_decode_f32_base64(t)
+        cases.append({"text": t, "status": st, "message": msg,
+                      "floats": _b64(out) if out is not None else None})
+    dump("wire_b64.json", {"source": "decode_f32_base64 base64.cpp:60-108 via oracle/_ref",
+                           "cases": cases})
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "calibration":
+    if len(sys.argv) > 1 and sys.argv[1] == "wire":
+        wire()
+    elif len(sys.argv) > 1 and sys.argv[1] == "calibration":
         calibration()
     elif len(sys.argv) > 1 and sys.argv[1] == "retrieval":
         if not O.ref_available():
@@ -287,3 +312,4 @@ if __name__ == "__main__":
         main()
         retrieval()
         calibration()
+        wire()

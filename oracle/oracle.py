@@ -326,3 +326,19 @@ def ref_fit_calibrate(raw, outcome, raws):
         raise RuntimeError(lib.ref_last_error().decode())
     n = int(nb[0])
     return lo[:n], hi[:n], val[:n], out
+
+
+# ------------------------------------------------------------------ base64
+def ref_decode_f32_base64(text: str):
+    """The reference's decode_f32_base64 (oracle/_ref) -> (floats | None, status, message)."""
+    lib = ref()
+    b = text.encode("latin-1")
+    cap = len(b) // 4 * 3 // 4 + 1
+    out = np.zeros(cap, np.float32)
+    n = np.zeros(1, np.int64)
+    fn = lib.ref_decode_f32_base64
+    fn.argtypes = [C.c_char_p, C.c_int64, f32p, C.c_int64, i64p]
+    st = fn(b, len(b), _p(out, f32p), cap, _p(n, i64p))
+    if st != 0:
+        return None, st - 1, lib.ref_last_error().decode()
+    return out[:int(n[0])], 0, ""

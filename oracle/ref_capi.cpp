@@ -23,6 +23,7 @@
 #include "semrank/kernels.hpp"
 #include "semrank/model.hpp"
 #include "semrank/calibration.hpp"
+#include "semrank/base64.hpp"
 #include "semrank/retrieval.hpp"
 #include "semrank/rng.hpp"
 #include "semrank/weights_io.hpp"
@@ -316,6 +317,16 @@ int ref_fit_calibrate(const double* raw, const int32_t* outcome, int32_t n, cons
       val[b] = head.blocks[b].value;
     }
     for (int i = 0; i < n_raws; ++i) out[i] = calibrate(head, raws[i]);
+  });
+}
+
+// decode_f32_base64 (base64.cpp:97-108); returns the reference's status
+// (1 + ErrorCode) and message via ref_last_error on malformed payloads.
+int ref_decode_f32_base64(const char* text, int64_t len, float* out, int64_t cap, int64_t* n_out) {
+  return run([&] {
+    const auto v = decode_f32_base64(std::string(text, static_cast<size_t>(len)));
+    for (size_t i = 0; i < v.size() && static_cast<int64_t>(i) < cap; ++i) out[i] = v[i];
+    *n_out = static_cast<int64_t>(v.size());
   });
 }
 

@@ -348,6 +348,17 @@ int32_t sr_engine_item_hidden(sr_engine* e, const sr_request* req, float* hidden
   });
 }
 
+int32_t sr_engine_score_b64(sr_engine* e, const int32_t* prefix, int32_t t_q, const char* text,
+                            const int64_t* char_off, int32_t n_items, const int64_t* item_ids,
+                            sr_result* res) {
+  return guard([&] {
+    if (!e || !res || !char_off || (t_q > 0 && !prefix) || (n_items > 0 && !text))
+      srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    e->e->score_b64(prefix, t_q, text, char_off, n_items, item_ids, res);
+  });
+}
+
 int32_t sr_engine_set_postprocess(sr_engine* e, const double* lo, const double* hi,
                                   const double* value, int32_t n_blocks,
                                   const int32_t* blend_task, const double* blend_w,

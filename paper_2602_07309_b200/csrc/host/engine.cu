@@ -471,8 +471,28 @@ void Engine::refill_plan(Plan& p, const sr_request* reqs, int n_req) {
     p.soft.ensure(std::max<size_t>(static_cast<size_t>(pk.n_soft) * d, 1));
     size_t off = 0;
     for (const auto& src : pk.soft_src) {
-      SR_CUDA_CHECK(cudaMemcpyAsync(p.soft.ptr + off * d, src.rows, src.n_rows * d * sizeof(float),
-                                    cudaMemcpyHostToDevice, stream_));
+      if (src.rows == kB64Rows) {
+        // base64 payloads: text to HBM, decoded in place into the rows
+        const int32_t n = b64_.n;
+        const int64_t chars = b64_.char_off[n];
+        b64_text_.ensure(static_cast<size_t>(std::max<int64_t>(chars, 4)));
+        b64_off_.ensure(static_cast<size_t>(2 * (n + 1)));
+        b64_err_.ensure(1);
+        SR_CUDA_CHECK(cudaMemcpyAsync(b64_text_.ptr, b64_.text, static_cast<size_t>(chars),
+                                      cudaMemcpyHostToDevice, stream_));
+        SR_CUDA_CHECK(cudaMemcpyAsync(b64_off_.ptr, b64_.char_off, (n + 1) * sizeof(int64_t),
+                                      cudaMemcpyHostToDevice, stream_));
+        SR_CUDA_CHECK(cudaMemcpyAsync(b64_off_.ptr + n + 1, b64_.byte_off.data(),
+                                      (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
+        SR_CUDA_CHECK(cudaMemsetAsync(b64_err_.ptr, 0xff, sizeof(unsigned long long), stream_));
+        SR_CUDA_CHECK(srk::b64_decode(b64_text_.ptr, b64_off_.ptr, b64_off_.ptr + n + 1, n,
+                                      reinterpret_cast<uint8_t*>(p.soft.ptr + off * d),
+                                      b64_err_.ptr, stream_));
+      } else {
+        SR_CUDA_CHECK(cudaMemcpyAsync(p.soft.ptr + off * d, src.rows,
+                                      src.n_rows * d * sizeof(float), cudaMemcpyHostToDevice,
+                                      stream_));
+      }
       off += src.n_rows;
     }
   }
@@ -603,6 +623,100 @@ void Engine::score(const sr_request* reqs, int n_req, sr_result* res) {
   }
   run_plan(*p);
   fetch(*p, res, n_req);
+}
+
+void Engine::score_b64(const int32_t* prefix, int32_t t_q, const char* text,
+                       const int64_t* char_off, int32_t n_items, const int64_t* item_ids,
+                       sr_result* res) {
+  if (n_items <= 0) fail(SR_PAYLOAD_INVALID, "request needs a non-empty items[]");
+  const int64_t d = cfg_.d_model;
+  // Host-side checks in the reference's order per item (base64.cpp:60-64,
+  // 97-101; service.cpp:365-369); character / padding checks run on the device.
+  int bad = -1;
+  std::string bad_msg;
+  bool bad_before_chars = false;  // the length check precedes the character scan
+  std::vector<int32_t> rows_off(n_items + 1, 0);
+  std::vector<int64_t> byte_off(n_items + 1, 0);
+  for (int32_t j = 0; j < n_items && bad < 0; ++j) {
+    const int64_t len = char_off[j + 1] - char_off[j];
+    if (len % 4 != 0) {
+      bad = j;
+      bad_msg = "base64 length must be mod 4";
+      bad_before_chars = true;
+      break;
+    }
+    const char* e = text + char_off[j + 1];
+    const int pad = (len >= 1 && e[-1] == '=') + (len >= 2 && e[-2] == '=');
+    const int64_t bytes = len / 4 * 3 - pad;
+    if (bytes % 4 != 0) {
+      bad = j;
+      bad_msg = "payload is not a whole number of float32 values";
+      break;
+    }
+    const int64_t floats = bytes / 4;
+    if (floats == 0 || floats % d != 0) {
+      bad = j;
+      bad_msg = "embedding payload is not [n x " + std::to_string(d) + "] for item " +
+                std::to_string(item_ids != nullptr ? item_ids[j] : j);
+      break;
+    }
+    rows_off[j + 1] = rows_off[j] + static_cast<int32_t>(floats / d);
+    byte_off[j + 1] = byte_off[j] + bytes;
+  }
+  SR_CUDA_CHECK(cudaSetDevice(device_));
+  auto first_char_error = [&](int32_t upto) -> unsigned long long {
+    // validate-only pass over items [0, upto)
+    if (upto <= 0) return ~0ull;
+    const int64_t chars = char_off[upto];
+    b64_text_.ensure(static_cast<size_t>(std::max<int64_t>(chars, 4)));
+    b64_off_.ensure(static_cast<size_t>(2 * (upto + 1)));
+    b64_err_.ensure(1);
+    SR_CUDA_CHECK(cudaMemcpyAsync(b64_text_.ptr, text, static_cast<size_t>(chars),
+                                  cudaMemcpyHostToDevice, stream_));
+    SR_CUDA_CHECK(cudaMemcpyAsync(b64_off_.ptr, char_off, (upto + 1) * sizeof(int64_t),
+                                  cudaMemcpyHostToDevice, stream_));
+    SR_CUDA_CHECK(cudaMemsetAsync(b64_err_.ptr, 0xff, sizeof(unsigned long long), stream_));
+    SR_CUDA_CHECK(srk::b64_decode(b64_text_.ptr, b64_off_.ptr, b64_off_.ptr, upto, nullptr,
+                                  b64_err_.ptr, stream_));
+    unsigned long long err = ~0ull;
+    SR_CUDA_CHECK(cudaMemcpyAsync(&err, b64_err_.ptr, sizeof(err), cudaMemcpyDeviceToHost,
+                                  stream_));
+    SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    return err;
+  };
+  auto raise_char = [](unsigned long long err) {
+    fail(SR_PAYLOAD_INVALID, (err & 3u) == 1u ? "misplaced base64 padding"
+                                              : "invalid base64 character");
+  };
+  if (bad >= 0) {
+    const unsigned long long err = first_char_error(bad_before_chars ? bad : bad + 1);
+    if (err != ~0ull) raise_char(err);
+    fail(SR_PAYLOAD_INVALID, bad_msg);
+  }
+  // item_offsets index soft rows; the rows come from the base64 text
+  sr_request req{};
+  req.prefix_tokens = prefix;
+  req.t_q = t_q;
+  req.n_items = n_items;
+  req.item_offsets = rows_off.data();
+  req.item_tokens = nullptr;
+  req.item_rows = kB64Rows;
+  req.item_ids = item_ids;
+  req.mode = SR_MODE_MIXED;
+  b64_.text = text;
+  b64_.char_off = char_off;
+  b64_.byte_off = std::move(byte_off);
+  b64_.n = n_items;
+  try {
+    score(&req, 1, res);
+  } catch (...) {
+    b64_ = B64Src{};
+    throw;
+  }
+  b64_ = B64Src{};
+  unsigned long long err = ~0ull;
+  SR_CUDA_CHECK(cudaMemcpy(&err, b64_err_.ptr, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err != ~0ull) raise_char(err);  // results are discarded, as the reference never scores
 }
 
 void Engine::item_hidden(const sr_request& req, float* hidden_out) {

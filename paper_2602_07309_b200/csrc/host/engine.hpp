@@ -148,6 +148,11 @@ class Engine {
   // Scores + top-k through a cached plan (host buffers in, host buffers out).
   void score(const sr_request* reqs, int n_req, sr_result* res);
   void item_hidden(const sr_request& req, float* hidden_out);
+  // /score wire ingest (service.cpp:326-391): mixed-mode items given as
+  // base64 float32 payloads (concatenated text, char offsets [n+1]), decoded
+  // on the device into the soft-row buffer (kernels/wire.cu), then scored.
+  void score_b64(const int32_t* prefix, int32_t t_q, const char* text, const int64_t* char_off,
+                 int32_t n_items, const int64_t* item_ids, sr_result* res);
 
   // Sharded: local pass + NCCL all-gather of per-rank top-k + merge.
   void run_plan_sharded(Plan& p, struct Comm* comm);
@@ -181,6 +186,16 @@ class Engine {
   DevBuf<double> post_blocks_, post_w_;
   DevBuf<int32_t> post_task_;
   std::vector<double> last_final_;
+  // pending base64 source of the mixed request being packed (score_b64)
+  struct B64Src {
+    const char* text = nullptr;
+    const int64_t* char_off = nullptr;
+    std::vector<int64_t> byte_off;
+    int32_t n = 0;
+  } b64_;
+  DevBuf<uint8_t> b64_text_;
+  DevBuf<int64_t> b64_off_;
+  DevBuf<unsigned long long> b64_err_;
   std::vector<LayerDev> layers_;
   std::vector<void*> allocs_;
   // workspace

@@ -25,6 +25,10 @@
 
 namespace srh {
 
+// Marker for mixed-mode rows that arrive as base64 text (Engine::score_b64).
+inline const float kB64RowsTag = 0.f;
+#define kB64Rows (&::srh::kB64RowsTag)
+
 sr_flop_report flops(int mode, int64_t t_q, int64_t t_i, int64_t n_items);
 
 struct ItemView {
@@ -58,7 +62,7 @@ struct PackedBatch {
     const float* rows;
     size_t n_rows;
   };
-  std::vector<SoftSrc> soft_src;
+  std::vector<SoftSrc> soft_src;  // rows == kB64Rows: decoded on the device
   int32_t n_soft = 0;
 };
 

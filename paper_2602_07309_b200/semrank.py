@@ -238,6 +238,7 @@ class ScoreItem:
     tokens: Sequence[int] = ()
     embedding: Optional[np.ndarray] = None  # mixed mode: [n_emb_tokens x d_model]
     n_emb_tokens: int = 0
+    embedding_b64: Optional[str] = None  # wire form (decoded on the device)
 
 
 @dataclass
@@ -489,13 +490,30 @@ class ScoringEngine:
         return res
 
     def score(self, request: ScoreRequest, k: int = 0) -> ScoreResult:
-        pr = _PackedRequest(request, self.config.d_model)
         rb = _ResultBuf(len(request.items), len(self.task_names), k)
-        _check(_lib.sr_engine_score(self._h, C.byref(pr.c), C.byref(rb.c)))
+        if (ScoreMode(request.mode) == ScoreMode.Mixed and request.items
+                and all(it.embedding_b64 is not None for it in request.items)):
+            self._score_b64(request, rb)
+        else:
+            pr = _PackedRequest(request, self.config.d_model)
+            _check(_lib.sr_engine_score(self._h, C.byref(pr.c), C.byref(rb.c)))
         res = self._to_result(request, rb)
         if self._post:
             res.final_scores = self._final(len(request.items))
         return res
+
+    def _score_b64(self, request: ScoreRequest, rb: "_ResultBuf") -> None:
+        """embedding_b64 items: the base64 text goes to the device as is."""
+        parts = [it.embedding_b64.encode("ascii", "replace") for it in request.items]
+        off = np.zeros(len(parts) + 1, np.int64)
+        off[1:] = np.cumsum([len(p) for p in parts])
+        text = b"".join(parts)
+        prefix = np.ascontiguousarray(np.asarray(request.prefix_tokens, np.int32).reshape(-1))
+        ids = _item_doc_ids(request.items)
+        _check(_lib.sr_engine_score_b64(
+            self._h, prefix.ctypes.data_as(C.POINTER(C.c_int32)), len(prefix), text,
+            off.ctypes.data_as(C.POINTER(C.c_int64)), len(parts),
+            ids.ctypes.data_as(C.POINTER(C.c_int64)) if ids is not None else None, C.byref(rb.c)))
 
     def set_postprocess(self, calibration: Optional["CalibrationHead"] = None,
                         score_blend: Optional[Dict[str, float]] = None) -> None:
@@ -671,6 +689,50 @@ class BatchPlan(Plan):
 def score_by_mode(engine: ScoringEngine, request: ScoreRequest, k: int = 0) -> ScoreResult:
     """score_by_mode (engine.cpp:379-387): dispatch on request.mode."""
     return engine.score(request, k)
+
+
+def tokenize(text: str, max_seq: int = 4096) -> List[int]:
+    """Byte tokenizer (tokenizer.cpp:10-20)."""
+    data = text.encode("utf-8")
+    if len(data) > max_seq:
+        raise SemrankError(ErrorCode.LengthOverflow,
+                           f"text of {len(data)} bytes exceeds max_seq {max_seq}")
+    return list(data)
+
+
+def parse_score_request_json(body: str, d_model: int, max_seq: int = 4096) -> ScoreRequest:
+    """The /score wire format (service.cpp:326-372); embedding_b64 items keep
+    their base64 text, which ScoringEngine.score decodes on the device."""
+    import json
+    try:
+        j = json.loads(body)
+    except ValueError as e:
+        raise SemrankError(ErrorCode.PayloadInvalid, f"request body is not JSON: {e}")
+    req = ScoreRequest(request_id=j.get("request_id", ""))
+    if "prefix_tokens" in j:
+        req.prefix_tokens = [int(t) for t in j["prefix_tokens"]]
+    elif "prefix_text" in j:
+        req.prefix_tokens = tokenize(j["prefix_text"], max_seq)
+    else:
+        raise SemrankError(ErrorCode.PayloadInvalid, "request needs prefix_text or prefix_tokens")
+    req.mode = score_mode_from_name(j.get("mode", "ibpc"))
+    req.latency_sensitive = bool(j.get("latency_sensitive", False))
+    items = j.get("items")
+    if not isinstance(items, list) or not items:
+        raise SemrankError(ErrorCode.PayloadInvalid, "request needs a non-empty items[]")
+    for it in items:
+        item = ScoreItem(id=it.get("id", ""))
+        if "tokens" in it:
+            item.tokens = [int(t) for t in it["tokens"]]
+        elif "text" in it:
+            item.tokens = tokenize(it["text"], max_seq)
+        elif "embedding_b64" in it:
+            item.embedding_b64 = it["embedding_b64"]
+        else:
+            raise SemrankError(ErrorCode.PayloadInvalid,
+                               f"item needs text, tokens, or embedding_b64: {item.id}")
+        req.items.append(item)
+    return req
 
 
 def topk_host(scores: np.ndarray, ids: Optional[np.ndarray], k: int):

@@ -205,3 +205,26 @@ def test_calibration_oracle_matches_reference_golden():
     F = lambda k: np.array([float(x) for x in g[k]])
     got = O.oracle_final_scores(F("raws")[:, None], F("lo"), F("hi"), F("value"))
     assert np.array_equal(got, F("calibrated"))
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built (no /root/reference)")
+def test_wire_golden_reproduces_on_reference():
+    """tests/golden/wire_b64.json is what the reference's decode_f32_base64 says."""
+    import base64 as b64
+    with open(os.path.join(os.path.dirname(__file__), "golden", "wire_b64.json")) as f:
+        cases = json.load(f)["cases"]
+    for c in cases:
+        out, st, msg = O.ref_decode_f32_base64(c["text"])
+        assert (st, msg) == (c["status"], c["message"])
+        if st == 0:
+            assert np.array_equal(out, np.frombuffer(b64.b64decode(c["floats"]), np.float32))
+
+
+def test_wire_golden_valid_payloads_are_standard_base64():
+    import base64 as b64
+    with open(os.path.join(os.path.dirname(__file__), "golden", "wire_b64.json")) as f:
+        cases = json.load(f)["cases"]
+    for c in cases:
+        if c["status"] == 0 and c["text"]:
+            want = np.frombuffer(b64.b64decode(c["floats"]), np.float32)
+            assert np.array_equal(np.frombuffer(b64.b64decode(c["text"]), np.float32), want)
