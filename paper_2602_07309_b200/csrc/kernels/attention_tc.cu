@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto epilogue = [&](const Pending& e) {
       // Row sum of both halves, O / l -> bf16 -> HBM.
       fin[half * 128 + r] = e.l;
-      named_bar_sync(1, kSoftmaxThreads);
+      named_bar_sync(1 + quad, 64);  // the two warps of this row quadrant
       const float lsum = e.l + fin[(half ^ 1) * 128 + r];
       mbar_wait(&pv_done[e.g_last & 1], (e.g_last >> 1) & 1);
       tc_fence_after();
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       fence_proxy_async_smem();
-      if constexpr (HD < 128) named_bar_sync(1, kSoftmaxThreads);  // halves share a box
+      if constexpr (HD < 128) named_bar_sync(1 + quad, 64);  // halves share a box
       else __syncwarp();
       tc_fence_before();
       mbar_arrive(&o_empty[e.li & 1]);
@@ -383,13 +383,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (warp == 2 && lane == 0 && g < 24) SRK_TRACE(1 + g);
         tc_fence_after();
         float s[kHalf];
+        {
+          // both 32-column loads in flight, one wait
+          uint32_t v[kHalf];
 #pragma unroll
-        for (int cc = 0; cc < kHalf / 32; ++cc) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem + lane_off + sb * kBK + half * kHalf + cc * 32, v);
+          for (int cc = 0; cc < kHalf / 32; ++cc)
+            tmem_ld_32x32b_x32(tmem + lane_off + sb * kBK + half * kHalf + cc * 32,
+                               *reinterpret_cast<uint32_t(*)[32]>(&v[cc * 32]));
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) s[cc * 32 + i] = __uint_as_float(v[i]);
+          for (int i = 0; i < kHalf; ++i) s[i] = __uint_as_float(v[i]);
         }
         // Visible iff in [kb, ke) and in ([pb, pe) U [ss, row]).
         const int a_lo = max(kb, sp.prefix_begin), a_hi = min(ke, sp.prefix_end);
@@ -433,11 +436,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             mx = fmaxf(ma, mb);
           }
         }
-        // Pair max exchange (double-buffered by block parity). The barrier also
-        // orders both halves' S reads before either writes P over S.
+        // Pair max exchange (double-buffered by block parity). Only the two
+        // warps sharing this row quadrant meet (named barrier 1 + quad, 64
+        // threads), not all eight; the barrier also orders both halves' S
+        // reads before either writes P over S (same TMEM lanes).
         float* slot = red + (g & 1) * 256;
         slot[half * 128 + r] = mx;
-        named_bar_sync(1, kSoftmaxThreads);
+        named_bar_sync(1 + quad, 64);
         mx = fmaxf(mx, slot[(half ^ 1) * 128 + r]);
 
         const bool move =
