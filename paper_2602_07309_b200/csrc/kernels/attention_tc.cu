@@ -40,10 +40,25 @@ namespace {
 
 constexpr int kTM = 128;     // query rows per tile (UMMA M)
 constexpr int kBK = 128;     // keys per block (UMMA N of S, K of PV)
-constexpr int kHalf = 64;    // keys per softmax thread per block
 constexpr int kBox = 16384;  // 128 rows x 128 B swizzle box
-constexpr int kThreads = 320;
-constexpr int kSoftmaxThreads = 256;
+// Softmax threads per query row: each of the SL warps of a TMEM lane quadrant
+// owns kBK / SL keys of every block. SL = 2 (8 softmax warps). SL = 4
+// (-DSRK_ATTN_SLICES=4, 16 softmax warps, 576 threads) was built to hide more
+// MUFU / TMEM latency but measured 2x slower at C2 (218k vs 112k cycles per
+// CTA): the per-row overhead (masks, exchange, barrier, hand-off) is paid by
+// twice as many threads, and at 576 threads ptxas caps registers at 96 (spills).
+#ifndef SRK_ATTN_SLICES
+#define SRK_ATTN_SLICES 2
+#endif
+template <int HD>
+struct Slices {
+  static constexpr int SL = HD == 128 ? SRK_ATTN_SLICES : 2;
+  static constexpr int KEYS = kBK / SL;        // keys per softmax thread per block
+  static constexpr int SOFTMAX = 128 * SL;     // softmax threads
+  static constexpr int THREADS = 64 + SOFTMAX; // + TMA warp + MMA warp
+  static constexpr int OCOLS = HD / SL;        // O columns per softmax thread
+};
+constexpr int kThreads = 320;  // attn_pp_kernel (kPPThreads) and helpers
 constexpr float kRescaleLog2 = 8.0f;  // rescale O only when the max grows by > 2^8
 
 template <int HD>
@@ -54,7 +69,8 @@ struct AttnCfg {
   static constexpr int K_OFF = Q_OFF + 2 * TILE;  // 2 stages
   static constexpr int V_OFF = K_OFF + 2 * TILE;  // 2 stages
   static constexpr int RED_OFF = V_OFF + 2 * TILE;
-  static constexpr int BAR_OFF = RED_OFF + 3 * 2 * 128 * 4;  // slots: parity 0/1, final sum
+  // slots: max exchange by block parity (2 x SL x 128) + row sums (SL x 128)
+  static constexpr int BAR_OFF = RED_OFF + 3 * Slices<HD>::SL * 128 * 4;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static constexpr int O_COL = 2 * kBK;  // O buffer b at O_COL + b * 128
   static constexpr int TMEM_COLS = 512;
@@ -126,12 +142,15 @@ struct Cursor {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv,
                    const __grid_constant__ CUtensorMap tm_out, const RowSpan* __restrict__ spans,
                    const AttnTile* __restrict__ tiles, int n_tiles, __nv_bfloat16* __restrict__ out,
                    int n_heads) {
   using C = AttnCfg<HD>;
+  constexpr int SL = Slices<HD>::SL, KEYS = Slices<HD>::KEYS, OCOLS = Slices<HD>::OCOLS;
+  constexpr int kSoftmaxThreads = Slices<HD>::SOFTMAX;
+  static_assert(OCOLS % 32 == 0 && KEYS % 32 == 0, "slice layout");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // Align inside the shared window without leaving the shared address space.
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -161,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tm_qkv);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&q_full[s], 1);
-      mbar_init(&q_empty[s], 8);  // one arrival per softmax warp after its O store
+      mbar_init(&q_empty[s], kSoftmaxThreads / 32);  // per softmax warp after its O store
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
       mbar_init(&v_full[s], 1);
@@ -278,12 +297,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ---------------------------------------------------------- softmax
-    const int quad = warp & 3;         // TMEM lane quadrant of this warp
-    const int half = (warp - 2) >> 2;  // 0: keys 0-63, 1: keys 64-127 of a block
-    const int r = quad * 32 + lane;    // tile row owned by this thread (shared with a partner)
+    const int quad = warp & 3;          // TMEM lane quadrant of this warp
+    const int slice = (warp - 2) >> 2;  // keys [slice * KEYS, +KEYS) of every block
+    const int r = quad * 32 + lane;     // tile row owned by this thread (with SL-1 partners)
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const float scale_log2 = 1.4426950408889634f * rsqrtf(static_cast<float>(HD));
-    float* fin = red + 2 * 256;
+    float* fin = red + 2 * SL * 128;
+    const uint32_t qbar = 1 + quad, qbar_n = 32 * SL;  // the SL warps of this quadrant
     Cursor c;
     c.next_item(tiles, n_tiles, n_items, blockIdx.x);
     int g = 0;
@@ -301,10 +321,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       float l = 0.f;
     } pend;
     auto epilogue = [&](const Pending& e) {
-      // Row sum of both halves, O / l -> bf16 -> HBM.
-      fin[half * 128 + r] = e.l;
-      named_bar_sync(1 + quad, 64);  // the two warps of this row quadrant
-      const float lsum = e.l + fin[(half ^ 1) * 128 + r];
+      // Row sum over the slices (fixed order: identical in every slice), O / l
+      // -> bf16 -> HBM.
+      fin[slice * 128 + r] = e.l;
+      named_bar_sync(qbar, qbar_n);
+      float lsum = 0.f;
+#pragma unroll
+      for (int k = 0; k < SL; ++k) lsum += fin[k * 128 + r];
       mbar_wait(&pv_done[e.g_last & 1], (e.g_last >> 1) & 1);
       tc_fence_after();
       const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
@@ -315,15 +338,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       // their live rows directly so neighbouring tiles are never touched.
       uint8_t* qbuf = sQ + (e.li & 1) * C::TILE;
       const bool slab_live = __all_sync(0xffffffff, e.live);
+      constexpr int CW = OCOLS < 32 ? OCOLS : 32;  // columns per TMEM load
 #pragma unroll 1
-      for (int cc = 0; cc < HD / 64; ++cc) {
+      for (int cc = 0; cc < OCOLS / CW; ++cc) {
         uint32_t v[32];
-        const int col = half * (HD / 2) + cc * 32;
-        tmem_ld_32x32b_x32(tmem + lane_off + C::O_COL + (e.li & 1) * 128 + col, v);
+        const int col = slice * OCOLS + cc * CW;
+        if constexpr (CW == 32)
+          tmem_ld_32x32b_x32(tmem + lane_off + C::O_COL + (e.li & 1) * 128 + col, v);
+        else
+          tmem_ld_32x32b_x16(tmem + lane_off + C::O_COL + (e.li & 1) * 128 + col,
+                             *reinterpret_cast<uint32_t(*)[16]>(v));
         tmem_ld_wait();
         uint4 pk[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < CW / 8; ++q) {
           const float* f = reinterpret_cast<const float*>(&v[q * 8]);
           pk[q] = make_uint4(pack_bf16x2(f[0] * inv, f[1] * inv), pack_bf16x2(f[2] * inv, f[3] * inv),
                              pack_bf16x2(f[4] * inv, f[5] * inv), pack_bf16x2(f[6] * inv, f[7] * inv));
@@ -331,27 +359,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (slab_live) {
           uint8_t* rowp = qbuf + (col >> 6) * kBox + r * 128;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < CW / 8; ++q) {
             const int chunk = ((col & 63) >> 3) + q;
             *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) * 16)) = pk[q];
           }
         } else if (e.live) {
           uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * d + e.h * HD + col);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) dst[q] = pk[q];
+          for (int q = 0; q < CW / 8; ++q) dst[q] = pk[q];
         }
       }
       fence_proxy_async_smem();
-      if constexpr (HD < 128) named_bar_sync(1 + quad, 64);  // halves share a box
+      // A 64-column box is written by 64 / OCOLS slices: they meet before the
+      // first of them stores it.
+      constexpr int SPB = 64 / OCOLS > 1 ? 64 / OCOLS : 1;  // slices per box
+      if constexpr (SPB > 1) named_bar_sync(qbar, qbar_n);
       else __syncwarp();
       tc_fence_before();
       mbar_arrive(&o_empty[e.li & 1]);
       if (lane == 0) {
-        // HD=128: warp (quad, half) owns box `half` rows [32 quad, +32).
-        // HD=64 : both halves wrote box 0; the half-0 warp stores it.
-        if (slab_live && (HD == 128 || half == 0))
-          tma_store_2d(&tm_out, qbuf + (HD == 128 ? half : 0) * kBox + quad * 32 * 128,
-                       e.h * HD + (HD == 128 ? half : 0) * 64, e.row0 + quad * 32);
+        // warp (quad, slice) with slice % SPB == 0 stores box slice / SPB of
+        // rows [32 quad, +32)
+        if (slab_live && slice % SPB == 0)
+          tma_store_2d(&tm_out, qbuf + (slice / SPB) * kBox + quad * 32 * 128,
+                       e.h * HD + (slice / SPB) * 64, e.row0 + quad * 32);
         bulk_commit();
         // Hand the Q buffer back once the store has read it: the producer
         // needs it for item li + 2, which may be the very next block (an
@@ -378,34 +409,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         int k0, kb, ke;
         c.range(k0, kb, ke);
         const int sb = g & 1;
-        const int kh = k0 + half * kHalf;  // first key of this thread's slice
+        const int kh = k0 + slice * KEYS;  // first key of this thread's slice
         mbar_wait(&s_full[sb], (g >> 1) & 1);
         if (warp == 2 && lane == 0 && g < 24) SRK_TRACE(1 + g);
         tc_fence_after();
-        float s[kHalf];
+        float s[KEYS];
         {
-          // both 32-column loads in flight, one wait
-          uint32_t v[kHalf];
+          // all 32-column loads of the slice in flight, one wait
+          uint32_t v[KEYS];
 #pragma unroll
-          for (int cc = 0; cc < kHalf / 32; ++cc)
-            tmem_ld_32x32b_x32(tmem + lane_off + sb * kBK + half * kHalf + cc * 32,
+          for (int cc = 0; cc < KEYS / 32; ++cc)
+            tmem_ld_32x32b_x32(tmem + lane_off + sb * kBK + slice * KEYS + cc * 32,
                                *reinterpret_cast<uint32_t(*)[32]>(&v[cc * 32]));
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < kHalf; ++i) s[i] = __uint_as_float(v[i]);
+          for (int i = 0; i < KEYS; ++i) s[i] = __uint_as_float(v[i]);
         }
         // Visible iff in [kb, ke) and in ([pb, pe) U [ss, row]).
         const int a_lo = max(kb, sp.prefix_begin), a_hi = min(ke, sp.prefix_end);
         const int b_lo = max(kb, sp.span_start), b_hi = min(ke, row + 1);
-        const bool full = live && ((kh >= a_lo && kh + kHalf <= a_hi) ||
-                                   (kh >= b_lo && kh + kHalf <= b_hi));
+        const bool full = live && ((kh >= a_lo && kh + KEYS <= a_hi) ||
+                                   (kh >= b_lo && kh + KEYS <= b_hi));
         float mx = -INFINITY;
         bool warp_empty = false;  // no visible key in this slice for any row of the warp
         if (__all_sync(0xffffffff, full)) {
           // two independent FMNMX3 chains
           float ma = -INFINITY, mb = -INFINITY;
 #pragma unroll
-          for (int i = 0; i < kHalf; i += 4) {
+          for (int i = 0; i < KEYS; i += 4) {
             ma = fmax3f(ma, s[i], s[i + 1]);
             mb = fmax3f(mb, s[i + 2], s[i + 3]);
           }
@@ -413,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           auto ivl = [&](int lo, int hi) -> uint64_t {
             lo = max(lo - kh, 0);
-            hi = min(hi - kh, kHalf);
+            hi = min(hi - kh, KEYS);
             if (!live || hi <= lo) return 0ull;
             const uint64_t upto_hi = hi >= 64 ? ~0ull : ((1ull << hi) - 1ull);
             return upto_hi & ~((1ull << lo) - 1ull);
@@ -423,13 +454,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!warp_empty) {
             const uint32_t v0 = static_cast<uint32_t>(vis), v1 = static_cast<uint32_t>(vis >> 32);
 #pragma unroll
-            for (int i = 0; i < kHalf; ++i) {
+            for (int i = 0; i < KEYS; ++i) {
               const bool ok = ((i < 32 ? v0 : v1) >> (i & 31)) & 1u;
               s[i] = ok ? s[i] : -INFINITY;
             }
             float ma = -INFINITY, mb = -INFINITY;
 #pragma unroll
-            for (int i = 0; i < kHalf; i += 4) {
+            for (int i = 0; i < KEYS; i += 4) {
               ma = fmax3f(ma, s[i], s[i + 1]);
               mb = fmax3f(mb, s[i + 2], s[i + 3]);
             }
@@ -440,10 +471,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // warps sharing this row quadrant meet (named barrier 1 + quad, 64
         // threads), not all eight; the barrier also orders both halves' S
         // reads before either writes P over S (same TMEM lanes).
-        float* slot = red + (g & 1) * 256;
-        slot[half * 128 + r] = mx;
-        named_bar_sync(1 + quad, 64);
-        mx = fmaxf(mx, slot[(half ^ 1) * 128 + r]);
+        float* slot = red + (g & 1) * SL * 128;
+        slot[slice * 128 + r] = mx;
+        named_bar_sync(qbar, qbar_n);
+#pragma unroll
+        for (int k = 0; k < SL; ++k) mx = fmaxf(mx, slot[k * 128 + r]);
 
         const bool move =
             mx > m_used && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2);
@@ -455,9 +487,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float corr = move ? ex2_approx((m_used - m_new) * scale_log2) : 1.f;
           l *= corr;
 #pragma unroll 1
-          for (int cc = 0; cc < HD / 64; ++cc) {
+          for (int cc = 0; cc < OCOLS / 32; ++cc) {
             uint32_t v[32];
-            const uint32_t a = tmem + lane_off + C::O_COL + (li & 1) * 128 + half * (HD / 2) + cc * 32;
+            const uint32_t a = tmem + lane_off + C::O_COL + (li & 1) * 128 + slice * OCOLS + cc * 32;
             tmem_ld_32x32b_x32(a, v);
             tmem_ld_wait();
 #pragma unroll
@@ -468,10 +500,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         m_used = m_new;
         const float base = m_used == -INFINITY ? 0.f : m_used * scale_log2;
         float rs = 0.f;
-        uint32_t pk[32];
+        uint32_t pk[KEYS / 2];
         if (warp_empty) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) pk[i] = 0u;
+          for (int i = 0; i < KEYS / 2; ++i) pk[i] = 0u;
         } else {
           // Packed fp32x2 scale-subtract and row sums (FFMA2 / FADD2), MUFU
           // exponentials: the softmax is issue-bound (ncu: 41% issue active,
@@ -480,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t sc2 = f32x2(scale_log2, scale_log2), nb2 = f32x2(-base, -base);
           uint64_t acc0 = f32x2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
-          for (int i = 0; i < kHalf; i += 2) {
+          for (int i = 0; i < KEYS; i += 2) {
             float a0, a1;
             f32x2_split(fma_f32x2(f32x2(s[i], s[i + 1]), sc2, nb2), a0, a1);
             const float p0 = ex2_approx(a0);
@@ -495,8 +527,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           rs = (r0 + r1) + (r2 + r3);
         }
         l += rs;
-        // P (bf16x2) over this half's 32 columns of the consumed S buffer.
-        tmem_st_32x32b_x32(tmem + lane_off + sb * kBK + half * 32, pk);
+        // P (bf16x2) over this slice's KEYS / 2 columns of the consumed S buffer
+        // (columns of slices <= this one, already read: the quadrant barrier).
+        if constexpr (KEYS == 64)
+          tmem_st_32x32b_x32(tmem + lane_off + sb * kBK + slice * 32, pk);
+        else
+          tmem_st_32x32b_x16(tmem + lane_off + sb * kBK + slice * (KEYS / 2),
+                             *reinterpret_cast<uint32_t(*)[16]>(pk));
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
@@ -548,7 +585,7 @@ cudaError_t launch_tc(const CUtensorMap& tm, const RowSpan* spans, const AttnTil
   cudaGetDevice(&dev);
   const int items = n_tiles * n_heads;
   const int grid = items < num_sms(dev) ? items : num_sms(dev);
-  return launch_k(kern, dim3(grid), dim3(kThreads), C::SMEM, stream, tm, tm_out, spans, tiles,
+  return launch_k(kern, dim3(grid), dim3(Slices<HD>::THREADS), C::SMEM, stream, tm, tm_out, spans, tiles,
                   n_tiles, out, n_heads);
 }
 
