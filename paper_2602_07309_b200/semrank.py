@@ -357,7 +357,7 @@ def request_report(config: ModelConfig, request: ScoreRequest):
 
 def _item_doc_ids(items: Sequence[ScoreItem]) -> Optional[np.ndarray]:
     try:
-        return np.array([int(it.id) for it in items], np.int64)
+        return np.fromiter(map(int, (it.id for it in items)), np.int64, len(items))
     except (TypeError, ValueError):
         return None
 
@@ -390,6 +390,37 @@ def _adjacent_rows(items) -> np.ndarray:
         [np.asarray(a, np.float32).reshape(-1) for a in arrs]))
 
 
+class _LazyItemScores(Sequence):
+    """ScoreResult.items (engine.hpp:46-51): built on first access from the
+    score matrix, so callers that only need the top-k or the matrix do not
+    pay for n_items Python dicts per call."""
+
+    def __init__(self, ids, scores, names):
+        self._ids, self._scores, self._names, self._items = ids, scores, names, None
+
+    def _build(self):
+        if self._items is None:
+            names = self._names
+            self._items = [ItemScores(i, dict(zip(names, row)))
+                           for i, row in zip(self._ids, self._scores.tolist())]
+        return self._items
+
+    def __len__(self):
+        return len(self._ids)
+
+    def __getitem__(self, i):
+        return self._build()[i]
+
+    def __iter__(self):
+        return iter(self._build())
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+    def __repr__(self):
+        return repr(self._build())
+
+
 class _PackedRequest:
     """Flattened sr_request; keeps the numpy buffers alive."""
 
@@ -397,7 +428,7 @@ class _PackedRequest:
         self.prefix = np.ascontiguousarray(np.asarray(req.prefix_tokens, np.int32).reshape(-1))
         mixed = ScoreMode(req.mode) == ScoreMode.Mixed
         lens = []
-        for it in req.items:
+        for it in (req.items if mixed else ()):
             if mixed:
                 n = it.n_emb_tokens
                 emb = np.asarray(it.embedding if it.embedding is not None else [], np.float32)
@@ -407,15 +438,17 @@ class _PackedRequest:
                 lens.append(n)
             else:
                 lens.append(len(it.tokens))
+        if not mixed:
+            lens = list(map(len, (it.tokens for it in req.items)))
         self.offsets = np.zeros(len(req.items) + 1, np.int32)
         self.offsets[1:] = np.cumsum(lens) if lens else []
         if mixed:
             self.rows = _adjacent_rows(req.items) if req.items else np.zeros(1, np.float32)
             self.tokens = np.zeros(1, np.int32)
         else:
-            self.tokens = np.ascontiguousarray(np.concatenate(
-                [np.asarray(it.tokens, np.int32).reshape(-1) for it in req.items])
-                if req.items else np.zeros(1, np.int32))
+            toks = [it.tokens for it in req.items]
+            self.tokens = (np.ascontiguousarray(np.concatenate(toks).astype(np.int32, copy=False))
+                           if toks and sum(lens) > 0 else np.zeros(1, np.int32))
             self.rows = None
         self.ids = item_ids if item_ids is not None else _item_doc_ids(req.items)
         I = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))
@@ -481,9 +514,7 @@ class ScoringEngine:
                           flops=FlopReport._from_c(rb.c.flops),
                           kv_incremental_per_item=rb.c.kv_incremental_per_item,
                           scores=rb.scores[:n].copy())
-        for i, it in enumerate(req.items):
-            res.items.append(ItemScores(it.id, {t: float(rb.scores[i, j])
-                                                for j, t in enumerate(self.task_names)}))
+        res.items = _LazyItemScores([it.id for it in req.items], res.scores, self.task_names)
         for j in range(rb.c.k_returned):
             res.topk.append((req.items[int(rb.idx[j])].id if rb.idx[j] >= 0 else str(rb.ids[j]),
                              float(rb.top[j])))
