@@ -443,8 +443,8 @@ void Engine::profile(Plan& p, int reps, float* ms_out, int32_t* launches_out) {
 }
 
 namespace {
-template <typename T>
-void put(DevBuf<T>& b, const std::vector<T>& v, cudaStream_t s) {
+template <typename T, typename A>
+void put(DevBuf<T>& b, const std::vector<T, A>& v, cudaStream_t s) {
   b.ensure(std::max<size_t>(v.size(), 1));
   if (!v.empty())
     SR_CUDA_CHECK(cudaMemcpyAsync(b.ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
@@ -554,8 +554,10 @@ void Engine::run_plan(Plan& p) {
 void Engine::fetch(Plan& p, sr_result* res, int n_req) {
   const auto& pk = p.pack;
   const int T = n_tasks();
-  std::vector<double> scores(static_cast<size_t>(pk.n_items) * T);
-  std::vector<srk::TopkEntry> top(static_cast<size_t>(n_req) * std::max(p.k, 0));
+  auto& scores = p.h_scores;
+  auto& top = p.h_top;
+  scores.resize(static_cast<size_t>(pk.n_items) * T);
+  top.resize(static_cast<size_t>(n_req) * std::max(p.k, 0));
   SR_CUDA_CHECK(cudaMemcpyAsync(scores.data(), p.scores.ptr, scores.size() * sizeof(double),
                                 cudaMemcpyDeviceToHost, stream_));
   if (post_on_) {

@@ -110,6 +110,8 @@ struct Plan {
   DevBuf<double> final;  // post-processed ranking key (set_postprocess)
   DevBuf<srk::TopkEntry> topk_scratch, topk_out;
   DevBuf<srk::TopkEntry> gathered, merged;  // sharded merge
+  pinned_vector<double> h_scores;           // fetch staging (page-locked)
+  pinned_vector<srk::TopkEntry> h_top;
   // graph
   cudaGraphExec_t graph = nullptr;
   int32_t launches = 0;

@@ -18,7 +18,12 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
+#include <mutex>
+#include <new>
 #include <vector>
+
+#include <cuda_runtime.h>
 
 #include "../kernels/launch.h"
 #include "model.hpp"
@@ -44,17 +49,65 @@ std::vector<int32_t> validate_request(const ModelConfig& cfg, const sr_request& 
 void report_for(const ModelConfig& cfg, const sr_request& req, const std::vector<int32_t>& lens,
                 sr_flop_report* flops_out, double* kv_out);
 
+// Page-locked host storage for the packed arrays, so their uploads are
+// asynchronous DMA (no driver staging copy per array); plain heap memory
+// when no device is present (host-only tests).
+template <typename T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <typename U>
+  PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();  // clear: fall back to pageable memory
+      p = std::malloc(n * sizeof(T));
+      if (p == nullptr) throw std::bad_alloc();
+      std::lock_guard<std::mutex> lock(registry_mu());
+      pageable_registry().push_back(p);
+    }
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t) {
+    {
+      std::lock_guard<std::mutex> lock(registry_mu());
+      auto& reg = pageable_registry();
+      for (auto& q : reg)
+        if (q == p) {
+          q = reg.back();
+          reg.pop_back();
+          std::free(p);
+          return;
+        }
+    }
+    cudaFreeHost(p);
+  }
+  static std::vector<void*>& pageable_registry() {
+    static std::vector<void*> r;
+    return r;
+  }
+  static std::mutex& registry_mu() {
+    static std::mutex m;
+    return m;
+  }
+  bool operator==(const PinnedAlloc&) const { return true; }
+  bool operator!=(const PinnedAlloc&) const { return false; }
+};
+template <typename T>
+using pinned_vector = std::vector<T, PinnedAlloc<T>>;
+
 struct PackedBatch {
   int32_t M = 0;                       // packed rows
   int32_t n_items = 0;                 // items over all requests
   int32_t max_seg_len = 0;             // longest request (items)
-  std::vector<int32_t> row_src;        // token id, or -(1 + soft row index)
-  std::vector<int32_t> row_pos;        // positional-embedding index
-  std::vector<srk::RowSpan> spans;     // attention mask per row
-  std::vector<srk::AttnTile> tiles;    // attention work tiles
-  std::vector<int32_t> last_rows;      // per item: packed row scored
-  std::vector<int64_t> ids;            // per item: doc id for the tie rule
-  std::vector<int32_t> seg_off;        // per request: item offsets [n_req + 1]
+  pinned_vector<int32_t> row_src;      // token id, or -(1 + soft row index)
+  pinned_vector<int32_t> row_pos;      // positional-embedding index
+  pinned_vector<srk::RowSpan> spans;   // attention mask per row
+  pinned_vector<srk::AttnTile> tiles;  // attention work tiles
+  pinned_vector<int32_t> last_rows;    // per item: packed row scored
+  pinned_vector<int64_t> ids;          // per item: doc id for the tie rule
+  pinned_vector<int32_t> seg_off;      // per request: item offsets [n_req + 1]
   // mixed-mode rows [R x d]: not copied on the host — each request's item
   // rows are already contiguous (item_offsets index them in order), so the
   // engine copies them straight from the caller's buffer into HBM.
