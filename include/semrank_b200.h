@@ -127,6 +127,7 @@ typedef struct sr_engine sr_engine;
 typedef struct sr_comm sr_comm;
 typedef struct sr_plan sr_plan;
 typedef struct sr_corpus sr_corpus;
+typedef struct sr_wire sr_wire;
 
 /* ------------------------------------------------------------ diagnostics */
 const char* sr_last_error(void);
@@ -249,6 +250,19 @@ int32_t sr_plan_run_sharded(sr_plan* p, sr_comm* c); /* resident variant */
 int32_t sr_engine_score_b64(sr_engine* e, const int32_t* prefix, int32_t t_q, const char* text,
                             const int64_t* char_off, int32_t n_items, const int64_t* item_ids,
                             sr_result* res);
+
+/* Native /score body parser (parse_score_request_json, service.cpp:326-372):
+ * one pass over the JSON; embedding_b64 payloads stay spans into `body`
+ * (which must outlive the handle) and are decoded on the device by
+ * sr_engine_score_wire. Errors as the reference (SR_PAYLOAD_INVALID,
+ * SR_LENGTH_OVERFLOW for text > max_seq, SR_PARAMETER for an unknown mode).
+ * Item ids that are all integers become the top-k doc ids. */
+int32_t sr_wire_parse(const char* body, int64_t len, int32_t max_seq, sr_wire** out);
+void sr_wire_destroy(sr_wire* w);
+int32_t sr_wire_info(const sr_wire* w, int32_t* n_items, int32_t* mode, int32_t* t_q);
+const char* sr_wire_request_id(const sr_wire* w);
+const char* sr_wire_item_id(const sr_wire* w, int32_t i);
+int32_t sr_engine_score_wire(sr_engine* e, const sr_wire* w, sr_result* res);
 
 /* ------------------------------ service post-processing
  * The step after scoring in SearchService::handle_search (service.cpp:242-277):

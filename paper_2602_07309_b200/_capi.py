@@ -101,6 +101,12 @@ _sig("sr_comm_destroy", None, vp)
 _sig("sr_engine_score_sharded", i32, vp, vp, P(RequestC), P(ResultC))
 _sig("sr_plan_run_sharded", i32, vp, vp)
 _sig("sr_engine_score_b64", i32, vp, P(i32), i32, C.c_char_p, P(i64), i32, P(i64), P(ResultC))
+_sig("sr_wire_parse", i32, C.c_char_p, i64, i32, P(vp))
+_sig("sr_wire_destroy", None, vp)
+_sig("sr_wire_info", i32, vp, P(i32), P(i32), P(i32))
+_sig("sr_wire_request_id", C.c_char_p, vp)
+_sig("sr_wire_item_id", C.c_char_p, vp, i32)
+_sig("sr_engine_score_wire", i32, vp, vp, P(ResultC))
 _sig("sr_engine_set_postprocess", i32, vp, P(f64), P(f64), P(f64), i32, P(i32), P(f64), i32)
 _sig("sr_engine_final_scores", i32, vp, P(f64), i32, P(i32))
 _sig("sr_corpus_create", i32, vp, vp, vp, i64, i32, i32, i32, P(vp))
@@ -131,7 +137,8 @@ HEADER_SYMBOLS = [
     "sr_plan_create_batch", "sr_plan_fetch_batch", "sr_plan_run", "sr_plan_sync", "sr_plan_fetch", "sr_plan_kernel_count", "sr_plan_destroy",
     "sr_plan_profile", "sr_plan_shape",
     "sr_nccl_unique_id", "sr_comm_create", "sr_comm_destroy", "sr_engine_score_sharded",
-    "sr_plan_run_sharded", "sr_engine_score_b64", "sr_engine_set_postprocess", "sr_engine_final_scores", "sr_corpus_create", "sr_corpus_destroy", "sr_corpus_topk",
+    "sr_plan_run_sharded", "sr_engine_score_b64", "sr_wire_parse", "sr_wire_destroy",
+    "sr_wire_info", "sr_wire_request_id", "sr_wire_item_id", "sr_engine_score_wire", "sr_engine_set_postprocess", "sr_engine_final_scores", "sr_corpus_create", "sr_corpus_destroy", "sr_corpus_topk",
     "sr_corpus_topk_sharded", "sr_corpus_last_candidates", "sr_corpus_last_scan_ms",
     "sr_kernel_gemm", "sr_kernel_gemm_ln", "sr_kernel_attention", "sr_kernel_layernorm",
     "sr_kernel_topk", "sr_debug_attention_trace", "sr_debug_gemm_trace",

@@ -2,12 +2,14 @@
 // srh::Error to sr_status and keep a thread-local error message.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
 
 #include "host/engine.hpp"
 #include "host/retrieval.hpp"
+#include "host/wire.hpp"
 #include "host/model.hpp"
 #include "host/planner.hpp"
 #include "kernels/launch.h"
@@ -47,6 +49,12 @@ struct sr_engine {
 
 struct sr_comm {
   srh::Comm* c = nullptr;
+};
+
+struct sr_wire {
+  srh::WireRequest w;
+  std::vector<int64_t> ids;  // item ids as doc ids when every id is an integer
+  bool numeric_ids = false;
 };
 
 struct sr_corpus {
@@ -356,6 +364,85 @@ int32_t sr_engine_score_b64(sr_engine* e, const int32_t* prefix, int32_t t_q, co
       srh::fail(SR_SPEC_VIOLATION, "null argument");
     std::lock_guard<std::mutex> lock(e->e->mutex());
     e->e->score_b64(prefix, t_q, text, char_off, n_items, item_ids, res);
+  });
+}
+
+int32_t sr_wire_parse(const char* body, int64_t len, int32_t max_seq, sr_wire** out) {
+  return guard([&] {
+    if (!out || (len > 0 && !body)) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    auto w = std::make_unique<sr_wire>();
+    w->w = srh::parse_wire(body, len, max_seq);
+    w->numeric_ids = true;
+    for (const auto& it : w->w.items) {
+      char* endp = nullptr;
+      const long long v = it.id.empty() ? 0 : std::strtoll(it.id.c_str(), &endp, 10);
+      if (it.id.empty() || *endp != '\0') {
+        w->numeric_ids = false;
+        break;
+      }
+      w->ids.push_back(v);
+    }
+    if (!w->numeric_ids) w->ids.clear();
+    *out = w.release();
+  });
+}
+
+void sr_wire_destroy(sr_wire* w) { delete w; }
+
+int32_t sr_wire_info(const sr_wire* w, int32_t* n_items, int32_t* mode, int32_t* t_q) {
+  return guard([&] {
+    if (!w) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    if (n_items) *n_items = static_cast<int32_t>(w->w.items.size());
+    if (mode) *mode = w->w.mode;
+    if (t_q) *t_q = static_cast<int32_t>(w->w.prefix.size());
+  });
+}
+
+const char* sr_wire_request_id(const sr_wire* w) { return w ? w->w.request_id.c_str() : ""; }
+
+const char* sr_wire_item_id(const sr_wire* w, int32_t i) {
+  if (!w || i < 0 || i >= static_cast<int32_t>(w->w.items.size())) return "";
+  return w->w.items[i].id.c_str();
+}
+
+int32_t sr_engine_score_wire(sr_engine* e, const sr_wire* w, sr_result* res) {
+  return guard([&] {
+    if (!e || !w || !res) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    const auto& r = w->w;
+    const int32_t n = static_cast<int32_t>(r.items.size());
+    const int64_t* ids = w->numeric_ids ? w->ids.data() : nullptr;
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    if (r.mode == SR_MODE_MIXED) {
+      std::vector<int64_t> b(n), en(n);
+      for (int32_t j = 0; j < n; ++j) {
+        const auto& it = r.items[j];
+        if (!it.b64)  // score_mixed needs an embedding per item (engine.cpp:243-251)
+          srh::fail(SR_PAYLOAD_INVALID, "mixed request item without embedding_b64: " + it.id);
+        const int64_t base = it.in_side ? r.body_len : 0;
+        b[j] = base + it.b64_begin;
+        en[j] = base + it.b64_end;
+      }
+      e->e->score_b64_spans(r.prefix.data(), static_cast<int32_t>(r.prefix.size()), r.body,
+                            r.body_len, r.side.data(), static_cast<int64_t>(r.side.size()),
+                            b.data(), en.data(), n, ids, res);
+      return;
+    }
+    std::vector<int32_t> off(n + 1, 0), tok;
+    for (int32_t j = 0; j < n; ++j) {
+      tok.insert(tok.end(), r.items[j].tokens.begin(), r.items[j].tokens.end());
+      off[j + 1] = static_cast<int32_t>(tok.size());
+    }
+    if (tok.empty()) tok.push_back(0);
+    sr_request req{};
+    req.prefix_tokens = r.prefix.data();
+    req.t_q = static_cast<int32_t>(r.prefix.size());
+    req.n_items = n;
+    req.item_offsets = off.data();
+    req.item_tokens = tok.data();
+    req.item_rows = nullptr;
+    req.item_ids = ids;
+    req.mode = r.mode;
+    e->e->score(&req, 1, res);
   });
 }
 

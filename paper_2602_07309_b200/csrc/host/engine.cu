@@ -474,18 +474,9 @@ void Engine::refill_plan(Plan& p, const sr_request* reqs, int n_req) {
       if (src.rows == kB64Rows) {
         // base64 payloads: text to HBM, decoded in place into the rows
         const int32_t n = b64_.n;
-        const int64_t chars = b64_.char_off[n];
-        b64_text_.ensure(static_cast<size_t>(std::max<int64_t>(chars, 4)));
-        b64_off_.ensure(static_cast<size_t>(2 * (n + 1)));
-        b64_err_.ensure(1);
-        SR_CUDA_CHECK(cudaMemcpyAsync(b64_text_.ptr, b64_.text, static_cast<size_t>(chars),
-                                      cudaMemcpyHostToDevice, stream_));
-        SR_CUDA_CHECK(cudaMemcpyAsync(b64_off_.ptr, b64_.char_off, (n + 1) * sizeof(int64_t),
-                                      cudaMemcpyHostToDevice, stream_));
-        SR_CUDA_CHECK(cudaMemcpyAsync(b64_off_.ptr + n + 1, b64_.byte_off.data(),
-                                      (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream_));
-        SR_CUDA_CHECK(cudaMemsetAsync(b64_err_.ptr, 0xff, sizeof(unsigned long long), stream_));
-        SR_CUDA_CHECK(srk::b64_decode(b64_text_.ptr, b64_off_.ptr, b64_off_.ptr + n + 1, n,
+        upload_b64_text();
+        SR_CUDA_CHECK(srk::b64_decode(b64_text_.ptr, b64_off_.ptr, b64_off_.ptr + n,
+                                      b64_off_.ptr + 2 * n, n,
                                       reinterpret_cast<uint8_t*>(p.soft.ptr + off * d),
                                       b64_err_.ptr, stream_));
       } else {
@@ -627,11 +618,41 @@ void Engine::score(const sr_request* reqs, int n_req, sr_result* res) {
   fetch(*p, res, n_req);
 }
 
+void Engine::upload_b64_text() {
+  const int32_t n = b64_.n;
+  const int64_t chars = b64_.la + b64_.lb;
+  b64_text_.ensure(static_cast<size_t>(std::max<int64_t>(chars, 4)));
+  b64_off_.ensure(static_cast<size_t>(3 * std::max(n, 1)));
+  b64_err_.ensure(1);
+  if (b64_.la > 0)
+    SR_CUDA_CHECK(cudaMemcpyAsync(b64_text_.ptr, b64_.a, static_cast<size_t>(b64_.la),
+                                  cudaMemcpyHostToDevice, stream_));
+  if (b64_.lb > 0)
+    SR_CUDA_CHECK(cudaMemcpyAsync(b64_text_.ptr + b64_.la, b64_.b, static_cast<size_t>(b64_.lb),
+                                  cudaMemcpyHostToDevice, stream_));
+  SR_CUDA_CHECK(cudaMemcpyAsync(b64_off_.ptr, b64_.spans.data(), b64_.spans.size() * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, stream_));
+  SR_CUDA_CHECK(cudaMemsetAsync(b64_err_.ptr, 0xff, sizeof(unsigned long long), stream_));
+}
+
 void Engine::score_b64(const int32_t* prefix, int32_t t_q, const char* text,
                        const int64_t* char_off, int32_t n_items, const int64_t* item_ids,
                        sr_result* res) {
+  std::vector<int64_t> begin(std::max(n_items, 0)), end(std::max(n_items, 0));
+  for (int32_t j = 0; j < n_items; ++j) {
+    begin[j] = char_off[j];
+    end[j] = char_off[j + 1];
+  }
+  score_b64_spans(prefix, t_q, text, n_items > 0 ? char_off[n_items] : 0, nullptr, 0,
+                  begin.data(), end.data(), n_items, item_ids, res);
+}
+
+void Engine::score_b64_spans(const int32_t* prefix, int32_t t_q, const char* a, int64_t la,
+                             const char* b, int64_t lb, const int64_t* begin, const int64_t* end,
+                             int32_t n_items, const int64_t* item_ids, sr_result* res) {
   if (n_items <= 0) fail(SR_PAYLOAD_INVALID, "request needs a non-empty items[]");
   const int64_t d = cfg_.d_model;
+  auto at = [&](int64_t pos) { return pos < la ? a[pos] : b[pos - la]; };
   // Host-side checks in the reference's order per item (base64.cpp:60-64,
   // 97-101; service.cpp:365-369); character / padding checks run on the device.
   int bad = -1;
@@ -640,15 +661,14 @@ void Engine::score_b64(const int32_t* prefix, int32_t t_q, const char* text,
   std::vector<int32_t> rows_off(n_items + 1, 0);
   std::vector<int64_t> byte_off(n_items + 1, 0);
   for (int32_t j = 0; j < n_items && bad < 0; ++j) {
-    const int64_t len = char_off[j + 1] - char_off[j];
+    const int64_t len = end[j] - begin[j];
     if (len % 4 != 0) {
       bad = j;
       bad_msg = "base64 length must be mod 4";
       bad_before_chars = true;
       break;
     }
-    const char* e = text + char_off[j + 1];
-    const int pad = (len >= 1 && e[-1] == '=') + (len >= 2 && e[-2] == '=');
+    const int pad = (len >= 1 && at(end[j] - 1) == '=') + (len >= 2 && at(end[j] - 2) == '=');
     const int64_t bytes = len / 4 * 3 - pad;
     if (bytes % 4 != 0) {
       bad = j;
@@ -666,32 +686,32 @@ void Engine::score_b64(const int32_t* prefix, int32_t t_q, const char* text,
     byte_off[j + 1] = byte_off[j] + bytes;
   }
   SR_CUDA_CHECK(cudaSetDevice(device_));
-  auto first_char_error = [&](int32_t upto) -> unsigned long long {
-    // validate-only pass over items [0, upto)
-    if (upto <= 0) return ~0ull;
-    const int64_t chars = char_off[upto];
-    b64_text_.ensure(static_cast<size_t>(std::max<int64_t>(chars, 4)));
-    b64_off_.ensure(static_cast<size_t>(2 * (upto + 1)));
-    b64_err_.ensure(1);
-    SR_CUDA_CHECK(cudaMemcpyAsync(b64_text_.ptr, text, static_cast<size_t>(chars),
-                                  cudaMemcpyHostToDevice, stream_));
-    SR_CUDA_CHECK(cudaMemcpyAsync(b64_off_.ptr, char_off, (upto + 1) * sizeof(int64_t),
-                                  cudaMemcpyHostToDevice, stream_));
-    SR_CUDA_CHECK(cudaMemsetAsync(b64_err_.ptr, 0xff, sizeof(unsigned long long), stream_));
-    SR_CUDA_CHECK(srk::b64_decode(b64_text_.ptr, b64_off_.ptr, b64_off_.ptr, upto, nullptr,
-                                  b64_err_.ptr, stream_));
-    unsigned long long err = ~0ull;
-    SR_CUDA_CHECK(cudaMemcpyAsync(&err, b64_err_.ptr, sizeof(err), cudaMemcpyDeviceToHost,
-                                  stream_));
-    SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
-    return err;
-  };
+  b64_.a = a;
+  b64_.la = la;
+  b64_.b = b;
+  b64_.lb = lb;
+  b64_.n = n_items;
+  b64_.spans.assign(begin, begin + n_items);
+  b64_.spans.insert(b64_.spans.end(), end, end + n_items);
+  b64_.spans.insert(b64_.spans.end(), byte_off.begin(), byte_off.begin() + n_items);
   auto raise_char = [](unsigned long long err) {
     fail(SR_PAYLOAD_INVALID, (err & 3u) == 1u ? "misplaced base64 padding"
                                               : "invalid base64 character");
   };
   if (bad >= 0) {
-    const unsigned long long err = first_char_error(bad_before_chars ? bad : bad + 1);
+    // validate-only pass over the items the reference would have decoded
+    const int32_t upto = bad_before_chars ? bad : bad + 1;
+    unsigned long long err = ~0ull;
+    if (upto > 0) {
+      upload_b64_text();
+      SR_CUDA_CHECK(srk::b64_decode(b64_text_.ptr, b64_off_.ptr, b64_off_.ptr + n_items,
+                                    b64_off_.ptr + 2 * n_items, upto, nullptr, b64_err_.ptr,
+                                    stream_));
+      SR_CUDA_CHECK(cudaMemcpyAsync(&err, b64_err_.ptr, sizeof(err), cudaMemcpyDeviceToHost,
+                                    stream_));
+      SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    }
+    b64_ = B64Src{};
     if (err != ~0ull) raise_char(err);
     fail(SR_PAYLOAD_INVALID, bad_msg);
   }
@@ -705,10 +725,6 @@ void Engine::score_b64(const int32_t* prefix, int32_t t_q, const char* text,
   req.item_rows = kB64Rows;
   req.item_ids = item_ids;
   req.mode = SR_MODE_MIXED;
-  b64_.text = text;
-  b64_.char_off = char_off;
-  b64_.byte_off = std::move(byte_off);
-  b64_.n = n_items;
   try {
     score(&req, 1, res);
   } catch (...) {

@@ -155,6 +155,11 @@ class Engine {
   // on the device into the soft-row buffer (kernels/wire.cu), then scored.
   void score_b64(const int32_t* prefix, int32_t t_q, const char* text, const int64_t* char_off,
                  int32_t n_items, const int64_t* item_ids, sr_result* res);
+  // Same with payload spans [begin[i], end[i]) inside text = a ++ b (the
+  // JSON body and its side buffer of unescaped payloads, host/wire.hpp).
+  void score_b64_spans(const int32_t* prefix, int32_t t_q, const char* a, int64_t la,
+                       const char* b, int64_t lb, const int64_t* begin, const int64_t* end,
+                       int32_t n_items, const int64_t* item_ids, sr_result* res);
 
   // Sharded: local pass + NCCL all-gather of per-rank top-k + merge.
   void run_plan_sharded(Plan& p, struct Comm* comm);
@@ -190,14 +195,17 @@ class Engine {
   std::vector<double> last_final_;
   // pending base64 source of the mixed request being packed (score_b64)
   struct B64Src {
-    const char* text = nullptr;
-    const int64_t* char_off = nullptr;
-    std::vector<int64_t> byte_off;
+    const char* a = nullptr;  // text = a ++ b
+    int64_t la = 0;
+    const char* b = nullptr;
+    int64_t lb = 0;
+    std::vector<int64_t> spans;  // begin[n] ++ end[n] ++ byte_off[n]
     int32_t n = 0;
   } b64_;
   DevBuf<uint8_t> b64_text_;
   DevBuf<int64_t> b64_off_;
   DevBuf<unsigned long long> b64_err_;
+  void upload_b64_text();
   std::vector<LayerDev> layers_;
   std::vector<void*> allocs_;
   // workspace

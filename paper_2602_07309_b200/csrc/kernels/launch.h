@@ -159,14 +159,14 @@ cudaError_t final_scores(const double* scores, int stride, int n, const double* 
                          int n_blocks, const int32_t* blend_task, const double* blend_w,
                          int n_blend, double* out, cudaStream_t stream);
 
-// Base64 (base64.cpp:60-108) of n_items concatenated payloads: text
-// [char_off[i], char_off[i+1]) (lengths multiples of 4, 4-byte aligned) ->
-// bytes at out + byte_off[i] (out may be null: validate only). first_err
-// (preset to ~0) receives min(text position << 2 | kind), kind 1 misplaced
-// padding, 2 invalid character.
-cudaError_t b64_decode(const uint8_t* text, const int64_t* char_off, const int64_t* byte_off,
-                       int n_items, uint8_t* out, unsigned long long* first_err,
-                       cudaStream_t stream);
+// Base64 (base64.cpp:60-108) of n_items payloads: text [char_begin[i],
+// char_end[i]) (lengths multiples of 4) -> bytes at out + byte_off[i] (out
+// may be null: validate only). first_err (preset to ~0) receives
+// min(item-ordered position << 2 | kind), kind 1 misplaced padding, 2 invalid
+// character; positions grow with the item index (the host orders spans so).
+cudaError_t b64_decode(const uint8_t* text, const int64_t* char_begin, const int64_t* char_end,
+                       const int64_t* byte_off, int n_items, uint8_t* out,
+                       unsigned long long* first_err, cudaStream_t stream);
 
 struct TopkEntry {
   double score;

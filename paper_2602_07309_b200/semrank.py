@@ -533,6 +533,29 @@ class ScoringEngine:
             res.final_scores = self._final(len(request.items))
         return res
 
+    def score_json(self, body, k: int = 0, max_seq: Optional[int] = None) -> ScoreResult:
+        """The /score wire path in native code: the body is parsed in one pass
+        (sr_wire_parse) and embedding_b64 payloads go to the device as spans of
+        the body, decoded in HBM (sr_engine_score_wire)."""
+        raw = body.encode("utf-8") if isinstance(body, str) else bytes(body)
+        h = C.c_void_p()
+        _check(_lib.sr_wire_parse(raw, len(raw), max_seq or self.config.max_seq, C.byref(h)))
+        try:
+            n, mode, tq = C.c_int32(), C.c_int32(), C.c_int32()
+            _check(_lib.sr_wire_info(h, C.byref(n), C.byref(mode), C.byref(tq)))
+            rb = _ResultBuf(n.value, len(self.task_names), k)
+            _check(_lib.sr_engine_score_wire(self._h, h, C.byref(rb.c)))
+            ids = [_lib.sr_wire_item_id(h, i).decode() for i in range(n.value)]
+            req = ScoreRequest(request_id=_lib.sr_wire_request_id(h).decode(), mode=ScoreMode(mode.value),
+                               items=[ScoreItem(id=i) for i in ids])
+        finally:
+            _lib.sr_wire_destroy(h)
+        del raw
+        res = self._to_result(req, rb)
+        if self._post:
+            res.final_scores = self._final(n.value)
+        return res
+
     def _score_b64(self, request: ScoreRequest, rb: "_ResultBuf") -> None:
         """embedding_b64 items: the base64 text goes to the device as is."""
         parts = [it.embedding_b64.encode("ascii", "replace") for it in request.items]

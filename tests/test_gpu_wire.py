@@ -98,3 +98,32 @@ def test_first_failing_item_wins(cuda):
                                      .decode()], f"is not [n x {d}]")
     # an error in a later item still fails the whole request, after device decode
     _expect_payload_error(eng, [7], [good, good[:-8] + "AAA=AAAA"], "misplaced base64 padding")
+
+
+def test_native_wire_path_matches_python_parse(cuda):
+    """ScoringEngine.score_json (native one-pass parser, payload spans of the
+    body decoded in HBM) == parse_score_request_json + score, bit for bit;
+    JSON escapes inside a payload ("\\/") and token / text items included."""
+    eng = toy_engine()
+    d = eng.config.d_model
+    rng = np.random.default_rng(8)
+    prefix = rng.integers(0, 256, 64)
+    rows = [rng.standard_normal((int(rng.integers(1, 4)), d)).astype(np.float32) * np.float32(0.08)
+            for _ in range(23)]
+    pays = [base64.b64encode(r.tobytes()).decode() for r in rows]
+    b = body(prefix, pays, ids=list(range(100, 123)))
+    # escape every '/' of one payload the way some JSON encoders do
+    k = next(i for i, p in enumerate(pays) if "/" in p)
+    b = b.replace(pays[k], pays[k].replace("/", "\\/"))
+    got = eng.score_json(b, k=5)
+    want = eng.score(sr.parse_score_request_json(b, d), k=5)
+    assert np.array_equal(got.scores, want.scores) and got.topk == want.topk
+    assert [it.item_id for it in got.items] == [str(i) for i in range(100, 123)]
+    toks = json.dumps({"request_id": "t", "prefix_text": "query: shoes", "mode": "multi_item",
+                       "items": [{"id": str(i), "text": f"item {i} text"} for i in range(40)]})
+    got = eng.score_json(toks, k=7)
+    want = eng.score(sr.parse_score_request_json(toks, d), k=7)
+    assert np.array_equal(got.scores, want.scores) and got.topk == want.topk
+    with pytest.raises(sr.SemrankError) as e:
+        eng.score_json(body(prefix, [pays[0], pays[1][:-1]]), k=2)
+    assert "base64 length must be mod 4" in str(e.value)

@@ -239,3 +239,51 @@ def test_engine_fails_loudly_without_gpu():
     with pytest.raises(sr.SemrankError) as e:
         sr.ScoringEngine(w)
     assert e.value.code == sr.ErrorCode.Cuda
+
+
+# ------------------------------------------------------- native /score parser
+def _wire(body, max_seq=4096):
+    import ctypes as C
+    from paper_2602_07309_b200._capi import lib
+    raw = body.encode() if isinstance(body, str) else body
+    h = C.c_void_p()
+    st = lib.sr_wire_parse(raw, len(raw), max_seq, C.byref(h))
+    if st != 0:
+        return st, lib.sr_last_error().decode(), None
+    n, mode, tq = C.c_int32(), C.c_int32(), C.c_int32()
+    lib.sr_wire_info(h, C.byref(n), C.byref(mode), C.byref(tq))
+    info = (n.value, mode.value, tq.value, lib.sr_wire_request_id(h).decode(),
+            [lib.sr_wire_item_id(h, i).decode() for i in range(n.value)])
+    lib.sr_wire_destroy(h)
+    return 0, "", info
+
+
+def test_native_wire_parser_follows_parse_score_request_json():
+    """service.cpp:326-372: fields, defaults, precedence and error messages."""
+    import json
+    import paper_2602_07309_b200 as sr
+    body = json.dumps({"request_id": "réq", "prefix_text": "hi \"there\"", "mode": "multi-item",
+                       "extra": {"nested": [1, {"x": None}]},
+                       "items": [{"id": "7", "text": "a\\nb"}, {"id": "9", "tokens": [1, 2]},
+                                 {"tokens": [3], "text": "ignored", "id": "11"}]})
+    st, msg, info = _wire(body)
+    assert st == 0, msg
+    n, mode, tq, rid, ids = info
+    assert (n, mode, tq, rid, ids) == (3, int(sr.ScoreMode.MultiItem), len(b'hi "there"'), "réq",
+                                       ["7", "9", "11"])
+    # default mode is ibpc (service.cpp:343)
+    assert _wire('{"prefix_tokens":[1],"items":[{"tokens":[2]}]}')[2][1] == int(sr.ScoreMode.Ibpc)
+    P = int(sr.ErrorCode.PayloadInvalid)
+    cases = [("{not json", P, "request body is not JSON"),
+             ('{"items":[{"tokens":[1]}]}', P, "request needs prefix_text or prefix_tokens"),
+             ('{"prefix_tokens":[1],"items":[]}', P, "request needs a non-empty items[]"),
+             ('{"prefix_tokens":[1],"items":{}}', P, "request needs a non-empty items[]"),
+             ('{"prefix_tokens":[1],"items":[{"id":"q"}]}', P,
+              "item needs text, tokens, or embedding_b64: q"),
+             ('{"prefix_tokens":[1],"mode":"bogus","items":[{"tokens":[1]}]}',
+              int(sr.ErrorCode.Parameter), "unknown scoring mode: bogus"),
+             ('{"prefix_text":"abcdef","items":[{"tokens":[1]}]}', int(sr.ErrorCode.LengthOverflow),
+              "exceeds max_seq 4")]
+    for body, code, text in cases:
+        st, msg, _ = _wire(body, max_seq=4)
+        assert st == code and text in msg, (body, st, msg)
