@@ -666,14 +666,10 @@ __global__ void __launch_bounds__(320, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-#ifdef SRK_EXP_RESID_STORE  // timing experiment only: plain store instead of add-reduce
-              tma_store_2d(&tmC, stg, n0 + c, r0);
-#else
               if constexpr (EPI == EPI_RESID_F32)  // x is re-read next by the LayerNorm
                 tma_reduce_add_2d_hint(&tmC, stg, n0 + c, r0, pol_keep);
               else
                 tma_store_2d(&tmC, stg, n0 + c, r0);
-#endif
               bulk_commit();
             }
           }
