@@ -593,7 +593,7 @@ int32_t sr_engine_score_sharded(sr_engine* e, sr_comm* c, const sr_request* loca
     auto p = e->e->make_plan(local_shard, 1, res->k);
     e->e->run_plan_sharded(*p, c->c);
     e->e->fetch(*p, res, 1);
-    if (c->c->nranks > 1) copy_topk_merged(*p, res, e->e->stream());
+    copy_topk_merged(*p, res, e->e->stream());
   });
 }
 
@@ -601,7 +601,7 @@ int32_t sr_plan_run_sharded(sr_plan* p, sr_comm* c) {
   return guard([&] {
     if (!p || !c) srh::fail(SR_SPEC_VIOLATION, "null argument");
     p->owner->e->run_plan_sharded(*p->p, c->c);
-    p->sharded_valid = c->c->nranks > 1;
+    p->sharded_valid = true;
   });
 }
 

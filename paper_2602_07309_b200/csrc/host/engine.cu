@@ -757,7 +757,9 @@ void Engine::item_hidden(const sr_request& req, float* hidden_out) {
 }
 
 void Engine::run_plan_sharded(Plan& p, Comm* c) {
-  if (c == nullptr || c->nranks <= 1) {
+  // nranks == 1 also takes the all-gather + merge (a copy): one code path,
+  // exercised by the single-GPU tests
+  if (c == nullptr) {
     run_plan(p);
     return;
   }

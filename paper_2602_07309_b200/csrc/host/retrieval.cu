@@ -186,8 +186,7 @@ int Corpus::topk_host(const float* query, int d_query, double w0, const double* 
 int Corpus::topk_sharded(Comm* c, const float* query, int d_query, double w0, const double* w,
                          int n_w, const uint8_t* keep, int k, int64_t* ids_out,
                          double* scores_out) {
-  if (c == nullptr || c->nranks <= 1)
-    return topk_host(query, d_query, w0, w, n_w, keep, k, ids_out, scores_out);
+  if (c == nullptr) return topk_host(query, d_query, w0, w, n_w, keep, k, ids_out, scores_out);
   if (k < 1) fail(SR_SPEC_VIOLATION, "top-K requires K >= 1");
   if (static_cast<long>(c->nranks) * k > 4096) fail(SR_PARAMETER, "nranks * k must be <= 4096");
   SR_CUDA_CHECK(cudaSetDevice(device_));

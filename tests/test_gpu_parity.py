@@ -336,6 +336,7 @@ def test_single_rank_nccl_sharded_path(cuda):
     comm = sr.Comm(1, 0, sr.Comm.unique_id(), 0)
     req = request(g["prefix"], g["items"])
     ids = np.arange(1000, 1064, dtype=np.int64)
-    res = eng.score_sharded(comm, req, 10, ids)
+    res = eng.score_sharded(comm, req, 10, ids)  # runs the NCCL all-gather + device merge
     local = eng.score(req, 10)
-    assert res.topk == local.topk and np.array_equal(res.scores, local.scores)
+    assert res.topk == [(str(1000 + int(i)), s) for i, s in local.topk]
+    assert np.array_equal(res.scores, local.scores)
