@@ -738,7 +738,7 @@ int32_t sr_kernel_attention(const void* qkv, const int32_t* spans_host, int32_t 
       CUtensorMap tm;
       err = srk::make_tmap_bf16_2d(&tm, qkv, M, 3 * n_heads * head_dim, 128, 64);
       if (err == cudaSuccess)
-        err = srk::attention_tc(tm, dsp, dt, static_cast<int>(tiles.size()),
+        err = srk::attention_tc(tm, qkv, dsp, dt, static_cast<int>(tiles.size()),
                                 static_cast<__nv_bfloat16*>(out), M, n_heads, head_dim, s);
     } else {
       err = srk::attention(static_cast<const __nv_bfloat16*>(qkv), dsp, dt,

@@ -280,7 +280,7 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
   };
   auto attention = [&]() {
     if (hd >= 64)
-      SR_CUDA_CHECK(srk::attention_tc(tm_qkv_, p.spans.ptr, p.tiles.ptr,
+      SR_CUDA_CHECK(srk::attention_tc(tm_qkv_, qkv_.ptr, p.spans.ptr, p.tiles.ptr,
                                       static_cast<int>(p.pack.tiles.size()), xn_.ptr, M, H, hd, s));
     else  // toy head sizes (16/32): the 64-row mma.sync kernel
       SR_CUDA_CHECK(srk::attention(qkv_.ptr, p.spans.ptr, p.tiles.ptr,

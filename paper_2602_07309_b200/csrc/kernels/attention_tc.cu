@@ -287,6 +287,8 @@ __global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
         umma_commit(&pv_done[st]);
         if (sc.valid) {
           // S_{g+2} reuses this TMEM buffer: PV_g must have read P_g first.
+          // (Issuing it right behind PV_g, relying on in-order tcgen05.mma
+          // execution, measured no faster.)
           mbar_wait(&pv_done[st], ph);
           issue_s();
         }
@@ -606,21 +608,27 @@ cudaError_t launch_tc(const CUtensorMap& tm, const RowSpan* spans, const AttnTil
 // staged (in the Q buffer) and stored.
 // TMEM (512 cols): S/P slot x at [128 x, +128), O slot x at [256 + 128 x, +HD).
 constexpr int kPPThreads = 352;
+// Key blocks of 64 rows (8 KB per 64-column box) so each slot gets a
+// 2-stage K and V ring inside the smem budget (2 Q + 2 x 2 K + 2 x 2 V).
+constexpr int kPB = 64;
+constexpr int kPStages = 2;
+constexpr int kKVBox = kPB * 128;
 
 template <int HD>
 struct PPCfg {
   static constexpr int NB = HD / 64;
-  static constexpr int TILE = NB * kBox;
-  static constexpr int Q_OFF = 0;         // [slot]
-  static constexpr int K_OFF = 2 * TILE;  // [slot]
-  static constexpr int V_OFF = 4 * TILE;  // [slot]
-  static constexpr int BAR_OFF = 6 * TILE;
+  static constexpr int TILE = NB * kBox;      // Q tile (128 rows)
+  static constexpr int KV_TILE = NB * kKVBox; // K / V block (64 rows)
+  static constexpr int Q_OFF = 0;                                  // [slot]
+  static constexpr int K_OFF = 2 * TILE;                           // [slot][stage]
+  static constexpr int V_OFF = K_OFF + 2 * kPStages * KV_TILE;     // [slot][stage]
+  static constexpr int BAR_OFF = V_OFF + 2 * kPStages * KV_TILE;
   static constexpr int SMEM = BAR_OFF + 512 + 1024;
   static constexpr int O_COL = 256;
 };
 
-enum PPBar : int { PB_Q_FULL = 0, PB_K_FULL, PB_K_EMPTY, PB_V_FULL, PB_V_EMPTY, PB_S_FULL,
-                   PB_P_FULL, PB_PV_DONE, PB_N };
+enum PPBar : int { PB_Q_FULL = 0, PB_K_FULL = 1, PB_K_EMPTY = 3, PB_V_FULL = 5,
+                   PB_V_EMPTY = 7, PB_S_FULL = 9, PB_P_FULL = 10, PB_PV_DONE = 11, PB_N = 12 };
 
 // One slot's (item, block) sequence: items first, first + stride, ...
 struct SlotCursor {
@@ -641,19 +649,19 @@ struct SlotCursor {
       if (!valid) return;
       t = tiles[it % n_tiles];
       h = it / n_tiles;
-      nb1 = (t.r1_end - t.r1_begin + kBK - 1) / kBK;
-      nblk = nb1 + (t.r2_end - t.r2_begin + kBK - 1) / kBK;
+      nb1 = (t.r1_end - t.r1_begin + kPB - 1) / kPB;
+      nblk = nb1 + (t.r2_end - t.r2_begin + kPB - 1) / kPB;
       j = 0;
       if (nblk > 0) return;
     }
   }
   __device__ void range(int& k0, int& kbeg, int& kend) const {
     if (j < nb1) {
-      k0 = t.r1_begin + j * kBK;
+      k0 = t.r1_begin + j * kPB;
       kbeg = t.r1_begin;
       kend = t.r1_end;
     } else {
-      k0 = t.r2_begin + (j - nb1) * kBK;
+      k0 = t.r2_begin + (j - nb1) * kPB;
       kbeg = t.r2_begin;
       kend = t.r2_end;
     }
@@ -678,6 +686,7 @@ __device__ __forceinline__ uint32_t chunk_bits(int lo, int hi) {
 template <int HD>
 __global__ void __launch_bounds__(kPPThreads, 1)
     attn_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                   const __grid_constant__ CUtensorMap tm_kv,
                    const __grid_constant__ CUtensorMap tm_out, const RowSpan* __restrict__ spans,
                    const AttnTile* __restrict__ tiles, int n_tiles, __nv_bfloat16* __restrict__ out,
                    int n_heads) {
@@ -699,13 +708,16 @@ __global__ void __launch_bounds__(kPPThreads, 1)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_qkv);
+    tma_prefetch_desc(&tm_kv);
     tma_prefetch_desc(&tm_out);
     for (int x = 0; x < 2; ++x) {
       mbar_init(bar(x, PB_Q_FULL), 1);
-      mbar_init(bar(x, PB_K_FULL), 1);
-      mbar_init(bar(x, PB_K_EMPTY), 1);
-      mbar_init(bar(x, PB_V_FULL), 1);
-      mbar_init(bar(x, PB_V_EMPTY), 1);
+      for (int st = 0; st < kPStages; ++st) {
+        mbar_init(bar(x, PB_K_FULL + st), 1);
+        mbar_init(bar(x, PB_K_EMPTY + st), 1);
+        mbar_init(bar(x, PB_V_FULL + st), 1);
+        mbar_init(bar(x, PB_V_EMPTY + st), 1);
+      }
       mbar_init(bar(x, PB_S_FULL), 1);
       mbar_init(bar(x, PB_P_FULL), 128);
       mbar_init(bar(x, PB_PV_DONE), 1);
@@ -729,22 +741,23 @@ __global__ void __launch_bounds__(kPPThreads, 1)
       const uint64_t keep = policy_evict_last();  // prefix K/V: re-read by every item tile
       SlotCursor c;
       c.init(tiles, n_tiles, n_items, blockIdx.x + x * G, 2 * G);
-      uint8_t* k_buf = sK + x * C::TILE;
-      uint8_t* v_buf = sV + x * C::TILE;
       for (int n = 0; c.valid; ++n) {
         int k0, kb, ke;
         c.range(k0, kb, ke);
-        const uint32_t ph = (n & 1) ^ 1;
-        mbar_wait(bar(x, PB_K_EMPTY), ph);
-        mbar_arrive_expect_tx(bar(x, PB_K_FULL), C::TILE);
+        const int st = n & 1;
+        const uint32_t ph = ((n >> 1) & 1) ^ 1;
+        uint8_t* k_buf = sK + (x * kPStages + st) * C::KV_TILE;
+        uint8_t* v_buf = sV + (x * kPStages + st) * C::KV_TILE;
+        mbar_wait(bar(x, PB_K_EMPTY + st), ph);
+        mbar_arrive_expect_tx(bar(x, PB_K_FULL + st), C::KV_TILE);
         for (int b = 0; b < C::NB; ++b)
-          tma_load_2d_hint(&tm_qkv, bar(x, PB_K_FULL), k_buf + b * kBox, d + c.h * HD + b * 64, k0,
-                           keep);
-        mbar_wait(bar(x, PB_V_EMPTY), ph);
-        mbar_arrive_expect_tx(bar(x, PB_V_FULL), C::TILE);
-        for (int b = 0; b < C::NB; ++b)
-          tma_load_2d_hint(&tm_qkv, bar(x, PB_V_FULL), v_buf + b * kBox, 2 * d + c.h * HD + b * 64,
+          tma_load_2d_hint(&tm_kv, bar(x, PB_K_FULL + st), k_buf + b * kKVBox, d + c.h * HD + b * 64,
                            k0, keep);
+        mbar_wait(bar(x, PB_V_EMPTY + st), ph);
+        mbar_arrive_expect_tx(bar(x, PB_V_FULL + st), C::KV_TILE);
+        for (int b = 0; b < C::NB; ++b)
+          tma_load_2d_hint(&tm_kv, bar(x, PB_V_FULL + st), v_buf + b * kKVBox,
+                           2 * d + c.h * HD + b * 64, k0, keep);
         c.advance(tiles);
       }
     }
@@ -752,7 +765,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------ MMA (both slots)
     if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16_f32(kTM, kBK);
+      constexpr uint32_t idesc_s = idesc_bf16_f32(kTM, kPB);
       constexpr uint32_t idesc_pv = idesc_bf16_f32_bmn(kTM, HD);
       SlotCursor c[2];
       int ns[2] = {0, 0}, np[2] = {0, 0}, nq[2] = {0, 0};
@@ -773,33 +786,35 @@ __global__ void __launch_bounds__(kPPThreads, 1)
               s_free[x] = true;
             }
             if (c[x].j == 0 && !mbar_test(bar(x, PB_Q_FULL), nq[x] & 1)) continue;
-            if (!mbar_test(bar(x, PB_K_FULL), ns[x] & 1)) continue;
+            const int kst = ns[x] & 1;
+            if (!mbar_test(bar(x, PB_K_FULL + kst), (ns[x] >> 1) & 1)) continue;
             tc_fence_after();
             if (c[x].j == 0) ++nq[x];
             const uint32_t q_addr = smem_u32(sQ + x * C::TILE);
-            const uint32_t k_addr = smem_u32(sK + x * C::TILE);
+            const uint32_t k_addr = smem_u32(sK + (x * kPStages + kst) * C::KV_TILE);
 #pragma unroll
             for (int s = 0; s < HD / 16; ++s) {
-              const uint32_t off = (s >> 2) * kBox + (s & 3) * 32;
-              umma_bf16(tmem + x * kBK, sw128_kmajor_desc(q_addr + off),
-                        sw128_kmajor_desc(k_addr + off), idesc_s, s > 0 ? 1u : 0u);
+              umma_bf16(tmem + x * kBK, sw128_kmajor_desc(q_addr + (s >> 2) * kBox + (s & 3) * 32),
+                        sw128_kmajor_desc(k_addr + (s >> 2) * kKVBox + (s & 3) * 32), idesc_s,
+                        s > 0 ? 1u : 0u);
             }
-            umma_commit(bar(x, PB_K_EMPTY));
+            umma_commit(bar(x, PB_K_EMPTY + kst));
             umma_commit(bar(x, PB_S_FULL));
             ++ns[x];
             want_s[x] = false;
           } else {
             // O_x += P_x V (P read from TMEM)
+            const int vst = np[x] & 1;
             if (!mbar_test(bar(x, PB_P_FULL), np[x] & 1)) continue;
-            if (!mbar_test(bar(x, PB_V_FULL), np[x] & 1)) continue;
+            if (!mbar_test(bar(x, PB_V_FULL + vst), (np[x] >> 1) & 1)) continue;
             tc_fence_after();
-            const uint32_t v_addr = smem_u32(sV + x * C::TILE);
+            const uint32_t v_addr = smem_u32(sV + (x * kPStages + vst) * C::KV_TILE);
 #pragma unroll
-            for (int s = 0; s < kBK / 16; ++s)
+            for (int s = 0; s < kPB / 16; ++s)
               umma_bf16_ts(tmem + C::O_COL + x * 128, tmem + x * kBK + s * 8,
-                           sw128_mnmajor_desc(v_addr + s * 16 * 128, kBox, 1024), idesc_pv,
+                           sw128_mnmajor_desc(v_addr + s * 16 * 128, kKVBox, 1024), idesc_pv,
                            (c[x].j > 0 || s > 0) ? 1u : 0u);
-            umma_commit(bar(x, PB_V_EMPTY));
+            umma_commit(bar(x, PB_V_EMPTY + vst));
             umma_commit(bar(x, PB_PV_DONE));
             ++np[x];
             s_free[x] = false;
@@ -846,19 +861,19 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         // visible keys of this row in the block, relative to k0
         const int a_lo = max(kb, sp.prefix_begin) - k0, a_hi = min(ke, sp.prefix_end) - k0;
         const int b_lo = max(kb, sp.span_start) - k0, b_hi = min(ke, row + 1) - k0;
-        const bool full = live && ((a_lo <= 0 && a_hi >= kBK) || (b_lo <= 0 && b_hi >= kBK));
+        const bool full = live && ((a_lo <= 0 && a_hi >= kPB) || (b_lo <= 0 && b_hi >= kPB));
         const bool all_full = __all_sync(0xffffffff, full);
         mbar_wait(bar(x, PB_S_FULL), g & 1);
         if (warp == 2 && lane == 0 && g < 24) SRK_TRACE(40 + g);
         tc_fence_after();
         // The whole 128-key row of S in registers: one TMEM round trip.
-        uint32_t v[kBK];
+        uint32_t v[kPB];
 #pragma unroll
-        for (int cc = 0; cc < kBK / 32; ++cc)
+        for (int cc = 0; cc < kPB / 32; ++cc)
           tmem_ld_32x32b_x32(t_s + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[cc * 32]));
-        uint32_t bits[kBK / 32];
+        uint32_t bits[kPB / 32];
 #pragma unroll
-        for (int cc = 0; cc < kBK / 32; ++cc)
+        for (int cc = 0; cc < kPB / 32; ++cc)
           bits[cc] = all_full ? 0xffffffffu
                               : (live ? (chunk_bits(a_lo - 32 * cc, a_hi - 32 * cc) |
                                          chunk_bits(b_lo - 32 * cc, b_hi - 32 * cc))
@@ -867,13 +882,13 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         float ma = -INFINITY, mb = -INFINITY;
         if (all_full) {
 #pragma unroll
-          for (int i = 0; i < kBK; i += 4) {
+          for (int i = 0; i < kPB; i += 4) {
             ma = fmax3f(ma, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
             mb = fmax3f(mb, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
           }
         } else {
 #pragma unroll
-          for (int i = 0; i < kBK; i += 2) {
+          for (int i = 0; i < kPB; i += 2) {
             if (!((bits[i >> 5] >> (i & 31)) & 1u)) v[i] = __float_as_uint(-INFINITY);
             if (!((bits[i >> 5] >> ((i + 1) & 31)) & 1u)) v[i + 1] = __float_as_uint(-INFINITY);
             if (i & 2) mb = fmax3f(mb, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
@@ -909,7 +924,7 @@ __global__ void __launch_bounds__(kPPThreads, 1)
         // (keys 32 cc .. 32 cc + 31 -> columns [16 cc, 16 cc + 16)), packed in
         // place into v[32 cc .. 32 cc + 15]; masked keys hold -inf -> 0.
 #pragma unroll
-        for (int cc = 0; cc < kBK / 32; ++cc) {
+        for (int cc = 0; cc < kPB / 32; ++cc) {
           uint32_t* w = &v[32 * cc];
           if (!__any_sync(0xffffffff, bits[cc] != 0u)) {
 #pragma unroll
@@ -1000,8 +1015,9 @@ __global__ void __launch_bounds__(kPPThreads, 1)
 }
 
 template <int HD>
-cudaError_t launch_pp(const CUtensorMap& tm, const RowSpan* spans, const AttnTile* tiles,
-                      int n_tiles, __nv_bfloat16* out, int M, int n_heads, cudaStream_t stream) {
+cudaError_t launch_pp(const CUtensorMap& tm, const void* qkv, const RowSpan* spans,
+                      const AttnTile* tiles, int n_tiles, __nv_bfloat16* out, int M, int n_heads,
+                      cudaStream_t stream) {
   using C = PPCfg<HD>;
   auto kern = attn_pp_kernel<HD>;
   static bool attr = false;
@@ -1010,8 +1026,12 @@ cudaError_t launch_pp(const CUtensorMap& tm, const RowSpan* spans, const AttnTil
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  CUtensorMap tm_out;
+  CUtensorMap tm_out, tm_kv;
   cudaError_t e = make_tmap_bf16_2d(&tm_out, out, M, static_cast<uint64_t>(n_heads) * HD, 32, 64);
+  if (e != cudaSuccess) return e;
+  // K / V blocks of kPB rows; rows past M are never visible (masked) and the
+  // packed buffer is padded, but keep the map exact: clip at M.
+  e = make_tmap_bf16_2d(&tm_kv, qkv, M, static_cast<uint64_t>(3 * n_heads) * HD, kPB, 64);
   if (e != cudaSuccess) return e;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1019,15 +1039,17 @@ cudaError_t launch_pp(const CUtensorMap& tm, const RowSpan* spans, const AttnTil
   // two items in flight per CTA
   const int want = (items + 1) / 2;
   const int grid = want < num_sms(dev) ? want : num_sms(dev);
-  return launch_k(kern, dim3(grid), dim3(kPPThreads), C::SMEM, stream, tm, tm_out, spans, tiles,
-                  n_tiles, out, n_heads);
+  return launch_k(kern, dim3(grid), dim3(kPPThreads), C::SMEM, stream, tm, tm_kv, tm_out, spans,
+                  tiles, n_tiles, out, n_heads);
 }
 
 // Opt-in (SRK_ATTN=pp). Measured on B200 at C2 (tools/attn_pp_trace.py):
-// 132k cycles per CTA vs 116k for attn_tc_kernel — with one K/V stage per
-// slot (smem: 2 Q + 2 K + 2 V tiles of 32 KB) each slot waits ~2.5k cycles
-// per block for its next S, and a thread owning a full 128-key row spends
-// ~2.5k cycles per block in softmax, so the two slots do not hide each other.
+// with 128-key blocks and one K/V stage per slot, 132k cycles per CTA vs 112k
+// for attn_tc_kernel; with 64-key blocks and 2-stage K/V rings per slot (this
+// version) 157-162k: the softmax of a 64-key block takes ~1.2k cycles per
+// slot, but each slot then waits ~2.7k cycles for its next S (PV -> S
+// dependency through the S/P buffer plus two commit -> mbarrier -> poll hops
+// per block), so the two slots still do not hide each other.
 bool attn_use_pp() {
   static const bool pp = [] {
     const char* v = std::getenv("SRK_ATTN");
@@ -1043,18 +1065,18 @@ cudaError_t attention_set_trace(unsigned long long* dev_buf) {
 
 int attention_tile_rows(int head_dim) { return head_dim >= 64 ? kTM : 64; }
 
-cudaError_t attention_tc(const CUtensorMap& tm_qkv, const RowSpan* spans, const AttnTile* tiles,
-                         int n_tiles, __nv_bfloat16* out, int M, int n_heads, int head_dim,
-                         cudaStream_t stream) {
+cudaError_t attention_tc(const CUtensorMap& tm_qkv, const void* qkv, const RowSpan* spans,
+                         const AttnTile* tiles, int n_tiles, __nv_bfloat16* out, int M,
+                         int n_heads, int head_dim, cudaStream_t stream) {
   if (n_tiles <= 0) return cudaSuccess;
   // SRK_ATTN=pp selects the two-slot ping-pong kernel (A/B runs).
   const bool pp = attn_use_pp();
   switch (head_dim) {
     case 64:
-      return pp ? launch_pp<64>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream)
+      return pp ? launch_pp<64>(tm_qkv, qkv, spans, tiles, n_tiles, out, M, n_heads, stream)
                 : launch_tc<64>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream);
     case 128:
-      return pp ? launch_pp<128>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream)
+      return pp ? launch_pp<128>(tm_qkv, qkv, spans, tiles, n_tiles, out, M, n_heads, stream)
                 : launch_tc<128>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream);
   }
   return cudaErrorInvalidValue;

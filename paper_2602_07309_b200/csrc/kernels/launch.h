@@ -133,9 +133,9 @@ cudaError_t attention(const __nv_bfloat16* qkv, const RowSpan* spans, const Attn
                       cudaStream_t stream);
 // tcgen05/TMEM path for head_dim in {64, 128}; tm_qkv maps the [rows x 3d]
 // bf16 qkv buffer with 64 x 128 boxes (make_tmap_bf16_2d(.., 128, 64)).
-cudaError_t attention_tc(const CUtensorMap& tm_qkv, const RowSpan* spans, const AttnTile* tiles,
-                         int n_tiles, __nv_bfloat16* out, int M, int n_heads, int head_dim,
-                         cudaStream_t stream);
+cudaError_t attention_tc(const CUtensorMap& tm_qkv, const void* qkv, const RowSpan* spans,
+                         const AttnTile* tiles, int n_tiles, __nv_bfloat16* out, int M,
+                         int n_heads, int head_dim, cudaStream_t stream);
 // Tuning aid: per-CTA clock64 timeline of attention_tc (nullptr disables).
 cudaError_t attention_set_trace(unsigned long long* dev_buf);
 cudaError_t gemm_set_trace(unsigned long long* dev_buf);
