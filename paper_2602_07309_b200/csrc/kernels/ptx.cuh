@@ -35,10 +35,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Blocking wait for the phase with this parity. The suspend-time hint (as
+// CUTLASS's ClusterBarrier) lets the hardware park the warp until the phase
+// completes instead of re-polling; ncu counts ~20% of the attention kernel's
+// instructions as try_wait/branch/yield, but measured per-tile and per-block
+// timings are the same with and without the hint (SRK_MBAR_SUSPEND_NS=0).
+#ifndef SRK_MBAR_SUSPEND_NS
+#define SRK_MBAR_SUSPEND_NS 0x989680
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done;
   do {
+#if SRK_MBAR_SUSPEND_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity), "r"(SRK_MBAR_SUSPEND_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -46,6 +63,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(done)
         : "r"(addr), "r"(parity)
         : "memory");
+#endif
   } while (!done);
 }
 
