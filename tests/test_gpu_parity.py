@@ -340,3 +340,21 @@ def test_single_rank_nccl_sharded_path(cuda):
     local = eng.score(req, 10)
     assert res.topk == [(str(1000 + int(i)), s) for i, s in local.topk]
     assert np.array_equal(res.scores, local.scores)
+
+
+def test_c4_dims_parity(cuda):
+    """BASELINE configs[3] layer shapes (d 2048, 16 heads, ff 6144: the QKV
+    GEMM at N 6144, W_out at K 6144) on two layers, against the C oracle on
+    bf16-rounded weights; a mixed 96/17/1-token request keeps the tails ragged."""
+    cfg = sr.ModelConfig(n_layers=2, d_model=2048, n_heads=16, d_ff=6144, vocab_size=300,
+                         max_seq=4096, head_specs=sr.ModelConfig.default_toy().head_specs)
+    eng = sr.ScoringEngine(sr.init_model(cfg, 2026, "fan_in"))
+    rng = np.random.default_rng(44)
+    prefix = list(rng.integers(0, 256, 256))
+    items = [list(rng.integers(0, 256, n)) for n in (96, 96, 17, 1, 96, 50)]
+    res = eng.score(request(prefix, items), k=3)
+    ref16 = oracle_bf16(cfg, 2026, 1).score(prefix, items)
+    d = np.abs(res.scores - ref16).max()
+    print(f"C4 dims (2 layers): max dev vs oracle(bf16 w) {d:.2e}")
+    assert d <= TOL
+    assert_topk_outside_ties([int(i) for i, _ in res.topk], ref16[:, 0], 3)
