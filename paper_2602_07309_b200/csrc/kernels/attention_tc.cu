@@ -70,7 +70,9 @@ struct AttnCfg {
   static constexpr int V_OFF = K_OFF + 2 * TILE;  // 2 stages
   static constexpr int RED_OFF = V_OFF + 2 * TILE;
   // slots: max exchange by block parity (2 x SL x 128) + row sums (SL x 128)
-  static constexpr int BAR_OFF = RED_OFF + 3 * Slices<HD>::SL * 128 * 4;
+  // + row sums handed to the epilogue warpgroup (2 items x SL x 128)
+  static constexpr int LSUM_OFF = RED_OFF + 3 * Slices<HD>::SL * 128 * 4;
+  static constexpr int BAR_OFF = LSUM_OFF + 2 * Slices<HD>::SL * 128 * 4;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static constexpr int O_COL = 2 * kBK;  // O buffer b at O_COL + b * 128
   static constexpr int TMEM_COLS = 512;
@@ -141,8 +143,11 @@ struct Cursor {
   }
 };
 
-template <int HD>
-__global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
+// EW: a dedicated epilogue warpgroup (warps 12-15) drains each item's O while
+// the softmax warps (4-11) start the next item; setmaxnreg moves registers
+// from the TMA / MMA / epilogue warpgroups to the two softmax warpgroups.
+template <int HD, bool EW>
+__global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv,
                    const __grid_constant__ CUtensorMap tm_out, const RowSpan* __restrict__ spans,
                    const AttnTile* __restrict__ tiles, int n_tiles, __nv_bfloat16* __restrict__ out,
@@ -169,7 +174,11 @@ __global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
   uint64_t* p_full = bars + 14;   // [2]
   uint64_t* pv_done = bars + 16;  // [2]
   uint64_t* o_empty = bars + 18;  // [2] by item parity
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  uint64_t* o_full = bars + 20;   // [2] EW: last PV of the item done
+  uint64_t* l_ready = bars + 22;  // [2] EW: the item's row sums are in smem
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+  float* lsum_slot = reinterpret_cast<float*>(smem + C::LSUM_OFF);  // [2][SL][128]
+  constexpr int SM_BASE = EW ? 4 : 2;  // first softmax warp
 
   const int n_items = n_tiles * n_heads;
   const int d = n_heads * HD;
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
     tma_prefetch_desc(&tm_qkv);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&q_full[s], 1);
-      mbar_init(&q_empty[s], kSoftmaxThreads / 32);  // per softmax warp after its O store
+      mbar_init(&q_empty[s], EW ? 4 : kSoftmaxThreads / 32);  // per storing warp
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
       mbar_init(&v_full[s], 1);
@@ -188,7 +197,9 @@ __global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
       mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], kSoftmaxThreads);
       mbar_init(&pv_done[s], 1);
-      mbar_init(&o_empty[s], kSoftmaxThreads);
+      mbar_init(&o_empty[s], EW ? 128 : kSoftmaxThreads);
+      mbar_init(&o_full[s], 1);
+      mbar_init(&l_ready[s], kSoftmaxThreads);
     }
     fence_barrier_init();
   }
@@ -201,8 +212,15 @@ __global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
+  // EW register split (2 x 128 x 184 + 2 x 128 x 72 = 65536): each role
+  // branch re-budgets its warpgroup first, so ptxas compiles the softmax
+  // code against 184 registers.
+  auto regs_down = [] {
+    if constexpr (EW) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;" ::: "memory");
+  };
 
   if (warp == 0) {
+    regs_down();
     // ------------------------------------------------------------- TMA
     if (lane == 0) {
       const uint64_t keep = policy_evict_last();  // prefix K/V: re-read by every item tile
@@ -210,7 +228,7 @@ __global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
       c.next_item(tiles, n_tiles, n_items, blockIdx.x);
       int g = 0;
       while (c.valid) {
-        if (c.j == 0) {
+        if (!EW && c.j == 0) {  // EW: warp 2 loads Q, ahead of the K/V stream
           const int qb = c.li & 1;
           mbar_wait(&q_empty[qb], ((c.li >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(&q_full[qb], C::TILE);
@@ -238,6 +256,7 @@ __global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
+    regs_down();
     // ------------------------------------------------------------- MMA
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(kTM, kBK);
@@ -285,6 +304,7 @@ __global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
         }
         umma_commit(&v_empty[st]);
         umma_commit(&pv_done[st]);
+        if (EW && pc.j + 1 == pc.nblk) umma_commit(&o_full[ob]);  // the item's O is final
         if (sc.valid) {
           // S_{g+2} reuses this TMEM buffer: PV_g must have read P_g first.
           // (Issuing it right behind PV_g, relying on in-order tcgen05.mma
@@ -297,10 +317,102 @@ __global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
       }
     }
     __syncwarp();
-  } else {
+  } else if (EW && warp == 2) {
+    regs_down();
+    // ------------------------------------------------------ Q loads (EW)
+    // Item i+1's Q loads as soon as the epilogue has released its buffer
+    // (early in item i), instead of when the K/V stream reaches the item.
+    if (lane == 0) {
+      Cursor c;
+      c.next_item(tiles, n_tiles, n_items, blockIdx.x);
+      while (c.valid) {
+        const int qb = c.li & 1;
+        mbar_wait(&q_empty[qb], ((c.li >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], C::TILE);
+        for (int b = 0; b < C::NB; ++b)
+          tma_load_2d(&tm_qkv, &q_full[qb], sQ + qb * C::TILE + b * kBox, c.h * HD + b * 64,
+                      c.t.q_begin);
+        c.j = c.nblk - 1;
+        c.advance(tiles, n_tiles, n_items);
+      }
+    }
+    __syncwarp();
+  } else if (EW && warp < 4) {
+    regs_down();  // warp 3 of the TMA / MMA warpgroup: idle
+  } else if (EW && warp >= 12) {
+    regs_down();
+    // ------------------------------------------ epilogue warpgroup (EW)
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    Cursor c;
+    c.next_item(tiles, n_tiles, n_items, blockIdx.x);
+    while (c.valid) {
+      const int li = c.li, ob = li & 1, h = c.h, row0 = c.t.q_begin;
+      const int row = row0 + r;
+      const bool live = row < c.t.q_end;
+      const uint32_t ph = (li >> 1) & 1;
+      mbar_wait(&l_ready[ob], ph);
+      float lsum = 0.f;
+#pragma unroll
+      for (int k = 0; k < SL; ++k) lsum += lsum_slot[(ob * SL + k) * 128 + r];
+      mbar_wait(&o_full[ob], ph);
+      tc_fence_after();
+      const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+      // O / l -> bf16, staged in the item's Q buffer (every S of the item has
+      // completed) and TMA-stored per 32-row slab; partially-live slabs
+      // (request tails) store their live rows directly.
+      uint8_t* qbuf = sQ + ob * C::TILE;
+      const bool slab_live = __all_sync(0xffffffff, live);
+#pragma unroll 1
+      for (int cc = 0; cc < HD / 32; ++cc) {
+        uint32_t v[32];
+        const int col = cc * 32;
+        tmem_ld_32x32b_x32(tmem + lane_off + C::O_COL + ob * 128 + col, v);
+        tmem_ld_wait();
+        uint4 pk[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float* f = reinterpret_cast<const float*>(&v[q * 8]);
+          pk[q] = make_uint4(pack_bf16x2(f[0] * inv, f[1] * inv), pack_bf16x2(f[2] * inv, f[3] * inv),
+                             pack_bf16x2(f[4] * inv, f[5] * inv), pack_bf16x2(f[6] * inv, f[7] * inv));
+        }
+        if (slab_live) {
+          uint8_t* rowp = qbuf + (col >> 6) * kBox + r * 128;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int chunk = ((col & 63) >> 3) + q;
+            *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) * 16)) = pk[q];
+          }
+        } else if (live) {
+          uint4* dst = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * d + h * HD + col);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dst[q] = pk[q];
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      tc_fence_before();
+      mbar_arrive(&o_empty[ob]);
+      if (lane == 0) {
+        if (slab_live)
+          for (int b = 0; b < C::NB; ++b)
+            tma_store_2d(&tm_out, qbuf + b * kBox + quad * 32 * 128, h * HD + b * 64,
+                         row0 + quad * 32);
+        bulk_commit();
+        bulk_wait_read0();  // the Q buffer is reloaded for item li + 2
+        mbar_arrive(&q_empty[ob]);
+      }
+      // next item (the epilogue walks items, not blocks)
+      c.j = c.nblk - 1;
+      c.advance(tiles, n_tiles, n_items);
+    }
+    if (lane == 0) bulk_wait0();
+  } else if (warp >= SM_BASE && warp < SM_BASE + kSoftmaxThreads / 32) {
+    if constexpr (EW) asm volatile("setmaxnreg.inc.sync.aligned.u32 184;" ::: "memory");
     // ---------------------------------------------------------- softmax
     const int quad = warp & 3;          // TMEM lane quadrant of this warp
-    const int slice = (warp - 2) >> 2;  // keys [slice * KEYS, +KEYS) of every block
+    const int slice = (warp - SM_BASE) >> 2;  // keys [slice * KEYS, +KEYS) of every block
     const int r = quad * 32 + lane;     // tile row owned by this thread (with SL-1 partners)
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const float scale_log2 = 1.4426950408889634f * rsqrtf(static_cast<float>(HD));
@@ -413,7 +525,7 @@ __global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
         const int sb = g & 1;
         const int kh = k0 + slice * KEYS;  // first key of this thread's slice
         mbar_wait(&s_full[sb], (g >> 1) & 1);
-        if (warp == 2 && lane == 0 && g < 24) SRK_TRACE(1 + g);
+        if (warp == SM_BASE && lane == 0 && g < 24) SRK_TRACE(1 + g);
         tc_fence_after();
         float s[KEYS];
         {
@@ -539,14 +651,24 @@ __global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
-        if (warp == 2 && lane == 0 && g < 24) SRK_TRACE(32 + g);
+        if (warp == SM_BASE && lane == 0 && g < 24) SRK_TRACE(32 + g);
         ++g;
         item_done = c.advance(tiles, n_tiles, n_items);
         if (first) {
           first = false;
-          if (pend.on) epilogue(pend);  // previous item, overlapping this item's MMAs
-          pend.on = false;
+          if constexpr (!EW) {
+            if constexpr (!EW) {
+      if (pend.on) epilogue(pend);
+    }  // previous item, overlapping this item's MMAs
+            pend.on = false;
+          }
         }
+      }
+      if constexpr (EW) {
+        // hand the row sums to the epilogue warpgroup and move on
+        lsum_slot[((li & 1) * SL + slice) * 128 + r] = l;
+        mbar_arrive(&l_ready[li & 1]);
+        continue;
       }
       pend.on = true;
       pend.li = li;
@@ -568,11 +690,21 @@ __global__ void __launch_bounds__(Slices<HD>::THREADS, 1)
   if (threadIdx.x == 0) SRK_TRACE(29);
 }
 
-template <int HD>
-cudaError_t launch_tc(const CUtensorMap& tm, const RowSpan* spans, const AttnTile* tiles,
-                      int n_tiles, __nv_bfloat16* out, int M, int n_heads, cudaStream_t stream) {
+// The epilogue-warpgroup variant is the default (SRK_ATTN_EW=0 selects the
+// 10-warp kernel whose softmax warps drain O themselves).
+bool attn_use_ew() {
+  static const bool ew = [] {
+    const char* v = std::getenv("SRK_ATTN_EW");
+    return Slices<128>::SL == 2 && (v == nullptr || std::atoi(v) != 0);
+  }();
+  return ew;
+}
+
+template <int HD, bool EW>
+cudaError_t launch_tc_v(const CUtensorMap& tm, const RowSpan* spans, const AttnTile* tiles,
+                        int n_tiles, __nv_bfloat16* out, int M, int n_heads, cudaStream_t stream) {
   using C = AttnCfg<HD>;
-  auto kern = attn_tc_kernel<HD>;
+  auto kern = attn_tc_kernel<HD, EW>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -587,8 +719,16 @@ cudaError_t launch_tc(const CUtensorMap& tm, const RowSpan* spans, const AttnTil
   cudaGetDevice(&dev);
   const int items = n_tiles * n_heads;
   const int grid = items < num_sms(dev) ? items : num_sms(dev);
-  return launch_k(kern, dim3(grid), dim3(Slices<HD>::THREADS), C::SMEM, stream, tm, tm_out, spans, tiles,
-                  n_tiles, out, n_heads);
+  return launch_k(kern, dim3(grid), dim3(EW ? 512 : Slices<HD>::THREADS), C::SMEM, stream, tm,
+                  tm_out, spans, tiles, n_tiles, out, n_heads);
+}
+
+template <int HD>
+cudaError_t launch_tc(const CUtensorMap& tm, const RowSpan* spans, const AttnTile* tiles,
+                      int n_tiles, __nv_bfloat16* out, int M, int n_heads, cudaStream_t stream) {
+  if (Slices<HD>::SL == 2 && attn_use_ew())
+    return launch_tc_v<HD, true>(tm, spans, tiles, n_tiles, out, M, n_heads, stream);
+  return launch_tc_v<HD, false>(tm, spans, tiles, n_tiles, out, M, n_heads, stream);
 }
 
 
