@@ -282,6 +282,44 @@ int32_t sr_engine_set_postprocess(sr_engine* e, const double* lo, const double* 
 /* Final scores [n_items] of the last score call (post-processing on). */
 int32_t sr_engine_final_scores(sr_engine* e, double* out, int32_t cap, int32_t* n_out);
 
+/* Deterministic score cache (midtier.hpp:16-69, midtier.cpp:14-100; probed
+ * and filled by SearchService::handle_search, service.cpp:160-234). Keys are
+ * (searcher_id, query_signature, entity_id, model_version); LRU over whole
+ * entries, get refreshes recency, a miss mutates nothing, put of a different
+ * row under an existing key is SR_CONSISTENCY, capacity 0 is SR_PARAMETER.
+ * Values are the engine's score rows (n_tasks doubles, column order as
+ * sr_result.scores). Thread-safe (one mutex). */
+typedef struct sr_score_cache sr_score_cache;
+int32_t sr_score_cache_create(int64_t capacity, sr_score_cache** out);
+void sr_score_cache_destroy(sr_score_cache* c);
+int64_t sr_score_cache_size(const sr_score_cache* c);
+int64_t sr_score_cache_capacity(const sr_score_cache* c);
+int32_t sr_score_cache_get(sr_score_cache* c, const char* searcher_id, uint64_t query_signature,
+                           int64_t entity_id, const char* model_version, double* scores,
+                           int32_t n_tasks, int32_t* hit);
+int32_t sr_score_cache_put(sr_score_cache* c, const char* searcher_id, uint64_t query_signature,
+                           int64_t entity_id, const char* model_version, const double* scores,
+                           int32_t n_tasks);
+/* canonical_query (midtier.cpp:14-44): lowercased, whitespace runs collapsed
+ * and trimmed, then "|attr=v1,v2" per attribute (byte order, values sorted).
+ * Filters are n_filters (attrs[i], values[i]) pairs; a repeated attr
+ * collects its values. Writes up to cap bytes (no terminator) and the full
+ * length to *len. sr_query_signature = fnv1a64(canonical_query(...)). */
+int32_t sr_canonical_query(const char* text, int32_t n_filters, const char* const* attrs,
+                           const char* const* values, char* out, int64_t cap, int64_t* len);
+int32_t sr_query_signature(const char* text, int32_t n_filters, const char* const* attrs,
+                           const char* const* values, uint64_t* out);
+uint64_t sr_fnv1a64(const char* data, int64_t len); /* midtier.cpp:46-53 */
+/* handle_search's cache path (service.cpp:160-234) around the device scorer:
+ * probe every item (req->item_ids = entity ids), score only the misses in
+ * one forward pass (request order), put their rows, then rank all rows on
+ * the device (post-processing when set, top-k by (key desc, id asc)).
+ * res->scores receives all rows; *n_hits the cache hits. flops describe the
+ * miss pass (zero when everything hit). */
+int32_t sr_engine_score_cached(sr_engine* e, sr_score_cache* c, const char* searcher_id,
+                               uint64_t query_signature, const char* model_version,
+                               const sr_request* req, sr_result* res, int32_t* n_hits);
+
 /* ------------------------------- exhaustive retrieval top-K
  * The candidate generator upstream of the ranker. Replaces
  *   std::vector<RankedDoc> exhaustive_topk(const Corpus&, const QuerySpec&,

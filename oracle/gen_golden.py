@@ -299,8 +299,53 @@ def wire():
                            "cases": cases})
 
 
+def score_cache():
+    """canonical_query / fnv1a64 / ScoreCache LRU traces (midtier.cpp:14-100)
+    from the reference, incl. test_midtier.cpp:18-85's cases."""
+    queries = [
+        ("Senior  ML Engineer ", [("region", "na"), ("region", "emea")]),
+        ("senior ml engineer", [("region", "emea"), ("region", "na")]),
+        ("nurse", []), ("doctor", []), ("a", [("x", "1")]), ("a", []),
+        ("", []), ("   ", []), ("\tMixed\nCASE  text\r\n", []),
+        ("q", [("b", "2"), ("a", "z"), ("a", "y"), ("B", "1")]),
+        ("Data Scientist", [("seniority", "senior"), ("region", "us"), ("region", "apac")]),
+        ("caf\u00e9 ZURICH", [("lang", "de")]),
+    ]
+    qcases = []
+    for text, filt in queries:
+        canon, h = O.ref_canonical_query(text, filt)
+        qcases.append({"text": text, "filters": filt, "canonical": canon, "fnv1a64": str(h)})
+    traces = []
+    # test_midtier.cpp:27-56 as a script
+    A, B, Cc = ("s", 1, 1, "v"), ("s", 1, 2, "v"), ("s", 1, 3, "v")
+    ops = [(0,) + A + (0.0,), (1,) + A + (0.9,), (0,) + A + (0.0,), (1,) + B + (0.5,),
+           (1,) + Cc + (0.1,), (0,) + A + (0.0,), (0,) + B + (0.0,), (0,) + Cc + (0.0,),
+           (0,) + B + (0.0,), (1,) + A + (0.9,), (0,) + B + (0.0,), (0,) + Cc + (0.0,),
+           (1,) + A + (0.9,), (1,) + A + (0.5,)]
+    st, msg, out = O.ref_cache_trace(2, ops)
+    traces.append({"capacity": 2, "ops": ops, "status": st, "message": msg, "out": out})
+    # random traces over several key fields (searchers, signatures, versions)
+    rng = np.random.default_rng(20261017)
+    for cap in (1, 4, 16):
+        ops = []
+        for _ in range(400):
+            e = int(rng.integers(0, 12))
+            who = ["s", "t"][int(rng.integers(0, 2))]
+            sig = [7, 2**63 + 5][int(rng.integers(0, 2))]
+            ver = ["v", "w"][int(rng.integers(0, 2))]
+            ops.append((int(rng.integers(0, 2)), who, sig, e, ver, float(e) + 0.25 * len(who + ver)))
+        st, msg, out = O.ref_cache_trace(cap, ops)
+        traces.append({"capacity": cap, "ops": ops, "status": st, "message": msg, "out": out})
+    st, msg, _ = O.ref_cache_trace(0, [])
+    dump("score_cache.json", {"source": "canonical_query/fnv1a64/ScoreCache midtier.cpp:14-100 "
+                                        "via oracle/_ref", "queries": qcases, "traces": traces,
+                              "zero_capacity": {"status": st, "message": msg}})
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "wire":
+    if len(sys.argv) > 1 and sys.argv[1] == "score_cache":
+        score_cache()
+    elif len(sys.argv) > 1 and sys.argv[1] == "wire":
         wire()
     elif len(sys.argv) > 1 and sys.argv[1] == "calibration":
         calibration()
@@ -313,3 +358,4 @@ if __name__ == "__main__":
         retrieval()
         calibration()
         wire()
+        score_cache()

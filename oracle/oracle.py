@@ -342,3 +342,47 @@ def ref_decode_f32_base64(text: str):
     if st != 0:
         return None, st - 1, lib.ref_last_error().decode()
     return out[:int(n[0])], 0, ""
+
+
+# ------------------------------------------------------------ score cache
+def ref_canonical_query(text: str, filters):
+    """canonical_query + fnv1a64 (midtier.cpp:14-53) via oracle/_ref.
+    filters: list of (attr, value) pairs."""
+    lib = ref()
+    n = len(filters)
+    A = (C.c_char_p * max(n, 1))(*[a.encode() for a, _ in filters])
+    V = (C.c_char_p * max(n, 1))(*[v.encode() for _, v in filters])
+    cap = 4 * (len(text.encode()) + sum(len(a) + len(v) + 2 for a, v in filters)) + 16
+    out = C.create_string_buffer(cap)
+    ln = C.c_int64(0)
+    h = C.c_uint64(0)
+    fn = lib.ref_canonical_query
+    fn.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p),
+                   C.c_char_p, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
+    st = fn(text.encode(), n, A, V, out, cap, C.byref(ln), C.byref(h))
+    if st != 0:
+        raise RuntimeError(lib.ref_last_error().decode())
+    return out.raw[:ln.value].decode(), int(h.value)
+
+
+def ref_cache_trace(capacity: int, ops):
+    """Run ops [(op, searcher, sig, entity, version, value)] on the
+    reference's ScoreCache -> (status, [(hit_or_status, value, size)])."""
+    lib = ref()
+    n = len(ops)
+    op = np.array([o[0] for o in ops] or [0], np.int32)
+    S = (C.c_char_p * max(n, 1))(*[o[1].encode() for o in ops])
+    sig = np.array([o[2] for o in ops] or [0], np.uint64)
+    ent = np.array([o[3] for o in ops] or [0], np.int64)
+    Vv = (C.c_char_p * max(n, 1))(*[o[4].encode() for o in ops])
+    val = np.array([o[5] for o in ops] or [0], np.float64)
+    hit = np.zeros(max(n, 1), np.int32)
+    outv = np.zeros(max(n, 1), np.float64)
+    size = np.zeros(max(n, 1), np.int64)
+    fn = lib.ref_cache_trace
+    fn.argtypes = [C.c_int64, C.c_int32, i32p, C.POINTER(C.c_char_p), C.POINTER(C.c_uint64), i64p,
+                   C.POINTER(C.c_char_p), f64p, i32p, f64p, i64p]
+    st = fn(capacity, n, _p(op, i32p), S, _p(sig, C.POINTER(C.c_uint64)), _p(ent, i64p), Vv,
+            _p(val, f64p), _p(hit, i32p), _p(outv, f64p), _p(size, i64p))
+    msg = lib.ref_last_error().decode() if st != 0 else ""
+    return st, msg, [(int(hit[i]), float(outv[i]), int(size[i])) for i in range(n)]

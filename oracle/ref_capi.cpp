@@ -25,6 +25,7 @@
 #include "semrank/calibration.hpp"
 #include "semrank/base64.hpp"
 #include "semrank/retrieval.hpp"
+#include "semrank/midtier.hpp"
 #include "semrank/rng.hpp"
 #include "semrank/weights_io.hpp"
 
@@ -327,6 +328,46 @@ int ref_decode_f32_base64(const char* text, int64_t len, float* out, int64_t cap
     const auto v = decode_f32_base64(std::string(text, static_cast<size_t>(len)));
     for (size_t i = 0; i < v.size() && static_cast<int64_t>(i) < cap; ++i) out[i] = v[i];
     *n_out = static_cast<int64_t>(v.size());
+  });
+}
+
+// canonical_query (midtier.cpp:14-44) with filters given as (attr, value)
+// pairs grouped into the reference's map<string, vector<string>>.
+int ref_canonical_query(const char* text, int32_t n, const char* const* attrs,
+                        const char* const* values, char* out, int64_t cap, int64_t* len,
+                        uint64_t* fnv) {
+  return run([&] {
+    std::map<std::string, std::vector<std::string>> filters;
+    for (int32_t i = 0; i < n; ++i) filters[attrs[i]].push_back(values[i]);
+    const auto c = canonical_query(text, filters);
+    std::memcpy(out, c.data(), std::min<size_t>(c.size(), static_cast<size_t>(cap)));
+    *len = static_cast<int64_t>(c.size());
+    *fnv = fnv1a64(c);
+  });
+}
+
+// A scripted ScoreCache trace (midtier.cpp:64-100): op[i] 0 = get, 1 = put
+// of {"relevance": value[i]} under key (searcher[i], sig[i], entity[i],
+// version[i]). out_hit[i] = hit (get) / status (put, 1 + ErrorCode or 0),
+// out_val[i] = the value a hit returned, out_size[i] = size() after the op.
+int ref_cache_trace(int64_t capacity, int32_t n_ops, const int32_t* op,
+                    const char* const* searcher, const uint64_t* sig, const int64_t* entity,
+                    const char* const* version, const double* value, int32_t* out_hit,
+                    double* out_val, int64_t* out_size) {
+  return run([&] {
+    ScoreCache cache(static_cast<std::size_t>(capacity));
+    for (int32_t i = 0; i < n_ops; ++i) {
+      const CacheKey key{searcher[i], sig[i], entity[i], version[i]};
+      out_val[i] = 0.0;
+      if (op[i] == 0) {
+        const auto got = cache.get(key);
+        out_hit[i] = got.has_value() ? 1 : 0;
+        if (got) out_val[i] = got->at("relevance");
+      } else {
+        out_hit[i] = run([&] { cache.put(key, TaskScoreMap{{"relevance", value[i]}}); });
+      }
+      out_size[i] = static_cast<int64_t>(cache.size());
+    }
   });
 }
 

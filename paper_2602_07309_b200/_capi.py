@@ -109,6 +109,18 @@ _sig("sr_wire_item_id", C.c_char_p, vp, i32)
 _sig("sr_engine_score_wire", i32, vp, vp, P(ResultC))
 _sig("sr_engine_set_postprocess", i32, vp, P(f64), P(f64), P(f64), i32, P(i32), P(f64), i32)
 _sig("sr_engine_final_scores", i32, vp, P(f64), i32, P(i32))
+_sig("sr_score_cache_create", i32, i64, P(vp))
+_sig("sr_score_cache_destroy", None, vp)
+_sig("sr_score_cache_size", i64, vp)
+_sig("sr_score_cache_capacity", i64, vp)
+_sig("sr_score_cache_get", i32, vp, C.c_char_p, u64, i64, C.c_char_p, P(f64), i32, P(i32))
+_sig("sr_score_cache_put", i32, vp, C.c_char_p, u64, i64, C.c_char_p, P(f64), i32)
+_sig("sr_canonical_query", i32, C.c_char_p, i32, P(C.c_char_p), P(C.c_char_p), C.c_char_p, i64,
+     P(i64))
+_sig("sr_query_signature", i32, C.c_char_p, i32, P(C.c_char_p), P(C.c_char_p), P(u64))
+_sig("sr_fnv1a64", u64, C.c_char_p, i64)
+_sig("sr_engine_score_cached", i32, vp, vp, C.c_char_p, u64, C.c_char_p, P(RequestC), P(ResultC),
+     P(i32))
 _sig("sr_corpus_create", i32, vp, vp, vp, i64, i32, i32, i32, P(vp))
 _sig("sr_corpus_destroy", None, vp)
 _sig("sr_corpus_topk", i32, vp, vp, i32, f64, vp, i32, vp, i32, P(i64), P(f64), P(i32))
@@ -138,7 +150,10 @@ HEADER_SYMBOLS = [
     "sr_plan_profile", "sr_plan_shape",
     "sr_nccl_unique_id", "sr_comm_create", "sr_comm_destroy", "sr_engine_score_sharded",
     "sr_plan_run_sharded", "sr_engine_score_b64", "sr_wire_parse", "sr_wire_destroy",
-    "sr_wire_info", "sr_wire_request_id", "sr_wire_item_id", "sr_engine_score_wire", "sr_engine_set_postprocess", "sr_engine_final_scores", "sr_corpus_create", "sr_corpus_destroy", "sr_corpus_topk",
+    "sr_wire_info", "sr_wire_request_id", "sr_wire_item_id", "sr_engine_score_wire", "sr_engine_set_postprocess", "sr_engine_final_scores",
+    "sr_score_cache_create", "sr_score_cache_destroy", "sr_score_cache_size",
+    "sr_score_cache_capacity", "sr_score_cache_get", "sr_score_cache_put", "sr_canonical_query",
+    "sr_query_signature", "sr_fnv1a64", "sr_engine_score_cached", "sr_corpus_create", "sr_corpus_destroy", "sr_corpus_topk",
     "sr_corpus_topk_sharded", "sr_corpus_last_candidates", "sr_corpus_last_scan_ms",
     "sr_kernel_gemm", "sr_kernel_gemm_ln", "sr_kernel_attention", "sr_kernel_layernorm",
     "sr_kernel_topk", "sr_debug_attention_trace", "sr_debug_gemm_trace",

@@ -9,6 +9,7 @@
 
 #include "host/engine.hpp"
 #include "host/retrieval.hpp"
+#include "host/score_cache.hpp"
 #include "host/wire.hpp"
 #include "host/model.hpp"
 #include "host/planner.hpp"
@@ -55,6 +56,10 @@ struct sr_wire {
   srh::WireRequest w;
   std::vector<int64_t> ids;  // item ids as doc ids when every id is an integer
   bool numeric_ids = false;
+};
+
+struct sr_score_cache {
+  std::unique_ptr<srh::ScoreCache> c;
 };
 
 struct sr_corpus {
@@ -467,6 +472,94 @@ int32_t sr_engine_final_scores(sr_engine* e, double* out, int32_t cap, int32_t* 
     if (out)
       for (int32_t i = 0; i < std::min(n, cap); ++i) out[i] = f[i];
     *n_out = n;
+  });
+}
+
+int32_t sr_score_cache_create(int64_t capacity, sr_score_cache** out) {
+  return guard([&] {
+    if (!out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    *out = nullptr;
+    if (capacity < 0) srh::fail(SR_PARAMETER, "cache capacity must be >= 1");
+    auto c = std::make_unique<sr_score_cache>();
+    c->c = std::make_unique<srh::ScoreCache>(static_cast<size_t>(capacity));
+    *out = c.release();
+  });
+}
+
+void sr_score_cache_destroy(sr_score_cache* c) { delete c; }
+int64_t sr_score_cache_size(const sr_score_cache* c) {
+  return c ? static_cast<int64_t>(c->c->size()) : -1;
+}
+int64_t sr_score_cache_capacity(const sr_score_cache* c) {
+  return c ? static_cast<int64_t>(c->c->capacity()) : -1;
+}
+
+int32_t sr_score_cache_get(sr_score_cache* c, const char* searcher_id, uint64_t query_signature,
+                           int64_t entity_id, const char* model_version, double* scores,
+                           int32_t n_tasks, int32_t* hit) {
+  return guard([&] {
+    if (!c || !searcher_id || !model_version || !scores || !hit)
+      srh::fail(SR_SPEC_VIOLATION, "null argument");
+    *hit = c->c->get({searcher_id, query_signature, entity_id, model_version}, scores, n_tasks) ? 1 : 0;
+  });
+}
+
+int32_t sr_score_cache_put(sr_score_cache* c, const char* searcher_id, uint64_t query_signature,
+                           int64_t entity_id, const char* model_version, const double* scores,
+                           int32_t n_tasks) {
+  return guard([&] {
+    if (!c || !searcher_id || !model_version || !scores)
+      srh::fail(SR_SPEC_VIOLATION, "null argument");
+    if (n_tasks < 1) srh::fail(SR_PARAMETER, "n_tasks must be >= 1");
+    c->c->put({searcher_id, query_signature, entity_id, model_version}, scores, n_tasks);
+  });
+}
+
+namespace {
+std::string canonical_of(const char* text, int32_t n_filters, const char* const* attrs,
+                         const char* const* values) {
+  if (!text || n_filters < 0 || (n_filters > 0 && (!attrs || !values)))
+    srh::fail(SR_SPEC_VIOLATION, "null argument");
+  std::vector<std::pair<std::string, std::string>> f;
+  f.reserve(static_cast<size_t>(n_filters));
+  for (int32_t i = 0; i < n_filters; ++i) {
+    if (!attrs[i] || !values[i]) srh::fail(SR_SPEC_VIOLATION, "null filter string");
+    f.emplace_back(attrs[i], values[i]);
+  }
+  return srh::canonical_query(text, f);
+}
+}  // namespace
+
+int32_t sr_canonical_query(const char* text, int32_t n_filters, const char* const* attrs,
+                           const char* const* values, char* out, int64_t cap, int64_t* len) {
+  return guard([&] {
+    if (!len) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    const std::string s = canonical_of(text, n_filters, attrs, values);
+    if (out && cap > 0) std::memcpy(out, s.data(), std::min<size_t>(s.size(), static_cast<size_t>(cap)));
+    *len = static_cast<int64_t>(s.size());
+  });
+}
+
+int32_t sr_query_signature(const char* text, int32_t n_filters, const char* const* attrs,
+                           const char* const* values, uint64_t* out) {
+  return guard([&] {
+    if (!out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    *out = srh::fnv1a64(canonical_of(text, n_filters, attrs, values));
+  });
+}
+
+uint64_t sr_fnv1a64(const char* data, int64_t len) {
+  return srh::fnv1a64(data ? data : "", data && len > 0 ? static_cast<size_t>(len) : 0);
+}
+
+int32_t sr_engine_score_cached(sr_engine* e, sr_score_cache* c, const char* searcher_id,
+                               uint64_t query_signature, const char* model_version,
+                               const sr_request* req, sr_result* res, int32_t* n_hits) {
+  return guard([&] {
+    if (!e || !c || !searcher_id || !model_version || !req || !res)
+      srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    e->e->score_cached(*c->c, searcher_id, query_signature, model_version, *req, res, n_hits);
   });
 }
 

@@ -849,4 +849,131 @@ void nccl_allgather_bytes(Comm* c, const void* send, void* recv, size_t bytes, c
              "ncclAllGather");
 }
 
+void Engine::rank(const double* h_scores, const int64_t* ids, int32_t n, sr_result* res) {
+  SR_CUDA_CHECK(cudaSetDevice(device_));
+  const int T = n_tasks();
+  const int32_t k = std::max(0, std::min(res->k, n));
+  if (res->scores && res->scores != h_scores)
+    std::memcpy(res->scores, h_scores, static_cast<size_t>(n) * T * sizeof(double));
+  res->k_returned = k;
+  last_final_.clear();
+  if (n == 0 || (k == 0 && !post_on_)) return;
+  if (k > 4096) fail(SR_PARAMETER, "k must be <= 4096");
+  rk_scores_.ensure(static_cast<size_t>(n) * T);
+  rk_final_.ensure(static_cast<size_t>(n));
+  rk_ids_.ensure(static_cast<size_t>(n));
+  rk_seg_.ensure(2);
+  const int chunks = (n + 4095) / 4096;
+  rk_scratch_.ensure(static_cast<size_t>(chunks) * std::max(k, 1));
+  rk_out_.ensure(static_cast<size_t>(std::max(k, 1)));
+  const int32_t seg[2] = {0, n};
+  SR_CUDA_CHECK(cudaMemcpyAsync(rk_scores_.ptr, h_scores, static_cast<size_t>(n) * T * sizeof(double),
+                                cudaMemcpyHostToDevice, stream_));
+  SR_CUDA_CHECK(cudaMemcpyAsync(rk_ids_.ptr, ids, static_cast<size_t>(n) * sizeof(int64_t),
+                                cudaMemcpyHostToDevice, stream_));
+  SR_CUDA_CHECK(cudaMemcpyAsync(rk_seg_.ptr, seg, sizeof(seg), cudaMemcpyHostToDevice, stream_));
+  const double* key = rk_scores_.ptr;
+  int stride = T;
+  if (post_on_) {
+    SR_CUDA_CHECK(srk::final_scores(rk_scores_.ptr, T, n, post_blocks_.ptr, post_nblocks_,
+                                    post_task_.ptr, post_w_.ptr, post_nblend_, rk_final_.ptr,
+                                    stream_));
+    key = rk_final_.ptr;
+    stride = 1;
+  }
+  std::vector<srk::TopkEntry> top(static_cast<size_t>(k));
+  if (k > 0) {
+    SR_CUDA_CHECK(srk::topk(key, stride, rk_ids_.ptr, rk_seg_.ptr, 1, n, k, rk_scratch_.ptr,
+                            static_cast<int>(rk_scratch_.cap), rk_out_.ptr, stream_));
+    SR_CUDA_CHECK(cudaMemcpyAsync(top.data(), rk_out_.ptr, top.size() * sizeof(srk::TopkEntry),
+                                  cudaMemcpyDeviceToHost, stream_));
+  }
+  if (post_on_) {
+    last_final_.resize(static_cast<size_t>(n));
+    SR_CUDA_CHECK(cudaMemcpyAsync(last_final_.data(), rk_final_.ptr, n * sizeof(double),
+                                  cudaMemcpyDeviceToHost, stream_));
+  }
+  SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  for (int32_t j = 0; j < k; ++j) {
+    if (res->topk_ids) res->topk_ids[j] = top[j].id;
+    if (res->topk_scores) res->topk_scores[j] = top[j].score;
+    if (res->topk_index) res->topk_index[j] = top[j].index;
+  }
+}
+
+void Engine::score_cached(ScoreCache& cache, const std::string& searcher_id, uint64_t signature,
+                          const std::string& model_version, const sr_request& req,
+                          sr_result* res, int32_t* n_hits) {
+  if (req.item_ids == nullptr)
+    fail(SR_SPEC_VIOLATION, "cached scoring needs item_ids (the cache keys' entity ids)");
+  if (req.n_items < 1) fail(SR_SPEC_VIOLATION, "request has no items");
+  if (req.item_offsets == nullptr) fail(SR_SPEC_VIOLATION, "item_offsets is null");
+  const int T = n_tasks();
+  const int32_t n = req.n_items;
+  std::vector<double> rows(static_cast<size_t>(n) * T);
+  std::vector<int32_t> miss;
+  CacheKey key{searcher_id, signature, 0, model_version};
+  for (int32_t i = 0; i < n; ++i) {  // probe everything first (service.cpp:166-180)
+    key.entity_id = req.item_ids[i];
+    if (!cache.get(key, rows.data() + static_cast<size_t>(i) * T, T)) miss.push_back(i);
+  }
+  if (n_hits) *n_hits = n - static_cast<int32_t>(miss.size());
+  if (!miss.empty()) {
+    // The misses as one request, in request order (service.cpp:196-221).
+    const bool mixed = req.mode == SR_MODE_MIXED;
+    const int64_t width = mixed ? cfg_.d_model : 1;
+    const int32_t m = static_cast<int32_t>(miss.size());
+    std::vector<int32_t> off(static_cast<size_t>(m) + 1, 0);
+    std::vector<int64_t> ids(static_cast<size_t>(m));
+    for (int32_t j = 0; j < m; ++j) {
+      const int32_t i = miss[j];
+      const int32_t len = req.item_offsets[i + 1] - req.item_offsets[i];
+      if (len < 0) fail(SR_SPEC_VIOLATION, "item_offsets must be non-decreasing");
+      off[j + 1] = off[j] + len;
+      ids[j] = req.item_ids[i];
+    }
+    std::vector<int32_t> toks;
+    std::vector<float> soft;
+    sr_request sub = req;
+    sub.n_items = m;
+    sub.item_offsets = off.data();
+    sub.item_ids = ids.data();
+    if (m == n) {
+      sub.item_tokens = req.item_tokens;
+      sub.item_rows = req.item_rows;
+    } else if (mixed) {
+      if (req.item_rows == nullptr) fail(SR_SPEC_VIOLATION, "item_rows is null");
+      soft.resize(static_cast<size_t>(off[m]) * width);
+      for (int32_t j = 0; j < m; ++j)
+        std::memcpy(soft.data() + static_cast<size_t>(off[j]) * width,
+                    req.item_rows + static_cast<size_t>(req.item_offsets[miss[j]]) * width,
+                    static_cast<size_t>(off[j + 1] - off[j]) * width * sizeof(float));
+      sub.item_rows = soft.data();
+    } else {
+      if (req.item_tokens == nullptr) fail(SR_SPEC_VIOLATION, "item_tokens is null");
+      toks.resize(static_cast<size_t>(off[m]));
+      for (int32_t j = 0; j < m; ++j)
+        std::memcpy(toks.data() + off[j], req.item_tokens + req.item_offsets[miss[j]],
+                    static_cast<size_t>(off[j + 1] - off[j]) * sizeof(int32_t));
+      sub.item_tokens = toks.data();
+    }
+    std::vector<double> got(static_cast<size_t>(m) * T);
+    sr_result sr{};
+    sr.scores = got.data();
+    score(&sub, 1, &sr);
+    res->flops = sr.flops;
+    res->kv_incremental_per_item = sr.kv_incremental_per_item;
+    for (int32_t j = 0; j < m; ++j) {  // service.cpp:225-233
+      std::memcpy(rows.data() + static_cast<size_t>(miss[j]) * T, got.data() + static_cast<size_t>(j) * T,
+                  T * sizeof(double));
+      key.entity_id = ids[j];
+      cache.put(key, got.data() + static_cast<size_t>(j) * T, T);
+    }
+  } else {
+    res->flops = sr_flop_report{};
+    res->kv_incremental_per_item = 0.0;
+  }
+  rank(rows.data(), req.item_ids, n, res);
+}
+
 }  // namespace srh

@@ -16,6 +16,7 @@
 
 #include "../kernels/launch.h"
 #include "model.hpp"
+#include "score_cache.hpp"
 #include "planner.hpp"
 
 namespace srh {
@@ -161,6 +162,18 @@ class Engine {
                        const char* b, int64_t lb, const int64_t* begin, const int64_t* end,
                        int32_t n_items, const int64_t* item_ids, sr_result* res);
 
+  // Ranks given raw score rows [n x n_tasks] (host): upload, the same
+  // post-processing and top-k kernels as the forward's tail, fetch. Used by
+  // score_cached, whose rows come partly from the cache.
+  void rank(const double* h_scores, const int64_t* ids, int32_t n, sr_result* res);
+  // handle_search's cache probe (service.cpp:160-234): rows of cached items
+  // come from `cache`, only the misses go through the forward (one pass, in
+  // request order), their rows are put back, then all rows are ranked.
+  // req.item_ids are the entity ids of the cache keys.
+  void score_cached(ScoreCache& cache, const std::string& searcher_id, uint64_t signature,
+                    const std::string& model_version, const sr_request& req, sr_result* res,
+                    int32_t* n_hits);
+
   // Sharded: local pass + NCCL all-gather of per-rank top-k + merge.
   void run_plan_sharded(Plan& p, struct Comm* comm);
 
@@ -193,6 +206,11 @@ class Engine {
   DevBuf<double> post_blocks_, post_w_;
   DevBuf<int32_t> post_task_;
   std::vector<double> last_final_;
+  // rank(): device rows, ids, one segment, top-k
+  DevBuf<double> rk_scores_, rk_final_;
+  DevBuf<int64_t> rk_ids_;
+  DevBuf<int32_t> rk_seg_;
+  DevBuf<srk::TopkEntry> rk_scratch_, rk_out_;
   // pending base64 source of the mixed request being packed (score_b64)
   struct B64Src {
     const char* a = nullptr;  // text = a ++ b

@@ -19,7 +19,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 from dataclasses import dataclass, field
-from typing import Dict, List, Optional, Sequence
+from typing import Dict, List, Mapping, Optional, Sequence
 
 import numpy as np
 
@@ -266,6 +266,7 @@ class ScoreResult:
     topk: List[tuple] = field(default_factory=list)  # (item_id, relevance or final score)
     scores: Optional[np.ndarray] = None  # [n_items x n_tasks], col 0 relevance
     final_scores: Optional[np.ndarray] = None  # [n_items] with post-processing on
+    cache_hits: int = 0  # score_cached: items served from the ScoreCache
 
 
 class MultiItemMask:  # engine.hpp:63-72
@@ -489,6 +490,89 @@ class CalibrationHead:  # calibration.hpp:17-27 (fitted offline by fit_isotonic)
         return bool(self.blocks)
 
 
+def _filter_arrays(filters: Optional[Mapping[str, Sequence[str]]]):
+    pairs = [(a, v) for a, vs in (filters or {}).items() for v in vs]
+    attrs = (C.c_char_p * max(len(pairs), 1))(*[a.encode() for a, _ in pairs])
+    vals = (C.c_char_p * max(len(pairs), 1))(*[v.encode() for _, v in pairs])
+    return len(pairs), attrs, vals
+
+
+def canonical_query(query_text: str, filters: Optional[Mapping[str, Sequence[str]]] = None) -> str:
+    """midtier.cpp:14-44 (native): lowercase, collapse and trim whitespace,
+    then ``|attr=v1,v2`` per attribute in sorted order with sorted values."""
+    n, attrs, vals = _filter_arrays(filters)
+    text = query_text.encode()
+    ln = C.c_int64(0)
+    _check(_lib.sr_canonical_query(text, n, attrs, vals, None, 0, C.byref(ln)))
+    buf = C.create_string_buffer(max(ln.value, 1))
+    _check(_lib.sr_canonical_query(text, n, attrs, vals, buf, ln.value, C.byref(ln)))
+    return buf.raw[:ln.value].decode()
+
+
+def fnv1a64(text) -> int:  # midtier.cpp:46-53
+    raw = text.encode() if isinstance(text, str) else bytes(text)
+    return int(_lib.sr_fnv1a64(raw, len(raw)))
+
+
+def query_signature(query_text: str, filters: Optional[Mapping[str, Sequence[str]]] = None) -> int:
+    """fnv1a64(canonical_query(...)), the signature handle_search keys the cache with."""
+    n, attrs, vals = _filter_arrays(filters)
+    out = C.c_uint64(0)
+    _check(_lib.sr_query_signature(query_text.encode(), n, attrs, vals, C.byref(out)))
+    return int(out.value)
+
+
+@dataclass(frozen=True)
+class CacheKey:  # midtier.hpp:30-37
+    searcher_id: str
+    query_signature: int
+    entity_id: int
+    model_version: str
+
+
+class ScoreCache:
+    """ScoreCache (midtier.hpp:42-69) in native code: LRU over whole entries,
+    get refreshes recency, a conflicting put raises Consistency. Rows are
+    stored in ``task_names`` order (the engine's: relevance, then heads)."""
+
+    def __init__(self, capacity: int, task_names: Optional[Sequence[str]] = None):
+        if task_names is None:
+            task_names = [kRelevanceTask] + [h.name for h in ModelConfig.default_toy().head_specs]
+        self.task_names = list(task_names)
+        h = C.c_void_p()
+        _check(_lib.sr_score_cache_create(int(capacity), C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.sr_score_cache_destroy(h)
+            self._h = C.c_void_p()
+
+    def get(self, key: CacheKey) -> Optional[Dict[str, float]]:
+        row = np.zeros(len(self.task_names), np.float64)
+        hit = C.c_int32(0)
+        _check(_lib.sr_score_cache_get(self._h, key.searcher_id.encode(), key.query_signature,
+                                       key.entity_id, key.model_version.encode(),
+                                       row.ctypes.data_as(C.POINTER(C.c_double)), len(row),
+                                       C.byref(hit)))
+        return dict(zip(self.task_names, row.tolist())) if hit.value else None
+
+    def put(self, key: CacheKey, scores: Mapping[str, float]) -> None:
+        if set(scores) != set(self.task_names):
+            raise SemrankError(ErrorCode.Alignment, "score map does not match the cache's tasks")
+        row = np.array([scores[t] for t in self.task_names], np.float64)
+        _check(_lib.sr_score_cache_put(self._h, key.searcher_id.encode(), key.query_signature,
+                                       key.entity_id, key.model_version.encode(),
+                                       row.ctypes.data_as(C.POINTER(C.c_double)), len(row)))
+
+    def size(self) -> int:
+        return int(_lib.sr_score_cache_size(self._h))
+
+    def capacity(self) -> int:
+        return int(_lib.sr_score_cache_capacity(self._h))
+
+
 class ScoringEngine:
     """ScoringEngine (engine.hpp:109-119) bound to one B200; serialises callers."""
 
@@ -529,6 +613,34 @@ class ScoringEngine:
             pr = _PackedRequest(request, self.config.d_model)
             _check(_lib.sr_engine_score(self._h, C.byref(pr.c), C.byref(rb.c)))
         res = self._to_result(request, rb)
+        if self._post:
+            res.final_scores = self._final(len(request.items))
+        return res
+
+    def score_cached(self, request: ScoreRequest, cache: ScoreCache, searcher_id: str,
+                     query_signature: int, k: int = 0, model_version: Optional[str] = None,
+                     entity_ids: Optional[Sequence[int]] = None) -> ScoreResult:
+        """handle_search's cache path (service.cpp:160-234): cached items are
+        served from ``cache``, the misses are scored in one device pass and put
+        back, then every row is ranked on the device. Item ids (or
+        ``entity_ids``) are the cache keys' entity ids; ``model_version``
+        defaults to the weights' version string."""
+        if cache.task_names != self.task_names:
+            raise SemrankError(ErrorCode.Alignment, "cache tasks differ from the engine's tasks")
+        ids = (np.ascontiguousarray(np.asarray(entity_ids, np.int64)) if entity_ids is not None
+               else _item_doc_ids(request.items))
+        if ids is None:
+            raise SemrankError(ErrorCode.SpecViolation,
+                               "cached scoring needs integer entity ids (item ids or entity_ids)")
+        pr = _PackedRequest(request, self.config.d_model, ids)
+        rb = _ResultBuf(len(request.items), len(self.task_names), k)
+        hits = C.c_int32(0)
+        version = self.weights.version if model_version is None else model_version
+        _check(_lib.sr_engine_score_cached(self._h, cache._h, searcher_id.encode(),
+                                           int(query_signature), version.encode(),
+                                           C.byref(pr.c), C.byref(rb.c), C.byref(hits)))
+        res = self._to_result(request, rb)
+        res.cache_hits = hits.value
         if self._post:
             res.final_scores = self._final(len(request.items))
         return res

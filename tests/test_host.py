@@ -287,3 +287,71 @@ def test_native_wire_parser_follows_parse_score_request_json():
     for body, code, text in cases:
         st, msg, _ = _wire(body, max_seq=4)
         assert st == code and text in msg, (body, st, msg)
+
+
+def _grouped(filters):
+    out = {}
+    for a, v in filters:
+        out.setdefault(a, []).append(v)
+    return out
+
+
+def test_canonical_query_and_signature_match_reference_golden():
+    """midtier.cpp:14-53 (test_midtier.cpp:18-25 plus whitespace / case /
+    non-ASCII / multi-attribute cases), golden from oracle/_ref."""
+    g = gold("score_cache.json")
+    for c in g["queries"]:
+        f = _grouped(c["filters"])
+        assert sr.canonical_query(c["text"], f) == c["canonical"], c
+        assert sr.query_signature(c["text"], f) == int(c["fnv1a64"]), c
+        assert sr.fnv1a64(c["canonical"]) == int(c["fnv1a64"])
+    assert sr.fnv1a64("") == 1469598103934665603  # midtier.cpp:47's basis
+
+
+def test_score_cache_lru_traces_match_reference_golden():
+    """ScoreCache (midtier.cpp:64-100): hits, misses, recency, eviction,
+    idempotent and conflicting puts, replayed from the reference's traces."""
+    g = gold("score_cache.json")
+    for t in g["traces"]:
+        cache = sr.ScoreCache(t["capacity"], task_names=["relevance"])
+        for (op, who, sig, ent, ver, val), (want, want_val, want_size) in zip(t["ops"], t["out"]):
+            key = sr.CacheKey(who, int(sig), int(ent), ver)
+            if op == 0:
+                got = cache.get(key)
+                assert (got is not None) == bool(want)
+                if got is not None:
+                    assert got["relevance"] == want_val
+            else:
+                try:
+                    cache.put(key, {"relevance": val})
+                    st = 0
+                except sr.SemrankError as e:
+                    st = int(e.code)
+                    assert "conflicting scores for one cache key" in str(e)
+                assert st == want
+            assert cache.size() == want_size
+        assert cache.capacity() == t["capacity"]
+    with pytest.raises(sr.SemrankError) as ei:
+        sr.ScoreCache(0)
+    assert int(ei.value.code) == g["zero_capacity"]["status"]
+    assert g["zero_capacity"]["message"] in str(ei.value)
+
+
+def test_score_cache_concurrent_readers_and_writers():
+    """test_midtier.cpp / test_service.cpp:393-410: one mutex, no lost entries."""
+    import threading
+    cache = sr.ScoreCache(64, task_names=["relevance"])
+
+    def work(t):
+        for i in range(200):
+            key = sr.CacheKey("s", t, i % 32, "v")
+            cache.put(key, {"relevance": float(i % 32)})
+            got = cache.get(key)
+            assert got is None or got["relevance"] == float(i % 32)
+
+    ths = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert cache.size() <= 64
