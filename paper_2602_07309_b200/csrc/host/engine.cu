@@ -480,9 +480,7 @@ void Engine::refill_plan(Plan& p, const sr_request* reqs, int n_req) {
                                       reinterpret_cast<uint8_t*>(p.soft.ptr + off * d),
                                       b64_err_.ptr, stream_));
       } else {
-        SR_CUDA_CHECK(cudaMemcpyAsync(p.soft.ptr + off * d, src.rows,
-                                      src.n_rows * d * sizeof(float), cudaMemcpyHostToDevice,
-                                      stream_));
+        up_.upload(p.soft.ptr + off * d, src.rows, src.n_rows * d * sizeof(float), stream_);
       }
       off += src.n_rows;
     }
@@ -624,12 +622,9 @@ void Engine::upload_b64_text() {
   b64_text_.ensure(static_cast<size_t>(std::max<int64_t>(chars, 4)));
   b64_off_.ensure(static_cast<size_t>(3 * std::max(n, 1)));
   b64_err_.ensure(1);
-  if (b64_.la > 0)
-    SR_CUDA_CHECK(cudaMemcpyAsync(b64_text_.ptr, b64_.a, static_cast<size_t>(b64_.la),
-                                  cudaMemcpyHostToDevice, stream_));
+  if (b64_.la > 0) up_.upload(b64_text_.ptr, b64_.a, static_cast<size_t>(b64_.la), stream_);
   if (b64_.lb > 0)
-    SR_CUDA_CHECK(cudaMemcpyAsync(b64_text_.ptr + b64_.la, b64_.b, static_cast<size_t>(b64_.lb),
-                                  cudaMemcpyHostToDevice, stream_));
+    up_.upload(b64_text_.ptr + b64_.la, b64_.b, static_cast<size_t>(b64_.lb), stream_);
   SR_CUDA_CHECK(cudaMemcpyAsync(b64_off_.ptr, b64_.spans.data(), b64_.spans.size() * sizeof(int64_t),
                                 cudaMemcpyHostToDevice, stream_));
   SR_CUDA_CHECK(cudaMemsetAsync(b64_err_.ptr, 0xff, sizeof(unsigned long long), stream_));

@@ -16,6 +16,7 @@
 
 #include "../kernels/launch.h"
 #include "model.hpp"
+#include "h2d.hpp"
 #include "score_cache.hpp"
 #include "planner.hpp"
 
@@ -224,6 +225,7 @@ class Engine {
   DevBuf<int64_t> b64_off_;
   DevBuf<unsigned long long> b64_err_;
   void upload_b64_text();
+  StagedUpload up_;  // caller-buffer uploads (soft rows, base64 text)
   std::vector<LayerDev> layers_;
   std::vector<void*> allocs_;
   // workspace
