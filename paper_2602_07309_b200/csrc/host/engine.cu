@@ -847,18 +847,21 @@ void nccl_allgather_bytes(Comm* c, const void* send, void* recv, size_t bytes, c
 void Engine::rank(const double* h_scores, const int64_t* ids, int32_t n, sr_result* res) {
   SR_CUDA_CHECK(cudaSetDevice(device_));
   const int T = n_tasks();
-  const int32_t k = std::max(0, std::min(res->k, n));
+  if (res->k < 0) fail(SR_PARAMETER, "top-k must be >= 0");
+  const int32_t k = std::min(res->k, n);
   if (res->scores && res->scores != h_scores)
     std::memcpy(res->scores, h_scores, static_cast<size_t>(n) * T * sizeof(double));
   res->k_returned = k;
   last_final_.clear();
   if (n == 0 || (k == 0 && !post_on_)) return;
-  if (k > 4096) fail(SR_PARAMETER, "k must be <= 4096");
+  if (k > 4096) fail(SR_PARAMETER, "top-k must be <= 4096");
+  const int chunks = (n + 4095) / 4096;
+  if (k > 0 && chunks > 1 && static_cast<long>(chunks) * k > 4096)
+    fail(SR_PARAMETER, "top-k too large for this many candidates");
   rk_scores_.ensure(static_cast<size_t>(n) * T);
   rk_final_.ensure(static_cast<size_t>(n));
   rk_ids_.ensure(static_cast<size_t>(n));
   rk_seg_.ensure(2);
-  const int chunks = (n + 4095) / 4096;
   rk_scratch_.ensure(static_cast<size_t>(chunks) * std::max(k, 1));
   rk_out_.ensure(static_cast<size_t>(std::max(k, 1)));
   const int32_t seg[2] = {0, n};
