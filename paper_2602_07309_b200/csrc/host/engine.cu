@@ -906,6 +906,8 @@ void Engine::score_cached(ScoreCache& cache, const std::string& searcher_id, uin
     fail(SR_SPEC_VIOLATION, "cached scoring needs item_ids (the cache keys' entity ids)");
   if (req.n_items < 1) fail(SR_SPEC_VIOLATION, "request has no items");
   if (req.item_offsets == nullptr) fail(SR_SPEC_VIOLATION, "item_offsets is null");
+  if (res->k < 0) fail(SR_PARAMETER, "top-k must be >= 0");
+  if (res->k > 4096) fail(SR_PARAMETER, "top-k must be <= 4096");
   const int T = n_tasks();
   const int32_t n = req.n_items;
   std::vector<double> rows(static_cast<size_t>(n) * T);
