@@ -422,6 +422,37 @@ class _LazyItemScores(Sequence):
         return repr(self._build())
 
 
+class _WireIds(Sequence):
+    """Item ids of a parsed /score body, read from the native handle on
+    demand (the handle and the body it points into live as long as this)."""
+
+    def __init__(self, h, raw: bytes, n: int):
+        self._h, self._raw, self._n, self._cache = h, raw, n, None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.sr_wire_destroy(h)
+            self._h = C.c_void_p()
+
+    def __len__(self):
+        return self._n
+
+    def __getitem__(self, i):
+        if self._cache is None:
+            if isinstance(i, slice):
+                return [self[j] for j in range(*i.indices(self._n))]
+            if not -self._n <= i < self._n:
+                raise IndexError(i)
+            return _lib.sr_wire_item_id(self._h, i % self._n).decode()
+        return self._cache[i]
+
+    def __iter__(self):
+        if self._cache is None:
+            self._cache = [_lib.sr_wire_item_id(self._h, i).decode() for i in range(self._n)]
+        return iter(self._cache)
+
+
 class _PackedRequest:
     """Flattened sr_request; keeps the numpy buffers alive."""
 
@@ -652,20 +683,28 @@ class ScoringEngine:
         raw = body.encode("utf-8") if isinstance(body, str) else bytes(body)
         h = C.c_void_p()
         _check(_lib.sr_wire_parse(raw, len(raw), max_seq or self.config.max_seq, C.byref(h)))
+        n, mode, tq = C.c_int32(), C.c_int32(), C.c_int32()
+        ids = None
         try:
-            n, mode, tq = C.c_int32(), C.c_int32(), C.c_int32()
             _check(_lib.sr_wire_info(h, C.byref(n), C.byref(mode), C.byref(tq)))
+            ids = _WireIds(h, raw, n.value)  # owns the handle from here on
             rb = _ResultBuf(n.value, len(self.task_names), k)
             _check(_lib.sr_engine_score_wire(self._h, h, C.byref(rb.c)))
-            ids = [_lib.sr_wire_item_id(h, i).decode() for i in range(n.value)]
-            req = ScoreRequest(request_id=_lib.sr_wire_request_id(h).decode(), mode=ScoreMode(mode.value),
-                               items=[ScoreItem(id=i) for i in ids])
+            rid = _lib.sr_wire_request_id(h).decode()
         finally:
-            _lib.sr_wire_destroy(h)
-        del raw
-        res = self._to_result(req, rb)
+            if ids is None:
+                _lib.sr_wire_destroy(h)
+        nv = n.value
+        res = ScoreResult(request_id=rid, mode=ScoreMode(mode.value),
+                          flops=FlopReport._from_c(rb.c.flops),
+                          kv_incremental_per_item=rb.c.kv_incremental_per_item,
+                          scores=rb.scores[:nv].copy())
+        res.items = _LazyItemScores(ids, res.scores, self.task_names)
+        for j in range(rb.c.k_returned):
+            res.topk.append((ids[int(rb.idx[j])] if rb.idx[j] >= 0 else str(rb.ids[j]),
+                             float(rb.top[j])))
         if self._post:
-            res.final_scores = self._final(n.value)
+            res.final_scores = self._final(nv)
         return res
 
     def _score_b64(self, request: ScoreRequest, rb: "_ResultBuf") -> None:

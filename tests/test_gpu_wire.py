@@ -119,6 +119,8 @@ def test_native_wire_path_matches_python_parse(cuda):
     want = eng.score(sr.parse_score_request_json(b, d), k=5)
     assert np.array_equal(got.scores, want.scores) and got.topk == want.topk
     assert [it.item_id for it in got.items] == [str(i) for i in range(100, 123)]
+    assert got.request_id == want.request_id and got.mode == want.mode
+    assert got.items[3].tasks == want.items[3].tasks
     toks = json.dumps({"request_id": "t", "prefix_text": "query: shoes", "mode": "multi_item",
                        "items": [{"id": str(i), "text": f"item {i} text"} for i in range(40)]})
     got = eng.score_json(toks, k=7)
