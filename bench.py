@@ -510,9 +510,10 @@ def run_retrieval(args):
                     "d2h_bytes_per_step": 16 * k + 8,
                     "path": "DeviceCorpus.topk -> sr_corpus_topk (host query in, host top-K out)"},
             "gpu_launches": 4 * args.steps, "clocks": clocks,
-            "roofline": {"bound": "hbm", "kernel": "retrieval_scan_kernel (fp32 pass)",
+            "roofline": {"bound": "hbm", "kernel": "retrieval_scan_bulk_kernel (fp32 TMA-streamed pass)",
                          "achieved": achieved, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                         "frac": achieved / peaks.get("hbm_gbs", 1.0), "traffic": None,
+                         "frac": achieved / peaks.get("hbm_gbs", 1.0),
+                         "traffic": load_traffic().get(f"{args.workload}_scan_dram_bytes_per_launch"),
                          "peak_source": f"{peak_kind} hbm_gbs",
                          "algorithmic_bytes_per_launch": n * bytes_per_doc,
                          "scan_ms": scan_ms, "candidates_rescored": corpus.last_candidates()},

@@ -176,14 +176,29 @@ __global__ void __launch_bounds__(kScanThreads)
 // reads its row as float4s in a rotated order (chunk (j + t) mod D/4), which
 // spreads each quarter-warp over distinct bank groups; the fp32 pass needs
 // only the error bound, not the reference's summation order.
-constexpr int kBulkStages = 3;
+//
+// Occupancy decides the bandwidth: the per-tile compute (two block barriers,
+// the candidate test) is serial within a CTA, so more CTAs per SM beat deeper
+// rings. Measured at 33.5M x d 32 (bench retrieval_xl): 1 CTA x 6 stages 0.51
+// of HBM peak, 2 CTAs x 3 stages (2048 candidates) 0.82, 3 CTAs x 2 stages
+// (1024 candidates) 0.98. The 3-CTA shape serves k <= 256; larger k (up to
+// kCandCap / 4 = 512) takes the 2-CTA shape.
 constexpr int kBulkTileBytes = 32768;
 
+template <int STAGES, int CAND>
+struct ScanShape {
+  static constexpr size_t smem(int D) {
+    return STAGES * kBulkTileBytes + CAND * sizeof(Cand) +
+           static_cast<size_t>((D + 3) & ~3) * sizeof(float) + 64;
+  }
+};
+
+template <int kBulkStages, int kCandCap>
 __global__ void __launch_bounds__(kScanThreads)
     retrieval_scan_bulk_kernel(RetrievalScan a, int32_t* __restrict__ g_cand, int g_cap,
                                int32_t* __restrict__ counters, long long docs_per_cta, int rows) {
   pdl_wait();
-  // dynamic smem: ring [3][32 KB] | candidates [kCandCap] | query [D] | barriers
+  // dynamic smem: ring [STAGES][32 KB] | candidates [CAND] | query [D] | barriers
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* ring = smem_raw;
   Cand* cand = reinterpret_cast<Cand*>(smem_raw + kBulkStages * kBulkTileBytes);
@@ -418,17 +433,21 @@ cudaError_t retrieval_scan(const RetrievalScan& a, int32_t* cand, int cand_cap, 
     const int rows = min(kScanThreads, kBulkTileBytes / (a.D * 4));
     int dev = 0;
     cudaGetDevice(&dev);
-    const int g2 = min(grid, 2 * num_sms(dev));  // two 100 KB CTAs per SM
+    const bool small_k = a.k <= 256;
+    const int per_sm = small_k ? 3 : 2;
+    const int g2 = min(grid, per_sm * num_sms(dev));
     long long per = (a.n + g2 - 1) / g2;
     per = (per + rows - 1) / rows * rows;
     const int blocks = static_cast<int>((a.n + per - 1) / per);
-    const size_t smem = kBulkStages * kBulkTileBytes + kCandCap * sizeof(Cand) +
-                        static_cast<size_t>((a.D + 3) & ~3) * sizeof(float) + 64;
-    e = cudaFuncSetAttribute(retrieval_scan_bulk_kernel,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    return launch_k(retrieval_scan_bulk_kernel, dim3(blocks), dim3(kScanThreads), smem, stream, a,
-                    cand, cand_cap, counters, per, rows);
+    auto go = [&](auto kern, size_t smem) {
+      cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (r != cudaSuccess) return r;
+      return launch_k(kern, dim3(blocks), dim3(kScanThreads), smem, stream, a, cand, cand_cap,
+                      counters, per, rows);
+    };
+    if (small_k) return go(retrieval_scan_bulk_kernel<2, 1024>, ScanShape<2, 1024>::smem(a.D));
+    return go(retrieval_scan_bulk_kernel<3, kCandCap>, ScanShape<3, kCandCap>::smem(a.D));
   }
   long long per = (a.n + grid - 1) / grid;
   per = (per + kScanThreads - 1) / kScanThreads * kScanThreads;

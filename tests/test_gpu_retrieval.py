@@ -37,6 +37,8 @@ def test_golden_cases_bit_identical(cuda):
     (5000, 7, 0, 512, True, True),       # D % 4 != 0, no features, k = max
     (10, 4, 1, 50, False, True),         # k above the corpus size
     (20_000, 16, 1, 1500, True, True),   # k > 512: full device sort path
+    (300_000, 32, 1, 256, True, True),   # largest k of the 3-CTA x 1024-candidate scan
+    (60_000, 32, 2, 400, False, False),  # 257..512: the 2-CTA x 2048-candidate scan
 ])
 def test_random_corpora_match_oracle(cuda, n, d, f, k, filt, unit):
     emb, feat, ids, color = random_corpus(n + d, n, d, f, unit=unit)
