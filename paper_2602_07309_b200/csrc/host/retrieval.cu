@@ -77,8 +77,10 @@ long long Corpus::prepare(const float* query, int d_query, double w0, const doub
   for (int i = 0; i < d_; ++i) na += static_cast<double>(query[i]) * query[i];
   if (na == 0.0) fail(SR_DEGENERATE_INPUT, "cosine of a zero vector");
   // staging: [q32 (d) | w32 (f)] as float, [qd (d) | wd (f)] as double
-  std::vector<float> f32(d_ + f_ + 1);
-  std::vector<double> f64(d_ + f_ + 1);
+  h32_.ensure(static_cast<size_t>(d_ + f_ + 1));
+  h64_.ensure(static_cast<size_t>(d_ + f_ + 1));
+  float* f32 = h32_.ptr;
+  double* f64 = h64_.ptr;
   for (int i = 0; i < d_; ++i) {
     f32[i] = query[i];
     f64[i] = static_cast<double>(query[i]);
@@ -91,10 +93,10 @@ long long Corpus::prepare(const float* query, int d_query, double w0, const doub
   }
   float* v32 = reinterpret_cast<float*>(vec_);
   double* v64 = vec_ + (d_ + f_ + 2);
-  SR_CUDA_CHECK(cudaMemcpyAsync(v32, f32.data(), f32.size() * sizeof(float), cudaMemcpyHostToDevice,
+  SR_CUDA_CHECK(cudaMemcpyAsync(v32, f32, (d_ + f_ + 1) * sizeof(float), cudaMemcpyHostToDevice,
                                 stream_));
-  SR_CUDA_CHECK(cudaMemcpyAsync(v64, f64.data(), f64.size() * sizeof(double),
-                                cudaMemcpyHostToDevice, stream_));
+  SR_CUDA_CHECK(cudaMemcpyAsync(v64, f64, (d_ + f_ + 1) * sizeof(double), cudaMemcpyHostToDevice,
+                                stream_));
   if (keep != nullptr)
     SR_CUDA_CHECK(cudaMemcpyAsync(keep_, keep, static_cast<size_t>(n_), cudaMemcpyHostToDevice,
                                   stream_));
@@ -133,8 +135,10 @@ int Corpus::topk(const float* query, int d_query, double w0, const double* w, in
     SR_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 2 * sizeof(int32_t), stream_));
     entries_.ensure(static_cast<size_t>(n_));
     SR_CUDA_CHECK(srk::retrieval_refine(a, nullptr, n_, entries_.ptr, counters_, stream_));
-    int32_t cnt[2] = {0, 0};
-    SR_CUDA_CHECK(cudaMemcpyAsync(cnt, counters_, sizeof(cnt), cudaMemcpyDeviceToHost, stream_));
+    hcnt_.ensure(2);
+    int32_t* cnt = hcnt_.ptr;
+    SR_CUDA_CHECK(cudaMemcpyAsync(cnt, counters_, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                  stream_));
     SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
     if (cnt[1] & 1) fail(SR_DEGENERATE_INPUT, "cosine of a zero vector");
     const size_t bytes = srk::retrieval_sort_scratch(n_);
@@ -150,8 +154,10 @@ int Corpus::topk(const float* query, int d_query, double w0, const double* w, in
   SR_CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
   SR_CUDA_CHECK(srk::retrieval_scan(a, cand_, cand_cap_, counters_, grid_, stream_));
   SR_CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
-  int32_t cnt[2] = {0, 0};
-  SR_CUDA_CHECK(cudaMemcpyAsync(cnt, counters_, sizeof(cnt), cudaMemcpyDeviceToHost, stream_));
+  hcnt_.ensure(2);
+  int32_t* cnt = hcnt_.ptr;
+  SR_CUDA_CHECK(cudaMemcpyAsync(cnt, counters_, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                stream_));
   SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
   SR_CUDA_CHECK(cudaEventElapsedTime(&last_scan_ms_, ev_[0], ev_[1]));
   if (cnt[1] & 1) fail(SR_DEGENERATE_INPUT, "cosine of a zero vector");
@@ -172,9 +178,10 @@ int Corpus::topk_host(const float* query, int d_query, double w0, const double* 
   out_.ensure(static_cast<size_t>(std::max(k, 1)));
   const int n = topk(query, d_query, w0, w, n_w, keep, k, out_.ptr);
   if (n == 0) return 0;
-  std::vector<srk::TopkEntry> h(n);
-  SR_CUDA_CHECK(cudaMemcpyAsync(h.data(), out_.ptr, sizeof(srk::TopkEntry) * n,
-                                cudaMemcpyDeviceToHost, stream_));
+  hout_.ensure(static_cast<size_t>(n));
+  srk::TopkEntry* h = hout_.ptr;
+  SR_CUDA_CHECK(cudaMemcpyAsync(h, out_.ptr, sizeof(srk::TopkEntry) * n, cudaMemcpyDeviceToHost,
+                                stream_));
   SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
   for (int j = 0; j < n; ++j) {
     if (ids_out) ids_out[j] = h[j].id;

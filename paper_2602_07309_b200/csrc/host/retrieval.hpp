@@ -70,6 +70,25 @@ class Corpus {
       cap = n;
     }
   };
+  template <typename T>
+  struct Pinned {  // page-locked host staging: small copies stay asynchronous
+    T* ptr = nullptr;
+    size_t cap = 0;
+    ~Pinned() {
+      if (ptr) cudaFreeHost(ptr);
+    }
+    void ensure(size_t n) {
+      if (n <= cap) return;
+      if (ptr) cudaFreeHost(ptr);
+      ptr = nullptr;
+      SR_CUDA_CHECK(cudaMallocHost(&ptr, n * sizeof(T)));
+      cap = n;
+    }
+  };
+  Pinned<float> h32_;
+  Pinned<double> h64_;
+  Pinned<int32_t> hcnt_;
+  Pinned<srk::TopkEntry> hout_;
   Buf<srk::TopkEntry> entries_, select_, out_, gathered_, merged_;
   Buf<uint8_t> sort_;
   static constexpr int kScanMaxK = 512;  // the fp32 pass keeps <= 2048 candidates per CTA

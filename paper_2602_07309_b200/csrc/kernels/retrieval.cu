@@ -184,6 +184,9 @@ __global__ void __launch_bounds__(kScanThreads)
 // (1024 candidates) 0.98. The 3-CTA shape serves k <= 256; larger k (up to
 // kCandCap / 4 = 512) takes the 2-CTA shape.
 constexpr int kBulkTileBytes = 32768;
+#ifndef SRK_SCAN_MIN_DOCS_PER_K
+#define SRK_SCAN_MIN_DOCS_PER_K 16
+#endif
 
 template <int STAGES, int CAND>
 struct ScanShape {
@@ -437,6 +440,9 @@ cudaError_t retrieval_scan(const RetrievalScan& a, int32_t* cand, int cand_cap, 
     const int per_sm = small_k ? 3 : 2;
     const int g2 = min(grid, per_sm * num_sms(dev));
     long long per = (a.n + g2 - 1) / g2;
+    // each CTA keeps ~k candidates: small corpora get fewer, longer CTAs so
+    // the exact rescoring does not see most of the corpus
+    per = std::max<long long>(per, static_cast<long long>(SRK_SCAN_MIN_DOCS_PER_K) * a.k);
     per = (per + rows - 1) / rows * rows;
     const int blocks = static_cast<int>((a.n + per - 1) / per);
     auto go = [&](auto kern, size_t smem) {
