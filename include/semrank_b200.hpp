@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -165,6 +166,94 @@ struct ScoreResult {  // engine.hpp:53-59 (+ topk)
 
 inline constexpr const char* kRelevanceTask = "relevance";
 
+// ----------------------------------------------- mid-tier score cache
+// midtier.hpp:16-69 over sr_score_cache / sr_canonical_query / sr_fnv1a64.
+inline std::string canonical_query(const std::string& query_text,
+                                   const std::map<std::string, std::vector<std::string>>& filters) {
+  std::vector<const char*> attrs, values;
+  for (const auto& [attr, vs] : filters)
+    for (const auto& v : vs) {
+      attrs.push_back(attr.c_str());
+      values.push_back(v.c_str());
+    }
+  int64_t len = 0;
+  const int32_t n = static_cast<int32_t>(attrs.size());
+  check(sr_canonical_query(query_text.c_str(), n, attrs.data(), values.data(), nullptr, 0, &len));
+  std::string out(static_cast<size_t>(len), '\0');
+  check(sr_canonical_query(query_text.c_str(), n, attrs.data(), values.data(), out.data(), len,
+                           &len));
+  return out;
+}
+
+inline std::uint64_t fnv1a64(const std::string& text) {
+  return sr_fnv1a64(text.data(), static_cast<int64_t>(text.size()));
+}
+
+struct CacheKey {  // midtier.hpp:30-37
+  std::string searcher_id;
+  std::uint64_t query_signature = 0;
+  std::int64_t entity_id = 0;
+  std::string model_version;
+  bool operator==(const CacheKey& o) const {
+    return searcher_id == o.searcher_id && query_signature == o.query_signature &&
+           entity_id == o.entity_id && model_version == o.model_version;
+  }
+};
+
+using TaskScoreMap = std::map<std::string, double>;
+
+class ScoreCache {  // midtier.hpp:42-69; rows kept in task order
+ public:
+  explicit ScoreCache(std::size_t capacity)
+      : ScoreCache(capacity, default_tasks()) {}
+  ScoreCache(std::size_t capacity, std::vector<std::string> task_names)
+      : tasks_(std::move(task_names)) {
+    sr_score_cache* c = nullptr;
+    check(sr_score_cache_create(static_cast<int64_t>(capacity), &c));
+    c_.reset(c);
+  }
+  std::optional<TaskScoreMap> get(const CacheKey& key) {
+    std::vector<double> row(tasks_.size());
+    int32_t hit = 0;
+    check(sr_score_cache_get(c_.get(), key.searcher_id.c_str(), key.query_signature, key.entity_id,
+                             key.model_version.c_str(), row.data(),
+                             static_cast<int32_t>(row.size()), &hit));
+    if (!hit) return std::nullopt;
+    TaskScoreMap m;
+    for (size_t i = 0; i < tasks_.size(); ++i) m[tasks_[i]] = row[i];
+    return m;
+  }
+  void put(const CacheKey& key, const TaskScoreMap& scores) {
+    std::vector<double> row;
+    for (const auto& t : tasks_) {
+      const auto it = scores.find(t);
+      if (it == scores.end() || scores.size() != tasks_.size())
+        throw Error(ErrorCode::Alignment, "score map does not match the cache's tasks");
+      row.push_back(it->second);
+    }
+    check(sr_score_cache_put(c_.get(), key.searcher_id.c_str(), key.query_signature, key.entity_id,
+                             key.model_version.c_str(), row.data(),
+                             static_cast<int32_t>(row.size())));
+  }
+  std::size_t size() const { return static_cast<std::size_t>(sr_score_cache_size(c_.get())); }
+  std::size_t capacity() const {
+    return static_cast<std::size_t>(sr_score_cache_capacity(c_.get()));
+  }
+  sr_score_cache* handle() const { return c_.get(); }
+
+ private:
+  static std::vector<std::string> default_tasks() {
+    std::vector<std::string> t{kRelevanceTask};
+    for (const auto& h : ModelConfig::default_toy().head_specs) t.push_back(h.name);
+    return t;
+  }
+  struct Del {
+    void operator()(sr_score_cache* c) const { sr_score_cache_destroy(c); }
+  };
+  std::vector<std::string> tasks_;
+  std::unique_ptr<sr_score_cache, Del> c_;
+};
+
 class ScoringEngine {  // engine.hpp:109-119
  public:
   explicit ScoringEngine(const ModelWeights& weights, int device = 0) : weights_(weights) {
@@ -175,60 +264,96 @@ class ScoringEngine {  // engine.hpp:109-119
   const ModelWeights& weights() const { return weights_; }
 
   ScoreResult score(const ScoreRequest& request, int k = 0) {
-    const int d = weights_.config.d_model;
-    const bool mixed = request.mode == ScoreMode::Mixed;
-    std::vector<int32_t> prefix(request.prefix_tokens.begin(), request.prefix_tokens.end());
-    std::vector<int32_t> off{0}, toks;
-    std::vector<float> rows;
-    std::vector<int64_t> ids;
-    bool numeric_ids = true;
-    for (const auto& it : request.items) {
-      if (mixed) {
-        if (it.n_emb_tokens < 1 || it.embedding.size() != static_cast<size_t>(it.n_emb_tokens) * d)
-          throw Error(ErrorCode::PayloadInvalid,
-                      "item " + it.id + " embedding payload is not [n x " + std::to_string(d) + "]");
-        rows.insert(rows.end(), it.embedding.begin(), it.embedding.end());
-        off.push_back(off.back() + it.n_emb_tokens);
-      } else {
-        toks.insert(toks.end(), it.tokens.begin(), it.tokens.end());
-        off.push_back(off.back() + static_cast<int32_t>(it.tokens.size()));
-      }
-      try {
-        size_t pos = 0;
-        ids.push_back(std::stoll(it.id, &pos));
-        numeric_ids = numeric_ids && pos == it.id.size();
-      } catch (...) {
-        numeric_ids = false;
-      }
-    }
-    sr_request req{prefix.data(), static_cast<int32_t>(prefix.size()),
-                   static_cast<int32_t>(request.items.size()), off.data(),
-                   toks.empty() ? nullptr : toks.data(), rows.empty() ? nullptr : rows.data(),
-                   numeric_ids ? ids.data() : nullptr, static_cast<int32_t>(request.mode)};
-    const int T = 1 + static_cast<int>(weights_.config.head_specs.size());
-    std::vector<double> scores(request.items.size() * T);
-    std::vector<int64_t> tid(k > 0 ? k : 1);
-    std::vector<double> tsc(k > 0 ? k : 1);
-    std::vector<int32_t> tix(k > 0 ? k : 1);
-    sr_result res{scores.data(), k, tid.data(), tsc.data(), tix.data(), {}, 0, 0};
-    check(sr_engine_score(e_.get(), &req, &res));
-    ScoreResult out;
-    out.request_id = request.request_id;
-    out.mode = request.mode;
-    out.flops = {res.flops.attention_units, res.flops.linear_units, res.flops.t_q,
-                 res.flops.t_i_mean, res.flops.n_items};
-    out.kv_incremental_per_item = res.kv_incremental_per_item;
-    for (size_t i = 0; i < request.items.size(); ++i) {
-      ItemScores s{request.items[i].id, {}};
-      s.tasks[kRelevanceTask] = scores[i * T];
-      for (int h = 1; h < T; ++h) s.tasks[weights_.config.head_specs[h - 1].name] = scores[i * T + h];
-      out.items.push_back(std::move(s));
-    }
-    for (int j = 0; j < res.k_returned; ++j) out.topk.push_back({request.items[tix[j]].id, tsc[j]});
-    return out;
+    Packed p(request, weights_.config.d_model);
+    Out o(request.items.size(), 1 + weights_.config.head_specs.size(), k);
+    check(sr_engine_score(e_.get(), &p.req, &o.res));
+    return o.result(request, weights_.config);
+  }
+
+  // handle_search's cache probe -> score misses -> put (service.cpp:160-234),
+  // then the page ranking on the device. Item ids must be integers (the cache
+  // keys' entity ids); *hits receives the number of cached items.
+  ScoreResult score_cached(const ScoreRequest& request, ScoreCache& cache,
+                           const std::string& searcher_id, std::uint64_t signature, int k = 0,
+                           int* hits = nullptr) {
+    Packed p(request, weights_.config.d_model);
+    if (!p.numeric_ids)
+      throw Error(ErrorCode::SpecViolation, "cached scoring needs integer item ids");
+    Out o(request.items.size(), 1 + weights_.config.head_specs.size(), k);
+    int32_t h = 0;
+    check(sr_engine_score_cached(e_.get(), cache.handle(), searcher_id.c_str(), signature,
+                                 weights_.version.c_str(), &p.req, &o.res, &h));
+    if (hits) *hits = h;
+    return o.result(request, weights_.config);
   }
 
  private:
+  struct Packed {  // sr_request over the request's flattened arrays
+    std::vector<int32_t> prefix, off{0}, toks;
+    std::vector<float> rows;
+    std::vector<int64_t> ids;
+    bool numeric_ids = true;
+    sr_request req{};
+    Packed(const ScoreRequest& request, int d) {
+      const bool mixed = request.mode == ScoreMode::Mixed;
+      prefix.assign(request.prefix_tokens.begin(), request.prefix_tokens.end());
+      for (const auto& it : request.items) {
+        if (mixed) {
+          if (it.n_emb_tokens < 1 ||
+              it.embedding.size() != static_cast<size_t>(it.n_emb_tokens) * d)
+            throw Error(ErrorCode::PayloadInvalid, "item " + it.id +
+                                                       " embedding payload is not [n x " +
+                                                       std::to_string(d) + "]");
+          rows.insert(rows.end(), it.embedding.begin(), it.embedding.end());
+          off.push_back(off.back() + it.n_emb_tokens);
+        } else {
+          toks.insert(toks.end(), it.tokens.begin(), it.tokens.end());
+          off.push_back(off.back() + static_cast<int32_t>(it.tokens.size()));
+        }
+        try {
+          size_t pos = 0;
+          ids.push_back(std::stoll(it.id, &pos));
+          numeric_ids = numeric_ids && pos == it.id.size();
+        } catch (...) {
+          numeric_ids = false;
+        }
+      }
+      req = sr_request{prefix.data(), static_cast<int32_t>(prefix.size()),
+                       static_cast<int32_t>(request.items.size()), off.data(),
+                       toks.empty() ? nullptr : toks.data(), rows.empty() ? nullptr : rows.data(),
+                       numeric_ids ? ids.data() : nullptr, static_cast<int32_t>(request.mode)};
+    }
+  };
+  struct Out {  // caller-side result buffers
+    size_t T;
+    std::vector<double> scores, tsc;
+    std::vector<int64_t> tid;
+    std::vector<int32_t> tix;
+    sr_result res{};
+    Out(size_t n, size_t tasks, int k)
+        : T(tasks), scores(n * tasks), tsc(k > 0 ? k : 1), tid(k > 0 ? k : 1),
+          tix(k > 0 ? k : 1) {
+      res = sr_result{scores.data(), k, tid.data(), tsc.data(), tix.data(), {}, 0, 0};
+    }
+    ScoreResult result(const ScoreRequest& request, const ModelConfig& cfg) const {
+      ScoreResult out;
+      out.request_id = request.request_id;
+      out.mode = request.mode;
+      out.flops = {res.flops.attention_units, res.flops.linear_units, res.flops.t_q,
+                   res.flops.t_i_mean, res.flops.n_items};
+      out.kv_incremental_per_item = res.kv_incremental_per_item;
+      for (size_t i = 0; i < request.items.size(); ++i) {
+        ItemScores s{request.items[i].id, {}};
+        s.tasks[kRelevanceTask] = scores[i * T];
+        for (size_t h = 1; h < T; ++h) s.tasks[cfg.head_specs[h - 1].name] = scores[i * T + h];
+        out.items.push_back(std::move(s));
+      }
+      for (int j = 0; j < res.k_returned; ++j)
+        out.topk.push_back({request.items[tix[j]].id, tsc[j]});
+      return out;
+    }
+  };
+
   struct Del {
     void operator()(sr_engine* e) const { sr_engine_destroy(e); }
   };

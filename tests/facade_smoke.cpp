@@ -22,6 +22,26 @@ int main(int argc, char** argv) {
   } catch (const Error& e) {
     if (e.code() != ErrorCode::SpecViolation) return 5;
   }
+  // mid-tier cache (test_midtier.cpp:18-56; signature from tests/golden/score_cache.json)
+  const auto canon = canonical_query("Senior  ML Engineer ", {{"region", {"na", "emea"}}});
+  if (canon != "senior ml engineer|region=emea,na") return 7;
+  if (fnv1a64(canon) != 9702648040046958735ull) return 8;
+  {
+    ScoreCache cache(2, {"relevance"});
+    const CacheKey ka{"s", 1, 1, "v"}, kb{"s", 1, 2, "v"}, kc{"s", 1, 3, "v"};
+    if (cache.get(ka)) return 9;
+    cache.put(ka, {{"relevance", 0.9}});
+    if (!cache.get(ka) || cache.get(ka)->at("relevance") != 0.9) return 10;
+    cache.put(kb, {{"relevance", 0.5}});
+    cache.put(kc, {{"relevance", 0.1}});
+    if (cache.size() != 2 || cache.get(ka) || !cache.get(kb) || !cache.get(kc)) return 11;
+    try {
+      cache.put(kb, {{"relevance", 0.6}});
+      return 12;
+    } catch (const Error& e) {
+      if (e.code() != ErrorCode::Consistency) return 13;
+    }
+  }
   if (argc > 1 && std::string(argv[1]) == "gpu") {
     ScoringEngine engine(w, 0);
     ScoreRequest req;
@@ -36,6 +56,16 @@ int main(int argc, char** argv) {
     }
     const auto r = engine.score(req, 2);
     if (r.items.size() != 4 || r.topk.size() != 2) return 6;
+    ScoreCache cache(16);
+    const auto sig = fnv1a64(canonical_query("nurse", {}));
+    int hits = -1;
+    const auto c1 = engine.score_cached(req, cache, "s", sig, 2, &hits);
+    if (hits != 0 || cache.size() != 4) return 14;
+    const auto c2 = engine.score_cached(req, cache, "s", sig, 2, &hits);
+    if (hits != 4) return 15;
+    for (int i = 0; i < 4; ++i)
+      if (c1.items[i].tasks != r.items[i].tasks || c2.items[i].tasks != r.items[i].tasks) return 16;
+    if (c2.topk != r.topk) return 17;
     std::printf("relevance[0]=%.6f top=%s\n", r.items[0].tasks.at(kRelevanceTask),
                 r.topk[0].first.c_str());
   }
