@@ -294,6 +294,15 @@ struct alignas(64) GemmLnArgs {
 #ifndef SRK_RESID_LN_STAGES
 #define SRK_RESID_LN_STAGES 5
 #endif
+// EPI_RESID_F32 (O / W_out add-reduction epilogue): staging buffers per
+// epilogue warp and ring depth (2 buffers let chunk c's reduction overlap the
+// TMEM drain of chunk c + 1, paid for with one ring stage).
+#ifndef SRK_RESID_STG_BUFS
+#define SRK_RESID_STG_BUFS SRK_PAIR_STG_BUFS
+#endif
+#ifndef SRK_RESID_STAGES
+#define SRK_RESID_STAGES SRK_PAIR_STAGES
+#endif
 template <int EPI>
 struct GemmPairCfg {
   static constexpr int BM = 128;  // rows per CTA (pair: 256)
@@ -307,10 +316,13 @@ struct GemmPairCfg {
   // variant with 16x256b TMEM loads was measured slower: 8 rows x 32 B per
   // store instruction made the epilogue LSU-bound, 2-3x the staged time.)
   static constexpr bool RESID_LN = EPI == EPI_RESID_LN;
-  static constexpr int STAGES = RESID_LN ? SRK_RESID_LN_STAGES : SRK_PAIR_STAGES;
+  static constexpr bool RESID_F32 = EPI == EPI_RESID_F32;
+  static constexpr int STAGES =
+      RESID_LN ? SRK_RESID_LN_STAGES : (RESID_F32 ? SRK_RESID_STAGES : SRK_PAIR_STAGES);
   static constexpr int TMEM_COLS = 2 * BN;  // double-buffered 128 x 256 fp32
   static constexpr int EPI_WARPS = 8;
-  static constexpr int STG_BUFS = RESID_LN ? 2 : SRK_PAIR_STG_BUFS;  // per epilogue warp
+  static constexpr int STG_BUFS =  // per epilogue warp
+      RESID_LN ? 2 : (RESID_F32 ? SRK_RESID_STG_BUFS : SRK_PAIR_STG_BUFS);
   static constexpr int STG_BYTES = 32 * 128;
   static constexpr int BAR_BYTES = 512;
   static constexpr int SMEM_BYTES =
