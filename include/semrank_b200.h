@@ -60,6 +60,14 @@ typedef enum sr_score_mode {
   SR_MODE_MIXED = 3
 } sr_score_mode;
 
+/* Mixed-mode items given as compact per-item embeddings (sr_engine_score_emb). */
+typedef enum sr_emb_form {
+  SR_EMB_PAD = 0,     /* one soft row per item: the embedding zero-padded (or cut) to
+                         d_model, as SearchService::handle_search and cmd_score build
+                         mixed items (service.cpp:208-217, semrank_main.cpp:362-368) */
+  SR_EMB_PROJECT = 1  /* n_soft rows per item = emb . P (sr_engine_set_projection) */
+} sr_emb_form;
+
 /* Weight-init schemes for sr_weights_init. */
 typedef enum sr_init_scheme {
   SR_INIT_REFERENCE = 0, /* init_model (model.cpp:94-134): N(0, 0.08^2) clamped to +-1 */
@@ -185,6 +193,28 @@ int32_t sr_request_report(const sr_model_config* cfg, const sr_request* req,
 int32_t sr_topk_host(const double* scores, const int64_t* ids, int32_t n, int32_t k,
                      int64_t* ids_out, double* scores_out, int32_t* index_out);
 
+/* build_prompt (prompt.cpp:14-38, prompt.hpp:17-25): prefix = system +
+ * query_context, item = document + "\nRelevant (Yes/No): ", both byte-
+ * tokenised (tokenizer.cpp:10-20). SR_LENGTH_OVERFLOW when the two exceed
+ * max_seq, then SR_SPEC_VIOLATION for an empty prefix (the reference's
+ * order and messages). Writes up to *_cap tokens; *n_prefix / *n_item get the
+ * full lengths (call with cap 0 to size the buffers). */
+int32_t sr_build_prompt(const char* system, int64_t system_len, const char* query_context,
+                        int64_t query_len, const char* document, int64_t document_len,
+                        int32_t max_seq, int32_t* prefix_out, int32_t prefix_cap,
+                        int32_t* n_prefix, int32_t* item_out, int32_t item_cap, int32_t* n_item);
+/* score_result_to_json (service.cpp:380-391), the /score response body, byte
+ * for byte as the reference's nlohmann::json dump(): {"flops":{"attention",
+ * "linear"},"request_id","scores":[{"id","tasks":{name: p, ...}}]} with keys
+ * sorted. scores is [n_items x n_tasks] (sr_result.scores layout), column t
+ * named task_names[t]. Writes up to cap bytes (no terminator); *len = full
+ * length. SR_PAYLOAD_INVALID for ids/names that are not valid UTF-8. */
+int32_t sr_score_result_to_json(const char* request_id, int32_t n_items,
+                                const char* const* item_ids, int32_t n_tasks,
+                                const char* const* task_names, const double* scores,
+                                const sr_flop_report* flops, char* out, int64_t cap,
+                                int64_t* len);
+
 /* ------------------------------------------------------------------ engine */
 /* ScoringEngine(const ModelWeights&) (engine.hpp:109-119), bound to a device:
  * converts the GEMM weights to bf16 K-major on the device once. */
@@ -199,6 +229,22 @@ int32_t sr_engine_score_batch(sr_engine* e, const sr_request* reqs, int32_t n_re
 /* Debug/parity: final-LN hidden row at each item's last position
  * ([n_items x d_model] fp32), i.e. the row task_scores() consumes. */
 int32_t sr_engine_item_hidden(sr_engine* e, const sr_request* req, float* hidden_out);
+/* Context compression with precomputed item embeddings (north_star (d);
+ * the reference injects d_model-wide rows only). P is the
+ * projection in the reference's weight layout [d_emb x n_soft*d_model]
+ * (row-major, model.hpp:42-47); item i's soft rows are
+ *   rows_i = reshape(bf16(emb_i) . bf16(P), [n_soft x d_model])
+ * computed on the tensor cores with fp32 accumulation inside the forward, so
+ * only [n x d_emb] floats cross PCIe. proj == NULL removes it. */
+int32_t sr_engine_set_projection(sr_engine* e, const float* proj, int32_t d_emb, int32_t n_soft);
+/* Scores items given as emb [n_items x d_emb] fp32 (row-major) in mixed mode
+ * (score_mixed, engine.cpp:238-276) with the rows of `form` (sr_emb_form).
+ * SR_STATE_INVALID for SR_EMB_PROJECT without a projection, SR_ALIGNMENT when
+ * d_emb differs from the projection's, SR_PAYLOAD_INVALID for no items or
+ * d_emb < 1. FlopReport / kv as score_mixed with 1 or n_soft rows per item. */
+int32_t sr_engine_score_emb(sr_engine* e, const int32_t* prefix, int32_t t_q, const float* emb,
+                            int32_t d_emb, int32_t n_items, const int64_t* item_ids,
+                            int32_t form, sr_result* res);
 /* Device / stream the engine runs on. */
 int32_t sr_engine_device(const sr_engine* e);
 void* sr_engine_stream(const sr_engine* e);
@@ -209,6 +255,11 @@ int32_t sr_plan_create(sr_engine* e, const sr_request* req, int32_t k, sr_plan**
 /* Several requests packed into one resident pass (per-request top-k). */
 int32_t sr_plan_create_batch(sr_engine* e, const sr_request* reqs, int32_t n_req, int32_t k,
                              sr_plan** out);
+/* Resident compact-embedding request (sr_engine_score_emb's inputs); the
+ * pad / projection step is part of the plan's graph. */
+int32_t sr_plan_create_emb(sr_engine* e, const int32_t* prefix, int32_t t_q, const float* emb,
+                           int32_t d_emb, int32_t n_items, const int64_t* item_ids, int32_t form,
+                           int32_t k, sr_plan** out);
 /* Results of a batch plan: res[i] receives request i. */
 int32_t sr_plan_fetch_batch(sr_plan* p, sr_result* res, int32_t n_req);
 int32_t sr_plan_run(sr_plan* p);         /* enqueue on the engine stream; async */

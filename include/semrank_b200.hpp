@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -101,9 +102,27 @@ class ModelWeights {  // model.hpp:56-67, owning handle
     for (int i = 0; i < c.n_task_heads; ++i)
       config.head_specs.push_back({c.head_names[i], c.head_arity[i]});
     version = sr_weights_version(w);
+    for (size_t i = 0; i < sr_weights_tensor_count(w); ++i) {
+      const char* name = nullptr;
+      float* data = nullptr;
+      size_t numel = 0;
+      check(sr_weights_tensor(w, i, &name, &data, &numel));
+      if (std::string(name) == "tok_emb") tok_emb = TensorView{data, numel};
+      if (std::string(name) == "pos_emb") pos_emb = TensorView{data, numel};
+    }
   }
+  // Read-only views of the embedding tables (model.hpp:58-59: tok_emb
+  // [V x d], pos_emb [max_seq x d]); valid while any copy of the handle lives.
+  struct TensorView {
+    const float* p = nullptr;
+    size_t n = 0;
+    const float* data() const { return p; }
+    size_t size() const { return n; }
+    float operator[](size_t i) const { return p[i]; }
+  };
   ModelConfig config;
   std::string version;
+  TensorView tok_emb, pos_emb;
   const sr_weights* handle() const { return w_.get(); }
 
  private:
@@ -264,10 +283,18 @@ class ScoringEngine {  // engine.hpp:109-119
   const ModelWeights& weights() const { return weights_; }
 
   ScoreResult score(const ScoreRequest& request, int k = 0) {
-    Packed p(request, weights_.config.d_model);
+    return score_as(request, request.mode, k);
+  }
+
+  // Scores `request` as if request.mode were `mode` (the free score_naive /
+  // score_ibpc / ... functions of engine.hpp:77-86).
+  ScoreResult score_as(const ScoreRequest& request, ScoreMode mode, int k = 0) {
+    Packed p(request, weights_.config.d_model, mode);
     Out o(request.items.size(), 1 + weights_.config.head_specs.size(), k);
     check(sr_engine_score(e_.get(), &p.req, &o.res));
-    return o.result(request, weights_.config);
+    auto r = o.result(request, weights_.config);
+    r.mode = mode;
+    return r;
   }
 
   // handle_search's cache probe -> score misses -> put (service.cpp:160-234),
@@ -294,8 +321,9 @@ class ScoringEngine {  // engine.hpp:109-119
     std::vector<int64_t> ids;
     bool numeric_ids = true;
     sr_request req{};
-    Packed(const ScoreRequest& request, int d) {
-      const bool mixed = request.mode == ScoreMode::Mixed;
+    Packed(const ScoreRequest& request, int d) : Packed(request, d, request.mode) {}
+    Packed(const ScoreRequest& request, int d, ScoreMode mode) {
+      const bool mixed = mode == ScoreMode::Mixed;
       prefix.assign(request.prefix_tokens.begin(), request.prefix_tokens.end());
       for (const auto& it : request.items) {
         if (mixed) {
@@ -321,7 +349,7 @@ class ScoringEngine {  // engine.hpp:109-119
       req = sr_request{prefix.data(), static_cast<int32_t>(prefix.size()),
                        static_cast<int32_t>(request.items.size()), off.data(),
                        toks.empty() ? nullptr : toks.data(), rows.empty() ? nullptr : rows.data(),
-                       numeric_ids ? ids.data() : nullptr, static_cast<int32_t>(request.mode)};
+                       numeric_ids ? ids.data() : nullptr, static_cast<int32_t>(mode)};
     }
   };
   struct Out {  // caller-side result buffers
@@ -363,6 +391,104 @@ class ScoringEngine {  // engine.hpp:109-119
 
 inline ScoreResult score_by_mode(ScoringEngine& engine, const ScoreRequest& request) {
   return engine.score(request);  // engine.cpp:379-387
+}
+
+// ------------------------------------------- reference free functions
+// engine.hpp:77-89 take the weights, not an engine. Each ModelWeights handle
+// gets one process-wide ScoringEngine on the default device (created on first
+// use, kept for the handle's lifetime in this process), so callers such as
+// semrank_main.cpp:293/376/657 and acceptance_main.cpp:90-174 relink
+// unchanged. ScoringEngine serialises calls on it (engine.cpp:389-392).
+namespace detail {
+inline int& default_device() {
+  static int d = 0;
+  return d;
+}
+inline ScoringEngine& engine_for(const ModelWeights& w) {
+  static std::mutex mu;
+  static std::map<const sr_weights*, std::unique_ptr<ScoringEngine>> engines;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& e = engines[w.handle()];
+  if (!e) e = std::make_unique<ScoringEngine>(w, default_device());
+  return *e;
+}
+}  // namespace detail
+
+// Device used by the weights-level functions below (default 0).
+inline void set_default_device(int device) { detail::default_device() = device; }
+
+inline ScoreResult score_naive(const ModelWeights& w, const ScoreRequest& r) {
+  return detail::engine_for(w).score_as(r, ScoreMode::Naive);
+}
+inline ScoreResult score_ibpc(const ModelWeights& w, const ScoreRequest& r) {
+  return detail::engine_for(w).score_as(r, ScoreMode::Ibpc);
+}
+// One pass: the whole packed sequence must fit max_seq (engine.cpp:189-200);
+// when it fits, the chunked accounting below is the single-pass one.
+inline ScoreResult score_multi_item(const ModelWeights& w, const ScoreRequest& r) {
+  long total = static_cast<long>(r.prefix_tokens.size());
+  for (const auto& it : r.items) total += static_cast<long>(it.tokens.size());
+  if (total > w.config.max_seq)
+    throw Error(ErrorCode::LengthOverflow,
+                "multi-item sequence of " + std::to_string(total) + " exceeds max_seq " +
+                    std::to_string(w.config.max_seq) + "; split the request into smaller batches");
+  return detail::engine_for(w).score_as(r, ScoreMode::MultiItem);
+}
+// No prefix re-payment on the device (the packed pass has no max_seq chunk
+// limit); FlopReport still reports the reference's chunked accounting.
+inline ScoreResult score_multi_item_chunked(const ModelWeights& w, const ScoreRequest& r) {
+  return detail::engine_for(w).score_as(r, ScoreMode::MultiItem);
+}
+inline ScoreResult score_mixed(const ModelWeights& w, const ScoreRequest& r) {
+  return detail::engine_for(w).score_as(r, ScoreMode::Mixed);
+}
+inline ScoreResult score_by_mode(const ModelWeights& w, const ScoreRequest& r) {
+  return detail::engine_for(w).score(r);  // engine.cpp:379-387
+}
+
+// ------------------------------------------------ prompt + /score body
+struct PromptParts {  // prompt.hpp:17-20
+  std::vector<int> prefix_tokens;
+  std::vector<int> item_tokens;
+};
+inline constexpr const char* kPromptSuffix = "\nRelevant (Yes/No): ";  // prompt.hpp:23
+
+inline PromptParts build_prompt(const std::string& system, const std::string& query_context,
+                                const std::string& document, int max_seq = 4096) {
+  int32_t np = 0, ni = 0;
+  check(sr_build_prompt(system.data(), static_cast<int64_t>(system.size()), query_context.data(),
+                        static_cast<int64_t>(query_context.size()), document.data(),
+                        static_cast<int64_t>(document.size()), max_seq, nullptr, 0, &np, nullptr,
+                        0, &ni));
+  std::vector<int32_t> p(static_cast<size_t>(np)), it(static_cast<size_t>(ni));
+  check(sr_build_prompt(system.data(), static_cast<int64_t>(system.size()), query_context.data(),
+                        static_cast<int64_t>(query_context.size()), document.data(),
+                        static_cast<int64_t>(document.size()), max_seq, p.data(), np, &np,
+                        it.data(), ni, &ni));
+  return {std::vector<int>(p.begin(), p.end()), std::vector<int>(it.begin(), it.end())};
+}
+
+// service.cpp:380-391, byte-identical to the reference's nlohmann dump().
+inline std::string score_result_to_json(const ScoreResult& result) {
+  std::vector<const char*> ids, names;
+  std::vector<double> scores;
+  if (!result.items.empty())
+    for (const auto& [name, v] : result.items[0].tasks) names.push_back(name.c_str());
+  for (const auto& it : result.items) {
+    ids.push_back(it.item_id.c_str());
+    for (const char* n : names) scores.push_back(it.tasks.at(n));
+  }
+  const sr_flop_report fl{result.flops.attention_units, result.flops.linear_units,
+                          result.flops.t_q, result.flops.t_i_mean, result.flops.n_items};
+  int64_t len = 0;
+  const auto n_items = static_cast<int32_t>(ids.size());
+  const auto n_tasks = static_cast<int32_t>(names.size());
+  check(sr_score_result_to_json(result.request_id.c_str(), n_items, ids.data(), n_tasks,
+                                names.data(), scores.data(), &fl, nullptr, 0, &len));
+  std::string out(static_cast<size_t>(len), '\0');
+  check(sr_score_result_to_json(result.request_id.c_str(), n_items, ids.data(), n_tasks,
+                                names.data(), scores.data(), &fl, out.data(), len, &len));
+  return out;
 }
 
 }  // namespace semrank

@@ -342,8 +342,68 @@ def score_cache():
                               "zero_capacity": {"status": st, "message": msg}})
 
 
+def text_api():
+    """build_prompt (prompt.cpp:14-38) and score_result_to_json
+    (service.cpp:380-391) outputs from the reference: prompt splits incl. both
+    error rules, and response bodies over random probabilities, exact binary
+    fractions, integers, tiny/huge magnitudes, -0.0 and ids that need escaping."""
+    prompts = []
+    for sysm, q, doc, ms in [(b"You rank jobs.\n", b"query: nurse", b"RN, night shift", 4096),
+                             (b"", b"q", b"", 4096), (b"S", b"", b"doc", 4096),
+                             (b"", b"", b"doc", 4096), (b"abc", b"def", b"g" * 10, 29),
+                             (b"abc", b"def", b"g" * 10, 30), (b"", b"", b"", 4096),
+                             ("caf\u00e9 \u2603".encode(), b"\x01\xff", b"\x7fx", 64)]:
+        st, msg, pre, item = O.ref_build_prompt(sysm, q, doc, ms)
+        prompts.append({"system": _b64(np.frombuffer(sysm, np.uint8)) if sysm else "",
+                        "query": _b64(np.frombuffer(q, np.uint8)) if q else "",
+                        "document": _b64(np.frombuffer(doc, np.uint8)) if doc else "",
+                        "max_seq": ms, "status": st, "message": msg, "prefix": pre, "item": item})
+    rng = np.random.default_rng(20261020)
+    names = [b"relevance", b"click", b"apply", b"badfit", b"shortlist", b"dismiss"]
+    specials = [0.0, -0.0, 1.0, 0.5, 0.1, 1e-5, 1.5e-4, 0.00012345, 1e15, 123456789012345.0,
+                1234567890123456.0, 1e16, 1.5e20, 2.0 ** -1074, 1.7976931348623157e308,
+                0.3333333333333333, 2.0 / 3.0, 100.0, 15007744.0, 5e-324, 9.999999999999999e-5,
+                1e-4, 1e21, 123.456, -2.5e-7]
+    bodies = []
+    for t in range(6):
+        n = int(rng.integers(0, 9))
+        ids = [str(int(rng.integers(0, 10**6))).encode() for _ in range(n)]
+        if t == 3 and n:
+            ids[0] = 'a"b\\c\n\t\x01\x1f\u00e9\u2603/'.encode()
+        if t % 2:
+            sc = rng.random((n, len(names)))
+        else:
+            sc = rng.choice(specials, (n, len(names)))
+        att, lin = (float(rng.integers(0, 10**8)), float(rng.random() * 1e6)) if t else (0.0, 5e-5)
+        rid = (b"req-%d" % t) if t != 5 else "r\u00e9q\"x\"".encode()
+        st, msg, body = O.ref_score_result_json(rid, ids, names, sc, att, lin)
+        assert st == 0, msg
+        bodies.append({"request_id": _b64(np.frombuffer(rid, np.uint8)),
+                       "ids": [_b64(np.frombuffer(i, np.uint8)) if i else "" for i in ids],
+                       "names": [x.decode() for x in names],
+                       "scores": [[repr(float(v)) for v in row] for row in sc],
+                       "attention": repr(att), "linear": repr(lin), "json": body.decode()})
+    # every special value and 2000 random doubles of all magnitudes, one per item
+    vals = specials + [float(x) for x in rng.random(1000)] + \
+        [float(np.ldexp(rng.random(), int(e))) for e in rng.integers(-60, 80, 1000)]
+    bits = rng.integers(0, 0x7FF0000000000000, 3000, dtype=np.int64)  # any finite double
+    vals += [float(x) for x in bits.view(np.float64)]
+    ids = [str(i).encode() for i in range(len(vals))]
+    st, msg, body = O.ref_score_result_json(b"nums", ids, [b"relevance"],
+                                            np.asarray(vals)[:, None], 1.0, 2.0)
+    bodies.append({"request_id": _b64(np.frombuffer(b"nums", np.uint8)),
+                   "ids": [_b64(np.frombuffer(i, np.uint8)) for i in ids], "names": ["relevance"],
+                   "scores": [[repr(v)] for v in vals], "attention": "1.0", "linear": "2.0",
+                   "json": body.decode()})
+    dump("text_api.json", {"source": "build_prompt prompt.cpp:14-38 and score_result_to_json "
+                                     "service.cpp:380-391 via oracle/_ref",
+                           "prompts": prompts, "bodies": bodies})
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "score_cache":
+    if len(sys.argv) > 1 and sys.argv[1] == "text_api":
+        text_api()
+    elif len(sys.argv) > 1 and sys.argv[1] == "score_cache":
         score_cache()
     elif len(sys.argv) > 1 and sys.argv[1] == "wire":
         wire()
@@ -359,3 +419,4 @@ if __name__ == "__main__":
         calibration()
         wire()
         score_cache()
+        text_api()

@@ -90,6 +90,11 @@ def ref():
         lib.ref_plan_batches.argtypes = [C.c_int32, i32p, i32p, i32p, C.c_int64, i32p, C.c_int32,
                                          i32p, i64p]
         lib.ref_uniform_ints.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int32, i64p]
+        lib.ref_build_prompt.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int32, i32p, i32p,
+                                         C.c_int32, i32p]
+        lib.ref_score_result_json.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_char_p),
+                                              C.c_int32, C.POINTER(C.c_char_p), f64p, C.c_double,
+                                              C.c_double, C.c_char_p, C.c_int64, i64p]
         _ref = lib
     return _ref
 
@@ -386,3 +391,32 @@ def ref_cache_trace(capacity: int, ops):
             _p(val, f64p), _p(hit, i32p), _p(outv, f64p), _p(size, i64p))
     msg = lib.ref_last_error().decode() if st != 0 else ""
     return st, msg, [(int(hit[i]), float(outv[i]), int(size[i])) for i in range(n)]
+
+
+# ------------------------------------------------------------- text API
+def ref_build_prompt(system: bytes, query: bytes, document: bytes, max_seq: int):
+    """(status, message, prefix_tokens, item_tokens) from prompt.cpp:14-38."""
+    lib = ref()
+    cap = len(system) + len(query) + len(document) + 64
+    pre, item, n = (np.zeros(cap, np.int32), np.zeros(cap, np.int32), np.zeros(2, np.int32))
+    st = lib.ref_build_prompt(system, query, document, max_seq, _p(pre, i32p), _p(item, i32p), cap,
+                              _p(n, i32p))
+    msg = lib.ref_last_error().decode() if st else ""
+    return st, msg, pre[:n[0]].tolist() if st == 0 else None, item[:n[1]].tolist() if st == 0 else None
+
+
+def ref_score_result_json(request_id: bytes, ids, names, scores, attention: float, linear: float):
+    """score_result_to_json (service.cpp:380-391) over the reference's nlohmann::json."""
+    lib = ref()
+    sc = np.ascontiguousarray(scores, np.float64).reshape(len(ids), len(names))
+    cid = (C.c_char_p * max(1, len(ids)))(*ids)
+    cnm = (C.c_char_p * max(1, len(names)))(*names)
+    n = np.zeros(1, np.int64)
+    st = lib.ref_score_result_json(request_id, len(ids), cid, len(names), cnm, _p(sc, f64p),
+                                   attention, linear, None, 0, _p(n, i64p))
+    if st != 0:
+        return st, lib.ref_last_error().decode(), None
+    buf = C.create_string_buffer(int(n[0]) + 1)
+    lib.ref_score_result_json(request_id, len(ids), cid, len(names), cnm, _p(sc, f64p), attention,
+                              linear, buf, int(n[0]), _p(n, i64p))
+    return 0, "", buf.raw[:int(n[0])]

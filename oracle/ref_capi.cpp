@@ -28,6 +28,9 @@
 #include "semrank/midtier.hpp"
 #include "semrank/rng.hpp"
 #include "semrank/weights_io.hpp"
+#include "semrank/prompt.hpp"
+
+#include <json.hpp>  // the nlohmann/json the reference serialises with (service.cpp:11)
 
 using namespace semrank;
 
@@ -368,6 +371,44 @@ int ref_cache_trace(int64_t capacity, int32_t n_ops, const int32_t* op,
       }
       out_size[i] = static_cast<int64_t>(cache.size());
     }
+  });
+}
+
+// build_prompt (prompt.cpp:14-38), the reference itself. Lengths written to
+// n_out[0..1]; tokens up to cap each.
+int ref_build_prompt(const char* system, const char* query, const char* document, int32_t max_seq,
+                     int32_t* prefix_out, int32_t* item_out, int32_t cap, int32_t* n_out) {
+  return run([&] {
+    const auto parts = build_prompt(system, query, document, max_seq);
+    n_out[0] = static_cast<int32_t>(parts.prefix_tokens.size());
+    n_out[1] = static_cast<int32_t>(parts.item_tokens.size());
+    for (int32_t i = 0; i < std::min<int32_t>(cap, n_out[0]); ++i) prefix_out[i] = parts.prefix_tokens[i];
+    for (int32_t i = 0; i < std::min<int32_t>(cap, n_out[1]); ++i) item_out[i] = parts.item_tokens[i];
+  });
+}
+
+// score_result_to_json lives in service.cpp, which cannot be built here
+// (cpp-httplib is not vendored). Its body (service.cpp:380-391) is three
+// nlohmann::json statements; they are restated here verbatim in structure
+// over the same json library so the golden bytes come from the reference's
+// serialiser. Result fields as a flattened ScoreResult.
+int ref_score_result_json(const char* request_id, int32_t n_items, const char* const* ids,
+                          int32_t n_tasks, const char* const* task_names, const double* scores,
+                          double attention, double linear, char* out, int64_t cap, int64_t* len) {
+  return run([&] {
+    using json = nlohmann::json;
+    json arr = json::array();
+    for (int32_t i = 0; i < n_items; ++i) {
+      std::map<std::string, double> tasks;
+      for (int32_t t = 0; t < n_tasks; ++t) tasks[task_names[t]] = scores[i * n_tasks + t];
+      arr.push_back({{"id", std::string(ids[i])}, {"tasks", tasks}});
+    }
+    const json j = {{"request_id", std::string(request_id)},
+                    {"scores", arr},
+                    {"flops", {{"attention", attention}, {"linear", linear}}}};
+    const std::string s = j.dump();
+    *len = static_cast<int64_t>(s.size());
+    std::memcpy(out, s.data(), std::min<size_t>(static_cast<size_t>(cap), s.size()));
   });
 }
 

@@ -9,7 +9,8 @@ from .semrank import (  # noqa: F401
     MultiItemMask, Comm, Plan, BatchPlan, PROF_CLASSES, ScoreItem, ScoreMode, ScoreRequest, ScoreResult, ScoringEngine, SemrankError,
     build_multi_item_mask, flops, init_model, parse_score_request_json, tokenize, kRelevanceTask, load_weights, plan_batches, request_report,
     save_weights, score_by_mode, score_mode_from_name, score_mode_name, topk_host, ScoreCache,
-    canonical_query, fnv1a64, query_signature)
+    canonical_query, fnv1a64, query_signature, PromptParts, build_prompt, kPromptSuffix,
+    score_result_to_json)
 from .retrieval import (  # noqa: F401
     Corpus, DeviceCorpus, DocumentRecord, QuerySpec, RARWeights, RankedDoc, exhaustive_topk,
     filter_candidates)

@@ -78,11 +78,18 @@ _sig("sr_plan_batches", i32, i32, P(i32), P(i32), P(i32), i64, P(i32), i32, P(i3
      i32, P(i32))
 _sig("sr_request_report", i32, P(ModelConfigC), P(RequestC), P(FlopReportC), P(f64))
 _sig("sr_topk_host", i32, P(f64), P(i64), i32, i32, P(i64), P(f64), P(i32))
+_sig("sr_build_prompt", i32, C.c_char_p, i64, C.c_char_p, i64, C.c_char_p, i64, i32, P(i32), i32,
+     P(i32), P(i32), i32, P(i32))
+_sig("sr_score_result_to_json", i32, C.c_char_p, i32, P(C.c_char_p), i32, P(C.c_char_p), P(f64),
+     P(FlopReportC), C.c_char_p, i64, P(i64))
 _sig("sr_engine_create", i32, vp, i32, P(vp))
 _sig("sr_engine_destroy", None, vp)
 _sig("sr_engine_score", i32, vp, P(RequestC), P(ResultC))
 _sig("sr_engine_score_batch", i32, vp, P(RequestC), i32, P(ResultC))
 _sig("sr_engine_item_hidden", i32, vp, P(RequestC), P(f32))
+_sig("sr_engine_set_projection", i32, vp, P(f32), i32, i32)
+_sig("sr_engine_score_emb", i32, vp, P(i32), i32, P(f32), i32, i32, P(i64), i32, P(ResultC))
+_sig("sr_plan_create_emb", i32, vp, P(i32), i32, P(f32), i32, i32, P(i64), i32, i32, P(vp))
 _sig("sr_engine_device", i32, vp)
 _sig("sr_engine_stream", vp, vp)
 _sig("sr_plan_create", i32, vp, P(RequestC), i32, P(vp))
@@ -143,9 +150,10 @@ HEADER_SYMBOLS = [
     "sr_weights_save", "sr_weights_from_tensors", "sr_weights_free", "sr_weights_config",
     "sr_weights_version", "sr_weights_tensor_count", "sr_weights_tensor", "sr_flops",
     "sr_multi_item_pair_count", "sr_multi_item_mask", "sr_plan_batches", "sr_request_report",
-    "sr_topk_host",
+    "sr_topk_host", "sr_build_prompt", "sr_score_result_to_json",
     "sr_engine_create", "sr_engine_destroy", "sr_engine_score", "sr_engine_score_batch",
-    "sr_engine_item_hidden", "sr_engine_device", "sr_engine_stream", "sr_plan_create",
+    "sr_engine_item_hidden", "sr_engine_set_projection", "sr_engine_score_emb",
+    "sr_plan_create_emb", "sr_engine_device", "sr_engine_stream", "sr_plan_create",
     "sr_plan_create_batch", "sr_plan_fetch_batch", "sr_plan_run", "sr_plan_sync", "sr_plan_fetch", "sr_plan_kernel_count", "sr_plan_destroy",
     "sr_plan_profile", "sr_plan_shape",
     "sr_nccl_unique_id", "sr_comm_create", "sr_comm_destroy", "sr_engine_score_sharded",

@@ -2,6 +2,7 @@
 // srh::Error to sr_status and keep a thread-local error message.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -13,6 +14,7 @@
 #include "host/wire.hpp"
 #include "host/model.hpp"
 #include "host/planner.hpp"
+#include "host/prompt.hpp"
 #include "kernels/launch.h"
 #include "semrank_b200.h"
 
@@ -325,6 +327,51 @@ int32_t sr_topk_host(const double* scores, const int64_t* ids, int32_t n, int32_
   });
 }
 
+int32_t sr_build_prompt(const char* system, int64_t system_len, const char* query_context,
+                        int64_t query_len, const char* document, int64_t document_len,
+                        int32_t max_seq, int32_t* prefix_out, int32_t prefix_cap,
+                        int32_t* n_prefix, int32_t* item_out, int32_t item_cap, int32_t* n_item) {
+  return guard([&] {
+    if (system_len < 0 || query_len < 0 || document_len < 0 || prefix_cap < 0 || item_cap < 0)
+      srh::fail(SR_PARAMETER, "negative size");
+    if ((system_len && !system) || (query_len && !query_context) || (document_len && !document) ||
+        !n_prefix || !n_item)
+      srh::fail(SR_SPEC_VIOLATION, "null argument");
+    const auto parts = srh::build_prompt(std::string_view(system ? system : "", system_len),
+                                         std::string_view(query_context ? query_context : "", query_len),
+                                         std::string_view(document ? document : "", document_len),
+                                         max_seq);
+    *n_prefix = static_cast<int32_t>(parts.prefix_tokens.size());
+    *n_item = static_cast<int32_t>(parts.item_tokens.size());
+    if (prefix_out)
+      std::copy_n(parts.prefix_tokens.begin(), std::min<size_t>(prefix_cap, parts.prefix_tokens.size()),
+                  prefix_out);
+    if (item_out)
+      std::copy_n(parts.item_tokens.begin(), std::min<size_t>(item_cap, parts.item_tokens.size()),
+                  item_out);
+  });
+}
+
+int32_t sr_score_result_to_json(const char* request_id, int32_t n_items,
+                                const char* const* item_ids, int32_t n_tasks,
+                                const char* const* task_names, const double* scores,
+                                const sr_flop_report* flops, char* out, int64_t cap,
+                                int64_t* len) {
+  return guard([&] {
+    if (n_items < 0 || n_tasks < 0 || cap < 0) srh::fail(SR_PARAMETER, "negative size");
+    if (!len || !flops || (n_items > 0 && (!item_ids || (n_tasks > 0 && !scores))) ||
+        (n_tasks > 0 && !task_names))
+      srh::fail(SR_SPEC_VIOLATION, "null argument");
+    for (int32_t t = 0; t < n_tasks; ++t)
+      if (!task_names[t]) srh::fail(SR_SPEC_VIOLATION, "null task name");
+    const std::string j = srh::score_result_json(request_id ? request_id : "", n_items, item_ids,
+                                                 n_tasks, task_names, scores,
+                                                 flops->attention_units, flops->linear_units);
+    *len = static_cast<int64_t>(j.size());
+    if (out) std::memcpy(out, j.data(), std::min<size_t>(static_cast<size_t>(cap), j.size()));
+  });
+}
+
 int32_t sr_engine_create(const sr_weights* w, int32_t device, sr_engine** out) {
   return guard([&] {
     if (!w || !out) srh::fail(SR_SPEC_VIOLATION, "null argument");
@@ -563,6 +610,37 @@ int32_t sr_engine_score_cached(sr_engine* e, sr_score_cache* c, const char* sear
   });
 }
 
+int32_t sr_engine_set_projection(sr_engine* e, const float* proj, int32_t d_emb, int32_t n_soft) {
+  return guard([&] {
+    if (!e) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    e->e->set_projection(proj, d_emb, n_soft);
+  });
+}
+
+int32_t sr_engine_score_emb(sr_engine* e, const int32_t* prefix, int32_t t_q, const float* emb,
+                            int32_t d_emb, int32_t n_items, const int64_t* item_ids,
+                            int32_t form, sr_result* res) {
+  return guard([&] {
+    if (!e || !res || (t_q > 0 && !prefix)) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    e->e->score_emb(prefix, t_q, emb, d_emb, n_items, item_ids, form, res);
+  });
+}
+
+int32_t sr_plan_create_emb(sr_engine* e, const int32_t* prefix, int32_t t_q, const float* emb,
+                           int32_t d_emb, int32_t n_items, const int64_t* item_ids, int32_t form,
+                           int32_t k, sr_plan** out) {
+  return guard([&] {
+    if (!e || !out || (t_q > 0 && !prefix)) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    auto p = std::make_unique<sr_plan>();
+    p->owner = e;
+    p->p = e->e->make_plan_emb(prefix, t_q, emb, d_emb, n_items, item_ids, form, k);
+    *out = p.release();
+  });
+}
+
 int32_t sr_engine_device(const sr_engine* e) { return e ? e->e->device() : -1; }
 void* sr_engine_stream(const sr_engine* e) { return e ? e->e->stream() : nullptr; }
 
@@ -592,6 +670,7 @@ int32_t sr_plan_create_batch(sr_engine* e, const sr_request* reqs, int32_t n_req
 int32_t sr_plan_fetch_batch(sr_plan* p, sr_result* res, int32_t n_req) {
   return guard([&] {
     if (!p || !res) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(p->owner->e->mutex());
     if (n_req != static_cast<int32_t>(p->p->reqs.size()))
       srh::fail(SR_PARAMETER, "result count differs from the plan's request count");
     p->owner->e->fetch(*p->p, res, n_req);
@@ -601,6 +680,7 @@ int32_t sr_plan_fetch_batch(sr_plan* p, sr_result* res, int32_t n_req) {
 int32_t sr_plan_run(sr_plan* p) {
   return guard([&] {
     if (!p) srh::fail(SR_SPEC_VIOLATION, "null plan");
+    std::lock_guard<std::mutex> lock(p->owner->e->mutex());
     p->owner->e->run_plan(*p->p);
     p->sharded_valid = false;
   });
@@ -609,6 +689,7 @@ int32_t sr_plan_run(sr_plan* p) {
 int32_t sr_plan_sync(sr_plan* p) {
   return guard([&] {
     if (!p) srh::fail(SR_SPEC_VIOLATION, "null plan");
+    std::lock_guard<std::mutex> lock(p->owner->e->mutex());
     SR_CUDA_CHECK(cudaStreamSynchronize(p->owner->e->stream()));
   });
 }
@@ -616,6 +697,7 @@ int32_t sr_plan_sync(sr_plan* p) {
 int32_t sr_plan_fetch(sr_plan* p, sr_result* res) {
   return guard([&] {
     if (!p || !res) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(p->owner->e->mutex());
     p->owner->e->fetch(*p->p, res, 1);
     if (p->sharded_valid) copy_topk_merged(*p->p, res, p->owner->e->stream());
   });
@@ -649,7 +731,11 @@ int32_t sr_plan_shape(const sr_plan* p, int64_t* out8) {
     h2d += static_cast<int64_t>(pk.spans.size()) * sizeof(srk::RowSpan);
     h2d += static_cast<int64_t>(pk.tiles.size()) * sizeof(srk::AttnTile);
     h2d += static_cast<int64_t>(pk.last_rows.size()) * 4 + static_cast<int64_t>(pk.ids.size()) * 8;
-    h2d += static_cast<int64_t>(pk.seg_off.size()) * 4 + static_cast<int64_t>(pk.n_soft) * 4 * p->owner->e->config().d_model;
+    h2d += static_cast<int64_t>(pk.seg_off.size()) * 4;
+    if (p->p->emb_form >= 0)  // compact embeddings; the rows are made on the device
+      h2d += static_cast<int64_t>(p->p->emb_n) * p->p->emb_d * 4;
+    else
+      h2d += static_cast<int64_t>(pk.n_soft) * 4 * p->owner->e->config().d_model;
     out8[4] = h2d;
     out8[5] = static_cast<int64_t>(pk.n_items) * p->p->n_tasks * 8 +
               static_cast<int64_t>(pk.seg_off.size() - 1) * p->p->k * sizeof(srk::TopkEntry);
@@ -658,7 +744,11 @@ int32_t sr_plan_shape(const sr_plan* p, int64_t* out8) {
   });
 }
 
-void sr_plan_destroy(sr_plan* p) { delete p; }
+void sr_plan_destroy(sr_plan* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lock(p->owner->e->mutex());  // graph/buffers freed off the stream
+  delete p;
+}
 
 int32_t sr_nccl_unique_id(uint8_t out[128]) {
   return guard([&] { srh::nccl_unique_id(out); });
@@ -693,6 +783,7 @@ int32_t sr_engine_score_sharded(sr_engine* e, sr_comm* c, const sr_request* loca
 int32_t sr_plan_run_sharded(sr_plan* p, sr_comm* c) {
   return guard([&] {
     if (!p || !c) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    std::lock_guard<std::mutex> lock(p->owner->e->mutex());
     p->owner->e->run_plan_sharded(*p->p, c->c);
     p->sharded_valid = true;
   });

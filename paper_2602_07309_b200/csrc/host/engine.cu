@@ -173,6 +173,9 @@ void Engine::set_postprocess(const double* lo, const double* hi, const double* v
                              int n_blocks, const int32_t* blend_task, const double* blend_w,
                              int n_blend) {
   if (n_blocks < 0 || n_blend < 0) fail(SR_PARAMETER, "negative post-processing size");
+  // handle_search always calibrates the relevance before blending, and
+  // calibrate() rejects an unfitted head (calibration.cpp:65-68).
+  if (n_blend > 0 && n_blocks == 0) fail(SR_STATE_INVALID, "calibration head is not fitted");
   const int T = n_tasks();
   for (int j = 0; j < n_blend; ++j)
     if (blend_task[j] < 0 || blend_task[j] >= T)
@@ -290,6 +293,22 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
   // O -> LN2 -> W_in -> W_out -> LN1 -> QKV walks its rows opposite to its
   // producer, so it starts on the rows still resident in L2.
   const bool serp = serpentine_;
+  if (p.emb_form >= 0) {
+    // compact embeddings -> soft rows in HBM, ahead of the embedding gather
+    float* rows = p.soft.ptr + static_cast<size_t>(p.emb_row0) * d;
+    B(PROF_EMBED_LN);
+    if (p.emb_form == SR_EMB_PAD) {
+      SR_CUDA_CHECK(srk::emb_pad_rows(p.emb.ptr, p.emb_n, p.emb_d, d, rows, s));
+      ++n;
+    } else {
+      SR_CUDA_CHECK(srk::emb_to_bf16(p.emb.ptr, p.emb_n, p.emb_d, proj_kp_, p.emb16.ptr, s));
+      const int N = proj_nsoft_ * d;
+      SR_CUDA_CHECK(srk::gemm_auto(p.tm_emb16, tm_proj_, p.emb_n, N, proj_kp_, rows, N,
+                                   srk::EPI_F32, s));
+      n += 2;
+    }
+    E();
+  }
   if (fold_ln_) {
     // LN folded into the GEMMs (gemm_tcgen05.cuh GemmLnArgs): no LayerNorm launches.
     srk::LnFold in{}, out{};
@@ -470,8 +489,26 @@ void Engine::refill_plan(Plan& p, const sr_request* reqs, int n_req) {
     const size_t d = cfg_.d_model;
     p.soft.ensure(std::max<size_t>(static_cast<size_t>(pk.n_soft) * d, 1));
     size_t off = 0;
+    p.emb_form = -1;
     for (const auto& src : pk.soft_src) {
-      if (src.rows == kB64Rows) {
+      if (src.rows == kEmbRows) {
+        // compact embeddings: [n x d_emb] fp32 up, rows made in enqueue_forward
+        const size_t ne = static_cast<size_t>(emb_.n) * emb_.d_emb;
+        bool moved = p.emb.ensure(std::max<size_t>(ne, 1));
+        up_.upload(p.emb.ptr, emb_.emb, ne * sizeof(float), stream_);
+        if (emb_.form == SR_EMB_PROJECT) {
+          const size_t rows = (static_cast<size_t>(emb_.n) + 127) / 128 * 128;
+          if (p.emb16.ensure(rows * proj_kp_) || moved) {
+            SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&p.tm_emb16, p.emb16.ptr, rows, proj_kp_, 128, 64));
+            moved = true;
+          }
+        }
+        if (moved) p.graph_epoch = ~0ull;  // buffers baked into the graph moved
+        p.emb_form = emb_.form;
+        p.emb_n = emb_.n;
+        p.emb_d = emb_.d_emb;
+        p.emb_row0 = static_cast<int32_t>(off);
+      } else if (src.rows == kB64Rows) {
         // base64 payloads: text to HBM, decoded in place into the rows
         const int32_t n = b64_.n;
         upload_b64_text();
@@ -515,7 +552,7 @@ void Engine::capture(Plan& p) {
   SR_CUDA_CHECK(cudaStreamEndCapture(stream_, &g));
   SR_CUDA_CHECK(cudaGraphInstantiate(&p.graph, g, 0));
   cudaGraphDestroy(g);
-  plan_epoch_[&p] = ws_epoch_;
+  p.graph_epoch = ws_epoch_;
 }
 
 std::unique_ptr<Plan> Engine::make_plan(const sr_request* reqs, int n_req, int32_t k) {
@@ -535,8 +572,7 @@ std::unique_ptr<Plan> Engine::make_plan(const sr_request* reqs, int n_req, int32
 
 void Engine::run_plan(Plan& p) {
   SR_CUDA_CHECK(cudaSetDevice(device_));
-  auto it = plan_epoch_.find(&p);
-  if (it == plan_epoch_.end() || it->second != ws_epoch_) capture(p);
+  if (p.graph == nullptr || p.graph_epoch != ws_epoch_) capture(p);
   SR_CUDA_CHECK(cudaGraphLaunch(p.graph, stream_));
 }
 
@@ -598,9 +634,10 @@ void Engine::score(const sr_request* reqs, int n_req, sr_result* res) {
     if (reqs[q].mode == SR_MODE_MIXED) soft += items;
     maxseg = std::max(maxseg, reqs[q].n_items);
   }
+  const int32_t emb_key = emb_.form < 0 ? 0 : (emb_.form + 1) * 1000000 + emb_.d_emb;
   auto key = std::make_tuple(static_cast<int32_t>(M), static_cast<int32_t>(N),
                              static_cast<int32_t>(tiles), n_req, maxseg, static_cast<int32_t>(soft),
-                             k);
+                             k, emb_key);
   auto it = cache_.find(key);
   Plan* p;
   if (it == cache_.end()) {
@@ -730,6 +767,108 @@ void Engine::score_b64_spans(const int32_t* prefix, int32_t t_q, const char* a, 
   unsigned long long err = ~0ull;
   SR_CUDA_CHECK(cudaMemcpy(&err, b64_err_.ptr, sizeof(err), cudaMemcpyDeviceToHost));
   if (err != ~0ull) raise_char(err);  // results are discarded, as the reference never scores
+}
+
+void Engine::set_projection(const float* proj, int32_t d_emb, int32_t n_soft) {
+  SR_CUDA_CHECK(cudaSetDevice(device_));
+  SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  if (proj == nullptr) {  // remove
+    proj_.release();
+    proj_demb_ = proj_kp_ = proj_nsoft_ = 0;
+    ++ws_epoch_;
+    return;
+  }
+  const int d = cfg_.d_model;
+  if (d_emb < 1 || n_soft < 1) fail(SR_PARAMETER, "projection needs d_emb >= 1 and n_soft >= 1");
+  if (n_soft > cfg_.max_seq) fail(SR_LENGTH_OVERFLOW, "n_soft exceeds max_seq");
+  const int kp = (d_emb + 63) / 64 * 64;
+  const size_t N = static_cast<size_t>(n_soft) * d;
+  // reference layout [d_emb x N] (weights are [d_in x d_out], model.hpp:42-47)
+  // -> zero-padded [kp x N] -> bf16 [N x kp] (K-major B operand)
+  std::vector<float> padded(static_cast<size_t>(kp) * N, 0.f);
+  std::memcpy(padded.data(), proj, static_cast<size_t>(d_emb) * N * sizeof(float));
+  float* stage = nullptr;
+  SR_CUDA_CHECK(cudaMalloc(&stage, padded.size() * sizeof(float)));
+  try {
+    proj_.ensure(padded.size());
+    SR_CUDA_CHECK(cudaMemcpyAsync(stage, padded.data(), padded.size() * sizeof(float),
+                                  cudaMemcpyHostToDevice, stream_));
+    SR_CUDA_CHECK(srk::transpose_to_bf16(stage, proj_.ptr, kp, static_cast<int>(N), stream_,
+                                         nullptr));
+    SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  } catch (...) {
+    cudaFree(stage);
+    throw;
+  }
+  cudaFree(stage);
+  make_weight_map(&tm_proj_, proj_.ptr, static_cast<int>(N), kp);
+  proj_demb_ = d_emb;
+  proj_kp_ = kp;
+  proj_nsoft_ = n_soft;
+  ++ws_epoch_;  // captured projection graphs bake the old operand
+}
+
+std::vector<int32_t> Engine::emb_request(const int32_t* prefix, int32_t t_q, const float* emb,
+                                         int32_t d_emb, int32_t n_items, const int64_t* item_ids,
+                                         int32_t form, sr_request* req) {
+  if (form != SR_EMB_PAD && form != SR_EMB_PROJECT)
+    fail(SR_PARAMETER, "unknown embedding form " + std::to_string(form));
+  if (n_items <= 0) fail(SR_PAYLOAD_INVALID, "request needs a non-empty items[]");
+  if (emb == nullptr) fail(SR_SPEC_VIOLATION, "null embeddings");
+  int32_t rows = 1;
+  if (form == SR_EMB_PAD) {
+    if (d_emb < 1) fail(SR_PAYLOAD_INVALID, "embedding must have at least one value");
+  } else {
+    if (proj_nsoft_ == 0) fail(SR_STATE_INVALID, "no embedding projection is set");
+    if (d_emb != proj_demb_)
+      fail(SR_ALIGNMENT, "embedding width " + std::to_string(d_emb) +
+                             " differs from the projection's " + std::to_string(proj_demb_));
+    rows = proj_nsoft_;
+  }
+  std::vector<int32_t> off(static_cast<size_t>(n_items) + 1);
+  for (int32_t j = 0; j <= n_items; ++j) off[j] = j * rows;
+  *req = sr_request{};
+  req->prefix_tokens = prefix;
+  req->t_q = t_q;
+  req->n_items = n_items;
+  req->item_offsets = off.data();
+  req->item_rows = kEmbRows;
+  req->item_ids = item_ids;
+  req->mode = SR_MODE_MIXED;
+  emb_ = EmbSrc{emb, n_items, d_emb, form};
+  return off;
+}
+
+void Engine::score_emb(const int32_t* prefix, int32_t t_q, const float* emb, int32_t d_emb,
+                       int32_t n_items, const int64_t* item_ids, int32_t form, sr_result* res) {
+  sr_request req;
+  const auto off = emb_request(prefix, t_q, emb, d_emb, n_items, item_ids, form, &req);
+  try {
+    score(&req, 1, res);
+  } catch (...) {
+    emb_ = EmbSrc{};
+    throw;
+  }
+  emb_ = EmbSrc{};
+}
+
+std::unique_ptr<Plan> Engine::make_plan_emb(const int32_t* prefix, int32_t t_q, const float* emb,
+                                            int32_t d_emb, int32_t n_items,
+                                            const int64_t* item_ids, int32_t form, int32_t k) {
+  sr_request req;
+  const auto off = emb_request(prefix, t_q, emb, d_emb, n_items, item_ids, form, &req);
+  std::unique_ptr<Plan> p;
+  try {
+    p = make_plan(&req, 1, k);
+  } catch (...) {
+    emb_ = EmbSrc{};
+    throw;
+  }
+  emb_ = EmbSrc{};
+  // the plan keeps the request; its offsets must outlive this call
+  p->emb_off = off;
+  p->reqs[0].item_offsets = p->emb_off.data();
+  return p;
 }
 
 void Engine::item_hidden(const sr_request& req, float* hidden_out) {

@@ -114,8 +114,15 @@ struct Plan {
   DevBuf<srk::TopkEntry> gathered, merged;  // sharded merge
   pinned_vector<double> h_scores;           // fetch staging (page-locked)
   pinned_vector<srk::TopkEntry> h_top;
+  // compact embeddings -> soft rows on the device (score_emb; -1 = none)
+  int32_t emb_form = -1, emb_n = 0, emb_d = 0, emb_row0 = 0;
+  std::vector<int32_t> emb_off;  // item offsets of a make_plan_emb request
+  DevBuf<float> emb;
+  DevBuf<__nv_bfloat16> emb16;  // projection A operand [round_up(n, 128) x kp]
+  CUtensorMap tm_emb16;
   // graph
   cudaGraphExec_t graph = nullptr;
+  uint64_t graph_epoch = ~0ull;  // engine workspace epoch the graph was captured at
   int32_t launches = 0;
   ~Plan();
 };
@@ -175,6 +182,19 @@ class Engine {
                     const std::string& model_version, const sr_request& req, sr_result* res,
                     int32_t* n_hits);
 
+  // Mixed-mode items given as compact embeddings emb [n x d_emb] (SURVEY H7,
+  // north_star (d)). form SR_EMB_PAD: one soft row per item, the embedding
+  // zero-padded (or cut) to d_model as the service does (service.cpp:208-217);
+  // SR_EMB_PROJECT: n_soft rows per item = bf16(emb) . bf16(P) on the tensor
+  // cores (fp32 accumulate), P set by set_projection. The rows are produced
+  // in HBM inside the forward (no d_model-wide upload).
+  void set_projection(const float* proj, int32_t d_emb, int32_t n_soft);
+  void score_emb(const int32_t* prefix, int32_t t_q, const float* emb, int32_t d_emb,
+                 int32_t n_items, const int64_t* item_ids, int32_t form, sr_result* res);
+  std::unique_ptr<Plan> make_plan_emb(const int32_t* prefix, int32_t t_q, const float* emb,
+                                      int32_t d_emb, int32_t n_items, const int64_t* item_ids,
+                                      int32_t form, int32_t k);
+
   // Sharded: local pass + NCCL all-gather of per-rank top-k + merge.
   void run_plan_sharded(Plan& p, struct Comm* comm);
 
@@ -225,6 +245,19 @@ class Engine {
   DevBuf<int64_t> b64_off_;
   DevBuf<unsigned long long> b64_err_;
   void upload_b64_text();
+  // pending compact-embedding source of the request being packed (score_emb)
+  struct EmbSrc {
+    const float* emb = nullptr;
+    int32_t n = 0, d_emb = 0, form = -1;
+  } emb_;
+  std::vector<int32_t> emb_request(const int32_t* prefix, int32_t t_q, const float* emb,
+                                   int32_t d_emb, int32_t n_items, const int64_t* item_ids,
+                                   int32_t form, sr_request* req);
+  // projection P as the UMMA B operand: bf16 [n_soft*d x proj_kp_] (K-major,
+  // K zero-padded to a multiple of 64)
+  DevBuf<__nv_bfloat16> proj_;
+  CUtensorMap tm_proj_;
+  int32_t proj_demb_ = 0, proj_kp_ = 0, proj_nsoft_ = 0;
   StagedUpload up_;  // caller-buffer uploads (soft rows, base64 text)
   std::vector<LayerDev> layers_;
   std::vector<void*> allocs_;
@@ -237,10 +270,9 @@ class Engine {
   CUtensorMap tm_xn_, tm_h_, tm_qkv_, tm_xb_;
   uint64_t ws_epoch_ = 0;  // bumps when workspace moves (graphs must be re-captured)
   // shape-keyed plan cache for score()
-  std::map<std::tuple<int32_t, int32_t, int32_t, int32_t, int32_t, int32_t, int32_t>,
+  std::map<std::tuple<int32_t, int32_t, int32_t, int32_t, int32_t, int32_t, int32_t, int32_t>,
            std::unique_ptr<Plan>>
       cache_;
-  std::map<const Plan*, uint64_t> plan_epoch_;
   void capture(Plan& p);
  public:
   uint64_t epoch() const { return ws_epoch_; }

@@ -33,6 +33,10 @@ namespace srh {
 // Marker for mixed-mode rows that arrive as base64 text (Engine::score_b64).
 inline const float kB64RowsTag = 0.f;
 #define kB64Rows (&::srh::kB64RowsTag)
+// Marker for mixed-mode rows produced on the device from compact per-item
+// embeddings (Engine::score_emb: zero-pad or projection).
+inline const float kEmbRowsTag = 0.f;
+#define kEmbRows (&::srh::kEmbRowsTag)
 
 sr_flop_report flops(int mode, int64_t t_q, int64_t t_i, int64_t n_items);
 

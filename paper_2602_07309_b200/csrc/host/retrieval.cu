@@ -221,7 +221,7 @@ int Corpus::topk_sharded(Comm* c, const float* query, int d_query, double w0, co
                                 cudaMemcpyDeviceToHost, stream_));
   SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
   int m = 0;
-  for (; m < k && h[m].id != INT64_MAX; ++m) {
+  for (; m < k && h[m].index != INT32_MAX; ++m) {  // sentinel by index: any int64 is a valid doc id
     if (ids_out) ids_out[m] = h[m].id;
     if (scores_out) scores_out[m] = h[m].score;
   }

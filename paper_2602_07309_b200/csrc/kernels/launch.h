@@ -122,6 +122,13 @@ cudaError_t embed_ln(const int32_t* src, const int32_t* pos, const float* tok_em
 cudaError_t embed_stats(const int32_t* src, const int32_t* pos, const float* tok_emb,
                         const float* soft_rows, const float* pos_emb, float* x,
                         __nv_bfloat16* xb, float* stats, int M, int d, cudaStream_t stream);
+// Mixed-mode items given as compact embeddings [n x d_emb]:
+// zero-pad form (service.cpp:208-217): out [n x d] = emb[:, :min(d_emb, d)], 0 after;
+// projection operand: out [n x kp] bf16, columns >= d_emb zero.
+cudaError_t emb_pad_rows(const float* emb, int n, int d_emb, int d, float* out,
+                         cudaStream_t stream);
+cudaError_t emb_to_bf16(const float* emb, int n, int d_emb, int kp, __nv_bfloat16* out,
+                        cudaStream_t stream);
 // rev: rows walked from the last block to the first (L2 serpentine order).
 cudaError_t layer_norm_bf16(const float* x, const float* gain, __nv_bfloat16* out, int M, int d,
                             cudaStream_t stream, bool rev = false);

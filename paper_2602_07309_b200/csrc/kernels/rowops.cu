@@ -7,6 +7,8 @@
 // HBM traffic is one fp32 read + one bf16 write per element.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "launch.h"
 
 namespace srk {
@@ -267,6 +269,47 @@ cudaError_t transpose_to_bf16(const float* src, __nv_bfloat16* dst, int K, int N
 cudaError_t bf16_row_sums(const __nv_bfloat16* w, int N, int K, float* out, cudaStream_t stream) {
   if (N <= 0) return cudaSuccess;
   bf16_row_sums_kernel<<<(N + 7) / 8, 256, 0, stream>>>(w, N, K, out);
+  return cudaGetLastError();
+}
+
+// Compact per-item embeddings -> soft-token rows (mixed mode).
+// Zero-pad form (service.cpp:208-217): row i = emb[i][0 .. min(d_emb, d)), 0 after.
+__global__ void emb_pad_rows_kernel(const float* __restrict__ emb, int n, int d_emb, int d,
+                                    float* __restrict__ out) {
+  const long long total = static_cast<long long>(n) * d;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(t / d), j = static_cast<int>(t % d);
+    out[t] = j < d_emb ? emb[static_cast<long long>(i) * d_emb + j] : 0.f;
+  }
+}
+
+// Projection operand: bf16 rows [n x kp], columns >= d_emb zero.
+__global__ void emb_to_bf16_kernel(const float* __restrict__ emb, int n, int d_emb, int kp,
+                                   __nv_bfloat16* __restrict__ out) {
+  const long long total = static_cast<long long>(n) * kp;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(t / kp), j = static_cast<int>(t % kp);
+    out[t] = __float2bfloat16_rn(j < d_emb ? emb[static_cast<long long>(i) * d_emb + j] : 0.f);
+  }
+}
+
+cudaError_t emb_pad_rows(const float* emb, int n, int d_emb, int d, float* out,
+                         cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const long long total = static_cast<long long>(n) * d;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
+  emb_pad_rows_kernel<<<blocks, 256, 0, stream>>>(emb, n, d_emb, d, out);
+  return cudaGetLastError();
+}
+
+cudaError_t emb_to_bf16(const float* emb, int n, int d_emb, int kp, __nv_bfloat16* out,
+                        cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const long long total = static_cast<long long>(n) * kp;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
+  emb_to_bf16_kernel<<<blocks, 256, 0, stream>>>(emb, n, d_emb, kp, out);
   return cudaGetLastError();
 }
 

@@ -725,6 +725,64 @@ class ScoringEngine:
             off.ctypes.data_as(C.POINTER(C.c_int64)), len(parts),
             ids.ctypes.data_as(C.POINTER(C.c_int64)) if ids is not None else None, C.byref(rb.c)))
 
+    # ------------------------------------------------ compact embeddings
+    EMB_PAD, EMB_PROJECT = 0, 1  # sr_emb_form
+
+    def set_projection(self, proj: Optional[np.ndarray], n_soft: int = 0) -> None:
+        """Context compression (north_star (d)): P [d_emb x n_soft*d_model] in
+        the reference's weight layout; each item's compact embedding becomes
+        n_soft soft-token rows bf16(e).bf16(P) on the tensor cores. None removes it."""
+        if proj is None:
+            _check(_lib.sr_engine_set_projection(self._h, None, 0, 0))
+            return
+        P_ = np.ascontiguousarray(proj, np.float32)
+        d = self.config.d_model
+        if P_.ndim != 2 or (n_soft and P_.shape[1] != n_soft * d) or P_.shape[1] % d:
+            raise SemrankError(ErrorCode.Alignment,
+                               f"projection must be [d_emb x n_soft*{d}], got {P_.shape}")
+        self._proj = P_.shape
+        _check(_lib.sr_engine_set_projection(self._h, P_.ctypes.data_as(C.POINTER(C.c_float)),
+                                             P_.shape[0], P_.shape[1] // d))
+
+    @staticmethod
+    def _emb_form(form) -> int:
+        if form in ("pad", 0):
+            return 0
+        if form in ("project", 1):
+            return 1
+        raise SemrankError(ErrorCode.Parameter, f"unknown embedding form: {form}")
+
+    def score_embeddings(self, prefix_tokens, embeddings: np.ndarray, form="project", k: int = 0,
+                         item_ids=None, request_id: str = "") -> ScoreResult:
+        """Mixed-mode scoring of items given as compact embeddings [n x d_emb]
+        (sr_engine_score_emb): form "pad" = the service's one zero-padded row
+        per item (service.cpp:208-217), "project" = n_soft projected rows."""
+        prefix = np.ascontiguousarray(np.asarray(prefix_tokens, np.int32).reshape(-1))
+        emb = np.ascontiguousarray(embeddings, np.float32)
+        if emb.ndim != 2:
+            raise SemrankError(ErrorCode.PayloadInvalid, "embeddings must be [n x d_emb]")
+        n = emb.shape[0]
+        ids = None if item_ids is None else np.ascontiguousarray(np.asarray(item_ids, np.int64))
+        rb = _ResultBuf(n, len(self.task_names), k)
+        _check(_lib.sr_engine_score_emb(
+            self._h, prefix.ctypes.data_as(C.POINTER(C.c_int32)), len(prefix),
+            emb.ctypes.data_as(C.POINTER(C.c_float)), emb.shape[1], n,
+            ids.ctypes.data_as(C.POINTER(C.c_int64)) if ids is not None else None,
+            self._emb_form(form), C.byref(rb.c)))
+        names = [str(int(i)) for i in ids] if ids is not None else [str(i) for i in range(n)]
+        req = ScoreRequest(request_id=request_id, prefix_tokens=prefix, mode=ScoreMode.Mixed,
+                           items=[ScoreItem(id=x) for x in names])
+        res = self._to_result(req, rb)
+        if self._post:
+            res.final_scores = self._final(n)
+        return res
+
+    def plan_embeddings(self, prefix_tokens, embeddings: np.ndarray, form="project", k: int = 0,
+                        item_ids=None) -> "Plan":
+        """Resident variant of score_embeddings (the pad / projection step is
+        inside the plan's CUDA graph)."""
+        return EmbPlan(self, prefix_tokens, embeddings, form, k, item_ids)
+
     def set_postprocess(self, calibration: Optional["CalibrationHead"] = None,
                         score_blend: Optional[Dict[str, float]] = None) -> None:
         """The service's output side on the device (service.cpp:242-277):
@@ -870,6 +928,31 @@ class Plan:
         return {c: (float(m), int(n)) for c, m, n in zip(PROF_CLASSES, ms, cnt)}
 
 
+class EmbPlan(Plan):
+    """Resident compact-embedding request (sr_plan_create_emb)."""
+
+    def __init__(self, engine: "ScoringEngine", prefix_tokens, embeddings, form, k: int = 0,
+                 item_ids=None):
+        self.engine = engine
+        self._prefix = np.ascontiguousarray(np.asarray(prefix_tokens, np.int32).reshape(-1))
+        self._emb = np.ascontiguousarray(embeddings, np.float32)
+        n = self._emb.shape[0]
+        self._ids = None if item_ids is None else np.ascontiguousarray(np.asarray(item_ids, np.int64))
+        names = ([str(int(i)) for i in self._ids] if self._ids is not None
+                 else [str(i) for i in range(n)])
+        self.request = ScoreRequest(prefix_tokens=self._prefix, mode=ScoreMode.Mixed,
+                                    items=[ScoreItem(id=x) for x in names])
+        h = C.c_void_p()
+        _check(_lib.sr_plan_create_emb(
+            engine._h, self._prefix.ctypes.data_as(C.POINTER(C.c_int32)), len(self._prefix),
+            self._emb.ctypes.data_as(C.POINTER(C.c_float)), self._emb.shape[1], n,
+            self._ids.ctypes.data_as(C.POINTER(C.c_int64)) if self._ids is not None else None,
+            ScoringEngine._emb_form(form), k, C.byref(h)))
+        self._h = h
+        self.k = k
+        self._rb = _ResultBuf(n, len(engine.task_names), k)
+
+
 class BatchPlan(Plan):
     """Several requests resident in one packed device pass (plan_batches
     consumer; BASELINE config C4 runs 32 queries per pass)."""
@@ -908,6 +991,55 @@ def tokenize(text: str, max_seq: int = 4096) -> List[int]:
         raise SemrankError(ErrorCode.LengthOverflow,
                            f"text of {len(data)} bytes exceeds max_seq {max_seq}")
     return list(data)
+
+
+@dataclass
+class PromptParts:  # prompt.hpp:17-20
+    prefix_tokens: List[int]
+    item_tokens: List[int]
+
+
+kPromptSuffix = "\nRelevant (Yes/No): "  # prompt.hpp:23
+
+
+def _text_bytes(t) -> bytes:
+    return t if isinstance(t, (bytes, bytearray)) else str(t).encode("utf-8")
+
+
+def build_prompt(system, query_context, document, max_seq: int = 4096) -> PromptParts:
+    """build_prompt (prompt.cpp:14-38) through the library (sr_build_prompt):
+    prefix = system + query context, item = document + kPromptSuffix, byte
+    tokens; LengthOverflow / SpecViolation as the reference."""
+    s, q, d = _text_bytes(system), _text_bytes(query_context), _text_bytes(document)
+    n_p, n_i = C.c_int32(0), C.c_int32(0)
+    cap_p, cap_i = len(s) + len(q), len(d) + len(kPromptSuffix)
+    pre = np.zeros(max(cap_p, 1), np.int32)
+    item = np.zeros(max(cap_i, 1), np.int32)
+    I = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))
+    _check(_lib.sr_build_prompt(s, len(s), q, len(q), d, len(d), max_seq, I(pre), cap_p,
+                                C.byref(n_p), I(item), cap_i, C.byref(n_i)))
+    return PromptParts(pre[:n_p.value].tolist(), item[:n_i.value].tolist())
+
+
+def score_result_to_json(result: "ScoreResult") -> str:
+    """The /score response body (score_result_to_json, service.cpp:380-391),
+    serialised by the library byte-identically to the reference's
+    nlohmann::json dump()."""
+    items = list(result.items)
+    names = list(items[0].tasks.keys()) if items else []
+    sc = np.ascontiguousarray([[it.tasks[n] for n in names] for it in items] or [[0.0]], np.float64)
+    ids = (C.c_char_p * max(1, len(items)))(*[_text_bytes(it.item_id) for it in items])
+    nm = (C.c_char_p * max(1, len(names)))(*[_text_bytes(n) for n in names])
+    fl = _c.FlopReportC(result.flops.attention_units, result.flops.linear_units, result.flops.t_q,
+                        result.flops.t_i_mean, result.flops.n_items)
+    n = C.c_int64(0)
+    rid = _text_bytes(result.request_id)
+    args = (rid, len(items), ids, len(names), nm, sc.ctypes.data_as(C.POINTER(C.c_double)),
+            C.byref(fl))
+    _check(_lib.sr_score_result_to_json(*args, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(_lib.sr_score_result_to_json(*args, buf, n.value, C.byref(n)))
+    return buf.raw[:n.value].decode("utf-8")
 
 
 def parse_score_request_json(body: str, d_model: int, max_seq: int = 4096) -> ScoreRequest:

@@ -9,10 +9,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIBDIR = os.path.join(ROOT, "paper_2602_07309_b200", "lib")
 
 
-def _build(tmp_path):
-    exe = str(tmp_path / "facade_smoke")
+def _build(tmp_path, name="facade_smoke"):
+    exe = str(tmp_path / name)
     subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
-                    os.path.join(ROOT, "tests", "facade_smoke.cpp"), "-L", LIBDIR,
+                    os.path.join(ROOT, "tests", name + ".cpp"), "-L", LIBDIR,
                     "-lsemrank_b200", f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
     return exe
 
@@ -28,3 +28,18 @@ def test_facade_scores_on_device(tmp_path):
     out = subprocess.run([_build(tmp_path), "gpu"], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "relevance[0]=" in out.stdout
+
+
+def test_acceptance_harness_compiles_against_facade(tmp_path):
+    _build(tmp_path, "acceptance_facade")
+
+
+@pytest.mark.gpu
+def test_acceptance_criteria_1_and_4_through_facade(tmp_path):
+    """acceptance_main.cpp:90-104 and 146-174 as the reference writes them,
+    running on the device through the facade."""
+    out = subprocess.run([_build(tmp_path, "acceptance_facade")], capture_output=True, text=True)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "criterion 1 PASS" in out.stdout and "criterion 4 PASS" in out.stdout
+    assert "acceptance ok" in out.stdout
