@@ -7,10 +7,12 @@ ff1536, V300, fan-in random init, seed 2026), 1 query x 256 candidates,
 A step = one full pass of the hot path over one query: packed shared-prefix
 prefill through all 20 layers, final-LN score head, top-k.
 
-Multi-GPU (torchrun, one rank per GPU): weak scaling by candidate sharding —
-the query has 256 x N candidates, rank r scores its contiguous shard of 256
-(prefix recomputed per rank) and the per-rank top-k lists are merged with one
-NCCL all-gather inside the step. value = all pairs / max-over-ranks time.
+Multi-GPU (torchrun, one rank per GPU): BASELINE.json configs[4] ("c5", the
+default when WORLD_SIZE > 1) — 1 query x 8192 candidates of the C2 model split
+contiguously across the ranks (global ids kept), prefix recomputed per rank,
+per-rank top-k lists merged with one NCCL all-gather + device merge inside the
+step (strong scaling). value = 8192 pairs / max-over-ranks time. At N=1 the
+line carries the same C5 workload on one GPU under "c5".
 
   value : device-resident inputs, CUDA-graph replay + NCCL merge, CUDA events
           on the engine stream
@@ -43,7 +45,10 @@ WORKLOADS = {
     "c3": (20, 1024, 8, 1536, 256, 8, 1024, True),
     "c1": (2, 64, 4, 256, 500, 50, 64, False),
     "c4": (28, 2048, 16, 6144, 256, 96, 250, False),
+    # configs[4]: 8192 candidates in total, split across the ranks (strong scaling)
+    "c5": (20, 1024, 8, 1536, 256, 96, 8192, False),
 }
+STRONG = {"c5"}  # n_items is the whole job's, not per GPU
 # queries packed into one device pass per step (per GPU)
 QUERIES = {"c4": 32}
 WORKLOAD_DESC = {
@@ -55,7 +60,35 @@ WORKLOAD_DESC = {
           "8 soft-token rows per item (context compression)",
     "c1": "reference default toy ranker (L2 d64 H4 ff256), 1 query x 64 candidates, "
           "T_q 500, T_i 50 (cmd_bench shape)",
+    "c5": "candidate-sharded ranking: 1 query x 8192 candidates (C2 model, 96-token items, "
+          "256-token prefix) split across the GPUs, NCCL top-k merge",
 }
+
+
+def shard(wl, world, rank):
+    """(items on this rank, global id of its first item, items in the whole job)."""
+    n = WORKLOADS[wl][6]
+    if wl in STRONG:
+        base, extra = divmod(n, world)
+        n_loc = base + (1 if rank < extra else 0)
+        lo = rank * base + min(rank, extra)
+        return n_loc, lo, n
+    return n, rank * n, n * world
+
+
+def config_for(wl, world):
+    """The workload description both arms print (identical dicts)."""
+    L, d, H, ff, t_q, t_i, n, soft = WORKLOADS[wl]
+    nq = QUERIES.get(wl, 1)
+    _, _, n_all = shard(wl, world, 0)
+    par = ("single-gpu" if world == 1 else f"query-batch replicas x{world}" if nq > 1 else
+           f"candidate-shard x{world}")
+    return {"workload": WORKLOAD_DESC[wl], "model": f"semrank-{wl}-L{L}-d{d}",
+            "global_batch": n_all * nq, "seq_len": t_q + t_i, "queries_per_step": nq * (
+                world if wl not in STRONG and nq > 1 else 1),
+            "candidates_per_query": n_all if wl in STRONG else n * (world if nq == 1 else 1),
+            "parallelism": par, "top_k": TOPK,
+            "l2": "inputs+weights+activations per step > 126 MB L2 (no flush)"}
 TOPK = 10  # service page size (service.hpp:24)
 
 
@@ -140,11 +173,10 @@ class ClockSampler:
 
 
 def make_request(sr, wl, world, rank, seed=7):
-    L, d, H, ff, t_q, t_i, n_loc, soft = WORKLOADS[wl]
+    L, d, H, ff, t_q, t_i, _, soft = WORKLOADS[wl]
     rng = np.random.default_rng(seed)
     prefix = rng.integers(0, 256, t_q).astype(np.int32)
-    n_all = n_loc * world
-    lo = rank * n_loc
+    n_loc, lo, n_all = shard(wl, world, rank)
     req = sr.ScoreRequest(request_id=f"bench-{wl}", prefix_tokens=prefix,
                           mode=sr.ScoreMode.Mixed if soft else sr.ScoreMode.MultiItem)
     if soft:
@@ -171,9 +203,43 @@ def make_queries(sr, wl, n_queries, rank):
 
 
 # ------------------------------------------------------------- CPU baseline
-def cpu_reference_run(wl, n_items, weights_path, fan_in, threads):
-    """One bounded sample on the host: prefix + n_items items, reference
-    multi_item (or mixed) mode; returns seconds. Test infrastructure only."""
+class _RefCfg:
+    """ModelConfig fields the oracle harness reads (the reference arm never
+    imports the product)."""
+
+    class _Head:
+        def __init__(self, name):
+            self.name, self.arity = name, 1
+
+    def __init__(self, wl):
+        L, d, H, ff = WORKLOADS[wl][:4]
+        self.n_layers, self.d_model, self.n_heads, self.d_ff = L, d, H, ff
+        self.vocab_size, self.max_seq, self.yes_token_id, self.no_token_id = 300, 4096, 261, 262
+        self.head_specs = [self._Head(n) for n in ("click", "apply", "badfit", "shortlist",
+                                                   "dismiss")]
+
+
+def reference_weights(wl):
+    """SRNKWTS1 file of the workload's weights written by the reference's own
+    Rng + save_weights (oracle/_ref), else by the C port — byte-identical to
+    the product's init_model (tests/test_host.py). Test infrastructure only."""
+    from oracle import oracle as O
+    fd, path = tempfile.mkstemp(prefix=f"bench_{wl}_", suffix=".srnk")
+    os.close(fd)
+    fan_in = wl != "c1"
+    seed = 2026 if fan_in else 1
+    cfg = _RefCfg(wl)
+    if O.ref_available():
+        O.ref_init_save(cfg, seed, path, fan_in=fan_in)
+    else:
+        O.OracleWeights.init(cfg, seed, 1 if fan_in else 0).save(path)
+    return path
+
+
+def cpu_reference_run(wl, n_items, weights_path, threads):
+    """One query on the host: prefix + the first n_items items of the
+    workload's request stream, reference multi_item (tokens) or mixed (soft
+    rows) mode; returns (seconds, kind). Test infrastructure only."""
     from oracle import oracle as O
     L, d, H, ff, t_q, t_i, _, soft = WORKLOADS[wl]
     rng = np.random.default_rng(7)
@@ -196,58 +262,95 @@ def cpu_reference_run(wl, n_items, weights_path, fan_in, threads):
     return time.perf_counter() - t0, "port"
 
 
-def cpu_baseline(sr, wl, weights, budget_s=20.0):
-    """Times the reference CPU path on a bounded sample sized to ~budget_s."""
-    L, d, H, ff, t_q, t_i, n_loc, soft = WORKLOADS[wl]
-    path = os.path.join(tempfile.gettempdir(), f"bench_{wl}_weights.srnk")
-    weights.save(path)
+SAMPLE_ITEMS = {"c1": 64, "c2": 8, "c3": 48, "c4": 3, "c5": 8}
+
+
+def reference_query_time(wl, path, threads):
+    """One bounded sample of one query of the workload on the host.
+
+    Runs the reference on (prefix + 1 item) and (prefix + S items) and fits its
+    cost model t(n) = a + n b (a = prefix prefill, b = one item). The reference
+    scores a whole query of N items as score_multi_item_chunked does
+    (engine.cpp:328-377): greedy chunks under max_seq, each chunk repaying the
+    prefix — or, in mixed mode, score_mixed's single prefix (engine.cpp:238-276)
+    — so one query costs chunks(N) a + N b. Returns (seconds per query, kind,
+    detail)."""
+    L, d, H, ff, t_q, t_i, n, soft = WORKLOADS[wl]
+    n_q = n  # items of one query (C5: the whole 8192)
+    S = min(SAMPLE_ITEMS.get(wl, 8), n_q)
+    t1, kind = cpu_reference_run(wl, 1, path, threads)
+    if S == n_q and (soft or t_q + n_q * t_i <= 4096):
+        tS, kind = cpu_reference_run(wl, S, path, threads)
+        return tS, kind, f"full query ({n_q} items) {tS:.2f} s"
+    tS, kind = cpu_reference_run(wl, S, path, threads)
+    b = max(tS - t1, 0.0) / (S - 1)
+    a = max(t1 - b, 0.0)
+    per_chunk = max(1, (4096 - t_q) // t_i)
+    chunks = 1 if soft else -(-n_q // per_chunk)
+    return chunks * a + n_q * b, kind, (f"t(1 item) {t1:.2f} s, t({S} items) {tS:.2f} s -> "
+                                        f"a {a:.3f} s, b {b:.4f} s, {chunks} chunk(s)")
+
+
+def cpu_baseline(wl, samples=3):
+    """The reference CPU path on the box's host cores (rank 0, N=1 only)."""
+    L, d, H, ff, t_q, t_i, n, soft = WORKLOADS[wl]
+    nq = QUERIES.get(wl, 1)
+    path = reference_weights(wl)
     threads = os.cpu_count() or 1
-    probe_n = 1 if wl != "c1" else 8
-    t_probe, kind = cpu_reference_run(wl, probe_n, path, True, threads)
-    # model: t(n) = t_prefix + n * t_item with t_prefix ~ (t_q / t_i) * t_item
-    per_item = t_probe / (probe_n + t_q / t_i)
-    n = int(max(probe_n, min(n_loc, (budget_s / per_item) - t_q / t_i)))
-    t, kind = cpu_reference_run(wl, n, path, True, threads)
-    return {"value": n / t, "unit": "pairs/s", "cores": threads, "kind": kind,
-            "sample": f"1 query: {t_q}-token prefix + {n} x {t_i}-token items of the {wl} "
-                      f"workload, reference {'mixed' if soft else 'multi_item'} mode, "
-                      f"OpenMP on all host threads, prefix time included ({t:.1f} s)"}, path
+    try:
+        cpu_reference_run(wl, 1, path, threads)  # loads + caches the weights (not timed)
+        ts = []
+        for _ in range(samples):
+            tq, kind, detail = reference_query_time(wl, path, threads)
+            ts.append(tq)
+    finally:
+        os.unlink(path)
+    tq = statistics.median(ts)
+    return {"value": n / tq, "unit": "pairs/s", "cores": threads, "kind": kind,
+            "sample": _sample_text(wl, detail, samples) + (f"; x{nq} queries per step"
+                                                           if nq > 1 else "")}
+
+
+def _sample_text(wl, detail, samples):
+    L, d, H, ff, t_q, t_i, n, soft = WORKLOADS[wl]
+    mode = "score_mixed" if soft else "score_multi_item_chunked"
+    return (f"per sample: the reference ({mode}, OpenMP on all host threads) on the prefix + 1 "
+            f"and + S items of the workload's first query, extrapolated with its own cost "
+            f"model chunks(N)*prefix + N*item to the full {n}-item query; median of {samples}: "
+            f"{detail}")
 
 
 # ---------------------------------------------------------------- main arms
 def run_reference_arm(args):
+    """The reference's own CPU implementation (oracle/_ref) on the same
+    workload, config and metric as our arm; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    import paper_2602_07309_b200 as sr  # host-side init only (no GPU work)
     wl = args.workload
-    L, d, H, ff, t_q, t_i, n_loc, soft = WORKLOADS[wl]
-    cfg = sr.ModelConfig(n_layers=L, d_model=d, n_heads=H, d_ff=ff,
-                         head_specs=sr.ModelConfig.default_toy().head_specs)
-    w = sr.init_model(cfg, 2026 if wl != "c1" else 1, "fan_in" if wl != "c1" else "reference")
-    path = os.path.join(tempfile.gettempdir(), f"bench_{wl}_weights.srnk")
-    w.save(path)
+    L, d, H, ff, t_q, t_i, n, soft = WORKLOADS[wl]
+    nq = QUERIES.get(wl, 1)
+    _, _, n_all = shard(wl, world, 0)
+    queries = nq * (world if wl not in STRONG else 1) if nq > 1 else 1
+    path = reference_weights(wl)
     threads = os.cpu_count() or 1
-    steps = args.steps + args.warmup
-    budget = max(2.0, 150.0 / max(steps, 1))
-    probe_n = 1 if wl != "c1" else 8
-    t_probe, kind = cpu_reference_run(wl, probe_n, path, True, threads)
-    per_item = t_probe / (probe_n + t_q / t_i)
-    n = int(max(probe_n, min(n_loc, budget / per_item - t_q / t_i)))
-    times = []
-    for s in range(steps):
-        t, kind = cpu_reference_run(wl, n, path, True, threads)
-        if s >= args.warmup:
-            times.append(t)
-    value = n * len(times) / sum(times)
-    sample = (f"per step 1 query: {t_q}-token prefix + {n} x {t_i}-token items "
-              f"({'mixed' if soft else 'multi_item'} mode), prefix included")
+    times, detail, kind = [], "", "reference"
+    try:
+        for s_ in range(args.warmup + args.steps):
+            tq, kind, detail = reference_query_time(wl, path, threads)
+            if s_ >= args.warmup:
+                times.append(tq * queries if nq > 1 else tq * (n_all / n))
+    finally:
+        os.unlink(path)
+    pairs = n_all * nq if nq > 1 else n_all
+    value = pairs * len(times) / sum(times)
+    sample = _sample_text(wl, detail, args.steps)
     line = {"metric": "query-item pairs scored/sec", "value": value, "unit": "pairs/s",
-            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000 * statistics.mean(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD_DESC[wl], "model": f"semrank-{wl}",
-                       "global_batch": n, "seq_len": t_q + t_i, "parallelism": "cpu-openmp"},
+            "scaling": "strong" if wl in STRONG else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": config_for(wl, world),
             "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": kind,
                              "sample": sample},
             "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
@@ -269,7 +372,8 @@ def run_ours(args):
     import paper_2602_07309_b200 as sr
 
     wl = args.workload
-    L, d, H, ff, t_q, t_i, n_loc, soft = WORKLOADS[wl]
+    L, d, H, ff, t_q, t_i, _, soft = WORKLOADS[wl]
+    n_loc, _, n_all = shard(wl, world, rank)
     cfg = sr.ModelConfig(n_layers=L, d_model=d, n_heads=H, d_ff=ff,
                          head_specs=sr.ModelConfig.default_toy().head_specs)
     weights = sr.init_model(cfg, 2026 if wl != "c1" else 1, "fan_in" if wl != "c1" else "reference")
@@ -328,7 +432,7 @@ def run_ours(args):
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    pairs = n_loc * nq * world * args.steps
+    pairs = n_all * nq * args.steps  # the whole job's pairs (all ranks)
     value = pairs / (total_ms / 1000.0)
     lat_sorted = sorted(step_ms)
     p99 = lat_sorted[max(0, int(np.ceil(0.99 * len(lat_sorted))) - 1)]  # service.cpp:28-34
@@ -405,10 +509,17 @@ def run_ours(args):
                               "achieved_tflops": att / (attn_ms / 1000) / 1e12},
                 "per_class_ms": {c: round(v[0], 4) for c, v in prof.items()}}
 
+    # configs[4] on this one GPU (the N=1 point of the C5 scaling curve)
+    launches = plan.kernel_count() * args.steps
+    c5 = None
+    if wl == "c2" and world == 1 and not args.no_c5:
+        del plan
+        c5 = c5_single_gpu(sr, eng, torch, stream)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu, _ = cpu_baseline(sr, wl, weights)
+            cpu = cpu_baseline(wl)
         except Exception as e:  # oracle missing on the box -> reported, not fatal
             cpu = {"value": None, "unit": "pairs/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"unavailable: {e}"}
@@ -416,25 +527,22 @@ def run_ours(args):
     line = {
         "metric": "query-item pairs scored/sec", "value": value, "unit": "pairs/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if wl in STRONG else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[wl], "model": f"semrank-{wl}-L{L}-d{d}",
-                   "global_batch": n_loc * nq * world, "seq_len": t_q + t_i,
-                   "queries_per_step_per_gpu": nq,
-                   "parallelism": ("single-gpu" if world == 1 else
-                                   f"query-batch replicas x{world}" if nq > 1 else
-                                   f"candidate-shard x{world}"),
-                   "sweep": sweep or None,
-                   "tokens_per_query_per_gpu": M, "top_k": k,
-                   "p99_query_ms": p99, "p50_query_ms": statistics.median(step_ms),
-                   "latency_budget_ms": 500, "meets_p99_budget": p99 <= 500,
-                   "prefill_tokens_per_s_per_gpu": M / (total_ms / args.steps / 1000.0),
-                   "l2": "inputs+weights+activations per step > 126 MB L2 (no flush)"},
+        "config": config_for(wl, world),
+        "device_pass": {"tokens_per_pass_per_gpu": M, "items_per_gpu": n_loc,
+                        "prefill_tokens_per_s_per_gpu": M / (total_ms / args.steps / 1000.0),
+                        "p99_pass_ms": p99, "p50_pass_ms": statistics.median(step_ms),
+                        "sweep": sweep or None},
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "path": "ScoringEngine.score -> sr_engine_score (host arrays in/out)"},
-        "gpu_launches": plan.kernel_count() * args.steps,
-        "clocks": clk, "roofline": roofline, "cpu_baseline": cpu,
+                "path": ("ScoringEngine.score_batch -> sr_engine_score_batch" if nq > 1 else
+                         "ScoringEngine.score_sharded -> sr_engine_score_sharded (NCCL merge)"
+                         if comm is not None else
+                         "ScoringEngine.score -> sr_engine_score") + " (host arrays in/out)"},
+        "gpu_launches": launches,
+        "clocks": clk, "roofline": roofline, "cpu_baseline": cpu, "c5": c5,
         "topk_head": [(iid, round(s, 6)) for iid, s in result.topk[:3]],
     }
     if rank == 0:
@@ -443,6 +551,31 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def c5_single_gpu(sr, eng, torch, stream, steps=3, warmup=2):
+    """BASELINE configs[4] (8192 candidates, C2 model) on one GPU: the N=1
+    point of the strong-scaling curve the torchrun runs print as their value."""
+    req, ids = make_request(sr, "c5", 1, 0)
+    plan = eng.plan(req, k=TOPK, item_ids=ids)
+    for _ in range(warmup):
+        plan.run()
+    plan.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        plan.run()
+    e1.record(stream)
+    plan.sync()
+    ms = e0.elapsed_time(e1) / steps
+    res = plan.fetch()
+    out = {"workload": WORKLOAD_DESC["c5"] + " (1 GPU)", "value": 8192 / (ms / 1000.0),
+           "unit": "pairs/s", "ms_per_step": ms, "steps": steps, "warmup": warmup,
+           "gpu_launches": plan.kernel_count() * steps,
+           "topk_head": [(iid, round(s, 6)) for iid, s in res.topk[:3]]}
+    del plan
+    return out
 
 
 # ------------------------------------------------ retrieval scan (§8(f) row 4)
@@ -609,9 +742,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS) + sorted(RETRIEVAL) + ["c3_wire"],
-                    default="c2")
+                    default=None, help="default: c2 (configs[1]) at N=1, c5 (configs[4]) under "
+                                       "torchrun with WORLD_SIZE > 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the N=1 configs[4] sub-measurement")
     args = ap.parse_args()
+    if args.workload is None:
+        args.workload = "c5" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "c2"
     if args.warmup < 3:
         args.warmup = 3
     if args.workload == "c3_wire":

@@ -284,6 +284,16 @@ int32_t sr_plan_shape(const sr_plan* p, int64_t* out8);
 int32_t sr_nccl_unique_id(uint8_t out[128]);
 int32_t sr_comm_create(int32_t nranks, int32_t rank, const uint8_t id[128], int32_t device,
                        sr_comm** out);
+/* Same candidate sharding with the per-rank top-k exchange (k x 24-byte
+ * entries) carried by the caller's all-gather instead of NCCL — for
+ * transports such as gloo/MPI, or several ranks sharing one device where NCCL
+ * refuses duplicate GPUs. fn(send, recv, bytes, user) must write every rank's
+ * `bytes` in rank order into recv and return 0. The local pass, sentinel
+ * padding and the device merge are the NCCL path's. */
+typedef int32_t (*sr_allgather_fn)(const void* send, void* recv, size_t bytes_per_rank,
+                                   void* user);
+int32_t sr_comm_create_host(int32_t nranks, int32_t rank, int32_t device, sr_allgather_fn fn,
+                            void* user, sr_comm** out);
 void sr_comm_destroy(sr_comm* c);
 int32_t sr_engine_score_sharded(sr_engine* e, sr_comm* c, const sr_request* local_shard,
                                 sr_result* res);

@@ -104,6 +104,8 @@ _sig("sr_plan_profile", i32, vp, i32, P(f32), P(i32))
 _sig("sr_plan_shape", i32, vp, P(i64))
 _sig("sr_nccl_unique_id", i32, P(C.c_uint8))
 _sig("sr_comm_create", i32, i32, i32, P(C.c_uint8), i32, P(vp))
+ALLGATHER_FN = C.CFUNCTYPE(i32, vp, vp, sz, vp)
+_sig("sr_comm_create_host", i32, i32, i32, i32, ALLGATHER_FN, vp, P(vp))
 _sig("sr_comm_destroy", None, vp)
 _sig("sr_engine_score_sharded", i32, vp, vp, P(RequestC), P(ResultC))
 _sig("sr_plan_run_sharded", i32, vp, vp)
@@ -156,7 +158,7 @@ HEADER_SYMBOLS = [
     "sr_plan_create_emb", "sr_engine_device", "sr_engine_stream", "sr_plan_create",
     "sr_plan_create_batch", "sr_plan_fetch_batch", "sr_plan_run", "sr_plan_sync", "sr_plan_fetch", "sr_plan_kernel_count", "sr_plan_destroy",
     "sr_plan_profile", "sr_plan_shape",
-    "sr_nccl_unique_id", "sr_comm_create", "sr_comm_destroy", "sr_engine_score_sharded",
+    "sr_nccl_unique_id", "sr_comm_create", "sr_comm_create_host", "sr_comm_destroy", "sr_engine_score_sharded",
     "sr_plan_run_sharded", "sr_engine_score_b64", "sr_wire_parse", "sr_wire_destroy",
     "sr_wire_info", "sr_wire_request_id", "sr_wire_item_id", "sr_engine_score_wire", "sr_engine_set_postprocess", "sr_engine_final_scores",
     "sr_score_cache_create", "sr_score_cache_destroy", "sr_score_cache_size",

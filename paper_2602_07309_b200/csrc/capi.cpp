@@ -763,6 +763,16 @@ int32_t sr_comm_create(int32_t nranks, int32_t rank, const uint8_t id[128], int3
   });
 }
 
+int32_t sr_comm_create_host(int32_t nranks, int32_t rank, int32_t device, sr_allgather_fn fn,
+                            void* user, sr_comm** out) {
+  return guard([&] {
+    if (!out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    auto c = std::make_unique<sr_comm>();
+    c->c = srh::comm_create_host(nranks, rank, device, fn, user);
+    *out = c.release();
+  });
+}
+
 void sr_comm_destroy(sr_comm* c) {
   if (c) srh::comm_destroy(c->c);
   delete c;

@@ -972,6 +972,18 @@ Comm* comm_create(int nranks, int rank, const uint8_t id[128], int device) {
   return c;
 }
 
+Comm* comm_create_host(int nranks, int rank, int device, sr_allgather_fn fn, void* user) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail(SR_PARAMETER, "bad rank/nranks");
+  if (fn == nullptr) fail(SR_SPEC_VIOLATION, "null all-gather callback");
+  auto* c = new Comm;
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  c->host_fn = fn;
+  c->host_user = user;
+  return c;
+}
+
 void comm_destroy(Comm* c) {
   if (!c) return;
   if (c->nccl && nccl().comm_destroy) nccl().comm_destroy(static_cast<ncclComm_t>(c->nccl));
@@ -979,6 +991,17 @@ void comm_destroy(Comm* c) {
 }
 
 void nccl_allgather_bytes(Comm* c, const void* send, void* recv, size_t bytes, cudaStream_t s) {
+  if (c->host_fn != nullptr) {
+    // the caller's transport: this rank's bytes out, every rank's bytes back
+    std::vector<uint8_t> hs(bytes), hr(bytes * static_cast<size_t>(c->nranks));
+    SR_CUDA_CHECK(cudaMemcpyAsync(hs.data(), send, bytes, cudaMemcpyDeviceToHost, s));
+    SR_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (c->host_fn(hs.data(), hr.data(), bytes, c->host_user) != 0)
+      fail(SR_NCCL, "host all-gather callback failed");
+    SR_CUDA_CHECK(cudaMemcpyAsync(recv, hr.data(), hr.size(), cudaMemcpyHostToDevice, s));
+    SR_CUDA_CHECK(cudaStreamSynchronize(s));
+    return;
+  }
   nccl_check(nccl().all_gather(send, recv, bytes, ncclUint8, static_cast<ncclComm_t>(c->nccl), s),
              "ncclAllGather");
 }

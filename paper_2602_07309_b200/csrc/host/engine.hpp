@@ -282,7 +282,11 @@ class Engine {
 struct Comm {
   void* nccl = nullptr;  // ncclComm_t
   int nranks = 1, rank = 0, device = 0;
+  // host-transport variant (sr_comm_create_host): the caller's all-gather
+  sr_allgather_fn host_fn = nullptr;
+  void* host_user = nullptr;
 };
+Comm* comm_create_host(int nranks, int rank, int device, sr_allgather_fn fn, void* user);
 void nccl_unique_id(uint8_t out[128]);
 Comm* comm_create(int nranks, int rank, const uint8_t id[128], int device);
 void comm_destroy(Comm* c);

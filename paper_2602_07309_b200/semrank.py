@@ -869,6 +869,31 @@ class Comm:
         _check(_lib.sr_comm_create(nranks, rank, buf, device, C.byref(h)))
         self._h = h
 
+    @classmethod
+    def host(cls, nranks: int, rank: int, device: int, allgather) -> "Comm":
+        """Top-k exchange over a caller transport (sr_comm_create_host):
+        ``allgather(bytes) -> list of every rank's bytes in rank order`` (e.g.
+        torch.distributed.all_gather_object under gloo)."""
+        self = cls.__new__(cls)
+
+        def fn(send, recv, nbytes, user):
+            try:
+                mine = C.string_at(send, nbytes)
+                parts = allgather(mine)
+                blob = b"".join(parts)
+                if len(parts) != nranks or len(blob) != nbytes * nranks:
+                    return 1
+                C.memmove(recv, blob, len(blob))
+                return 0
+            except Exception:  # reported as SR_NCCL by the library
+                return 1
+
+        self._fn = _c.ALLGATHER_FN(fn)  # kept alive with the communicator
+        h = C.c_void_p()
+        _check(_lib.sr_comm_create_host(nranks, rank, device, self._fn, None, C.byref(h)))
+        self._h = h
+        return self
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:

@@ -11,7 +11,9 @@ Tolerances (max |score difference| on probabilities in [0, 1]):
   bf16; measured round 1: toy 2.5e-3, C2 1.8e-3 (3.1e-3 vs fp32 weights),
   C3 1.5e-3 — see DESIGN.md §5).
 Top-k must equal the oracle ordering outside ties; a tie is a pair of oracle
-scores within 2*TOL of each other.
+scores within 2 x the max relevance deviation measured in the same test (a
+per-item error e can only swap items closer than 2e). Full-request parity at
+the BASELINE configs is in test_gpu_headline.py.
 Structural properties that the reference tests hold exactly are held
 exactly here too (mode equivalence on one device pass, isolation, batch ==
 single, resident plan == score call).
@@ -60,11 +62,14 @@ def oracle_bf16(cfg, seed, scheme):
     return w
 
 
-def assert_topk_outside_ties(got_ids, ref_rel, k, tol=TOL):
+def assert_topk_outside_ties(got_ids, ref_rel, k, got_rel=None, tol=TOL):
+    """Top-k equals the oracle order outside ties; a tie = two oracle scores
+    within 2 x the measured max relevance deviation (got_rel given), else 2 x tol."""
+    window = 2 * (float(np.abs(np.asarray(got_rel) - ref_rel).max()) if got_rel is not None else tol)
     order = sorted(range(len(ref_rel)), key=lambda i: (-ref_rel[i], i))[:k]
     for j, (a, b) in enumerate(zip(got_ids, order)):
         if a != b:
-            assert abs(ref_rel[a] - ref_rel[b]) <= 2 * tol, f"top-k differs at rank {j} outside ties"
+            assert abs(ref_rel[a] - ref_rel[b]) <= window, f"top-k differs at rank {j} outside ties"
 
 
 _ENGINES = {}
@@ -87,7 +92,7 @@ def test_toy_bench_parity_and_topk(cuda):
     d16, d32 = np.abs(res.scores - ref16).max(), np.abs(res.scores - ref32).max()
     print(f"toy bench: max dev vs oracle(bf16 w) {d16:.2e}, vs reference fp32 {d32:.2e}")
     assert d16 <= TOL and d32 <= TOL
-    assert_topk_outside_ties([int(i) for i, _ in res.topk], ref16[:, 0], 10)
+    assert_topk_outside_ties([int(i) for i, _ in res.topk], ref16[:, 0], 10, res.scores[:, 0])
     # flop report as the reference reports it for multi_item
     fl = res.flops
     assert [fl.attention_units, fl.linear_units, fl.t_q, fl.t_i_mean, fl.n_items] == \
@@ -121,7 +126,7 @@ def test_acceptance_criterion_1_shape(cuda):
         ref16 = ow.score(r["prefix"], r["items"])
         assert np.abs(res.scores - ref16).max() <= TOL
         assert np.abs(res.scores - np.asarray(r["multi_item"])).max() <= TOL
-        assert_topk_outside_ties([int(i) for i, _ in res.topk], ref16[:, 0], 10)
+        assert_topk_outside_ties([int(i) for i, _ in res.topk], ref16[:, 0], 10, res.scores[:, 0])
 
 
 def test_mixed_mode_substitute_embedding_and_one_token(cuda):
@@ -357,4 +362,4 @@ def test_c4_dims_parity(cuda):
     d = np.abs(res.scores - ref16).max()
     print(f"C4 dims (2 layers): max dev vs oracle(bf16 w) {d:.2e}")
     assert d <= TOL
-    assert_topk_outside_ties([int(i) for i, _ in res.topk], ref16[:, 0], 3)
+    assert_topk_outside_ties([int(i) for i, _ in res.topk], ref16[:, 0], 3, res.scores[:, 0])
