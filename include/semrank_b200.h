@@ -277,6 +277,50 @@ int32_t sr_plan_profile(sr_plan* p, int32_t reps, float* ms_out, int32_t* launch
  * call, D2H bytes per call, k, tasks}. */
 int32_t sr_plan_shape(const sr_plan* p, int64_t* out8);
 
+/* ------------------------------- serving scheduler
+ * Latency-bounded dynamic batching in front of one engine. Callers submit
+ * whole requests from any thread (deep-copied at submit unless borrow is set, validated with the
+ * scoring error categories); one dispatcher thread packs the queued requests
+ * FIFO into device passes — the greedy rule of plan_batches
+ * (engine.cpp:278-326) over whole requests under max_rows, at most
+ * max_queries per pass and, with budget_ms > 0, only while
+ * age(oldest) + est_ms(rows) <= budget_ms (est learned from the passes run) —
+ * and completes each ticket. Replaces callers queueing on ScoringEngine's
+ * mutex (engine.cpp:389-392). Latency = submit -> completion (host clock:
+ * queueing, H2D, device pass, D2H); p50/p99 by nearest rank as the
+ * service's percentile_of (service.cpp:28-34). */
+typedef struct sr_sched sr_sched;
+typedef struct sr_sched_options {
+  int32_t max_queries; /* >= 1 */
+  int64_t max_rows;    /* packed-row budget per pass (>= 1) */
+  double budget_ms;    /* latency rule (0 = off) */
+  int32_t max_wait_us; /* an unfilled pass waits this long after its oldest arrival (0 = no wait) */
+  int32_t k;           /* top-k per request */
+  int32_t borrow;      /* nonzero: request arrays are borrowed until sr_sched_wait
+                          returns (no copy at submit) */
+} sr_sched_options;
+typedef struct sr_sched_stats {
+  int64_t submitted, completed, failed, batches;
+  double mean_batch, p50_ms, p99_ms, max_ms, mean_ms;
+  double ms_per_row; /* current pass-time estimate */
+  double busy_ms;    /* summed pass durations */
+} sr_sched_stats;
+/* One pass over n_req requests (tests: a host stand-in for the engine). */
+typedef int32_t (*sr_sched_exec_fn)(const sr_request* reqs, int32_t n_req, sr_result* res,
+                                    void* user);
+int32_t sr_sched_create(sr_engine* e, const sr_sched_options* opt, sr_sched** out);
+int32_t sr_sched_create_host(const sr_model_config* cfg, const sr_sched_options* opt,
+                             sr_sched_exec_fn fn, void* user, sr_sched** out);
+int32_t sr_sched_submit(sr_sched* s, const sr_request* req, uint64_t* ticket);
+/* Blocks until the ticket completes; res as sr_engine_score (caller buffers,
+ * k <= options.k). Returns the request's own status. */
+int32_t sr_sched_wait(sr_sched* s, uint64_t ticket, sr_result* res, double* latency_ms,
+                      int32_t* batch_queries);
+/* Counters and latency percentiles since the last reset. */
+int32_t sr_sched_get_stats(sr_sched* s, int32_t reset, sr_sched_stats* out);
+/* Fails still-queued tickets with SR_STATE_INVALID, joins the dispatcher. */
+void sr_sched_destroy(sr_sched* s);
+
 /* ------------------------------------------------------- multi-GPU (NCCL) */
 /* Candidate sharding: every rank holds the full weights, scores its shard
  * of the items (with global item ids) and the per-rank top-k lists are merged

@@ -102,6 +102,24 @@ _sig("sr_plan_kernel_count", i32, vp, P(i32))
 _sig("sr_plan_destroy", None, vp)
 _sig("sr_plan_profile", i32, vp, i32, P(f32), P(i32))
 _sig("sr_plan_shape", i32, vp, P(i64))
+class SchedOptionsC(C.Structure):
+    _fields_ = [("max_queries", i32), ("max_rows", i64), ("budget_ms", f64),
+                ("max_wait_us", i32), ("k", i32), ("borrow", i32)]
+
+
+class SchedStatsC(C.Structure):
+    _fields_ = [("submitted", i64), ("completed", i64), ("failed", i64), ("batches", i64),
+                ("mean_batch", f64), ("p50_ms", f64), ("p99_ms", f64), ("max_ms", f64),
+                ("mean_ms", f64), ("ms_per_row", f64), ("busy_ms", f64)]
+
+
+SCHED_EXEC_FN = C.CFUNCTYPE(i32, P(RequestC), i32, P(ResultC), vp)
+_sig("sr_sched_create", i32, vp, P(SchedOptionsC), P(vp))
+_sig("sr_sched_create_host", i32, P(ModelConfigC), P(SchedOptionsC), SCHED_EXEC_FN, vp, P(vp))
+_sig("sr_sched_submit", i32, vp, P(RequestC), P(u64))
+_sig("sr_sched_wait", i32, vp, u64, P(ResultC), P(f64), P(i32))
+_sig("sr_sched_get_stats", i32, vp, i32, P(SchedStatsC))
+_sig("sr_sched_destroy", None, vp)
 _sig("sr_nccl_unique_id", i32, P(C.c_uint8))
 _sig("sr_comm_create", i32, i32, i32, P(C.c_uint8), i32, P(vp))
 ALLGATHER_FN = C.CFUNCTYPE(i32, vp, vp, sz, vp)
@@ -157,7 +175,8 @@ HEADER_SYMBOLS = [
     "sr_engine_item_hidden", "sr_engine_set_projection", "sr_engine_score_emb",
     "sr_plan_create_emb", "sr_engine_device", "sr_engine_stream", "sr_plan_create",
     "sr_plan_create_batch", "sr_plan_fetch_batch", "sr_plan_run", "sr_plan_sync", "sr_plan_fetch", "sr_plan_kernel_count", "sr_plan_destroy",
-    "sr_plan_profile", "sr_plan_shape",
+    "sr_plan_profile", "sr_plan_shape", "sr_sched_create", "sr_sched_create_host",
+    "sr_sched_submit", "sr_sched_wait", "sr_sched_get_stats", "sr_sched_destroy",
     "sr_nccl_unique_id", "sr_comm_create", "sr_comm_create_host", "sr_comm_destroy", "sr_engine_score_sharded",
     "sr_plan_run_sharded", "sr_engine_score_b64", "sr_wire_parse", "sr_wire_destroy",
     "sr_wire_info", "sr_wire_request_id", "sr_wire_item_id", "sr_engine_score_wire", "sr_engine_set_postprocess", "sr_engine_final_scores",

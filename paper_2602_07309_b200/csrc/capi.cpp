@@ -15,6 +15,7 @@
 #include "host/model.hpp"
 #include "host/planner.hpp"
 #include "host/prompt.hpp"
+#include "host/scheduler.hpp"
 #include "kernels/launch.h"
 #include "semrank_b200.h"
 
@@ -399,6 +400,91 @@ int32_t sr_engine_score_batch(sr_engine* e, const sr_request* reqs, int32_t n_re
     e->e->score(reqs, n_req, res);
   });
 }
+
+// ------------------------------------------------------------ scheduler
+struct sr_sched {
+  std::unique_ptr<srh::Scheduler> s;
+};
+
+static srh::SchedOptions sched_options(const sr_sched_options* o) {
+  srh::SchedOptions so;
+  if (o) {
+    so.max_queries = o->max_queries;
+    so.max_rows = o->max_rows;
+    so.budget_ms = o->budget_ms;
+    so.max_wait_us = o->max_wait_us;
+    so.k = o->k;
+    so.borrow = o->borrow != 0;
+  }
+  return so;
+}
+
+int32_t sr_sched_create(sr_engine* e, const sr_sched_options* opt, sr_sched** out) {
+  return guard([&] {
+    if (!e || !out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    srh::Engine* eng = e->e.get();
+    auto s = std::make_unique<sr_sched>();
+    s->s = std::make_unique<srh::Scheduler>(
+        [eng](const sr_request* reqs, int n, sr_result* res) {
+          std::lock_guard<std::mutex> lock(eng->mutex());
+          eng->score(reqs, n, res);
+        },
+        eng->config(), sched_options(opt));
+    *out = s.release();
+  });
+}
+
+int32_t sr_sched_create_host(const sr_model_config* cfg, const sr_sched_options* opt,
+                             sr_sched_exec_fn fn, void* user, sr_sched** out) {
+  return guard([&] {
+    if (!cfg || !fn || !out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    const auto c = srh::ModelConfig::from_c(*cfg);
+    c.validate();
+    auto s = std::make_unique<sr_sched>();
+    s->s = std::make_unique<srh::Scheduler>(
+        [fn, user](const sr_request* reqs, int n, sr_result* res) {
+          const int32_t st = fn(reqs, n, res, user);
+          if (st != SR_OK) srh::fail(static_cast<sr_status>(st), "scheduler pass failed");
+        },
+        c, sched_options(opt));
+    *out = s.release();
+  });
+}
+
+int32_t sr_sched_submit(sr_sched* s, const sr_request* req, uint64_t* ticket) {
+  return guard([&] {
+    if (!s || !req || !ticket) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    *ticket = s->s->submit(*req);
+  });
+}
+
+int32_t sr_sched_wait(sr_sched* s, uint64_t ticket, sr_result* res, double* latency_ms,
+                      int32_t* batch_queries) {
+  return guard([&] {
+    if (!s) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    s->s->wait(ticket, res, latency_ms, batch_queries);
+  });
+}
+
+int32_t sr_sched_get_stats(sr_sched* s, int32_t reset, sr_sched_stats* out) {
+  return guard([&] {
+    if (!s || !out) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    const srh::SchedStats st = s->s->stats(reset != 0);
+    out->submitted = st.submitted;
+    out->completed = st.completed;
+    out->failed = st.failed;
+    out->batches = st.batches;
+    out->mean_batch = st.mean_batch;
+    out->p50_ms = st.p50_ms;
+    out->p99_ms = st.p99_ms;
+    out->max_ms = st.max_ms;
+    out->mean_ms = st.mean_ms;
+    out->ms_per_row = st.ms_per_row;
+    out->busy_ms = st.busy_ms;
+  });
+}
+
+void sr_sched_destroy(sr_sched* s) { delete s; }
 
 int32_t sr_engine_item_hidden(sr_engine* e, const sr_request* req, float* hidden_out) {
   return guard([&] {

@@ -1004,6 +1004,100 @@ class BatchPlan(Plan):
         return out
 
 
+class Scheduler:
+    """Latency-bounded dynamic batching in front of one engine (SURVEY §8(f)
+    row 1; include/semrank_b200.h sr_sched_*). ``submit`` deep-copies and
+    queues a whole request and returns a ticket; the native dispatcher packs
+    queued requests FIFO into device passes (plan_batches' greedy rule over
+    whole requests, engine.cpp:278-326, under ``max_rows``; at most
+    ``max_queries`` per pass; with ``budget_ms`` only while the oldest
+    request's age plus the learned pass time fits the budget). ``wait``
+    returns (ScoreResult, latency_ms, queries in its pass); latency is
+    submit -> completion on the host clock. ``stats`` reports nearest-rank
+    p50/p99 (service.cpp:28-34).
+
+    ``executor`` (tests only) replaces the engine with a host function
+    ``fn(requests: list[RequestC], results: list[ResultC]) -> None`` that fills
+    the result buffers; ``config`` is then the model config to validate against."""
+
+    def __init__(self, engine: Optional["ScoringEngine"] = None, *, max_queries: int = 8,
+                 max_rows: int = 1 << 22, budget_ms: float = 0.0, max_wait_us: int = 0,
+                 k: int = 10, borrow: bool = True, executor=None,
+                 config: Optional[ModelConfig] = None):
+        self.engine = engine
+        self.k = k
+        self.config = engine.config if engine is not None else config
+        self.task_names = [kRelevanceTask] + [h.name for h in self.config.head_specs]
+        opt = _c.SchedOptionsC(max_queries, max_rows, float(budget_ms), max_wait_us, k,
+                               int(bool(borrow)))
+        self.borrow = bool(borrow)
+        h = C.c_void_p()
+        self._pending: Dict[int, tuple] = {}
+        if executor is None:
+            if engine is None:
+                raise SemrankError(ErrorCode.SpecViolation, "scheduler needs an engine")
+            _check(_lib.sr_sched_create(engine._h, C.byref(opt), C.byref(h)))
+        else:
+            def fn(reqs, n, ress, user):
+                try:
+                    executor([reqs[i] for i in range(n)], [ress[i] for i in range(n)])
+                    return 0
+                except SemrankError as e:
+                    return int(e.code)
+                except Exception:  # noqa: BLE001
+                    return int(ErrorCode.StateInvalid)
+            self._fn = _c.SCHED_EXEC_FN(fn)
+            cfg = self._cfg_keep = self.config._to_c()
+            _check(_lib.sr_sched_create_host(C.byref(cfg), C.byref(opt), self._fn, None,
+                                             C.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.sr_sched_destroy(h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def pack(self, request: ScoreRequest) -> "_PackedRequest":
+        """Flattened request for repeated submission (bench load generators)."""
+        return _PackedRequest(request, self.config.d_model)
+
+    def submit(self, request: ScoreRequest, packed: Optional["_PackedRequest"] = None) -> int:
+        pr = packed if packed is not None else _PackedRequest(request, self.config.d_model)
+        t = C.c_uint64(0)
+        _check(_lib.sr_sched_submit(self._h, C.byref(pr.c), C.byref(t)))
+        self._pending[t.value] = (request, pr)  # pr keeps borrowed arrays alive
+        return t.value
+
+    def wait(self, ticket: int):
+        request, _pr = self._pending.pop(ticket)
+        rb = _ResultBuf(len(request.items), len(self.task_names), self.k)
+        lat, nb = C.c_double(0), C.c_int32(0)
+        _check(_lib.sr_sched_wait(self._h, ticket, C.byref(rb.c), C.byref(lat), C.byref(nb)))
+        if self.engine is not None:
+            res = self.engine._to_result(request, rb)
+        else:
+            res = ScoreResult(request_id=request.request_id, mode=ScoreMode(request.mode),
+                              scores=rb.scores[:len(request.items)].copy())
+            for j in range(rb.c.k_returned):
+                res.topk.append((request.items[int(rb.idx[j])].id, float(rb.top[j])))
+        return res, lat.value, nb.value
+
+    def stats(self, reset: bool = False) -> dict:
+        st = _c.SchedStatsC()
+        _check(_lib.sr_sched_get_stats(self._h, int(reset), C.byref(st)))
+        return {f: getattr(st, f) for f, _ in _c.SchedStatsC._fields_}
+
+
 def score_by_mode(engine: ScoringEngine, request: ScoreRequest, k: int = 0) -> ScoreResult:
     """score_by_mode (engine.cpp:379-387): dispatch on request.mode."""
     return engine.score(request, k)

@@ -147,13 +147,16 @@ def test_c3_projected_embeddings_every_item(cuda):
         compare("c3proj", res.scores, g, [int(i) for i, _ in res.topk])
         assert res.kv_incremental_per_item == 8.0
         assert [res.flops.attention_units, res.flops.linear_units] == meta["flops"][:2]
-        # same rows given d_model-wide -> the same device pass, bit for bit
+        # the same rows projected on the host (fp32 sums of the same bf16
+        # products, another summation order): the pass sees inputs that differ
+        # in the last fp32 bits, which bf16 activation rounding turns into
+        # score noise of the same size as the device-vs-oracle error.
         rows = H.project_rows(emb, proj, 8, 1024)
         assert H.sha(rows) == meta["rows_sha256"]
         wide = eng.score(soft_request(prefix, list(rows)), k=K)
         print("c3proj: device projection vs host rows max |dp|",
               float(np.abs(wide.scores - res.scores).max()))
-        assert np.abs(wide.scores - res.scores).max() <= 2e-3
+        assert np.abs(wide.scores - res.scores).max() <= TOL16
         # resident plan with the projection inside the graph
         plan = eng.plan_embeddings(prefix, emb, "project", k=K)
         plan.run()
