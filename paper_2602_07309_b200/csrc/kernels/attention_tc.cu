@@ -60,6 +60,31 @@ struct Slices {
 };
 constexpr int kThreads = 320;  // attn_pp_kernel (kPPThreads) and helpers
 constexpr float kRescaleLog2 = 8.0f;  // rescale O only when the max grows by > 2^8
+// One exponential pair in kPolyEvery goes to the FMA pipe (0 = all on MUFU).
+// Measured (tools/attn_trace.py, C2 layer): every 4th pair shortens the
+// exponential phase ~1.3k -> ~1.05k cycles per block but the kernel slows
+// 91.8k -> 100.2k cycles per CTA, so MUFU-only is the default.
+#ifndef SRK_ATTN_POLY_EVERY
+#define SRK_ATTN_POLY_EVERY 0
+#endif
+constexpr int kPolyEvery = SRK_ATTN_POLY_EVERY;
+#ifndef SRK_ATTN_S_WAIT
+#define SRK_ATTN_S_WAIT 0
+#endif
+
+// Max of N floats with 8 independent FMNMX3 chains (latency-bound otherwise).
+template <int N>
+__device__ __forceinline__ float max_tree(const float (&s)[N]) {
+  static_assert(N % 16 == 0, "max_tree");
+  float m[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) m[c] = fmaxf(s[2 * c], s[2 * c + 1]);
+#pragma unroll
+  for (int i = 16; i < N; i += 16)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) m[c] = fmax3f(m[c], s[i + 2 * c], s[i + 2 * c + 1]);
+  return fmaxf(fmax3f(m[0], m[1], m[2]), fmax3f(fmaxf(m[3], m[4]), fmax3f(m[5], m[6], m[7]), -INFINITY));
+}
 
 template <int HD>
 struct AttnCfg {
@@ -81,11 +106,34 @@ struct AttnCfg {
 // Optional per-CTA timeline (clock64 stamps, 64 slots per CTA, first 256
 // CTAs); enabled by attention_set_trace() for kernel tuning only.
 __device__ unsigned long long* g_attn_trace = nullptr;
-#define SRK_TRACE(slot)                                                                     \
-  do {                                                                                      \
-    if (g_attn_trace != nullptr && blockIdx.x < 256)                                        \
-      g_attn_trace[blockIdx.x * 64 + (slot)] = static_cast<unsigned long long>(clock64()); \
+#ifndef SRK_TRACE_STRIDE
+#define SRK_TRACE_STRIDE 64
+#endif
+#define SRK_TRACE(slot)                                                                      \
+  do {                                                                                       \
+    if (srk_trace != nullptr && blockIdx.x < 256)                                            \
+      srk_trace[blockIdx.x * SRK_TRACE_STRIDE + (slot)] =                                    \
+          static_cast<unsigned long long>(clock64());                                        \
   } while (0)
+// Phase stamps inside the softmax of blocks 8..15 (tuning builds with
+// -DSRK_ATTN_PHASES -DSRK_TRACE_STRIDE=256): slot 64 + 16 (g - 8) + phase.
+#ifdef SRK_ATTN_PHASES
+#define SRK_PHASE(cond, g, ph) \
+  do {                         \
+    if ((cond) && (g) >= 8 && (g) < 16) SRK_TRACE(64 + 16 * ((g) - 8) + (ph)); \
+  } while (0)
+#define SRK_ITEM(cond, li, k) \
+  do {                        \
+    if ((cond) && (li) < 8) SRK_TRACE(192 + 8 * (li) + (k)); \
+  } while (0)
+#else
+#define SRK_PHASE(cond, g, ph) \
+  do {                         \
+  } while (0)
+#define SRK_ITEM(cond, li, k) \
+  do {                        \
+  } while (0)
+#endif
 
 // Walks the (item, block) sequence of one CTA.
 struct Cursor {
@@ -183,6 +231,8 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
   const int n_items = n_tiles * n_heads;
   const int d = n_heads * HD;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // read once: asm "memory" clobbers would otherwise reload it at every stamp
+  unsigned long long* const srk_trace = g_attn_trace;
   if (threadIdx.x == 0) SRK_TRACE(0);
 
   if (warp == 0 && lane == 0) {
@@ -219,16 +269,24 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
     if constexpr (EW) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;" ::: "memory");
   };
 
-  if (warp == 0) {
+#ifndef SRK_ATTN_SPLIT_KV
+#define SRK_ATTN_SPLIT_KV 1
+#endif
+  constexpr bool kSplitKV = EW && SRK_ATTN_SPLIT_KV;
+  if (warp == 0 || (kSplitKV && warp == 3)) {
     regs_down();
     // ------------------------------------------------------------- TMA
+    // EW: warp 0 streams K, warp 3 streams V, so a K load never queues behind
+    // the wait for a V stage (which frees only when PV of two blocks back has
+    // run) — the K ring is what bounds how early S of the next block can go.
+    const bool do_k = !kSplitKV || warp == 0, do_v = !kSplitKV || warp == 3;
     if (lane == 0) {
       const uint64_t keep = policy_evict_last();  // prefix K/V: re-read by every item tile
       Cursor c;
       c.next_item(tiles, n_tiles, n_items, blockIdx.x);
       int g = 0;
       while (c.valid) {
-        if (!EW && c.j == 0) {  // EW: warp 2 loads Q, ahead of the K/V stream
+        if (!EW && c.j == 0) {  // EW: warp 2 loads Q, ahead of the K/V stream (!EW: one producer)
           const int qb = c.li & 1;
           mbar_wait(&q_empty[qb], ((c.li >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(&q_full[qb], C::TILE);
@@ -240,16 +298,22 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
         c.range(k0, kb, ke);
         const int st = g & 1;
         const uint32_t ph = ((g >> 1) & 1) ^ 1;
-        mbar_wait(&k_empty[st], ph);
-        mbar_arrive_expect_tx(&k_full[st], C::TILE);
-        for (int b = 0; b < C::NB; ++b)
-          tma_load_2d_hint(&tm_qkv, &k_full[st], sK + st * C::TILE + b * kBox,
-                           d + c.h * HD + b * 64, k0, keep);
-        mbar_wait(&v_empty[st], ph);
-        mbar_arrive_expect_tx(&v_full[st], C::TILE);
-        for (int b = 0; b < C::NB; ++b)
-          tma_load_2d_hint(&tm_qkv, &v_full[st], sV + st * C::TILE + b * kBox,
-                           2 * d + c.h * HD + b * 64, k0, keep);
+        if (do_k) {
+          mbar_wait(&k_empty[st], ph);
+          SRK_PHASE(true, g, 10);
+          mbar_arrive_expect_tx(&k_full[st], C::TILE);
+          for (int b = 0; b < C::NB; ++b)
+            tma_load_2d_hint(&tm_qkv, &k_full[st], sK + st * C::TILE + b * kBox,
+                             d + c.h * HD + b * 64, k0, keep);
+        }
+        if (do_v) {
+          mbar_wait(&v_empty[st], ph);
+          SRK_PHASE(true, g, 11);
+          mbar_arrive_expect_tx(&v_full[st], C::TILE);
+          for (int b = 0; b < C::NB; ++b)
+            tma_load_2d_hint(&tm_qkv, &v_full[st], sV + st * C::TILE + b * kBox,
+                             2 * d + c.h * HD + b * 64, k0, keep);
+        }
         ++g;
         c.advance(tiles, n_tiles, n_items);
       }
@@ -269,8 +333,10 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
         const int st = gs & 1;
         const int qb = sc.li & 1;
         if (sc.j == 0) mbar_wait(&q_full[qb], (sc.li >> 1) & 1);
+        if (sc.j == 0) SRK_ITEM(true, sc.li, 4);
         mbar_wait(&k_full[st], (gs >> 1) & 1);
         tc_fence_after();
+        SRK_PHASE(true, gs, 6);
         const uint32_t q_addr = smem_u32(sQ + qb * C::TILE);
         const uint32_t k_addr = smem_u32(sK + st * C::TILE);
 #pragma unroll
@@ -293,8 +359,10 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
         const int ob = pc.li & 1;
         if (pc.j == 0) mbar_wait(&o_empty[ob], ((pc.li >> 1) & 1) ^ 1);
         mbar_wait(&p_full[st], ph);
+        SRK_PHASE(true, g, 8);
         mbar_wait(&v_full[st], ph);
         tc_fence_after();
+        SRK_PHASE(true, g, 7);
         const uint32_t v_addr = smem_u32(sV + st * C::TILE);
 #pragma unroll
         for (int s = 0; s < kBK / 16; ++s) {
@@ -306,10 +374,13 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
         umma_commit(&pv_done[st]);
         if (EW && pc.j + 1 == pc.nblk) umma_commit(&o_full[ob]);  // the item's O is final
         if (sc.valid) {
-          // S_{g+2} reuses this TMEM buffer: PV_g must have read P_g first.
-          // (Issuing it right behind PV_g, relying on in-order tcgen05.mma
-          // execution, measured no faster.)
+          // S_{g+2} reuses this TMEM buffer, whose P_g the PV_g just issued
+          // reads. tcgen05.mma from one thread executes in issue order, so
+          // S_{g+2} goes right behind PV_g (SRK_ATTN_S_WAIT=1: wait for PV_g's
+          // commit first, one mbarrier round trip on the MMA chain per block).
+#if SRK_ATTN_S_WAIT
           mbar_wait(&pv_done[st], ph);
+#endif
           issue_s();
         }
         ++g;
@@ -328,6 +399,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
       while (c.valid) {
         const int qb = c.li & 1;
         mbar_wait(&q_empty[qb], ((c.li >> 1) & 1) ^ 1);
+        SRK_ITEM(true, c.li, 3);
         mbar_arrive_expect_tx(&q_full[qb], C::TILE);
         for (int b = 0; b < C::NB; ++b)
           tma_load_2d(&tm_qkv, &q_full[qb], sQ + qb * C::TILE + b * kBox, c.h * HD + b * 64,
@@ -337,8 +409,8 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
       }
     }
     __syncwarp();
-  } else if (EW && warp < 4) {
-    regs_down();  // warp 3 of the TMA / MMA warpgroup: idle
+  } else if (EW && !kSplitKV && warp == 3) {
+    regs_down();  // idle
   } else if (EW && warp >= 12) {
     regs_down();
     // ------------------------------------------ epilogue warpgroup (EW)
@@ -353,10 +425,12 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
       const bool live = row < c.t.q_end;
       const uint32_t ph = (li >> 1) & 1;
       mbar_wait(&l_ready[ob], ph);
+      SRK_ITEM(quad == 0 && lane == 0, li, 0);
       float lsum = 0.f;
 #pragma unroll
       for (int k = 0; k < SL; ++k) lsum += lsum_slot[(ob * SL + k) * 128 + r];
       mbar_wait(&o_full[ob], ph);
+      SRK_ITEM(quad == 0 && lane == 0, li, 1);
       tc_fence_after();
       const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
       // O / l -> bf16, staged in the item's Q buffer (every S of the item has
@@ -402,6 +476,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
         bulk_commit();
         bulk_wait_read0();  // the Q buffer is reloaded for item li + 2
         mbar_arrive(&q_empty[ob]);
+        SRK_ITEM(quad == 0, li, 2);
       }
       // next item (the epilogue walks items, not blocks)
       c.j = c.nblk - 1;
@@ -526,6 +601,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
         const int kh = k0 + slice * KEYS;  // first key of this thread's slice
         mbar_wait(&s_full[sb], (g >> 1) & 1);
         if (warp == SM_BASE && lane == 0 && g < 24) SRK_TRACE(1 + g);
+        if (c.j == 0) SRK_ITEM(warp == SM_BASE && lane == 0, c.li, 5);
         tc_fence_after();
         float s[KEYS];
         {
@@ -539,6 +615,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
 #pragma unroll
           for (int i = 0; i < KEYS; ++i) s[i] = __uint_as_float(v[i]);
         }
+        SRK_PHASE(warp == SM_BASE && lane == 0, g, 0);
         // Visible iff in [kb, ke) and in ([pb, pe) U [ss, row]).
         const int a_lo = max(kb, sp.prefix_begin), a_hi = min(ke, sp.prefix_end);
         const int b_lo = max(kb, sp.span_start), b_hi = min(ke, row + 1);
@@ -547,14 +624,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
         float mx = -INFINITY;
         bool warp_empty = false;  // no visible key in this slice for any row of the warp
         if (__all_sync(0xffffffff, full)) {
-          // two independent FMNMX3 chains
-          float ma = -INFINITY, mb = -INFINITY;
-#pragma unroll
-          for (int i = 0; i < KEYS; i += 4) {
-            ma = fmax3f(ma, s[i], s[i + 1]);
-            mb = fmax3f(mb, s[i + 2], s[i + 3]);
-          }
-          mx = fmaxf(ma, mb);
+          mx = max_tree<KEYS>(s);
         } else {
           auto ivl = [&](int lo, int hi) -> uint64_t {
             lo = max(lo - kh, 0);
@@ -572,24 +642,20 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
               const bool ok = ((i < 32 ? v0 : v1) >> (i & 31)) & 1u;
               s[i] = ok ? s[i] : -INFINITY;
             }
-            float ma = -INFINITY, mb = -INFINITY;
-#pragma unroll
-            for (int i = 0; i < KEYS; i += 4) {
-              ma = fmax3f(ma, s[i], s[i + 1]);
-              mb = fmax3f(mb, s[i + 2], s[i + 3]);
-            }
-            mx = fmaxf(ma, mb);
+            mx = max_tree<KEYS>(s);
           }
         }
         // Pair max exchange (double-buffered by block parity). Only the two
         // warps sharing this row quadrant meet (named barrier 1 + quad, 64
         // threads), not all eight; the barrier also orders both halves' S
         // reads before either writes P over S (same TMEM lanes).
+        SRK_PHASE(warp == SM_BASE && lane == 0, g, 1);
         float* slot = red + (g & 1) * SL * 128;
         slot[slice * 128 + r] = mx;
         named_bar_sync(qbar, qbar_n);
 #pragma unroll
         for (int k = 0; k < SL; ++k) mx = fmaxf(mx, slot[k * 128 + r]);
+        SRK_PHASE(warp == SM_BASE && lane == 0, g, 2);
 
         const bool move =
             mx > m_used && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2);
@@ -612,6 +678,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
           }
         }
         m_used = m_new;
+        SRK_PHASE(warp == SM_BASE && lane == 0, g, 3);
         const float base = m_used == -INFINITY ? 0.f : m_used * scale_log2;
         float rs = 0.f;
         uint32_t pk[KEYS / 2];
@@ -627,10 +694,17 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
           uint64_t acc0 = f32x2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
           for (int i = 0; i < KEYS; i += 2) {
-            float a0, a1;
-            f32x2_split(fma_f32x2(f32x2(s[i], s[i + 1]), sc2, nb2), a0, a1);
-            const float p0 = ex2_approx(a0);
-            const float p1 = ex2_approx(a1);
+            const uint64_t a2 = fma_f32x2(f32x2(s[i], s[i + 1]), sc2, nb2);
+            float p0, p1;
+            if (kPolyEvery > 0 && (i >> 1) % kPolyEvery == kPolyEvery - 1) {
+              // this pair on the FMA pipe: MUFU is the softmax's binding unit
+              f32x2_split(ex2_poly_x2(a2), p0, p1);
+            } else {
+              float a0, a1;
+              f32x2_split(a2, a0, a1);
+              p0 = ex2_approx(a0);
+              p1 = ex2_approx(a1);
+            }
             if (i & 2) acc1 = add_f32x2(acc1, f32x2(p0, p1));
             else acc0 = add_f32x2(acc0, f32x2(p0, p1));
             pk[i >> 1] = pack_bf16x2(p0, p1);
@@ -641,6 +715,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
           rs = (r0 + r1) + (r2 + r3);
         }
         l += rs;
+        SRK_PHASE(warp == SM_BASE && lane == 0, g, 4);
         // P (bf16x2) over this slice's KEYS / 2 columns of the consumed S buffer
         // (columns of slices <= this one, already read: the quadrant barrier).
         if constexpr (KEYS == 64)
@@ -649,6 +724,9 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
           tmem_st_32x32b_x16(tmem + lane_off + sb * kBK + slice * (KEYS / 2),
                              *reinterpret_cast<uint32_t(*)[16]>(pk));
         tmem_st_wait();
+        SRK_PHASE(warp == SM_BASE && lane == 0, g, 5);
+        SRK_PHASE(warp > SM_BASE && warp < SM_BASE + 4 && lane == 0, g, 12 + (warp - SM_BASE));
+        SRK_PHASE(warp == SM_BASE + 4 && lane == 0, g, 9);
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
         if (warp == SM_BASE && lane == 0 && g < 24) SRK_TRACE(32 + g);
@@ -844,6 +922,8 @@ __global__ void __launch_bounds__(kPPThreads, 1)
   const int d = n_heads * HD;
   const int G = static_cast<int>(gridDim.x);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // read once: asm "memory" clobbers would otherwise reload it at every stamp
+  unsigned long long* const srk_trace = g_attn_trace;
   if (threadIdx.x == 0) SRK_TRACE(0);
 
   if (warp == 0 && lane == 0) {

@@ -438,6 +438,11 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t cta_mas
 }
 
 // ------------------------------------------------------------- misc utils
+__device__ __forceinline__ uint64_t f32x2(float lo, float hi);
+__device__ __forceinline__ void f32x2_split(uint64_t v, float& lo, float& hi);
+__device__ __forceinline__ uint64_t fma_f32x2(uint64_t a, uint64_t b, uint64_t c);
+__device__ __forceinline__ uint64_t add_f32x2(uint64_t a, uint64_t b);
+__device__ __forceinline__ uint64_t f32x2_neg(uint64_t a) { return a ^ 0x8000000080000000ull; }
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -466,6 +471,34 @@ __device__ __forceinline__ float ex2_poly(float x) {
   const int e = (__float_as_int(t) - 0x4B400000) << 23;
   const float r = __int_as_float(__float_as_int(p) + e);
   return xc <= -127.0f ? 0.0f : r;
+}
+
+// Two 2^x on the FMA/ALU pipes, packed fp32x2 (FFMA2 / FADD2 for the
+// reduction and the degree-4 polynomial), for the share of a softmax's
+// exponentials taken off MUFU (FlashAttention-4). Same scheme as ex2_poly;
+// inputs <= -126 give +0 (as ex2.approx.ftz of a masked -inf score).
+#ifndef SRK_EX2_C4
+#define SRK_EX2_C4 9.6181291076284772e-3f
+#endif
+__device__ __forceinline__ uint64_t ex2_poly_x2(uint64_t x2) {
+  float x0, x1;
+  f32x2_split(x2, x0, x1);
+  const float c0 = fmaxf(x0, -126.0f), c1 = fmaxf(x1, -126.0f);
+  const uint64_t xc = f32x2(c0, c1);
+  const uint64_t magic = f32x2(12582912.0f, 12582912.0f);
+  const uint64_t t = add_f32x2(xc, magic);
+  const uint64_t f = add_f32x2(xc, add_f32x2(magic, f32x2_neg(t)));
+  uint64_t p = fma_f32x2(f32x2(SRK_EX2_C4, SRK_EX2_C4), f,
+                         f32x2(5.5504108664821580e-2f, 5.5504108664821580e-2f));
+  p = fma_f32x2(p, f, f32x2(2.4022650695910071e-1f, 2.4022650695910071e-1f));
+  p = fma_f32x2(p, f, f32x2(6.9314718055994531e-1f, 6.9314718055994531e-1f));
+  p = fma_f32x2(p, f, f32x2(1.0f, 1.0f));
+  float t0, t1, p0, p1;
+  f32x2_split(t, t0, t1);
+  f32x2_split(p, p0, p1);
+  const float r0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23) - (0x4B400000 << 23));
+  const float r1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23) - (0x4B400000 << 23));
+  return f32x2(c0 <= -126.0f ? 0.0f : r0, c1 <= -126.0f ? 0.0f : r1);
 }
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n_threads) {
