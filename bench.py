@@ -43,12 +43,17 @@ WORKLOADS = {
     # name: (n_layers, d_model, n_heads, d_ff, t_q, t_i, n_items per GPU, soft_tokens)
     "c2": (20, 1024, 8, 1536, 256, 96, 256, False),
     "c3": (20, 1024, 8, 1536, 256, 8, 1024, True),
+    "c3_rows": (20, 1024, 8, 1536, 256, 8, 1024, True),
     "c1": (2, 64, 4, 256, 500, 50, 64, False),
     "c4": (28, 2048, 16, 6144, 256, 96, 250, False),
     # configs[4]: 8192 candidates in total, split across the ranks (strong scaling)
     "c5": (20, 1024, 8, 1536, 256, 96, 8192, False),
 }
 STRONG = {"c5"}  # n_items is the whole job's, not per GPU
+# configs[2] context compression: items arrive as compact d_emb embeddings and
+# are projected on the device into t_i soft-token rows (sr_engine_set_projection;
+# SURVEY H7, north_star (d)). "c3_rows" sends the d_model-wide rows instead.
+EMB = {"c3": 256}
 SERVE_WORKLOADS = {"c2", "c4"}  # token-item workloads served through sr_sched_*
 # queries packed into one device pass per step (per GPU)
 QUERIES = {"c4": 32}
@@ -57,7 +62,9 @@ WORKLOAD_DESC = {
           "candidates per step in one packed pass, 256-token prefixes, 96-token items",
     "c2": "0.6B-class pruned SLM (L20 d1024 H8 ff1536), 1 query x 256 candidates, "
           "256-token shared prefix, 96-token items",
-    "c3": "0.6B-class pruned SLM, 1 query x 1024 candidates, 256-token prefix, "
+    "c3": "0.6B-class pruned SLM, 1 query x 1024 candidates, 256-token prefix, items as "
+          "256-d embeddings projected on the device into 8 soft-token rows (context compression)",
+    "c3_rows": "0.6B-class pruned SLM, 1 query x 1024 candidates, 256-token prefix, "
           "8 soft-token rows per item (context compression)",
     "c1": "reference default toy ranker (L2 d64 H4 ff256), 1 query x 64 candidates, "
           "T_q 500, T_i 50 (cmd_bench shape)",
@@ -263,7 +270,7 @@ def cpu_reference_run(wl, n_items, weights_path, threads):
     return time.perf_counter() - t0, "port"
 
 
-SAMPLE_ITEMS = {"c1": 64, "c2": 8, "c3": 48, "c4": 3, "c5": 8}
+SAMPLE_ITEMS = {"c1": 64, "c2": 8, "c3": 48, "c3_rows": 48, "c4": 3, "c5": 8}
 
 
 def reference_query_time(wl, path, threads):
@@ -388,6 +395,16 @@ def run_ours(args):
         reqs = make_queries(sr, wl, nq, rank)
         req, ids = reqs[0], None
         plan = sr.BatchPlan(eng, reqs, k)
+    elif wl in EMB:
+        # compact embeddings in, projection to soft rows inside the device pass
+        req, ids = None, None
+        rng = np.random.default_rng(7)
+        prefix = rng.integers(0, 256, t_q).astype(np.int32)
+        emb = rng.standard_normal((n_loc, EMB[wl])).astype(np.float32)
+        proj = (np.random.default_rng(2027).standard_normal((EMB[wl], t_i * d))
+                * (0.08 / np.sqrt(EMB[wl]))).astype(np.float32)
+        eng.set_projection(proj, t_i)
+        plan = eng.plan_embeddings(prefix, emb, "project", k=k)
     else:
         req, ids = make_request(sr, wl, world, rank)
         if world > 1:
@@ -445,6 +462,8 @@ def run_ours(args):
     def e2e_call():
         if nq > 1:
             eng.score_batch(reqs, k)
+        elif wl in EMB:
+            eng.score_embeddings(prefix, emb, "project", k=k)
         elif comm is not None:
             eng.score_sharded(comm, req, k, ids)
         else:
@@ -544,6 +563,8 @@ def run_ours(args):
                 "path": ("ScoringEngine.score_batch -> sr_engine_score_batch" if nq > 1 else
                          "ScoringEngine.score_sharded -> sr_engine_score_sharded (NCCL merge)"
                          if comm is not None else
+                         "ScoringEngine.score_embeddings -> sr_engine_score_emb (projection on "
+                         "the device)" if wl in EMB else
                          "ScoringEngine.score -> sr_engine_score") + " (host arrays in/out)"},
         "gpu_launches": launches,
         "clocks": clk, "roofline": roofline, "cpu_baseline": cpu, "c5": c5,
@@ -819,7 +840,7 @@ def run_wire(args):
             "warmup": args.warmup, "ms_per_step": per_q * 1000, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic N(0, 0.08^2) rows, base64 float32 wire payloads",
-            "config": {"workload": WORKLOAD_DESC["c3"] + ", items as embedding_b64 in a JSON body",
+            "config": {"workload": WORKLOAD_DESC["c3_rows"] + ", items as embedding_b64 in a JSON body",
                        "body_bytes": len(body), "python_json_path_ms": py_ms},
             "e2e": {"value": n_loc / per_q, "unit": "pairs/s", "h2d_bytes_per_step": len(body),
                     "d2h_bytes_per_step": n_loc * 6 * 8,
