@@ -281,3 +281,17 @@ def test_pingpong_attention_variant_matches_torch(cuda):
                         os.path.abspath(__file__), "-k", "attention_segment_mask"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_two_tile_attention_variant_matches_torch(cuda):
+    """The opt-in two-tile ping-pong attention kernel (SRK_ATTN=fa,
+    kernels/attention_fa.cu, head 128) against the same fp32 references, in a
+    child process."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, SRK_ATTN="fa")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.abspath(__file__), "-k", "attention_segment_mask"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
