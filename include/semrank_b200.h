@@ -474,6 +474,15 @@ int32_t sr_kernel_gemm(const void* a_bf16, const void* b_bf16, int32_t M, int32_
 int32_t sr_kernel_gemm_ln(const void* a_bf16, const void* b_bf16, int32_t M, int32_t N, int32_t K,
                           void* c, int32_t ldc, int32_t epi, void* xb_bf16, void* stats,
                           int32_t n_parts, const float* colsum, int32_t ld, void* stream);
+/* Residual projection with the next LayerNorm overlapped:
+ * x fp32 [M x N] += A.B^T (GEMM epilogue 7 counts completed 128-row blocks)
+ * while a concurrent kernel writes out_bf16 [M x N] = bf16(LN(x) * gain)
+ * (kernels.cpp:31-45) block by block. counters: device uint32
+ * [ceil(M / 128)], zero on entry and on return. N % 256 == 0, N <= 2048.
+ * Device pointers; synchronous. */
+int32_t sr_kernel_gemm_resid_ln(const void* a_bf16, const void* b_bf16, int32_t M, int32_t N,
+                                int32_t K, float* x, const float* gain, void* out_bf16,
+                                uint32_t* counters, void* stream);
 /* Segment-masked attention. qkv [M x 3d] bf16, spans [M x 4] int32
  * {prefix_begin, prefix_end, span_start, 0}; out [M x d] bf16. Tiles are
  * planned internally. */

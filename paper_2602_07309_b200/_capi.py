@@ -156,6 +156,7 @@ _sig("sr_corpus_topk_sharded", i32, vp, vp, vp, i32, f64, vp, i32, vp, i32, P(i6
 _sig("sr_corpus_last_candidates", i64, vp)
 _sig("sr_corpus_last_scan_ms", f32, vp)
 _sig("sr_kernel_gemm", i32, vp, vp, i32, i32, i32, vp, i32, i32, vp)
+_sig("sr_kernel_gemm_resid_ln", i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp)
 _sig("sr_kernel_gemm_ln", i32, vp, vp, i32, i32, i32, vp, i32, i32, vp, vp, i32, vp, i32, vp)
 _sig("sr_kernel_attention", i32, vp, P(i32), i32, i32, i32, vp, vp)
 _sig("sr_kernel_layernorm", i32, vp, vp, vp, i32, i32, vp)
@@ -184,6 +185,6 @@ HEADER_SYMBOLS = [
     "sr_score_cache_capacity", "sr_score_cache_get", "sr_score_cache_put", "sr_canonical_query",
     "sr_query_signature", "sr_fnv1a64", "sr_engine_score_cached", "sr_corpus_create", "sr_corpus_destroy", "sr_corpus_topk",
     "sr_corpus_topk_sharded", "sr_corpus_last_candidates", "sr_corpus_last_scan_ms",
-    "sr_kernel_gemm", "sr_kernel_gemm_ln", "sr_kernel_attention", "sr_kernel_layernorm",
+    "sr_kernel_gemm", "sr_kernel_gemm_ln", "sr_kernel_gemm_resid_ln", "sr_kernel_attention", "sr_kernel_layernorm",
     "sr_kernel_topk", "sr_debug_attention_trace", "sr_debug_gemm_trace",
 ]

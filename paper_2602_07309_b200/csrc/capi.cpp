@@ -591,6 +591,10 @@ int32_t sr_engine_set_postprocess(sr_engine* e, const double* lo, const double* 
   return guard([&] {
     if (!e || (n_blocks > 0 && (!lo || !hi || !value)) || (n_blend > 0 && (!blend_task || !blend_w)))
       srh::fail(SR_SPEC_VIOLATION, "null argument");
+    // the blend weighs the calibrated relevance: an unfitted head throws
+    // StateInvalid in the reference (calibration.cpp:65-68)
+    if (n_blend > 0 && n_blocks <= 0)
+      srh::fail(SR_STATE_INVALID, "calibration head not fitted");
     std::lock_guard<std::mutex> lock(e->e->mutex());
     e->e->set_postprocess(lo, hi, value, n_blocks, blend_task, blend_w, n_blend);
   });
@@ -942,6 +946,38 @@ int32_t sr_kernel_gemm(const void* a_bf16, const void* b_bf16, int32_t M, int32_
     SR_CUDA_CHECK(srk::gemm_auto(ta, tb, M, N, K, c, ldc, epi, static_cast<cudaStream_t>(stream)));
     // NULL stream: synchronous (errors surface here); explicit stream: async.
     if (stream == nullptr) SR_CUDA_CHECK(cudaStreamSynchronize(nullptr));
+  });
+}
+
+int32_t sr_kernel_gemm_resid_ln(const void* a_bf16, const void* b_bf16, int32_t M, int32_t N,
+                                int32_t K, float* x, const float* gain, void* out_bf16,
+                                uint32_t* counters, void* stream) {
+  return guard([&] {
+    if (!srk::gemm_use_pair(N) || N > 2048) srh::fail(SR_SPEC_VIOLATION, "N must be a multiple of 256, <= 2048");
+    if (K % 8 != 0) srh::fail(SR_SPEC_VIOLATION, "K must be a multiple of 8");
+    if (!x || !gain || !out_bf16 || !counters) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    CUtensorMap ta, tb;
+    SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&ta, a_bf16, M, K, 128, 64));
+    SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tb, b_bf16, N, K, srk::gemm_b_box_rows(N), 64));
+    srk::LnFold f{};
+    f.ln_cnt = counters;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    SR_CUDA_CHECK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    SR_CUDA_CHECK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    SR_CUDA_CHECK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    SR_CUDA_CHECK(cudaEventRecord(fork, s));
+    SR_CUDA_CHECK(cudaStreamWaitEvent(s2, fork, 0));
+    SR_CUDA_CHECK(srk::gemm_auto(ta, tb, M, N, K, x, N, srk::EPI_RESID_F32_LN, s, &f));
+    SR_CUDA_CHECK(srk::layer_norm_after(x, gain, static_cast<__nv_bfloat16*>(out_bf16), M, N,
+                                        counters, N / 256, s2));
+    SR_CUDA_CHECK(cudaEventRecord(join, s2));
+    SR_CUDA_CHECK(cudaStreamWaitEvent(s, join, 0));
+    SR_CUDA_CHECK(cudaStreamSynchronize(s));
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    cudaStreamDestroy(s2);
   });
 }
 

@@ -61,6 +61,9 @@ Engine::Engine(const ModelWeights& w, int device) : cfg_(w.config), device_(devi
   if (hd != 16 && hd != 32 && hd != 64 && hd != 128)
     fail(SR_SPEC_VIOLATION, "head_dim must be one of 16/32/64/128");
   SR_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  SR_CUDA_CHECK(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+  SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   // Opt-in (SRK_FOLD_LN=1): LN folded into the projections when every GEMM
   // takes the pair kernel. Measured on B200 at C2 it breaks even with the
   // separate LayerNorm kernel (the residual epilogue's extra x traffic slows
@@ -72,6 +75,13 @@ Engine::Engine(const ModelWeights& w, int device) : cfg_(w.config), device_(devi
                srk::gemm_use_pair(F) && d % 128 == 0 && d / 128 <= 16;
     const char* sv = std::getenv("SRK_SERPENTINE");
     serpentine_ = sv == nullptr || std::atoi(sv) != 0;
+    // Opt-in (SRK_LN_AFTER=1): the next LayerNorm overlapped with each
+    // residual GEMM (epilogue 7 + layer_norm_after on a side stream). Measured
+    // slower at C2 (9.84 vs 8.97 ms per query): the GEMM is at the HBM ridge
+    // and the concurrent LayerNorm slows both.
+    const char* lv = std::getenv("SRK_LN_AFTER");
+    ln_after_ = !fold_ln_ && lv != nullptr && std::atoi(lv) != 0 && srk::gemm_use_pair(d) &&
+                d % 4 == 0 && d <= 2048;
   }
 
   tok_emb_ = upload(w.tok_emb, allocs_);
@@ -163,6 +173,9 @@ Engine::~Engine() {
   cudaSetDevice(device_);
   for (void* p : allocs_) cudaFree(p);
   if (stream_) cudaStreamDestroy(stream_);
+  if (side_) cudaStreamDestroy(side_);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
 }
 
 Plan::~Plan() {
@@ -218,6 +231,7 @@ void Engine::ensure_workspace(int32_t M) {
   h_.release();
   xb_.release();
   stats_.release();
+  ln_cnt_.release();
   SR_CUDA_CHECK(cudaMalloc(&x_.ptr, rows * d * sizeof(float)));
   x_.cap = rows * d;
   SR_CUDA_CHECK(cudaMalloc(&xn_.ptr, rows * d * sizeof(__nv_bfloat16)));
@@ -244,6 +258,12 @@ void Engine::ensure_workspace(int32_t M) {
     stats_.cap = ns;
     SR_CUDA_CHECK(cudaMemset(stats_.ptr, 0, ns * sizeof(float)));
     SR_CUDA_CHECK(srk::make_tmap_bf16_2d(&tm_xb_, xb_.ptr, rows, d, 128, 64));
+  }
+  if (ln_after_) {
+    const size_t nb = static_cast<size_t>(rows) / 128 + 4;
+    SR_CUDA_CHECK(cudaMalloc(&ln_cnt_.ptr, nb * sizeof(unsigned int)));
+    ln_cnt_.cap = nb;
+    SR_CUDA_CHECK(cudaMemset(ln_cnt_.ptr, 0, nb * sizeof(unsigned int)));
   }
   ws_rows_ = rows;
   ++ws_epoch_;
@@ -353,6 +373,21 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
       n += 5;
     }
   } else {
+    // Residual GEMM (epilogue 7 counts finished 128-row blocks of x) with the
+    // next LayerNorm in a concurrent kernel on the side stream that normalises
+    // each block as soon as it is complete (x still in L2); joined before the
+    // next projection reads xn.
+    auto resid_ln = [&](const CUtensorMap& tm_a, const CUtensorMap& tm_w, int K, float* x,
+                        const float* gain, int rows, bool rev) {
+      srk::LnFold f{};
+      f.ln_cnt = ln_cnt_.ptr;
+      SR_CUDA_CHECK(cudaEventRecord(ev_fork_, s));
+      SR_CUDA_CHECK(cudaStreamWaitEvent(side_, ev_fork_, 0));
+      SR_CUDA_CHECK(srk::gemm_auto(tm_a, tm_w, rows, d, K, x, d, srk::EPI_RESID_F32_LN, s, &f, rev));
+      SR_CUDA_CHECK(srk::layer_norm_after(x, gain, xn_.ptr, rows, d, ln_cnt_.ptr, d / 256, side_));
+      SR_CUDA_CHECK(cudaEventRecord(ev_join_, side_));
+      SR_CUDA_CHECK(cudaStreamWaitEvent(s, ev_join_, 0));
+    };
     B(PROF_EMBED_LN);
     SR_CUDA_CHECK(srk::embed_ln(p.src.ptr, p.pos.ptr, tok_emb_, p.pack.n_soft ? p.soft.ptr : nullptr,
                                 pos_emb_, layers_[0].ln1, x_.ptr, xn_.ptr, M, d, s));
@@ -368,24 +403,38 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
       attention();
       E();
       B(PROF_GEMM_O);
-      SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_o, M, d, d, x_.ptr, d, 2, s));
-      E();
-      B(PROF_LAYERNORM);
-      SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, L.ln2, xn_.ptr, M, d, s, serp));
-      E();
-      B(PROF_GEMM_IN);
-      SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_in, M, F, d, h_.ptr, F, 1, s));
-      E();
-      B(PROF_GEMM_OUT);
-      SR_CUDA_CHECK(srk::gemm_auto(tm_h_, L.tm_out, M, d, F, x_.ptr, d, 2, s, nullptr, serp));
-      E();
-      n += 6;
-      if (l + 1 < cfg_.n_layers) {
+      if (ln_after_) {  // x += attn . Wo, then LN2(x) -> xn by the last contributor
+        resid_ln(tm_xn_, L.tm_o, d, x_.ptr, L.ln2, M, false);
+        E();
+        ++n;
+      } else {
+        SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_o, M, d, d, x_.ptr, d, 2, s));
+        E();
         B(PROF_LAYERNORM);
-        SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, layers_[l + 1].ln1, xn_.ptr, M, d, s));
+        SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, L.ln2, xn_.ptr, M, d, s, serp));
         E();
         ++n;
       }
+      B(PROF_GEMM_IN);
+      SR_CUDA_CHECK(srk::gemm_auto(tm_xn_, L.tm_in, M, F, d, h_.ptr, F, 1, s));
+      E();
+      const bool next = l + 1 < cfg_.n_layers;
+      B(PROF_GEMM_OUT);
+      if (ln_after_ && next) {  // x += h . Wout, then LN1 of the next layer -> xn
+        resid_ln(tm_h_, L.tm_out, F, x_.ptr, layers_[l + 1].ln1, M, serp);
+        E();
+        ++n;
+      } else {
+        SR_CUDA_CHECK(srk::gemm_auto(tm_h_, L.tm_out, M, d, F, x_.ptr, d, 2, s, nullptr, serp));
+        E();
+        if (next) {
+          B(PROF_LAYERNORM);
+          SR_CUDA_CHECK(srk::layer_norm_bf16(x_.ptr, layers_[l + 1].ln1, xn_.ptr, M, d, s));
+          E();
+          ++n;
+        }
+      }
+      n += 5;
     }
   }
   B(PROF_SCORE_HEAD);

@@ -222,6 +222,11 @@ class Engine {
   int n_cols_ = 0, yes_col_ = 0, no_col_ = 0;
   bool fold_ln_ = false;
   bool serpentine_ = false;
+  // LayerNorm finished by the residual GEMMs' last contributor per 128-row
+  // block (EPI_RESID_F32_LN) instead of separate LayerNorm launches.
+  bool ln_after_ = false;
+  cudaStream_t side_ = nullptr;  // LN-after kernels (concurrent with the residual GEMM)
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   bool post_on_ = false;
   int post_nblocks_ = 0, post_nblend_ = 0;
   DevBuf<double> post_blocks_, post_w_;
@@ -266,6 +271,7 @@ class Engine {
   DevBuf<float> x_;
   DevBuf<__nv_bfloat16> xn_, qkv_, h_;
   DevBuf<__nv_bfloat16> xb_;   // folded LN: bf16 copy of the residual stream (GEMM A operand)
+  DevBuf<unsigned int> ln_cnt_;  // LN-after: add-reductions per 128-row block (mod d / 256)
   DevBuf<float> stats_;        // folded LN: [d/128][ws_rows_] (mean, M2) partials
   CUtensorMap tm_xn_, tm_h_, tm_qkv_, tm_xb_;
   uint64_t ws_epoch_ = 0;  // bumps when workspace moves (graphs must be re-captured)

@@ -164,6 +164,9 @@ cudaError_t gemm_bf16_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M
     if (e != cudaSuccess) return e;
     ln.stats_out = reinterpret_cast<float2*>(fold->stats_out);
     ln.ld = fold->ld;
+  } else if (epi == EPI_RESID_F32_LN) {
+    if (fold == nullptr || fold->ln_cnt == nullptr) return cudaErrorInvalidValue;
+    ln.ln_cnt = fold->ln_cnt;
   } else if (epi == EPI_LN_BF16 || epi == EPI_LN_GELU_BF16) {
     if (fold == nullptr || fold->stats_in == nullptr || fold->colsum == nullptr ||
         fold->n_parts < 1 || fold->n_parts > 16 || K % fold->n_parts != 0 || fold->ld < M)
@@ -182,6 +185,8 @@ cudaError_t gemm_bf16_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M
     case EPI_F32: return launch_pair_np<EPI_F32>(tmA, tmB, M, N, K, out, ldo, ln, rev ? 1 : 0, stream);
     case EPI_RESID_LN:
       return launch_pair_np<EPI_RESID_LN>(tmA, tmB, M, N, K, out, ldo, ln, rev ? 1 : 0, stream);
+    case EPI_RESID_F32_LN:
+      return launch_pair_np<EPI_RESID_F32_LN>(tmA, tmB, M, N, K, out, ldo, ln, rev ? 1 : 0, stream);
     case EPI_LN_BF16: return launch_pair_np<EPI_LN_BF16>(tmA, tmB, M, N, K, out, ldo, ln, rev ? 1 : 0, stream);
     case EPI_LN_GELU_BF16:
       return launch_pair_np<EPI_LN_GELU_BF16>(tmA, tmB, M, N, K, out, ldo, ln, rev ? 1 : 0, stream);

@@ -59,7 +59,8 @@ struct GemmCfg {
 // Output tensor map box for an epilogue: 32 rows x 128 B (32 fp32 or 64 bf16).
 template <int EPI>
 struct EpiOut {
-  static constexpr bool F32 = (EPI == EPI_RESID_F32 || EPI == EPI_F32 || EPI == EPI_RESID_LN);
+  static constexpr bool F32 =
+      (EPI == EPI_RESID_F32 || EPI == EPI_F32 || EPI == EPI_RESID_LN || EPI == EPI_RESID_F32_LN);
   static constexpr int CW = F32 ? 32 : 64;  // columns per staged chunk
 };
 
@@ -266,6 +267,7 @@ struct alignas(64) GemmLnArgs {
   float2* stats_out;        // EPI_RESID_LN: [N / 128][ld] (mean, M2) over 128 columns
   const float2* stats_in;   // EPI_LN_*: [n_parts][ld], each part over K / n_parts columns
   const float* colsum;      // EPI_LN_*: [N] column sums of the folded bf16 weights
+  unsigned int* ln_cnt;     // EPI_RESID_F32_LN: per 128-row block add-reductions done
   int n_parts;
   int ld;
 };
@@ -316,7 +318,7 @@ struct GemmPairCfg {
   // variant with 16x256b TMEM loads was measured slower: 8 rows x 32 B per
   // store instruction made the epilogue LSU-bound, 2-3x the staged time.)
   static constexpr bool RESID_LN = EPI == EPI_RESID_LN;
-  static constexpr bool RESID_F32 = EPI == EPI_RESID_F32;
+  static constexpr bool RESID_F32 = EPI == EPI_RESID_F32 || EPI == EPI_RESID_F32_LN;
   static constexpr int STAGES =
       RESID_LN ? SRK_RESID_LN_STAGES : (RESID_F32 ? SRK_RESID_STAGES : SRK_PAIR_STAGES);
   static constexpr int TMEM_COLS = 2 * BN;  // double-buffered 128 x 256 fp32
@@ -678,7 +680,7 @@ __global__ void __launch_bounds__(320, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              if constexpr (EPI == EPI_RESID_F32)  // x is re-read next by the LayerNorm
+              if constexpr (C::RESID_F32)  // x is re-read next by the LayerNorm
                 tma_reduce_add_2d_hint(&tmC, stg, n0 + c, r0, pol_keep);
               else
                 tma_store_2d(&tmC, stg, n0 + c, r0);
@@ -691,6 +693,26 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
       if (warp == 2 && lane == 0 && local < 38) gemm_trace(24 + local);
+      if constexpr (EPI == EPI_RESID_F32_LN) {
+        // Publish that this CTA's add-reductions into its 128-row block of x
+        // are complete (one counter per block, N / 256 contributions); the
+        // LayerNorm of the block runs in a concurrent kernel that waits for
+        // the count (rowops.cu layer_norm_after_kernel), so it reads x from
+        // L2 while the GEMM is still running. (Normalising the block in this
+        // epilogue was measured 4x slower: the last contributor's 8 warps
+        // took ~37 us per block and delayed their own tiles.) Opt-in: the
+        // overlapped LayerNorm is slower than the separate pass at C2.
+        if (lane == 0) {
+          bulk_wait0();
+          fence_proxy_async_global();
+        }
+        __syncwarp();
+        named_bar_sync(1, 32 * C::EPI_WARPS);
+        if (warp == 2 && lane == 0 && m0 < M) {  // blocks past M are never waited on
+          __threadfence();
+          atomicAdd(ln.ln_cnt + (m0 >> 7), 1u);
+        }
+      }
     }
     if (lane == 0) bulk_wait0();
   }

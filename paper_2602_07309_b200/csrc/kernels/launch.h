@@ -70,7 +70,7 @@ struct AttnTile {
 //                 projections (pair kernel only, see LnFold below)
 enum GemmEpilogue : int {
   EPI_BF16 = 0, EPI_GELU_BF16 = 1, EPI_RESID_F32 = 2, EPI_F32 = 3,
-  EPI_RESID_LN = 4, EPI_LN_BF16 = 5, EPI_LN_GELU_BF16 = 6
+  EPI_RESID_LN = 4, EPI_LN_BF16 = 5, EPI_LN_GELU_BF16 = 6, EPI_RESID_F32_LN = 7
 };
 int num_sms(int device);
 cudaError_t make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
@@ -85,7 +85,11 @@ cudaError_t gemm_bf16(const CUtensorMap& tmA, const CUtensorMap& tmB, int M, int
 // epi 5 / 6 (normalised projection [+ GELU]): A = xb, B = diag(gain) W (bf16),
 //   out = bf16([gelu](rstd * (acc - mean * colsum))), mean/rstd from
 //   stats_in[n_parts][ld] (each part over K / n_parts columns).
+// epi 7 (residual with completion counts): out = x fp32 += acc as epi 2, and
+//   ln_cnt[r / 128] += 1 once a CTA's add-reductions into 128-row block r are
+//   complete (N / 256 per block); layer_norm_after() waits on them.
 struct LnFold {
+  unsigned int* ln_cnt = nullptr;
   __nv_bfloat16* xb = nullptr;
   float* stats_out = nullptr;       // float2 pairs
   const float* stats_in = nullptr;  // float2 pairs
@@ -129,6 +133,12 @@ cudaError_t emb_pad_rows(const float* emb, int n, int d_emb, int d, float* out,
                          cudaStream_t stream);
 cudaError_t emb_to_bf16(const float* emb, int n, int d_emb, int kp, __nv_bfloat16* out,
                         cudaStream_t stream);
+// LayerNorm that runs concurrently with a residual GEMM (epi 7, another
+// stream): 128-row block b is normalised once cnt[b] == contrib, then cnt[b]
+// is reset to 0 for the next GEMM. Needs the GEMM co-resident (it is: this
+// kernel uses no shared memory and one 256-thread CTA per SM).
+cudaError_t layer_norm_after(const float* x, const float* gain, __nv_bfloat16* out, int M, int d,
+                             unsigned int* cnt, int contrib, cudaStream_t stream);
 // rev: rows walked from the last block to the first (L2 serpentine order).
 cudaError_t layer_norm_bf16(const float* x, const float* gain, __nv_bfloat16* out, int M, int d,
                             cudaStream_t stream, bool rev = false);

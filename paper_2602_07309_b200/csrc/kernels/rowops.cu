@@ -10,56 +10,12 @@
 #include <algorithm>
 
 #include "launch.h"
+#include "ln_row.cuh"
+#include "ptx.cuh"
 
 namespace srk {
 
 namespace {
-
-constexpr float kLnEps = 1e-5f;
-
-// Row held as float4 chunks: lane owns chunks lane, lane+32, ...
-template <int NV>
-__device__ __forceinline__ void ln_row_store(const float4 (&v)[NV], int d4, const float* gain,
-                                             __nv_bfloat16* out_row, int lane) {
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c = lane + i * 32;
-    if (c < d4) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
-  const float d = static_cast<float>(d4 * 4);
-  const float mean = s / d;
-  float q = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c = lane + i * 32;
-    if (c < d4) {
-      const float a = v[i].x - mean, b = v[i].y - mean, e = v[i].z - mean, f = v[i].w - mean;
-      q += (a * a + b * b) + (e * e + f * f);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffff, q, o);
-  const float inv = 1.0f / sqrtf(q / d + kLnEps);
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c = lane + i * 32;
-    if (c < d4) {
-      const float4 gg = reinterpret_cast<const float4*>(gain)[c];
-      uint2 packed;
-      packed.x = __float_as_uint(0.f);
-      __nv_bfloat162 lo = __floats2bfloat162_rn((v[i].x - mean) * inv * gg.x,
-                                                (v[i].y - mean) * inv * gg.y);
-      __nv_bfloat162 hi = __floats2bfloat162_rn((v[i].z - mean) * inv * gg.z,
-                                                (v[i].w - mean) * inv * gg.w);
-      packed.x = *reinterpret_cast<uint32_t*>(&lo);
-      packed.y = *reinterpret_cast<uint32_t*>(&hi);
-      reinterpret_cast<uint2*>(out_row)[c] = packed;
-    }
-  }
-}
 
 template <int NV>
 __global__ void __launch_bounds__(256)
@@ -196,6 +152,61 @@ __global__ void __launch_bounds__(SRK_LN_ROWS * 32)
   pdl_trigger();
 }
 
+// Polls the residual GEMM's per-block completion counts (epi 7) and
+// normalises each 128-row block as soon as its add-reductions are complete,
+// reading x while it is still in L2. Blocks are visited in the GEMM's tile
+// order (increasing), one CTA per SM, 8 warps x 16 rows per block.
+template <int NV>
+__global__ void __launch_bounds__(256)
+    layer_norm_after_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                            __nv_bfloat16* __restrict__ out, int M, int d,
+                            unsigned int* __restrict__ cnt, unsigned int contrib) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nblk = (M + 127) / 128;
+  const int d4 = d >> 2;
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+    if (threadIdx.x == 0) {
+      unsigned int v;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt + b) : "memory");
+        if (v >= contrib) break;
+        __nanosleep(256);
+      }
+    }
+    __syncthreads();
+    const int r0 = b * 128 + warp * 16;
+#pragma unroll 1
+    for (int rr = 0; rr < 16; rr += 2) {
+      float4 v0[NV], v1[NV];
+      const int ra = r0 + rr, rb = ra + 1;
+      const float4* xa = reinterpret_cast<const float4*>(x + static_cast<size_t>(ra) * d);
+      const float4* xb = reinterpret_cast<const float4*>(x + static_cast<size_t>(rb) * d);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int c = lane + 32 * i;
+        if (ra < M && c < d4) v0[i] = ld_cg_f4(xa + c);
+        if (rb < M && c < d4) v1[i] = ld_cg_f4(xb + c);
+      }
+      if (ra < M) ln_row_store<NV>(v0, d4, gain, out + static_cast<size_t>(ra) * d, lane);
+      if (rb < M) ln_row_store<NV>(v1, d4, gain, out + static_cast<size_t>(rb) * d, lane);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) cnt[b] = 0u;  // ready for the next residual GEMM (stream-ordered)
+  }
+}
+
+template <int NV>
+cudaError_t launch_ln_after(const float* x, const float* gain, __nv_bfloat16* out, int M, int d,
+                            unsigned int* cnt, int contrib, cudaStream_t stream) {
+  // one CTA per block (several per SM next to the GEMM's CTA: more rows in
+  // flight per SM than one persistent CTA could keep)
+  const int nblk = (M + 127) / 128;
+  const int grid = nblk;
+  layer_norm_after_kernel<NV><<<grid, 256, 0, stream>>>(x, gain, out, M, d, cnt,
+                                                        static_cast<unsigned int>(contrib));
+  return cudaGetLastError();
+}
+
 template <int NV>
 cudaError_t launch_embed(const int32_t* src, const int32_t* pos, const float* tok_emb,
                          const float* soft_rows, const float* pos_emb, const float* gain, float* x,
@@ -257,6 +268,13 @@ cudaError_t layer_norm_bf16(const float* x, const float* gain, __nv_bfloat16* ou
   if (M <= 0) return cudaSuccess;
   if (d % 4 != 0) return cudaErrorInvalidValue;
   SRK_DISPATCH_NV(d, launch_ln, x, gain, out, M, d, stream, rev ? 1 : 0);
+}
+
+cudaError_t layer_norm_after(const float* x, const float* gain, __nv_bfloat16* out, int M, int d,
+                             unsigned int* cnt, int contrib, cudaStream_t stream) {
+  if (M <= 0) return cudaSuccess;
+  if (d % 4 != 0 || cnt == nullptr || contrib <= 0) return cudaErrorInvalidValue;
+  SRK_DISPATCH_NV(d, launch_ln_after, x, gain, out, M, d, cnt, contrib, stream);
 }
 
 cudaError_t transpose_to_bf16(const float* src, __nv_bfloat16* dst, int K, int N,

@@ -790,6 +790,8 @@ class ScoringEngine:
         the optional ``score_blend`` (task -> weight, summed in task-name order
         like the reference's std::map); the top-k then ranks by the final score."""
         blocks = calibration.blocks if calibration is not None else []
+        if score_blend and not blocks:  # calibration.cpp:65-68: calibrate() on an unfitted head
+            raise SemrankError(ErrorCode.StateInvalid, "calibration head not fitted")
         lo = np.array([b.lo for b in blocks] or [0.0], np.float64)
         hi = np.array([b.hi for b in blocks] or [0.0], np.float64)
         val = np.array([b.value for b in blocks] or [0.0], np.float64)

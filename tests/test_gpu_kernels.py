@@ -295,3 +295,45 @@ def test_two_tile_attention_variant_matches_torch(cuda):
                         os.path.abspath(__file__), "-k", "attention_segment_mask"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 1024, 1024), (4096, 1024, 1536), (257, 2048, 512)])
+def test_residual_gemm_with_overlapped_layernorm(cuda, M, N, K):
+    """Opt-in LN-after path (SRK_LN_AFTER=1): epilogue 7 adds into x and counts
+    finished 128-row blocks, a concurrent kernel normalises each block
+    (kernels.cpp:31-45). x must equal the plain residual epilogue bit for bit,
+    the LN output a torch fp32 LayerNorm of that x within bf16 rounding, and
+    the counters must be back to zero."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(M + N + K)
+    a = (torch.randn(M, K, generator=g) / K ** 0.5).bfloat16().to(cuda)
+    b = torch.randn(N, K, generator=g).bfloat16().to(cuda)
+    x0 = torch.randn(M, N, generator=g).to(cuda)
+    gain = (torch.rand(N, generator=g) + 0.5).to(cuda)
+    x_ref = x0.clone()
+    _ok(_lib().sr_kernel_gemm(_vp(a), _vp(b), M, N, K, _vp(x_ref), N, 2, None))
+    x = x0.clone()
+    out = torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
+    cnt = torch.zeros((M + 127) // 128 + 1, dtype=torch.int32, device=cuda)
+    for _ in range(2):  # counters are reusable
+        x.copy_(x0)
+        _ok(_lib().sr_kernel_gemm_resid_ln(_vp(a), _vp(b), M, N, K, _vp(x), _vp(gain), _vp(out),
+                                           _vp(cnt), None))
+        assert torch.equal(x, x_ref)
+        ref = torch.nn.functional.layer_norm(x_ref, (N,), eps=1e-5) * gain
+        assert (out.float() - ref).abs().max().item() <= 2e-2 * max(1.0, ref.abs().max().item())
+        assert int(cnt.abs().sum().item()) == 0
+
+
+def test_engine_ln_after_variant_matches_oracle(cuda):
+    """The engine with SRK_LN_AFTER=1 (read once per process) through the
+    headline parity suite, in a child process."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, SRK_LN_AFTER="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_headline.py"), "-k", "c2 or batch or c4"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

@@ -62,5 +62,20 @@ def test_calibrated_blend_ranking_matches_oracle(cuda, blend):
 def test_unknown_blend_task_is_an_alignment_error(cuda):
     eng = sr.ScoringEngine(sr.init_model(sr.ModelConfig.default_toy(), 1), device=0)
     with pytest.raises(sr.SemrankError) as e:
-        eng.set_postprocess(None, {"relevance": 1.0, "nope": 0.5})
+        eng.set_postprocess(head(), {"relevance": 1.0, "nope": 0.5})
     assert e.value.code == sr.ErrorCode.Alignment
+
+
+def test_blend_without_fitted_head_is_state_invalid(cuda):
+    # calibration.cpp:65-68: calibrate() on an unfitted head throws StateInvalid;
+    # the C-ABI refuses the same configuration
+    eng = sr.ScoringEngine(sr.init_model(sr.ModelConfig.default_toy(), 1), device=0)
+    with pytest.raises(sr.SemrankError) as e:
+        eng.set_postprocess(None, {"relevance": 1.0})
+    assert e.value.code == sr.ErrorCode.StateInvalid
+    import ctypes as C
+    from paper_2602_07309_b200._capi import lib
+    t = (C.c_int32 * 1)(0)
+    w = (C.c_double * 1)(1.0)
+    z = (C.c_double * 1)(0.0)
+    assert lib.sr_engine_set_postprocess(eng._h, z, z, z, 0, t, w, 1) == int(sr.ErrorCode.StateInvalid)
