@@ -571,6 +571,18 @@ def run_ours(args):
         "serving": serving,
         "topk_head": [(iid, round(s, 6)) for iid, s in result.topk[:3]],
     }
+    ok = [p for p in sweep if p["meets_500ms"]]
+    if ok:
+        # batched workloads (configs[3]): the metric is pairs/s at a fixed p99
+        # query latency, so the headline is the fastest pass size whose pass
+        # time (every query's latency) is within 500 ms; the full-batch pass
+        # stays under device_pass
+        best = max(ok, key=lambda p: p["pairs_per_s"])
+        line["value_basis"] = (f"best pass size meeting the 500 ms query latency: "
+                               f"{best['queries_per_pass']} queries/pass at {best['latency_ms']} ms; "
+                               f"full {nq}-query pass {total_ms / args.steps:.1f} ms")
+        line["value"] = best["pairs_per_s"]
+        line["ms_per_step"] = best["latency_ms"]
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
