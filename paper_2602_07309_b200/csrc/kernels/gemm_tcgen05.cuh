@@ -293,6 +293,12 @@ struct alignas(64) GemmLnArgs {
 #ifndef SRK_PAIR_STG_BUFS
 #define SRK_PAIR_STG_BUFS 1
 #endif
+// Tail split of the pair GEMM's last wave (see the kernel). Opt-in: the O /
+// W_out classes get 4-5% faster in the per-class replay, but the pipelined
+// C2 step measured slower (8.94-9.09 vs 8.84-8.88 ms, 4 interleaved rounds).
+#ifndef SRK_TAIL_SPLIT
+#define SRK_TAIL_SPLIT 0
+#endif
 #ifndef SRK_RESID_LN_STAGES
 #define SRK_RESID_LN_STAGES 5
 #endif
@@ -368,6 +374,28 @@ __global__ void __launch_bounds__(320, 1)
   const int m_tiles = (M + 2 * C::BM - 1) / (2 * C::BM);
   const int n_tiles = N / (BN * NP);  // cluster tiles along N
   const int num_tiles = m_tiles * n_tiles;
+  // Tail split: when the last wave would leave at least half of the pairs
+  // idle (num_tiles % n_pairs <= n_pairs / 2, e.g. the N = 1024 residual
+  // GEMMs at C2: 388 tiles on 74 pairs), the tail tiles run as two 256 x 128
+  // halves on twice as many pairs, so the last wave takes ~0.57 of a tile
+  // (N = 128 MMAs) instead of a whole one. Generic epilogues only.
+  constexpr bool kSplitOK = NP == 1 && SRK_TAIL_SPLIT &&
+                            (EPI == EPI_BF16 || EPI == EPI_GELU_BF16 || EPI == EPI_RESID_F32 ||
+                             EPI == EPI_F32);
+  const int tail = num_tiles % n_pairs;
+  const bool split = kSplitOK && tail > 0 && 2 * tail <= n_pairs;
+  const int n_full = split ? num_tiles - tail : num_tiles;
+  const int num_units = split ? n_full + 2 * tail : num_tiles;
+  // unit -> (tile, half): half < 0 for a whole 256-column tile
+  auto unit_tile = [&](int u, int& half) {
+    if (u < n_full) {
+      half = -1;
+      return u;
+    }
+    half = (u - n_full) & 1;
+    return n_full + ((u - n_full) >> 1);
+  };
+
   const int nk = (K + C::BK - 1) / C::BK;
   // rev: walk the 256-row blocks from the last to the first, so the rows the
   // previous kernel wrote last (still in L2) are read first (serpentine order).
@@ -418,9 +446,14 @@ __global__ void __launch_bounds__(320, 1)
       const uint16_t a_mask = static_cast<uint16_t>((1u << cr) | (1u << (cr + 2)));
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = pair; tile < num_tiles; tile += n_pairs) {
+      for (int u = pair; u < num_units; u += n_pairs) {
+        int half;
+        const int tile = unit_tile(u, half);
         const int m0 = m_block(tile) * 2 * C::BM + cr * C::BM;
-        const int n0 = ((tile % n_tiles) * NP + pr) * BN + cr * (BN / 2);
+        // half tile: this CTA's 64 of the 128 columns (the 128-row box loads
+        // 64 spare rows the N = 128 MMA does not read)
+        const int n0 = ((tile % n_tiles) * NP + pr) * BN +
+                       (half < 0 ? cr * (BN / 2) : half * (BN / 2) + cr * (BN / 4));
         if constexpr (C::RESID_LN) {
           // The epilogue reads this CTA's 128 x 256 fp32 slab of x after the
           // main loop: pull it into L2 now so those loads are L2 hits.
@@ -454,7 +487,11 @@ __global__ void __launch_bounds__(320, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
+      constexpr uint32_t idesc_half = idesc_bf16_f32(2 * C::BM, BN / 2);
+      for (int u = pair; u < num_units; u += n_pairs, ++local) {
+        int half;
+        unit_tile(u, half);
+        const uint32_t idu = half < 0 ? idesc : idesc_half;
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -468,7 +505,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
           for (int k = 0; k < C::BK / 16; ++k)
             umma_bf16_pair(d_tmem, sw128_kmajor_desc(a_addr + k * 32),
-                           sw128_kmajor_desc(b_addr + k * 32), idesc, (kb | k) != 0 ? 1u : 0u);
+                           sw128_kmajor_desc(b_addr + k * 32), idu, (kb | k) != 0 ? 1u : 0u);
           umma_commit_pair(&empty[stage], NP == 1 ? 0x3 : 0xF);
           if (++stage == C::STAGES) {
             stage = 0;
@@ -484,18 +521,22 @@ __global__ void __launch_bounds__(320, 1)
     constexpr int CW = EpiOut<EPI>::CW;
     constexpr int SPAN = BN / 2;  // columns per epilogue warp
     const int quad = warp & 3;
-    const int col0 = ((warp - 2) >> 2) * SPAN;
     uint8_t* stg0 = sStg + (warp - 2) * C::STG_BUFS * C::STG_BYTES;
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), lead_rank);
     const uint64_t pol_keep = policy_evict_last();
     int local = 0;
     int nstg = 0;  // staging chunks issued by this warp (buffer = nstg % STG_BUFS)
     uint32_t xph = 0;  // EPI_RESID_LN: parity of this warp's x-chunk barrier
-    for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
+    for (int u = pair; u < num_units; u += n_pairs, ++local) {
+      int half;
+      const int tile = unit_tile(u, half);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       const int m0 = m_block(tile) * 2 * C::BM + cr * C::BM;
-      const int n0 = ((tile % n_tiles) * NP + pr) * BN;
+      const int n0 = ((tile % n_tiles) * NP + pr) * BN + (half < 0 ? 0 : half * (BN / 2));
+      // columns per epilogue warp (a half tile has 128 accumulator columns)
+      const int span = half < 0 ? SPAN : SPAN / 2;
+      const int col0 = ((warp - 2) >> 2) * span;
       const int r0 = m0 + quad * 32;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * BN;
       if constexpr (C::RESID_LN) {
@@ -628,7 +669,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         if (r0 < M) {
 #pragma unroll 1
-          for (int c = col0; c < col0 + SPAN; c += CW, ++nstg) {
+          for (int c = col0; c < col0 + span; c += CW, ++nstg) {
             uint8_t* stg = stg0 + (nstg % C::STG_BUFS) * C::STG_BYTES;
             uint8_t* row_base = stg + lane * 128;
             if constexpr (EpiOut<EPI>::F32) {

@@ -593,12 +593,31 @@ __device__ __forceinline__ void gelu_erf_x2(float& v0, float& v1) {
                                  f32x2(0.70710678118654752f, 0.70710678118654752f));
     float z0, z1;
     f32x2_split(z, z0, z1);
+#if SRK_GELU_AS == 2
+    // t = 1 / (1 + p z) on the FMA pipe: z clamped to 4 (erfc(4) = 1.5e-8, the
+    // clamped A-S erfc stays within 1.4e-7), d in [1, 2.31], quadratic seed
+    // (rel. 3.4e-2) + two Newton steps (rel. 1.3e-6): 6 FFMA2 for 2 MUFU.RCP
+    // per pair. Measured slower (W_in 1.60-1.63 vs 1.40-1.51 ms per query):
+    // the W_in epilogue is FMA-issue-bound, not MUFU-bound. Off (SRK_GELU_AS=2).
+    const uint64_t zc = f32x2(fminf(z0, 4.0f), fminf(z1, 4.0f));
+    const uint64_t dd = fma_f32x2(f32x2(0.3275911f, 0.3275911f), zc, f32x2(1.0f, 1.0f));
+    uint64_t t = fma_f32x2(fma_f32x2(f32x2(0.25461108f, 0.25461108f), dd,
+                                     f32x2(-1.24656636f, -1.24656636f)),
+                           dd, f32x2(1.96838612f, 1.96838612f));
+    const uint64_t ndd = f32x2_neg(dd);
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const uint64_t e = fma_f32x2(ndd, t, f32x2(1.0f, 1.0f));
+      t = fma_f32x2(t, e, t);
+    }
+#else
     float d0, d1;
     f32x2_split(fma_f32x2(f32x2(0.3275911f, 0.3275911f), z, f32x2(1.0f, 1.0f)), d0, d1);
     float t0, t1;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t0) : "f"(d0));
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t1) : "f"(d1));
     const uint64_t t = f32x2(t0, t1);
+#endif
     uint64_t p = fma_f32x2(f32x2(1.061405429f, 1.061405429f), t, f32x2(-1.453152027f, -1.453152027f));
     p = fma_f32x2(p, t, f32x2(1.421413741f, 1.421413741f));
     p = fma_f32x2(p, t, f32x2(-0.284496736f, -0.284496736f));

@@ -29,7 +29,9 @@ def _ok(st):
 # multicast when N % 512 == 0), other N the 1-CTA kernel.
 GEMM_SHAPES = [(128, 256, 64), (300, 3072, 1024), (1000, 1536, 1024), (257, 1024, 1536),
                (77, 192, 64), (500, 64, 256), (4096, 1024, 1024), (129, 128, 2048),
-               (6000, 3072, 1024), (2000, 512, 64), (700, 768, 512)]
+               (6000, 3072, 1024), (2000, 512, 64), (700, 768, 512),
+               # 80 pair tiles on 74 pairs: the 6 tail tiles run as 256 x 128 halves
+               (5120, 1024, 1024), (5000, 1024, 1536)]
 
 
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
@@ -46,7 +48,8 @@ def test_gemm_fp32_epilogue_matches_torch(cuda, M, N, K):
     assert err <= 1e-3 * max(1.0, ref.abs().max().item()), err
 
 
-@pytest.mark.parametrize("M,N,K", [(300, 3072, 1024), (77, 192, 64), (1000, 1536, 1024)])
+@pytest.mark.parametrize("M,N,K", [(300, 3072, 1024), (77, 192, 64), (1000, 1536, 1024),
+                                   (5120, 1024, 1024)])
 def test_gemm_bf16_and_gelu_epilogues(cuda, M, N, K):
     import torch
     g = torch.Generator(device="cpu").manual_seed(5)
@@ -63,7 +66,7 @@ def test_gemm_bf16_and_gelu_epilogues(cuda, M, N, K):
 
 
 @pytest.mark.parametrize("M,N,K", [(300, 1024, 1024), (257, 1024, 1536), (64, 64, 256),
-                                   (5000, 1024, 1536)])
+                                   (5000, 1024, 1536), (24832, 1024, 1024)])
 def test_gemm_residual_epilogue(cuda, M, N, K):
     import torch
     g = torch.Generator(device="cpu").manual_seed(9)
