@@ -1311,16 +1311,23 @@ bool attn_use_pp() {
 }  // namespace
 
 cudaError_t attention_fa_set_trace(unsigned long long* dev_buf);
+cudaError_t attention_eo_set_trace(unsigned long long* dev_buf);
 cudaError_t attention_set_trace(unsigned long long* dev_buf) {
   cudaError_t e = attention_fa_set_trace(dev_buf);
+  if (e != cudaSuccess) return e;
+  e = attention_eo_set_trace(dev_buf);
   if (e != cudaSuccess) return e;
   return cudaMemcpyToSymbol(g_attn_trace, &dev_buf, sizeof(dev_buf));
 }
 
 int attention_tile_rows(int head_dim) { return head_dim >= 64 ? kTM : 64; }
 
-// attention_fa.cu: two query tiles per CTA (head 128, the default).
+// attention_fa.cu: two query tiles per CTA (head 128, opt-in SRK_ATTN=fa).
 bool attn_use_fa();
+// attention_eo.cu: softmax warps own alternate key blocks (head 128, SRK_ATTN=eo).
+bool attn_use_eo();
+cudaError_t attention_eo(const CUtensorMap& tm_qkv, const RowSpan* spans, const AttnTile* tiles,
+                         int n_tiles, __nv_bfloat16* out, int n_heads, cudaStream_t stream);
 cudaError_t attention_fa(const CUtensorMap& tm_qkv, const RowSpan* spans, const AttnTile* tiles,
                          int n_tiles, __nv_bfloat16* out, int n_heads, cudaStream_t stream);
 
@@ -1330,6 +1337,8 @@ cudaError_t attention_tc(const CUtensorMap& tm_qkv, const void* qkv, const RowSp
   if (n_tiles <= 0) return cudaSuccess;
   if (head_dim == 128 && attn_use_fa())
     return attention_fa(tm_qkv, spans, tiles, n_tiles, out, n_heads, stream);
+  if (head_dim == 128 && attn_use_eo())
+    return attention_eo(tm_qkv, spans, tiles, n_tiles, out, n_heads, stream);
   // SRK_ATTN=pp selects the two-slot ping-pong kernel (A/B runs).
   const bool pp = attn_use_pp();
   switch (head_dim) {

@@ -340,3 +340,17 @@ def test_engine_ln_after_variant_matches_oracle(cuda):
                         os.path.join(here, "test_gpu_headline.py"), "-k", "c2 or batch or c4"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_block_parity_attention_variant_matches_torch(cuda):
+    """The opt-in attention kernel whose softmax warps own alternate key
+    blocks (SRK_ATTN=eo, kernels/attention_eo.cu, head 128) against the same
+    fp32 references, in a child process."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, SRK_ATTN="eo")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.abspath(__file__), "-k", "attention_segment_mask"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
