@@ -372,11 +372,20 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SR_BENCH_COMM=host (test aid): ranks exchange their top-k through the
+    # product's host-transport communicator over gloo, so the N > 1 path can be
+    # exercised with several ranks on one GPU (NCCL refuses that).
+    host_comm = os.environ.get("SR_BENCH_COMM") == "host"
+    if host_comm:
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if host_comm:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2602_07309_b200 as sr
 
     wl = args.workload
@@ -407,7 +416,13 @@ def run_ours(args):
         plan = eng.plan_embeddings(prefix, emb, "project", k=k)
     else:
         req, ids = make_request(sr, wl, world, rank)
-        if world > 1:
+        if world > 1 and host_comm:
+            def allgather(b):
+                out = [None] * world
+                dist.all_gather_object(out, b)
+                return out
+            comm = sr.Comm.host(world, rank, local, allgather)
+        elif world > 1:
             uid = sr.Comm.unique_id() if rank == 0 else bytes(128)
             obj = [uid]
             dist.broadcast_object_list(obj, src=0)
@@ -561,7 +576,7 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "path": ("ScoringEngine.score_batch -> sr_engine_score_batch" if nq > 1 else
-                         "ScoringEngine.score_sharded -> sr_engine_score_sharded (NCCL merge)"
+                         ("ScoringEngine.score_sharded -> sr_engine_score_sharded (" + ("host-transport" if host_comm else "NCCL") + " merge)")
                          if comm is not None else
                          "ScoringEngine.score_embeddings -> sr_engine_score_emb (projection on "
                          "the device)" if wl in EMB else
