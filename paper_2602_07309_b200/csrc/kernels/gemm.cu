@@ -157,6 +157,8 @@ cudaError_t gemm_bf16_pair(const CUtensorMap& tmA, const CUtensorMap& tmB, int M
   if (N % GemmPairCfg<EPI_BF16>::BN != 0 || K % 8 != 0) return cudaErrorInvalidValue;
   GemmLnArgs ln;
   std::memset(&ln, 0, sizeof(ln));
+  ln.resid_out = static_cast<float*>(out);
+  ln.resid_ld = ldo;
   if (epi == EPI_RESID_LN) {
     if (fold == nullptr || fold->xb == nullptr || fold->stats_out == nullptr || fold->ld < M)
       return cudaErrorInvalidValue;

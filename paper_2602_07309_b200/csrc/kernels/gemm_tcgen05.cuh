@@ -268,6 +268,8 @@ struct alignas(64) GemmLnArgs {
   const float2* stats_in;   // EPI_LN_*: [n_parts][ld], each part over K / n_parts columns
   const float* colsum;      // EPI_LN_*: [N] column sums of the folded bf16 weights
   unsigned int* ln_cnt;     // EPI_RESID_F32_LN: per 128-row block add-reductions done
+  float* resid_out;         // EPI_RESID_F32 (SRK_RESID_RED): x [M x ld] for red.global.add
+  int resid_ld;
   int n_parts;
   int ld;
 };
@@ -296,6 +298,16 @@ struct alignas(64) GemmLnArgs {
 // Tail split of the pair GEMM's last wave (see the kernel). Opt-in: the O /
 // W_out classes get 4-5% faster in the per-class replay, but the pipelined
 // C2 step measured slower (8.94-9.09 vs 8.84-8.88 ms, 4 interleaved rounds).
+// Residual epilogue by vector reductions from registers (REDG.ADD.F32x4)
+// instead of smem staging + TMA add-reduce. Motivation (tools/gemm_trace.py,
+// C2): the staged reduction's shared-memory traffic stretches the O GEMM's
+// main loop from 6.1 (bf16-epilogue GEMMs of the same K) to 8.5 us per tile.
+// Measured: the register path needs 11.7 us per tile of epilogue (32 rows x
+// 16 B per warp reduction: LSU / L2-request bound) and O / W_out get slower
+// (1.84 / 2.02 vs 1.32 / 1.71 ms per query). Off.
+#ifndef SRK_RESID_RED
+#define SRK_RESID_RED 0
+#endif
 #ifndef SRK_TAIL_SPLIT
 #define SRK_TAIL_SPLIT 0
 #endif
@@ -672,6 +684,25 @@ __global__ void __launch_bounds__(320, 1)
           for (int c = col0; c < col0 + span; c += CW, ++nstg) {
             uint8_t* stg = stg0 + (nstg % C::STG_BUFS) * C::STG_BYTES;
             uint8_t* row_base = stg + lane * 128;
+            if constexpr (C::RESID_F32 && SRK_RESID_RED) {
+              // x += acc straight from registers with vector reductions
+              // (REDG.ADD.F32x4): no shared-memory staging, whose traffic
+              // otherwise slows the operand-bound main loop of this GEMM.
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(t_row + c, r);
+              tmem_ld_wait();
+              const int row = r0 + lane;
+              if (row < M) {
+                float* dst = ln.resid_out + static_cast<size_t>(row) * ln.resid_ld + n0 + c;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * q),
+                               "f"(__uint_as_float(r[4 * q])), "f"(__uint_as_float(r[4 * q + 1])),
+                               "f"(__uint_as_float(r[4 * q + 2])), "f"(__uint_as_float(r[4 * q + 3]))
+                               : "memory");
+              }
+              continue;
+            }
             if constexpr (EpiOut<EPI>::F32) {
               uint32_t r[32];
               tmem_ld_32x32b_x32(t_row + c, r);
