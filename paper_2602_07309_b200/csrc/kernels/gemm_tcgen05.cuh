@@ -302,9 +302,11 @@ struct alignas(64) GemmLnArgs {
 // instead of smem staging + TMA add-reduce. Motivation (tools/gemm_trace.py,
 // C2): the staged reduction's shared-memory traffic stretches the O GEMM's
 // main loop from 6.1 (bf16-epilogue GEMMs of the same K) to 8.5 us per tile.
-// Measured: the register path needs 11.7 us per tile of epilogue (32 rows x
-// 16 B per warp reduction: LSU / L2-request bound) and O / W_out get slower
-// (1.84 / 2.02 vs 1.32 / 1.71 ms per query). Off.
+// Measured: the register path needs 11.7 us per tile of epilogue (=1: 32x32b
+// loads, 32 rows x 16 B per warp reduction) or 8.3 us (=2: 16x256b loads, 8
+// rows x one full 32 B sector per warp reduction) against 3.65 us staged, so
+// the GEMM turns epilogue-bound: O / W_out 1.84 / 2.02 (=1), 1.49 / 1.78 (=2)
+// vs 1.30 / 1.68 ms per query. Off.
 #ifndef SRK_RESID_RED
 #define SRK_RESID_RED 0
 #endif
@@ -684,7 +686,37 @@ __global__ void __launch_bounds__(320, 1)
           for (int c = col0; c < col0 + span; c += CW, ++nstg) {
             uint8_t* stg = stg0 + (nstg % C::STG_BUFS) * C::STG_BYTES;
             uint8_t* row_base = stg + lane * 128;
-            if constexpr (C::RESID_F32 && SRK_RESID_RED) {
+            if constexpr (C::RESID_F32 && SRK_RESID_RED == 2) {
+              // 16x256b TMEM loads: four lanes own 32 contiguous bytes of a
+              // row, so each REDG.ADD.F32x2 warp instruction covers 8 rows x
+              // one full 32-byte sector
+              if ((c - col0) % 64 != 0) continue;  // one pass per 64 columns
+              const int t0 = lane & 3, t1 = lane >> 2;
+#pragma unroll 1
+              for (int hh = 0; hh < 2; ++hh) {
+                uint32_t r[32];
+                tmem_ld_16x256b_x8(tmem_base + (static_cast<uint32_t>(quad * 32 + hh * 16) << 16) +
+                                       acc * BN + c, r);
+                tmem_ld_wait();
+                const int ra = r0 + hh * 16 + t1, rb = ra + 8;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const int col = n0 + c + 8 * i + 2 * t0;
+                  if (ra < M)
+                    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(
+                                     ln.resid_out + static_cast<size_t>(ra) * ln.resid_ld + col),
+                                 "f"(__uint_as_float(r[4 * i])), "f"(__uint_as_float(r[4 * i + 1]))
+                                 : "memory");
+                  if (rb < M)
+                    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(
+                                     ln.resid_out + static_cast<size_t>(rb) * ln.resid_ld + col),
+                                 "f"(__uint_as_float(r[4 * i + 2])), "f"(__uint_as_float(r[4 * i + 3]))
+                                 : "memory");
+                }
+              }
+              continue;
+            }
+            if constexpr (C::RESID_F32 && SRK_RESID_RED == 1) {
               // x += acc straight from registers with vector reductions
               // (REDG.ADD.F32x4): no shared-memory staging, whose traffic
               // otherwise slows the operand-bound main loop of this GEMM.
