@@ -117,7 +117,7 @@ class DeviceCorpus:
         self.n, self.d, self.f = emb.shape[0], emb.shape[1], feat.shape[1]
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:  # not at interpreter teardown
             _lib.sr_corpus_destroy(self._h)
             self._h = None
 

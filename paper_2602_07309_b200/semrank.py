@@ -155,7 +155,7 @@ class ModelWeights:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:  # not at interpreter teardown
             _lib.sr_weights_free(h)
             self._h = C.c_void_p()
 
@@ -581,7 +581,7 @@ class ScoreCache:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:  # not at interpreter teardown
             _lib.sr_score_cache_destroy(h)
             self._h = C.c_void_p()
 
@@ -624,7 +624,7 @@ class ScoringEngine:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:  # not at interpreter teardown
             _lib.sr_engine_destroy(h)
             self._h = C.c_void_p()
 
@@ -898,7 +898,7 @@ class Comm:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:  # not at interpreter teardown
             _lib.sr_comm_destroy(h)
             self._h = C.c_void_p()
 
@@ -919,7 +919,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:  # not at interpreter teardown
             _lib.sr_plan_destroy(h)
             self._h = C.c_void_p()
 
@@ -1056,7 +1056,7 @@ class Scheduler:
 
     def close(self) -> None:
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:  # not at interpreter teardown
             _lib.sr_sched_destroy(h)
             self._h = C.c_void_p()
 
