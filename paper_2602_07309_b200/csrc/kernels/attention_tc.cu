@@ -82,6 +82,11 @@ constexpr bool kPrefetchS = SRK_ATTN_PREFETCH != 0;
 // sees (C2: 1.16 -> 1.05 x the needed exponentials). Measured slower (1.77 vs
 // 1.54 ms per query: the warp-uniform branches inside the unrolled exp loop
 // cost more than the MUFU work they save). Off.
+// PV over only the K-steps a partial key block covers.
+#ifndef SRK_ATTN_SHORT_PV
+#define SRK_ATTN_SHORT_PV 1
+#endif
+constexpr bool kShortPV = SRK_ATTN_SHORT_PV != 0;
 #ifndef SRK_ATTN_SKIP_HALVES
 #define SRK_ATTN_SKIP_HALVES 0
 #endif
@@ -396,8 +401,17 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
         tc_fence_after();
         SRK_PHASE(true, g, 7);
         const uint32_t v_addr = smem_u32(sV + st * C::TILE);
+        // a partial block (the tail of a key range) needs only ceil(w / 16)
+        // K-steps of PV: its P columns past w are zero
+        int nk = kBK / 16;
+        if constexpr (kShortPV) {
+          int k0, kb, ke;
+          pc.range(k0, kb, ke);
+          nk = (min(kBK, ke - k0) + 15) >> 4;
+        }
 #pragma unroll
         for (int s = 0; s < kBK / 16; ++s) {
+          if (s >= nk) break;
           umma_bf16_ts(tmem + C::O_COL + ob * 128, tmem + st * kBK + s * 8,
                        sw128_mnmajor_desc(v_addr + s * 16 * 128, kBox, 1024), idesc_pv,
                        (pc.j > 0 || s > 0) ? 1u : 0u);
