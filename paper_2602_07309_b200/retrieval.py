@@ -14,6 +14,7 @@ is no host scoring path.
 from __future__ import annotations
 
 import ctypes as C
+import sys as _sys
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence
 
@@ -117,7 +118,7 @@ class DeviceCorpus:
         self.n, self.d, self.f = emb.shape[0], emb.shape[1], feat.shape[1]
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib is not None:  # not at interpreter teardown
+        if getattr(self, "_h", None) and _lib is not None and not _sys.is_finalizing():  # process exit frees it
             _lib.sr_corpus_destroy(self._h)
             self._h = None
 

@@ -17,6 +17,7 @@ scores on the host.
 from __future__ import annotations
 
 import ctypes as C
+import sys as _sys
 import enum
 from dataclasses import dataclass, field
 from typing import Dict, List, Mapping, Optional, Sequence
@@ -155,7 +156,7 @@ class ModelWeights:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib is not None:  # not at interpreter teardown
+        if h is not None and h.value and _lib is not None and not _sys.is_finalizing():  # process exit frees it
             _lib.sr_weights_free(h)
             self._h = C.c_void_p()
 
@@ -581,7 +582,7 @@ class ScoreCache:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib is not None:  # not at interpreter teardown
+        if h is not None and h.value and _lib is not None and not _sys.is_finalizing():  # process exit frees it
             _lib.sr_score_cache_destroy(h)
             self._h = C.c_void_p()
 
@@ -624,7 +625,7 @@ class ScoringEngine:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib is not None:  # not at interpreter teardown
+        if h is not None and h.value and _lib is not None and not _sys.is_finalizing():  # process exit frees it
             _lib.sr_engine_destroy(h)
             self._h = C.c_void_p()
 
@@ -898,7 +899,7 @@ class Comm:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib is not None:  # not at interpreter teardown
+        if h is not None and h.value and _lib is not None and not _sys.is_finalizing():  # process exit frees it
             _lib.sr_comm_destroy(h)
             self._h = C.c_void_p()
 
@@ -919,7 +920,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib is not None:  # not at interpreter teardown
+        if h is not None and h.value and _lib is not None and not _sys.is_finalizing():  # process exit frees it
             _lib.sr_plan_destroy(h)
             self._h = C.c_void_p()
 
@@ -1056,7 +1057,7 @@ class Scheduler:
 
     def close(self) -> None:
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib is not None:  # not at interpreter teardown
+        if h is not None and h.value and _lib is not None and not _sys.is_finalizing():  # process exit frees it
             _lib.sr_sched_destroy(h)
             self._h = C.c_void_p()
 
