@@ -68,6 +68,9 @@ constexpr float kRescaleLog2 = 8.0f;  // rescale O only when the max grows by > 
 #define SRK_ATTN_POLY_EVERY 0
 #endif
 constexpr int kPolyEvery = SRK_ATTN_POLY_EVERY;
+#ifndef SRK_ATTN_POLY3
+#define SRK_ATTN_POLY3 1
+#endif
 #ifndef SRK_ATTN_S_WAIT
 #define SRK_ATTN_S_WAIT 0
 #endif
@@ -795,7 +798,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
             float p0, p1;
             if (kPolyEvery > 0 && (i >> 1) % kPolyEvery == kPolyEvery - 1) {
               // this pair on the FMA pipe: MUFU is the softmax's binding unit
-              f32x2_split(ex2_poly_x2(a2), p0, p1);
+              f32x2_split(SRK_ATTN_POLY3 ? ex2_poly3_x2(a2) : ex2_poly_x2(a2), p0, p1);
             } else {
               float a0, a1;
               f32x2_split(a2, a0, a1);
