@@ -32,6 +32,8 @@ Fixtures (tests/golden/headline_*.npz + headline.json):
   c4      configs[3]: L28 d2048 H16 ff6144, query 0 of the bench batch, first
           32 of its 250 items, all 28 layers
   batch   2 queries in one pass (plan_batches generalisation), C2 model, ragged
+  ragged  C2 model, one query whose items straddle the 128-row attention tiles
+          (lengths 1 ... 400, prefix 100)
   c5      configs[4]: 1 query x 8192 items (C2 model); ref16 for all 8192,
           ref32 for a 128-item random subset
 """
@@ -60,8 +62,8 @@ C4 = dict(n_layers=28, d_model=2048, n_heads=16, d_ff=6144)
 
 
 from tests.headline_inputs import (bf16, batch_requests, emb_request, pad_rows,  # noqa: E402,F401
-                                    project_rows, projection_matrix, sha, soft_request,
-                                    tokens_request)
+                                    project_rows, projection_matrix, ragged_long_request, sha,
+                                    soft_request, tokens_request)
 
 
 # ------------------------------------------------------------------ oracles
@@ -219,6 +221,18 @@ def gen_batch():
          **arrays)
 
 
+def gen_ragged():
+    cfg, path, dg = weights(C2)
+    prefix, items = ragged_long_request()
+    s32, fl = ref32(path, prefix, items=items)
+    s16 = ref16(path, prefix, items=items)
+    save("ragged", {**common_meta(cfg, dg, "engine.cpp:186-236 with items across attention tiles"),
+                    "request": "ragged_long_request(): numpy default_rng(31)", "t_q": len(prefix),
+                    "lens": [len(i) for i in items], "inputs_sha256": sha(prefix, *items),
+                    "flops": fl.tolist(), "top10_ref32": top10(s32), "top10_ref16": top10(s16)},
+         ref32=s32, ref16=s16)
+
+
 def gen_c5():
     cfg, path, dg = weights(C2)
     prefix, toks = tokens_request(7, 256, 96, 8192)
@@ -240,7 +254,7 @@ def gen_c5():
          ref16=done, ref32_subset=s32)
 
 
-GENS = {"c2": gen_c2, "pad": gen_pad, "batch": gen_batch, "c3proj": gen_c3proj, "c3": gen_c3,
+GENS = {"ragged": gen_ragged, "c2": gen_c2, "pad": gen_pad, "batch": gen_batch, "c3proj": gen_c3proj, "c3": gen_c3,
         "c4": gen_c4, "c5": gen_c5}
 
 

@@ -81,4 +81,15 @@ def batch_requests():
     return out
 
 
+def ragged_long_request():
+    """One query whose items straddle the 128-row attention tiles: lengths 1, 2,
+    127-129, 255-256, 300-400 and random ones, prefix not a multiple of 128."""
+    rng = np.random.default_rng(31)
+    prefix = rng.integers(0, 256, 100).astype(np.int32)
+    lens = [1, 2, 127, 128, 129, 255, 256, 300, 400, 1, 64, 96, 97, 33]
+    lens += [int(L) for L in rng.integers(1, 401, 18)]
+    items = [rng.integers(0, 256, L).astype(np.int32) for L in lens]
+    return prefix, items
+
+
 C5_SUBSET_SEED = 5

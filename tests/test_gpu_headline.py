@@ -14,7 +14,8 @@ Tolerances (max |dp| over all items and tasks, probabilities in [0, 1]):
   TOL32 = 6e-3 vs ref32   (adds the weight rounding itself)
 Measured on B200 over whole requests (round 2, profiles/r02_parity.json):
   c2 2.5e-3 / 4.1e-3, c3 3.4e-3, c3 projected 4.6e-3, 2-query batch 3.3e-3,
-  zero-pad 2.5e-3 / 4.1e-3 (ref16 / ref32).
+  zero-pad 2.5e-3 / 4.1e-3 (ref16 / ref32); ragged_long (items across tiles)
+  in profiles/r02_parity.json.
 Top-k: the device's top-10 must equal the oracle's order outside ties, where a
 tie is two oracle scores within 2 x (the max relevance deviation measured in
 the same test) of each other: a device error of e per item can only swap
@@ -205,6 +206,22 @@ def test_two_query_batch_every_item(cuda):
     bp.sync()
     for a, b in zip(bp.fetch_all(), got):
         assert np.array_equal(a.scores, b.scores) and a.topk == b.topk
+
+
+def test_ragged_items_across_tiles_every_item(cuda):
+    """C2 model, one query whose items straddle the 128-row attention tiles
+    (lengths 1 ... 400, a 100-token prefix): every item vs the reference and
+    its bf16-weight restatement, in every token mode."""
+    meta, g = fixture("ragged")
+    prefix, items = H.ragged_long_request()
+    assert H.sha(prefix, *items) == meta["inputs_sha256"]
+    eng = engine(meta)
+    res = eng.score(token_request(prefix, items), k=K)
+    compare("ragged", res.scores, g, [int(i) for i, _ in res.topk])
+    for mode in (sr.ScoreMode.Naive, sr.ScoreMode.Ibpc):  # one packed pass for every mode
+        r = token_request(prefix, items)
+        r.mode = mode
+        assert np.array_equal(eng.score(r, k=K).scores, res.scores)
 
 
 def test_c4_full_depth_every_item(cuda):
