@@ -34,6 +34,7 @@ Fixtures (tests/golden/headline_*.npz + headline.json):
   batch   2 queries in one pass (plan_batches generalisation), C2 model, ragged
   ragged  C2 model, one query whose items straddle the 128-row attention tiles
           (lengths 1 ... 400, prefix 100)
+  ragged_soft  C2 model, mixed mode with 1 ... 20 soft rows per item
   c5      configs[4]: 1 query x 8192 items (C2 model); ref16 for all 8192,
           ref32 for a 128-item random subset
 """
@@ -62,8 +63,8 @@ C4 = dict(n_layers=28, d_model=2048, n_heads=16, d_ff=6144)
 
 
 from tests.headline_inputs import (bf16, batch_requests, emb_request, pad_rows,  # noqa: E402,F401
-                                    project_rows, projection_matrix, ragged_long_request, sha,
-                                    soft_request, tokens_request)
+                                    project_rows, projection_matrix, ragged_long_request,
+                                    ragged_soft_request, sha, soft_request, tokens_request)
 
 
 # ------------------------------------------------------------------ oracles
@@ -233,6 +234,19 @@ def gen_ragged():
          ref32=s32, ref16=s16)
 
 
+def gen_ragged_soft():
+    cfg, path, dg = weights(C2)
+    prefix, rows = ragged_soft_request()
+    s32, fl = ref32(path, prefix, rows=rows)
+    s16 = ref16(path, prefix, rows=rows)
+    save("ragged_soft", {**common_meta(cfg, dg, "engine.cpp:238-276 with 1 ... 20 rows per item"),
+                         "request": "ragged_soft_request(): numpy default_rng(37)",
+                         "t_q": len(prefix), "counts": [len(r) for r in rows],
+                         "inputs_sha256": sha(prefix, *rows), "flops": fl.tolist(),
+                         "top10_ref32": top10(s32), "top10_ref16": top10(s16)},
+         ref32=s32, ref16=s16)
+
+
 def gen_c5():
     cfg, path, dg = weights(C2)
     prefix, toks = tokens_request(7, 256, 96, 8192)
@@ -254,7 +268,7 @@ def gen_c5():
          ref16=done, ref32_subset=s32)
 
 
-GENS = {"ragged": gen_ragged, "c2": gen_c2, "pad": gen_pad, "batch": gen_batch, "c3proj": gen_c3proj, "c3": gen_c3,
+GENS = {"ragged": gen_ragged, "ragged_soft": gen_ragged_soft, "c2": gen_c2, "pad": gen_pad, "batch": gen_batch, "c3proj": gen_c3proj, "c3": gen_c3,
         "c4": gen_c4, "c5": gen_c5}
 
 

@@ -92,4 +92,13 @@ def ragged_long_request():
     return prefix, items
 
 
+def ragged_soft_request():
+    """Mixed-mode query with 1 ... 20 soft rows per item (N(0, 0.08^2))."""
+    rng = np.random.default_rng(37)
+    prefix = rng.integers(0, 256, 64).astype(np.int32)
+    counts = [1, 20, 2, 19, 8] + [int(c) for c in rng.integers(1, 21, 35)]
+    rows = [rng.standard_normal((c, 1024)).astype(np.float32) * np.float32(0.08) for c in counts]
+    return prefix, rows
+
+
 C5_SUBSET_SEED = 5

@@ -224,6 +224,25 @@ def test_ragged_items_across_tiles_every_item(cuda):
         assert np.array_equal(eng.score(r, k=K).scores, res.scores)
 
 
+def test_ragged_soft_rows_and_mixed_mode_batch(cuda):
+    """C2 model, mixed mode with 1 ... 20 soft rows per item, every item vs
+    the reference; then the same query packed in one pass together with the
+    ragged token query (requests of different modes in one batch) gives each
+    request its own scores."""
+    meta, g = fixture("ragged_soft")
+    prefix, rows = H.ragged_soft_request()
+    assert H.sha(prefix, *rows) == meta["inputs_sha256"]
+    eng = engine(meta)
+    soft = soft_request(prefix, rows)
+    res = eng.score(soft, k=K)
+    compare("ragged_soft", res.scores, g, [int(i) for i, _ in res.topk])
+    meta_t, g_t = fixture("ragged")
+    p2, items = H.ragged_long_request()
+    both = eng.score_batch([soft, token_request(p2, items)], k=K)
+    compare("mixed_batch_soft", both[0].scores, g, [int(i) for i, _ in both[0].topk])
+    compare("mixed_batch_tokens", both[1].scores, g_t, [int(i) for i, _ in both[1].topk])
+
+
 def test_c4_full_depth_every_item(cuda):
     """configs[3] model (L28 d2048 H16 ff6144), all 28 layers: query 0 of the
     bench batch, its first 32 items, vs the reference; and inside a 2-query
