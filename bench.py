@@ -54,7 +54,7 @@ STRONG = {"c5"}  # n_items is the whole job's, not per GPU
 # are projected on the device into t_i soft-token rows (sr_engine_set_projection;
 # SURVEY H7, north_star (d)). "c3_rows" sends the d_model-wide rows instead.
 EMB = {"c3": 256}
-SERVE_WORKLOADS = {"c2", "c4"}  # token-item workloads served through sr_sched_*
+SERVE_WORKLOADS = {"c2", "c4", "c3_rows"}  # served through sr_sched_* (c3_rows: soft rows)
 # queries packed into one device pass per step (per GPU)
 QUERIES = {"c4": 32}
 WORKLOAD_DESC = {
@@ -666,7 +666,10 @@ def serving_sweep(sr, eng, wl, pass_ms, seconds=3.0, max_queries=8):
             s.stats(reset=True)
             for frac in SERVE_LOADS:
                 rate = frac * cap_qps
-                n = max(40, int(rate * seconds))
+                # enough arrivals that the drain after the last one (about one
+                # latency) stays small against the window: >= 150 queries,
+                # at most 12 s per point (slow passes, e.g. C4 at 50 ms)
+                n = max(40, int(rate * min(12.0, max(seconds, 150.0 / rate))))
                 gaps = rng.exponential(1.0 / rate, n)
                 tickets, done = [], threading.Event()
                 lock = threading.Condition()
