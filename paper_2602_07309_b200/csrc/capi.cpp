@@ -962,22 +962,27 @@ int32_t sr_kernel_gemm_resid_ln(const void* a_bf16, const void* b_bf16, int32_t 
     srk::LnFold f{};
     f.ln_cnt = counters;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    cudaStream_t s2 = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-    SR_CUDA_CHECK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
-    SR_CUDA_CHECK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    SR_CUDA_CHECK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-    SR_CUDA_CHECK(cudaEventRecord(fork, s));
-    SR_CUDA_CHECK(cudaStreamWaitEvent(s2, fork, 0));
+    // side stream + fork/join events, released on every path (RAII)
+    struct Side {
+      cudaStream_t s2 = nullptr;
+      cudaEvent_t fork = nullptr, join = nullptr;
+      ~Side() {
+        if (fork) cudaEventDestroy(fork);
+        if (join) cudaEventDestroy(join);
+        if (s2) cudaStreamDestroy(s2);
+      }
+    } sd;
+    SR_CUDA_CHECK(cudaStreamCreateWithFlags(&sd.s2, cudaStreamNonBlocking));
+    SR_CUDA_CHECK(cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming));
+    SR_CUDA_CHECK(cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming));
+    SR_CUDA_CHECK(cudaEventRecord(sd.fork, s));
+    SR_CUDA_CHECK(cudaStreamWaitEvent(sd.s2, sd.fork, 0));
     SR_CUDA_CHECK(srk::gemm_auto(ta, tb, M, N, K, x, N, srk::EPI_RESID_F32_LN, s, &f));
     SR_CUDA_CHECK(srk::layer_norm_after(x, gain, static_cast<__nv_bfloat16*>(out_bf16), M, N,
-                                        counters, N / 256, s2));
-    SR_CUDA_CHECK(cudaEventRecord(join, s2));
-    SR_CUDA_CHECK(cudaStreamWaitEvent(s, join, 0));
+                                        counters, N / 256, sd.s2));
+    SR_CUDA_CHECK(cudaEventRecord(sd.join, sd.s2));
+    SR_CUDA_CHECK(cudaStreamWaitEvent(s, sd.join, 0));
     SR_CUDA_CHECK(cudaStreamSynchronize(s));
-    cudaEventDestroy(fork);
-    cudaEventDestroy(join);
-    cudaStreamDestroy(s2);
   });
 }
 
