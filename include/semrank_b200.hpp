@@ -273,6 +273,8 @@ class ScoreCache {  // midtier.hpp:42-69; rows kept in task order
   std::unique_ptr<sr_score_cache, Del> c_;
 };
 
+class Scheduler;
+
 class ScoringEngine {  // engine.hpp:109-119
  public:
   explicit ScoringEngine(const ModelWeights& weights, int device = 0) : weights_(weights) {
@@ -387,6 +389,79 @@ class ScoringEngine {  // engine.hpp:109-119
   };
   ModelWeights weights_;
   std::unique_ptr<sr_engine, Del> e_;
+  friend class Scheduler;
+};
+
+// Latency-bounded dynamic batching in front of one engine (sr_sched_*,
+// SURVEY §8(f) row 1): any thread submits whole requests and waits on its
+// ticket; one native dispatcher packs queued requests into device passes
+// (plan_batches' FIFO rule, engine.cpp:278-326, plus a latency budget) — the
+// replacement for callers serialising on ScoringEngine's mutex
+// (engine.cpp:389-392). Requests are copied at submit.
+class Scheduler {
+ public:
+  struct Options {
+    int max_queries = 8;                    // requests per device pass
+    std::int64_t max_rows = std::int64_t(1) << 22;  // packed rows per pass
+    double budget_ms = 0.0;                 // latency rule (0 = off)
+    int max_wait_us = 0;                    // hold an unfilled pass this long
+    int k = 10;                             // top-k per request
+  };
+  struct Stats {
+    std::int64_t submitted = 0, completed = 0, failed = 0, batches = 0;
+    double mean_batch = 0, p50_ms = 0, p99_ms = 0, max_ms = 0, mean_ms = 0;
+  };
+
+  Scheduler(ScoringEngine& engine, const Options& o) : engine_(engine), k_(o.k) {
+    sr_sched_options so{o.max_queries, o.max_rows, o.budget_ms, o.max_wait_us, o.k, 0};
+    sr_sched* s = nullptr;
+    check(sr_sched_create(engine.e_.get(), &so, &s));
+    s_.reset(s);
+  }
+
+  std::uint64_t submit(const ScoreRequest& request) {
+    ScoringEngine::Packed p(request, engine_.weights_.config.d_model);
+    std::uint64_t t = 0;
+    check(sr_sched_submit(s_.get(), &p.req, &t));  // deep-copied by the dispatcher
+    std::lock_guard<std::mutex> lock(mu_);
+    pending_.emplace(t, request);
+    return t;
+  }
+
+  // Blocks until the ticket's pass is done; rethrows the request's own error.
+  ScoreResult wait(std::uint64_t ticket, double* latency_ms = nullptr) {
+    ScoreRequest request;
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      auto it = pending_.find(ticket);
+      if (it == pending_.end()) throw Error(ErrorCode::StateInvalid, "unknown ticket");
+      request = std::move(it->second);
+      pending_.erase(it);
+    }
+    ScoringEngine::Out o(request.items.size(), 1 + engine_.weights_.config.head_specs.size(), k_);
+    double lat = 0;
+    int32_t nq = 0;
+    check(sr_sched_wait(s_.get(), ticket, &o.res, &lat, &nq));
+    if (latency_ms) *latency_ms = lat;
+    return o.result(request, engine_.weights_.config);
+  }
+
+  Stats stats(bool reset = false) {
+    sr_sched_stats st{};
+    check(sr_sched_get_stats(s_.get(), reset ? 1 : 0, &st));
+    return {st.submitted, st.completed, st.failed, st.batches, st.mean_batch,
+            st.p50_ms, st.p99_ms, st.max_ms, st.mean_ms};
+  }
+
+ private:
+  struct Del {
+    void operator()(sr_sched* s) const { sr_sched_destroy(s); }
+  };
+  ScoringEngine& engine_;
+  int k_;
+  std::mutex mu_;
+  std::map<std::uint64_t, ScoreRequest> pending_;
+  std::unique_ptr<sr_sched, Del> s_;  // destroyed first: joins the dispatcher
 };
 
 inline ScoreResult score_by_mode(ScoringEngine& engine, const ScoreRequest& request) {

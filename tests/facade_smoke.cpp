@@ -1,6 +1,7 @@
 // Compiles a reference-style caller against the C++ facade
 // (include/semrank_b200.hpp) and exercises the host-side API. Built and run by
 // tests/test_facade.py; with a GPU present it also scores one request.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -66,6 +67,26 @@ int main(int argc, char** argv) {
     for (int i = 0; i < 4; ++i)
       if (c1.items[i].tasks != r.items[i].tasks || c2.items[i].tasks != r.items[i].tasks) return 16;
     if (c2.topk != r.topk) return 17;
+    {
+      // the serving scheduler: concurrent-style submit / wait, each result
+      // identical to scoring the request alone (one request per pass here)
+      Scheduler::Options so;
+      so.max_queries = 4;
+      so.k = 2;
+      Scheduler sched(engine, so);
+      std::vector<std::uint64_t> tickets;
+      for (int q = 0; q < 3; ++q) tickets.push_back(sched.submit(req));
+      for (auto t : tickets) {
+        double lat = -1;
+        const auto s = sched.wait(t, &lat);
+        if (s.items.size() != 4 || s.topk != r.topk || lat < 0) return 18;
+        for (int i = 0; i < 4; ++i)
+          if (std::abs(s.items[i].tasks.at(kRelevanceTask) - r.items[i].tasks.at(kRelevanceTask)) >
+              6e-3)
+            return 19;
+      }
+      if (sched.stats().completed != 3) return 20;
+    }
     std::printf("relevance[0]=%.6f top=%s\n", r.items[0].tasks.at(kRelevanceTask),
                 r.topk[0].first.c_str());
   }
