@@ -299,6 +299,71 @@ class ScoringEngine {  // engine.hpp:109-119
     return r;
   }
 
+  // Several requests in one packed device pass (plan_batches generalised,
+  // engine.cpp:278-326); results in request order.
+  std::vector<ScoreResult> score_batch(const std::vector<ScoreRequest>& requests, int k = 0) {
+    const int d = weights_.config.d_model;
+    const size_t T = 1 + weights_.config.head_specs.size();
+    std::vector<Packed> ps;
+    std::vector<Out> os;
+    ps.reserve(requests.size());
+    os.reserve(requests.size());
+    std::vector<sr_request> reqs;
+    std::vector<sr_result> res;
+    for (const auto& r : requests) {
+      ps.emplace_back(r, d);
+      os.emplace_back(r.items.size(), T, k);
+    }
+    for (size_t i = 0; i < requests.size(); ++i) {
+      reqs.push_back(ps[i].req);
+      res.push_back(os[i].res);
+    }
+    check(sr_engine_score_batch(e_.get(), reqs.data(), static_cast<int32_t>(reqs.size()),
+                                res.data()));
+    std::vector<ScoreResult> out;
+    for (size_t i = 0; i < requests.size(); ++i) {
+      os[i].res = res[i];  // k_returned / flops written by the call
+      out.push_back(os[i].result(requests[i], weights_.config));
+    }
+    return out;
+  }
+
+  // Mixed items from compact retrieval embeddings (north_star (d)):
+  // set_projection(P [d_emb x n_soft*d_model], n_soft) once, then
+  // score_embeddings(..., EmbForm::Project) builds n_soft soft rows per item on
+  // the device; EmbForm::Pad is the service's one zero-padded row per item
+  // (service.cpp:208-217). Item i's id is item_ids[i] (default: its index).
+  enum class EmbForm { Pad = SR_EMB_PAD, Project = SR_EMB_PROJECT };
+  void set_projection(const std::vector<float>& proj, int d_emb, int n_soft) {
+    check(sr_engine_set_projection(e_.get(), proj.empty() ? nullptr : proj.data(), d_emb,
+                                   n_soft));
+  }
+  ScoreResult score_embeddings(const std::string& request_id, const std::vector<int>& prefix,
+                               const std::vector<float>& emb, int d_emb, EmbForm form, int k = 0,
+                               const std::vector<std::int64_t>& item_ids = {}) {
+    if (d_emb < 1 || emb.size() % static_cast<size_t>(d_emb) != 0)
+      throw Error(ErrorCode::PayloadInvalid, "embeddings are not [n x d_emb]");
+    const size_t n = emb.size() / static_cast<size_t>(d_emb);
+    std::vector<std::int64_t> ids = item_ids;
+    if (ids.empty())
+      for (size_t i = 0; i < n; ++i) ids.push_back(static_cast<std::int64_t>(i));
+    std::vector<int32_t> pre(prefix.begin(), prefix.end());
+    const size_t T = 1 + weights_.config.head_specs.size();
+    ScoreRequest shape;  // ids / order for the result
+    shape.request_id = request_id;
+    shape.mode = ScoreMode::Mixed;
+    for (size_t i = 0; i < n; ++i) {
+      ScoreItem it;
+      it.id = std::to_string(ids[i]);
+      shape.items.push_back(std::move(it));
+    }
+    Out o(n, T, k);
+    check(sr_engine_score_emb(e_.get(), pre.data(), static_cast<int32_t>(pre.size()), emb.data(),
+                              d_emb, static_cast<int32_t>(n), ids.data(),
+                              static_cast<int32_t>(form), &o.res));
+    return o.result(shape, weights_.config);
+  }
+
   // handle_search's cache probe -> score misses -> put (service.cpp:160-234),
   // then the page ranking on the device. Item ids must be integers (the cache
   // keys' entity ids); *hits receives the number of cached items.

@@ -68,6 +68,30 @@ int main(int argc, char** argv) {
       if (c1.items[i].tasks != r.items[i].tasks || c2.items[i].tasks != r.items[i].tasks) return 16;
     if (c2.topk != r.topk) return 17;
     {
+      // batched pass: each request's scores within the bf16 tolerance of its own pass
+      ScoreRequest req2 = req;
+      req2.request_id = "facade2";
+      req2.items.pop_back();
+      const auto both = engine.score_batch({req, req2}, 2);
+      if (both.size() != 2 || both[0].items.size() != 4 || both[1].items.size() != 3) return 21;
+      for (int i = 0; i < 3; ++i)
+        if (std::abs(both[1].items[i].tasks.at(kRelevanceTask) -
+                     r.items[i].tasks.at(kRelevanceTask)) > 6e-3)
+          return 22;
+      // compact embeddings: service zero-pad form and a device projection
+      const int d_emb = 16, n_soft = 2, d = cfg.d_model;
+      std::vector<float> emb(3 * d_emb);
+      for (size_t i = 0; i < emb.size(); ++i) emb[i] = 0.01f * static_cast<float>(i % 7);
+      const auto pad = engine.score_embeddings("pad", req.prefix_tokens, emb, d_emb,
+                                               ScoringEngine::EmbForm::Pad, 2, {7, 8, 9});
+      if (pad.items.size() != 3 || pad.items[0].item_id != "7" || pad.topk.size() != 2) return 23;
+      std::vector<float> proj(static_cast<size_t>(d_emb) * n_soft * d, 0.001f);
+      engine.set_projection(proj, d_emb, n_soft);
+      const auto pr = engine.score_embeddings("proj", req.prefix_tokens, emb, d_emb,
+                                              ScoringEngine::EmbForm::Project, 2);
+      if (pr.items.size() != 3 || pr.kv_incremental_per_item != n_soft) return 24;
+    }
+    {
       // the serving scheduler: concurrent-style submit / wait, each result
       // identical to scoring the request alone (one request per pass here)
       Scheduler::Options so;
