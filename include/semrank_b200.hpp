@@ -364,6 +364,50 @@ class ScoringEngine {  // engine.hpp:109-119
     return o.result(shape, weights_.config);
   }
 
+  // The service's output side on the device (service.cpp:242-277): calibrated
+  // relevance from a fitted isotonic head (calibration.cpp:65-88) and the
+  // optional score blend (task -> weight, applied in task-name order like the
+  // reference's std::map); the top-k then ranks by the final score, available
+  // per item through final_scores(). An empty head and blend turn it off.
+  struct CalibrationBlock {  // calibration.hpp:18-23
+    double lo = 0, hi = 0, value = 0;
+  };
+  void set_postprocess(const std::vector<CalibrationBlock>& head,
+                       const std::map<std::string, double>& blend = {}) {
+    std::vector<double> lo, hi, val;
+    for (const auto& b : head) {
+      lo.push_back(b.lo);
+      hi.push_back(b.hi);
+      val.push_back(b.value);
+    }
+    std::vector<int32_t> task;
+    std::vector<double> w;
+    for (const auto& [name, weight] : blend) {  // std::map: task-name order
+      int32_t t = -1;
+      if (name == kRelevanceTask) t = 0;
+      for (size_t h = 0; h < weights_.config.head_specs.size() && t < 0; ++h)
+        if (weights_.config.head_specs[h].name == name) t = static_cast<int32_t>(h + 1);
+      if (t < 0) throw Error(ErrorCode::Alignment, "blend references unknown task: " + name);
+      task.push_back(t);
+      w.push_back(weight);
+    }
+    check(sr_engine_set_postprocess(e_.get(), lo.empty() ? nullptr : lo.data(),
+                                    hi.empty() ? nullptr : hi.data(),
+                                    val.empty() ? nullptr : val.data(),
+                                    static_cast<int32_t>(lo.size()),
+                                    task.empty() ? nullptr : task.data(),
+                                    w.empty() ? nullptr : w.data(),
+                                    static_cast<int32_t>(task.size())));
+  }
+  // Final (calibrated / blended) scores of the last score call, item order.
+  std::vector<double> final_scores(size_t n_items) {
+    std::vector<double> out(n_items > 0 ? n_items : 1);
+    int32_t got = 0;
+    check(sr_engine_final_scores(e_.get(), out.data(), static_cast<int32_t>(out.size()), &got));
+    out.resize(static_cast<size_t>(got));
+    return out;
+  }
+
   // handle_search's cache probe -> score misses -> put (service.cpp:160-234),
   // then the page ranking on the device. Item ids must be integers (the cache
   // keys' entity ids); *hits receives the number of cached items.

@@ -92,6 +92,26 @@ int main(int argc, char** argv) {
       if (pr.items.size() != 3 || pr.kv_incremental_per_item != n_soft) return 24;
     }
     {
+      // service post-processing: a two-block isotonic head and a blend
+      engine.set_postprocess({{0.0, 0.5, 0.2}, {0.5, 1.0, 0.9}},
+                             {{"relevance", 1.0}, {"click", 0.5}});
+      const auto pp = engine.score(req, 2);
+      const auto fin = engine.final_scores(req.items.size());
+      if (fin.size() != 4 || pp.topk.size() != 2) return 25;
+      for (int i = 0; i < 4; ++i) {
+        const double rel = pp.items[i].tasks.at(kRelevanceTask);
+        const double cal = rel <= 0.5 ? 0.2 : 0.9;  // calibration.cpp:69-85
+        if (std::abs(fin[i] - (cal + 0.5 * pp.items[i].tasks.at("click"))) > 1e-9) return 26;
+      }
+      try {
+        engine.set_postprocess({}, {{"relevance", 1.0}});  // blend without a fitted head
+        return 27;
+      } catch (const Error& e) {
+        if (e.code() != ErrorCode::StateInvalid) return 28;
+      }
+      engine.set_postprocess({});
+    }
+    {
       // the serving scheduler: concurrent-style submit / wait, each result
       // identical to scoring the request alone (one request per pass here)
       Scheduler::Options so;
