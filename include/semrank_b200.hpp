@@ -275,6 +275,34 @@ class ScoreCache {  // midtier.hpp:42-69; rows kept in task order
 
 class Scheduler;
 
+// Candidate sharding across GPUs: one process per GPU, each
+// scoring a contiguous shard of the items with global item ids; the per-rank
+// top-k lists are merged with the reference's comparator
+// (retrieval.cpp:144-165) over NCCL. Rank 0 makes the id, the caller's own
+// bootstrap broadcasts it, every rank constructs a Comm.
+class Comm {
+ public:
+  using Id = std::vector<std::uint8_t>;
+  static Id unique_id() {
+    Id id(128);
+    check(sr_nccl_unique_id(id.data()));
+    return id;
+  }
+  Comm(int nranks, int rank, const Id& id, int device) {
+    if (id.size() != 128) throw Error(ErrorCode::Parameter, "NCCL id must be 128 bytes");
+    sr_comm* c = nullptr;
+    check(sr_comm_create(nranks, rank, id.data(), device, &c));
+    c_.reset(c);
+  }
+  sr_comm* handle() const { return c_.get(); }
+
+ private:
+  struct Del {
+    void operator()(sr_comm* c) const { sr_comm_destroy(c); }
+  };
+  std::unique_ptr<sr_comm, Del> c_;
+};
+
 class ScoringEngine {  // engine.hpp:109-119
  public:
   explicit ScoringEngine(const ModelWeights& weights, int device = 0) : weights_(weights) {
@@ -408,6 +436,21 @@ class ScoringEngine {  // engine.hpp:109-119
     return out;
   }
 
+  // This rank's shard (items with global ids) scored and merged across the
+  // ranks of `comm`: every rank returns the global top-k; `items` holds this
+  // shard's scores only.
+  ScoreResult score_sharded(Comm& comm, const ScoreRequest& shard, int k) {
+    Packed p(shard, weights_.config.d_model);
+    if (!p.numeric_ids)
+      throw Error(ErrorCode::SpecViolation, "sharded scoring needs integer (global) item ids");
+    Out o(shard.items.size(), 1 + weights_.config.head_specs.size(), k);
+    check(sr_engine_score_sharded(e_.get(), comm.handle(), &p.req, &o.res));
+    ScoreResult r = o.result(shard, weights_.config, /*topk_from_items=*/false);
+    for (int j = 0; j < o.res.k_returned; ++j)
+      r.topk.push_back({std::to_string(o.tid[j]), o.tsc[j]});
+    return r;
+  }
+
   // handle_search's cache probe -> score misses -> put (service.cpp:160-234),
   // then the page ranking on the device. Item ids must be integers (the cache
   // keys' entity ids); *hits receives the number of cached items.
@@ -474,7 +517,8 @@ class ScoringEngine {  // engine.hpp:109-119
           tix(k > 0 ? k : 1) {
       res = sr_result{scores.data(), k, tid.data(), tsc.data(), tix.data(), {}, 0, 0};
     }
-    ScoreResult result(const ScoreRequest& request, const ModelConfig& cfg) const {
+    ScoreResult result(const ScoreRequest& request, const ModelConfig& cfg,
+                       bool topk_from_items = true) const {
       ScoreResult out;
       out.request_id = request.request_id;
       out.mode = request.mode;
@@ -487,8 +531,9 @@ class ScoringEngine {  // engine.hpp:109-119
         for (size_t h = 1; h < T; ++h) s.tasks[cfg.head_specs[h - 1].name] = scores[i * T + h];
         out.items.push_back(std::move(s));
       }
-      for (int j = 0; j < res.k_returned; ++j)
-        out.topk.push_back({request.items[tix[j]].id, tsc[j]});
+      if (topk_from_items)
+        for (int j = 0; j < res.k_returned; ++j)
+          out.topk.push_back({request.items[tix[j]].id, tsc[j]});
       return out;
     }
   };

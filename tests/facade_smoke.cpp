@@ -112,6 +112,13 @@ int main(int argc, char** argv) {
       engine.set_postprocess({});
     }
     {
+      // candidate sharding through NCCL at one rank: the merged top-k is the
+      // single-GPU top-k (global ids = the items' numeric ids)
+      Comm comm(1, 0, Comm::unique_id(), 0);
+      const auto sh = engine.score_sharded(comm, req, 2);
+      if (sh.topk != r.topk) return 29;
+    }
+    {
       // the serving scheduler: concurrent-style submit / wait, each result
       // identical to scoring the request alone (one request per pass here)
       Scheduler::Options so;
