@@ -273,6 +273,51 @@ class ScoreCache {  // midtier.hpp:42-69; rows kept in task order
   std::unique_ptr<sr_score_cache, Del> c_;
 };
 
+// Exhaustive retrieval top-K on the device: replaces
+// exhaustive_topk (retrieval.hpp:60-70, retrieval.cpp:134-173) — score =
+// w0 cos(q, e_d) + sum_i w_i f_i(d), exact top-K by (score desc, doc_id asc),
+// scores identical to the reference's doubles. The corpus is columnar and
+// copied to the device once; filters are the caller's keep mask
+// (filter_candidates, retrieval.cpp:79-97).
+struct RankedDoc {  // retrieval.hpp:59-62
+  std::int64_t doc_id = 0;
+  double score = 0;
+  bool operator==(const RankedDoc& o) const { return doc_id == o.doc_id && score == o.score; }
+};
+class Corpus {
+ public:
+  Corpus(const std::vector<float>& embeddings, const std::vector<float>& features,
+         const std::vector<std::int64_t>& doc_ids, int d_emb, int n_features, int device = 0) {
+    const std::int64_t n = static_cast<std::int64_t>(doc_ids.size());
+    if (embeddings.size() != static_cast<size_t>(n) * d_emb ||
+        features.size() != static_cast<size_t>(n) * n_features)
+      throw Error(ErrorCode::Alignment, "corpus columns do not match the document count");
+    sr_corpus* c = nullptr;
+    check(sr_corpus_create(embeddings.data(), features.empty() ? nullptr : features.data(),
+                           doc_ids.data(), n, d_emb, n_features, device, &c));
+    c_.reset(c);
+  }
+  std::vector<RankedDoc> topk(const std::vector<float>& query, double w0,
+                              const std::vector<double>& w, int k,
+                              const std::vector<std::uint8_t>& keep = {}) {
+    std::vector<std::int64_t> ids(k > 0 ? k : 1);
+    std::vector<double> sc(k > 0 ? k : 1);
+    int32_t n = 0;
+    check(sr_corpus_topk(c_.get(), query.data(), static_cast<int32_t>(query.size()), w0,
+                         w.empty() ? nullptr : w.data(), static_cast<int32_t>(w.size()),
+                         keep.empty() ? nullptr : keep.data(), k, ids.data(), sc.data(), &n));
+    std::vector<RankedDoc> out;
+    for (int i = 0; i < n; ++i) out.push_back({ids[i], sc[i]});
+    return out;
+  }
+
+ private:
+  struct Del {
+    void operator()(sr_corpus* c) const { sr_corpus_destroy(c); }
+  };
+  std::unique_ptr<sr_corpus, Del> c_;
+};
+
 class Scheduler;
 
 // Candidate sharding across GPUs: one process per GPU, each

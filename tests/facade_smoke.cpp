@@ -119,6 +119,23 @@ int main(int argc, char** argv) {
       if (sh.topk != r.topk) return 29;
     }
     {
+      // retrieval top-K: 50 docs, d_emb 4, one feature; ties by doc id
+      std::vector<float> embv, feat;
+      std::vector<std::int64_t> ids;
+      for (int i = 0; i < 50; ++i) {
+        for (int j = 0; j < 4; ++j) embv.push_back(1.0f + 0.01f * static_cast<float>((i * 7 + j) % 11));
+        feat.push_back(static_cast<float>(i % 5));
+        ids.push_back(1000 - i);
+      }
+      Corpus corpus(embv, feat, ids, 4, 1, 0);
+      const auto top = corpus.topk({1.f, 1.f, 1.f, 1.f}, 1.0, {0.1}, 5);
+      if (top.size() != 5) return 30;
+      for (size_t i = 1; i < top.size(); ++i)
+        if (top[i - 1].score < top[i].score ||
+            (top[i - 1].score == top[i].score && top[i - 1].doc_id > top[i].doc_id))
+          return 31;
+    }
+    {
       // the serving scheduler: concurrent-style submit / wait, each result
       // identical to scoring the request alone (one request per pass here)
       Scheduler::Options so;
