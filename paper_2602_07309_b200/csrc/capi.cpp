@@ -1055,12 +1055,27 @@ int32_t sr_kernel_attention(const void* qkv, const int32_t* spans_host, int32_t 
     cudaMemcpy(dsp, spans.data(), sizeof(srk::RowSpan) * M, cudaMemcpyHostToDevice);
     cudaMemcpy(dt, tiles.data(), sizeof(srk::AttnTile) * tiles.size(), cudaMemcpyHostToDevice);
     cudaError_t err;
+    int2* dw = nullptr;
     if (head_dim >= 64) {
       CUtensorMap tm;
       err = srk::make_tmap_bf16_2d(&tm, qkv, M, 3 * n_heads * head_dim, 128, 64);
+      // the engine's LPT work order (SRK_ATTN_LPT=0: head-major)
+      std::vector<int2> work;
+      const char* lpt = std::getenv("SRK_ATTN_LPT");
+      if (lpt == nullptr || std::atoi(lpt) != 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        srk::attention_work_lpt(tiles.data(), static_cast<int>(tiles.size()), n_heads,
+                                srk::attention_ctas(static_cast<int>(tiles.size()), n_heads, dev),
+                                work);
+        if (err == cudaSuccess) err = cudaMalloc(&dw, sizeof(int2) * work.size());
+        if (err == cudaSuccess)
+          err = cudaMemcpy(dw, work.data(), sizeof(int2) * work.size(), cudaMemcpyHostToDevice);
+      }
       if (err == cudaSuccess)
         err = srk::attention_tc(tm, qkv, dsp, dt, static_cast<int>(tiles.size()),
-                                static_cast<__nv_bfloat16*>(out), M, n_heads, head_dim, s);
+                                static_cast<__nv_bfloat16*>(out), M, n_heads, head_dim, s, dw,
+                                static_cast<int>(work.size()));
     } else {
       err = srk::attention(static_cast<const __nv_bfloat16*>(qkv), dsp, dt,
                            static_cast<int>(tiles.size()), static_cast<__nv_bfloat16*>(out), M,
@@ -1069,6 +1084,7 @@ int32_t sr_kernel_attention(const void* qkv, const int32_t* spans_host, int32_t 
     if (err == cudaSuccess) err = cudaStreamSynchronize(s);
     cudaFree(dsp);
     cudaFree(dt);
+    if (dw) cudaFree(dw);
     SR_CUDA_CHECK(err);
   });
 }

@@ -79,6 +79,9 @@ Engine::Engine(const ModelWeights& w, int device) : cfg_(w.config), device_(devi
     // residual GEMM (epilogue 7 + layer_norm_after on a side stream). Measured
     // slower at C2 (9.84 vs 8.97 ms per query): the GEMM is at the HBM ridge
     // and the concurrent LayerNorm slows both.
+    // LPT order of the attention work items (SRK_ATTN_LPT=0: head-major)
+    const char* av = std::getenv("SRK_ATTN_LPT");
+    attn_lpt_ = av == nullptr || std::atoi(av) != 0;
     const char* lv = std::getenv("SRK_LN_AFTER");
     ln_after_ = !fold_ln_ && lv != nullptr && std::atoi(lv) != 0 && srk::gemm_use_pair(d) &&
                 d % 4 == 0 && d <= 2048;
@@ -304,7 +307,8 @@ int32_t Engine::enqueue_forward(Plan& p, float* hidden_out, Profiler* prof) {
   auto attention = [&]() {
     if (hd >= 64)
       SR_CUDA_CHECK(srk::attention_tc(tm_qkv_, qkv_.ptr, p.spans.ptr, p.tiles.ptr,
-                                      static_cast<int>(p.pack.tiles.size()), xn_.ptr, M, H, hd, s));
+                                      static_cast<int>(p.pack.tiles.size()), xn_.ptr, M, H, hd, s,
+                                      p.n_attn_work ? p.attn_work.ptr : nullptr, p.n_attn_work));
     else  // toy head sizes (16/32): the 64-row mma.sync kernel
       SR_CUDA_CHECK(srk::attention(qkv_.ptr, p.spans.ptr, p.tiles.ptr,
                                    static_cast<int>(p.pack.tiles.size()), xn_.ptr, M, H, hd, s));
@@ -530,6 +534,16 @@ void Engine::refill_plan(Plan& p, const sr_request* reqs, int n_req) {
   put(p.pos, pk.row_pos, stream_);
   put(p.spans, pk.spans, stream_);
   put(p.tiles, pk.tiles, stream_);
+  p.n_attn_work = 0;
+  if (attn_lpt_ && cfg_.head_dim() >= 64 && !pk.tiles.empty()) {
+    // longest-processing-time order of the (tile, head) items over the
+    // persistent attention CTAs (attention_work_lpt)
+    const int ctas = srk::attention_ctas(static_cast<int>(pk.tiles.size()), cfg_.n_heads, device_);
+    srk::attention_work_lpt(pk.tiles.data(), static_cast<int>(pk.tiles.size()), cfg_.n_heads, ctas,
+                            p.attn_work_host);
+    put(p.attn_work, p.attn_work_host, stream_);
+    p.n_attn_work = static_cast<int32_t>(p.attn_work_host.size());
+  }
   put(p.last_rows, pk.last_rows, stream_);
   put(p.ids, pk.ids, stream_);
   put(p.seg_off, pk.seg_off, stream_);

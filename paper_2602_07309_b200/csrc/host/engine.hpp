@@ -105,6 +105,9 @@ struct Plan {
   DevBuf<int32_t> src, pos, last_rows, seg_off;
   DevBuf<srk::RowSpan> spans;
   DevBuf<srk::AttnTile> tiles;
+  DevBuf<int2> attn_work;           // LPT order of the attention work items
+  std::vector<int2> attn_work_host;
+  int32_t n_attn_work = 0;
   DevBuf<int64_t> ids;
   DevBuf<float> soft;
   // outputs
@@ -225,6 +228,7 @@ class Engine {
   // LayerNorm finished by the residual GEMMs' last contributor per 128-row
   // block (EPI_RESID_F32_LN) instead of separate LayerNorm launches.
   bool ln_after_ = false;
+  bool attn_lpt_ = true;
   cudaStream_t side_ = nullptr;  // LN-after kernels (concurrent with the residual GEMM)
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   bool post_on_ = false;

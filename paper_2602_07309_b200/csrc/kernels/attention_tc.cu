@@ -28,7 +28,10 @@
 // TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+HD) O1 [384,384+HD).
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <queue>
+#include <vector>
 #include <string>
 
 #include "launch.h"
@@ -193,19 +196,37 @@ struct Cursor {
   // Descriptor of the next item of this CTA, fetched one item ahead so the
   // global-load latency stays off the item boundary.
   AttnTile t_pre;
-  int item_pre = -1;
+  int item_pre = -1, h_pre = 0;
+
+  // Optional host-made work list (attention_work_lpt): item -> (tile, head),
+  // tile < 0 = an empty slot; n_items is then the list's length.
+  const int2* work = nullptr;
+
+  __device__ AttnTile fetch(const AttnTile* tiles, int n_tiles, int n_items, int it, int& hh) const {
+    if (work != nullptr) {
+      const int2 w = work[it];
+      hh = w.y;
+      if (w.x < 0) return AttnTile{0, 0, 0, 0, 0, 0, 0, 0};  // no blocks: skipped
+      return tiles[w.x];
+    }
+    hh = head_of(it, n_tiles, n_items);
+    return tiles[tile_of(it, n_tiles, n_items)];
+  }
 
   __device__ void load_item(const AttnTile* tiles, int n_tiles, int n_items, int item_) {
     item = item_;
     valid = item < n_items;
     if (!valid) return;
-    t = item == item_pre ? t_pre : tiles[tile_of(item, n_tiles, n_items)];
+    int hh = 0, hp = 0;
+    t = item == item_pre ? t_pre : fetch(tiles, n_tiles, n_items, item, hh);
+    if (item == item_pre) hh = h_pre;
     const int nx = item + static_cast<int>(gridDim.x);
     if (nx < n_items) {
-      t_pre = tiles[tile_of(nx, n_tiles, n_items)];
+      t_pre = fetch(tiles, n_tiles, n_items, nx, hp);
+      h_pre = hp;
       item_pre = nx;
     }
-    h = head_of(item, n_tiles, n_items);
+    h = hh;
     nb1 = (t.r1_end - t.r1_begin + kBK - 1) / kBK;
     nblk = nb1 + (t.r2_end - t.r2_begin + kBK - 1) / kBK;
     j = 0;
@@ -245,7 +266,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv,
                    const __grid_constant__ CUtensorMap tm_out, const RowSpan* __restrict__ spans,
                    const AttnTile* __restrict__ tiles, int n_tiles, __nv_bfloat16* __restrict__ out,
-                   int n_heads) {
+                   int n_heads, const int2* __restrict__ work, int n_work) {
   using C = AttnCfg<HD>;
   constexpr int SL = Slices<HD>::SL, KEYS = Slices<HD>::KEYS, OCOLS = Slices<HD>::OCOLS;
   constexpr int kSoftmaxThreads = Slices<HD>::SOFTMAX;
@@ -274,7 +295,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
   float* lsum_slot = reinterpret_cast<float*>(smem + C::LSUM_OFF);  // [2][SL][128]
   constexpr int SM_BASE = EW ? 4 : 2;  // first softmax warp
 
-  const int n_items = n_tiles * n_heads;
+  const int n_items = work != nullptr ? n_work : n_tiles * n_heads;
   const int d = n_heads * HD;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // read once: asm "memory" clobbers would otherwise reload it at every stamp
@@ -329,6 +350,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
     if (lane == 0) {
       const uint64_t keep = policy_evict_last();  // prefix K/V: re-read by every item tile
       Cursor c;
+      c.work = work;
       c.next_item(tiles, n_tiles, n_items, blockIdx.x);
       int g = 0;
       while (c.valid) {
@@ -372,6 +394,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
       constexpr uint32_t idesc_s = idesc_bf16_f32(kTM, kBK);
       constexpr uint32_t idesc_pv = idesc_bf16_f32_bmn(kTM, HD);
       Cursor sc, pc;  // next block to issue S for / next block to issue PV for
+      sc.work = work;
       sc.next_item(tiles, n_tiles, n_items, blockIdx.x);
       pc = sc;
       int gs = 0;  // global index of sc
@@ -458,6 +481,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
     // (early in item i), instead of when the K/V stream reaches the item.
     if (lane == 0) {
       Cursor c;
+      c.work = work;
       c.next_item(tiles, n_tiles, n_items, blockIdx.x);
       while (c.valid) {
         const int qb = c.li & 1;
@@ -481,6 +505,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
     const int r = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     Cursor c;
+    c.work = work;
     c.next_item(tiles, n_tiles, n_items, blockIdx.x);
     while (c.valid) {
       const int li = c.li, ob = li & 1, h = c.h, row0 = c.t.q_begin;
@@ -557,6 +582,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
     float* fin = red + 2 * SL * 128;
     const uint32_t qbar = 1 + quad, qbar_n = 32 * SL;  // the SL warps of this quadrant
     Cursor c;
+    c.work = work;
     c.next_item(tiles, n_tiles, n_items, blockIdx.x);
     int g = 0;
     uint32_t nv[KEYS];  // S of the next block, prefetched (kPrefetchS)
@@ -880,7 +906,8 @@ bool attn_use_ew() {
 
 template <int HD, bool EW>
 cudaError_t launch_tc_v(const CUtensorMap& tm, const RowSpan* spans, const AttnTile* tiles,
-                        int n_tiles, __nv_bfloat16* out, int M, int n_heads, cudaStream_t stream) {
+                        int n_tiles, __nv_bfloat16* out, int M, int n_heads, cudaStream_t stream,
+                        const int2* work, int n_work) {
   using C = AttnCfg<HD>;
   auto kern = attn_tc_kernel<HD, EW>;
   static bool attr = false;
@@ -895,18 +922,18 @@ cudaError_t launch_tc_v(const CUtensorMap& tm, const RowSpan* spans, const AttnT
   if (e != cudaSuccess) return e;
   int dev = 0;
   cudaGetDevice(&dev);
-  const int items = n_tiles * n_heads;
-  const int grid = items < num_sms(dev) ? items : num_sms(dev);
+  const int grid = attention_ctas(n_tiles, n_heads, dev);
   return launch_k(kern, dim3(grid), dim3(EW ? 512 : Slices<HD>::THREADS), C::SMEM, stream, tm,
-                  tm_out, spans, tiles, n_tiles, out, n_heads);
+                  tm_out, spans, tiles, n_tiles, out, n_heads, work, n_work);
 }
 
 template <int HD>
 cudaError_t launch_tc(const CUtensorMap& tm, const RowSpan* spans, const AttnTile* tiles,
-                      int n_tiles, __nv_bfloat16* out, int M, int n_heads, cudaStream_t stream) {
+                      int n_tiles, __nv_bfloat16* out, int M, int n_heads, cudaStream_t stream,
+                      const int2* work, int n_work) {
   if (Slices<HD>::SL == 2 && attn_use_ew())
-    return launch_tc_v<HD, true>(tm, spans, tiles, n_tiles, out, M, n_heads, stream);
-  return launch_tc_v<HD, false>(tm, spans, tiles, n_tiles, out, M, n_heads, stream);
+    return launch_tc_v<HD, true>(tm, spans, tiles, n_tiles, out, M, n_heads, stream, work, n_work);
+  return launch_tc_v<HD, false>(tm, spans, tiles, n_tiles, out, M, n_heads, stream, work, n_work);
 }
 
 
@@ -1400,9 +1427,53 @@ cudaError_t attention_eo(const CUtensorMap& tm_qkv, const RowSpan* spans, const 
 cudaError_t attention_fa(const CUtensorMap& tm_qkv, const RowSpan* spans, const AttnTile* tiles,
                          int n_tiles, __nv_bfloat16* out, int n_heads, cudaStream_t stream);
 
+int attention_ctas(int n_tiles, int n_heads, int device) {
+  const int items = n_tiles * n_heads;
+  return items < num_sms(device) ? items : num_sms(device);
+}
+
+void attention_work_lpt(const AttnTile* tiles, int n_tiles, int n_heads, int ctas,
+                        std::vector<int2>& out) {
+  // cost of a (tile, head) item in key blocks, + ~1/2 block of per-item work
+  // (Q load, O epilogue hand-off); identical for every head of a tile
+  std::vector<std::pair<double, int>> items;  // (cost, tile)
+  items.reserve(static_cast<size_t>(n_tiles));
+  for (int t = 0; t < n_tiles; ++t) {
+    const AttnTile& a = tiles[t];
+    const int nb = (a.r1_end - a.r1_begin + kBK - 1) / kBK + (a.r2_end - a.r2_begin + kBK - 1) / kBK;
+    items.push_back({nb + 0.5, t});
+  }
+  std::vector<int> seq;
+  for (int t = 0; t < n_tiles; ++t) seq.push_back(t);
+  std::stable_sort(seq.begin(), seq.end(),
+                   [&](int a, int b) { return items[a].first > items[b].first; });
+  std::vector<std::vector<int2>> lists(static_cast<size_t>(ctas));
+  // at most `cap` items per CTA, so the list length (a kernel argument baked
+  // into captured graphs) depends only on (n_tiles, n_heads, ctas)
+  const size_t n_items = static_cast<size_t>(n_tiles) * n_heads;
+  const size_t cap = (n_items + ctas - 1) / ctas + 1;
+  // min-load CTA first (ties: lowest index), items heaviest first, heads of a
+  // tile consecutively so concurrent CTAs share the tile's rows in L2
+  std::priority_queue<std::pair<double, int>, std::vector<std::pair<double, int>>,
+                      std::greater<std::pair<double, int>>>
+      heap;
+  for (int c = 0; c < ctas; ++c) heap.push({0.0, c});
+  for (int t : seq)
+    for (int h = 0; h < n_heads; ++h) {
+      auto [l, c] = heap.top();
+      heap.pop();
+      lists[c].push_back(make_int2(t, h));
+      if (lists[c].size() < cap) heap.push({l + items[t].first, c});
+    }
+  out.assign(cap * static_cast<size_t>(ctas), make_int2(-1, 0));
+  for (int c = 0; c < ctas; ++c)
+    for (size_t k = 0; k < lists[c].size(); ++k) out[k * ctas + c] = lists[c][k];
+}
+
 cudaError_t attention_tc(const CUtensorMap& tm_qkv, const void* qkv, const RowSpan* spans,
                          const AttnTile* tiles, int n_tiles, __nv_bfloat16* out, int M,
-                         int n_heads, int head_dim, cudaStream_t stream) {
+                         int n_heads, int head_dim, cudaStream_t stream, const int2* work,
+                         int n_work) {
   if (n_tiles <= 0) return cudaSuccess;
   if (head_dim == 128 && attn_use_fa())
     return attention_fa(tm_qkv, spans, tiles, n_tiles, out, n_heads, stream);
@@ -1413,10 +1484,12 @@ cudaError_t attention_tc(const CUtensorMap& tm_qkv, const void* qkv, const RowSp
   switch (head_dim) {
     case 64:
       return pp ? launch_pp<64>(tm_qkv, qkv, spans, tiles, n_tiles, out, M, n_heads, stream)
-                : launch_tc<64>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream);
+                : launch_tc<64>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream, work,
+                                n_work);
     case 128:
       return pp ? launch_pp<128>(tm_qkv, qkv, spans, tiles, n_tiles, out, M, n_heads, stream)
-                : launch_tc<128>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream);
+                : launch_tc<128>(tm_qkv, spans, tiles, n_tiles, out, M, n_heads, stream, work,
+                                 n_work);
   }
   return cudaErrorInvalidValue;
 }

@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 
 #include <utility>
+#include <vector>
 
 namespace srk {
 
@@ -150,9 +151,19 @@ cudaError_t attention(const __nv_bfloat16* qkv, const RowSpan* spans, const Attn
                       cudaStream_t stream);
 // tcgen05/TMEM path for head_dim in {64, 128}; tm_qkv maps the [rows x 3d]
 // bf16 qkv buffer with 64 x 128 boxes (make_tmap_bf16_2d(.., 128, 64)).
+// work / n_work: optional device work list from attention_work_lpt (item ->
+// (tile, head)); nullptr = head-major order.
 cudaError_t attention_tc(const CUtensorMap& tm_qkv, const void* qkv, const RowSpan* spans,
                          const AttnTile* tiles, int n_tiles, __nv_bfloat16* out, int M,
-                         int n_heads, int head_dim, cudaStream_t stream);
+                         int n_heads, int head_dim, cudaStream_t stream,
+                         const int2* work = nullptr, int n_work = 0);
+// Longest-processing-time assignment of the (tile, head) work items to the
+// persistent attention CTAs (cost = key blocks of the tile + per-item
+// overhead), laid out for the kernel's strided walk: out[k * ctas + c] is the
+// k-th item of CTA c, (-1, 0) where a CTA has fewer. ctas = attention_ctas().
+int attention_ctas(int n_tiles, int n_heads, int device);
+void attention_work_lpt(const AttnTile* tiles, int n_tiles, int n_heads, int ctas,
+                        std::vector<int2>& out);
 // Tuning aid: per-CTA clock64 timeline of attention_tc (nullptr disables).
 cudaError_t attention_set_trace(unsigned long long* dev_buf);
 cudaError_t gemm_set_trace(unsigned long long* dev_buf);

@@ -50,3 +50,9 @@ for b in [0, 1, 77, 147]:
     print("  epilogues:", e)
 ends = t[:148, 29] - t[:148, 0]
 print("cta cycles: mean", ends.mean(), "min", ends.min(), "max", ends.max())
+# per-CTA absolute start / end spread (the kernel ends with the slowest CTA)
+starts = t[:148, 0]
+endabs = t[:148, 29]
+print("start spread (cycles)", int(starts.max() - starts.min()),
+      "| end spread", int(endabs.max() - endabs.min()),
+      "| longest CTA / mean", round(float(ends.max() / ends.mean()), 3))
