@@ -398,6 +398,26 @@ def _adjacent_rows(arrs) -> np.ndarray:
         [np.asarray(a, np.float32).reshape(-1) for a in arrs]))
 
 
+class _LazyIds(Sequence):
+    """Item ids as strings for an int64 id array (or 0..n-1), converted on
+    access."""
+
+    def __init__(self, ids_or_n):
+        self._ids = ids_or_n
+
+    def __len__(self):
+        return self._ids if isinstance(self._ids, int) else len(self._ids)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        if isinstance(self._ids, int):
+            if not -self._ids <= i < self._ids:
+                raise IndexError(i)
+            return str(i % self._ids)
+        return str(int(self._ids[i]))
+
+
 class _LazyItemScores(Sequence):
     """ScoreResult.items (engine.hpp:46-51): built on first access from the
     score matrix, so callers that only need the top-k or the matrix do not
@@ -770,10 +790,15 @@ class ScoringEngine:
             emb.ctypes.data_as(C.POINTER(C.c_float)), emb.shape[1], n,
             ids.ctypes.data_as(C.POINTER(C.c_int64)) if ids is not None else None,
             self._emb_form(form), C.byref(rb.c)))
-        names = [str(int(i)) for i in ids] if ids is not None else [str(i) for i in range(n)]
-        req = ScoreRequest(request_id=request_id, prefix_tokens=prefix, mode=ScoreMode.Mixed,
-                           items=[ScoreItem(id=x) for x in names])
-        res = self._to_result(req, rb)
+        # item ids as strings, made on access only (no per-item objects per call)
+        names = _LazyIds(ids if ids is not None else n)
+        res = ScoreResult(request_id=request_id, mode=ScoreMode.Mixed,
+                          flops=FlopReport._from_c(rb.c.flops),
+                          kv_incremental_per_item=rb.c.kv_incremental_per_item,
+                          scores=rb.scores[:n].copy())
+        res.items = _LazyItemScores(names, res.scores, self.task_names)
+        for j in range(rb.c.k_returned):
+            res.topk.append((names[int(rb.idx[j])], float(rb.top[j])))
         if self._post:
             res.final_scores = self._final(n)
         return res
