@@ -287,7 +287,9 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
   uint64_t* v_empty = bars + 10;  // [2]
   uint64_t* s_full = bars + 12;   // [2]
   uint64_t* p_full = bars + 14;   // [2]
-  uint64_t* pv_done = bars + 16;  // [2]
+  // [2] waited only before an O rescale or the item's epilogue; the phases no
+  // one needs complete unwaited (compute-sanitizer synccheck: "missing wait")
+  uint64_t* pv_done = bars + 16;
   uint64_t* o_empty = bars + 18;  // [2] by item parity
   uint64_t* o_full = bars + 20;   // [2] EW: last PV of the item done
   uint64_t* l_ready = bars + 22;  // [2] EW: the item's row sums are in smem
@@ -861,9 +863,10 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
         if (first) {
           first = false;
           if constexpr (!EW) {
-            if constexpr (!EW) {
-      if (pend.on) epilogue(pend);
-    }  // previous item, overlapping this item's MMAs
+            // the previous item's epilogue, overlapping this item's MMAs.
+            // Its pv_done wait is parity-safe: PV of block g_last + 2 (same
+            // barrier) needs a P this warp has not produced yet.
+            if (pend.on) epilogue(pend);
             pend.on = false;
           }
         }
