@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import sys as _sys
+from itertools import accumulate as _accumulate
 import enum
 from dataclasses import dataclass, field
 from typing import Dict, List, Mapping, Optional, Sequence
@@ -480,55 +481,78 @@ class _WireIds(Sequence):
         return iter(self._cache)
 
 
-class _PackedRequest:
-    """Flattened sr_request; keeps the numpy buffers alive."""
+_PI32, _PI64, _PF32, _PF64 = (C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_float),
+                              C.POINTER(C.c_double))
+_SCALAR = {_PI32: C.c_int32, _PI64: C.c_int64, _PF32: C.c_float, _PF64: C.c_double}
 
-    def __init__(self, req: ScoreRequest, d_model: int, item_ids: Optional[np.ndarray] = None):
+
+def _ptr(a: np.ndarray, ptype):
+    """Typed pointer to a contiguous array's data (~3x cheaper than
+    ndarray.ctypes.data_as; read-only buffers take the slow path)."""
+    try:
+        return ptype(_SCALAR[ptype].from_buffer(a))
+    except (TypeError, ValueError):
+        return a.ctypes.data_as(ptype)
+
+
+class _PackedRequest:
+    """Flattened sr_request; keeps the numpy buffers alive. ``want_ids``
+    False leaves sr_request.item_ids null (the result's top-k is then mapped
+    back to the items by index)."""
+
+    def __init__(self, req: ScoreRequest, d_model: int, item_ids: Optional[np.ndarray] = None,
+                 want_ids: bool = True):
         self.prefix = np.ascontiguousarray(np.asarray(req.prefix_tokens, np.int32).reshape(-1))
+        items = req.items
+        n = len(items)
         mixed = ScoreMode(req.mode) == ScoreMode.Mixed
-        arrs = None
         if mixed:
-            lens = [it.n_emb_tokens for it in req.items]
-            arrs = [it.embedding for it in req.items]
-            for i, (it, n, e) in enumerate(zip(req.items, lens, arrs)):
+            lens = [it.n_emb_tokens for it in items]
+            arrs = [it.embedding for it in items]
+            for i, (it, ln, e) in enumerate(zip(items, lens, arrs)):
                 if type(e) is not np.ndarray:
                     e = arrs[i] = np.asarray(e if e is not None else [], np.float32)
-                if n < 1 or e.size != n * d_model:
+                if ln < 1 or e.size != ln * d_model:
                     raise SemrankError(ErrorCode.PayloadInvalid,
                                        f"item {it.id} embedding payload is not [n x {d_model}]")
-        else:
-            lens = list(map(len, (it.tokens for it in req.items)))
-        self.offsets = np.zeros(len(req.items) + 1, np.int32)
-        self.offsets[1:] = np.cumsum(lens) if lens else []
-        if mixed:
-            self.rows = _adjacent_rows(arrs) if req.items else np.zeros(1, np.float32)
+            self.rows = _adjacent_rows(arrs) if items else np.zeros(1, np.float32)
             self.tokens = np.zeros(1, np.int32)
         else:
-            toks = [it.tokens for it in req.items]
+            toks = [it.tokens for it in items]
+            lens = [len(t) for t in toks]
             self.tokens = (np.ascontiguousarray(np.concatenate(toks).astype(np.int32, copy=False))
-                           if toks and sum(lens) > 0 else np.zeros(1, np.int32))
+                           if toks and any(lens) else np.zeros(1, np.int32))
             self.rows = None
-        self.ids = item_ids if item_ids is not None else _item_doc_ids(req.items)
-        I = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))
+        self.offsets = np.fromiter(_accumulate(lens, initial=0), np.int32, n + 1)
+        self.ids = (item_ids if item_ids is not None
+                    else _item_doc_ids(items) if want_ids else None)
         self.c = _c.RequestC(
-            I(self.prefix), len(self.prefix), len(req.items), I(self.offsets), I(self.tokens),
-            self.rows.ctypes.data_as(C.POINTER(C.c_float)) if self.rows is not None else None,
-            self.ids.ctypes.data_as(C.POINTER(C.c_int64)) if self.ids is not None else None,
+            _ptr(self.prefix, _PI32), len(self.prefix), n, _ptr(self.offsets, _PI32),
+            _ptr(self.tokens, _PI32),
+            _ptr(self.rows, _PF32) if self.rows is not None else None,
+            _ptr(self.ids, _PI64) if self.ids is not None else None,
             int(req.mode))
 
 
 class _ResultBuf:
     def __init__(self, n_items: int, n_tasks: int, k: int):
-        self.scores = np.zeros((max(n_items, 1), n_tasks), np.float64)
+        # every field the caller reads is written by the library (scores for
+        # n_items rows, the first k_returned top-k entries)
+        self.scores = np.empty((max(n_items, 1), n_tasks), np.float64)
         self.kk = max(k, 1)
-        self.ids = np.zeros(self.kk, np.int64)
-        self.top = np.zeros(self.kk, np.float64)
-        self.idx = np.zeros(self.kk, np.int32)
-        self.c = _c.ResultC(self.scores.ctypes.data_as(C.POINTER(C.c_double)), k,
-                            self.ids.ctypes.data_as(C.POINTER(C.c_int64)),
-                            self.top.ctypes.data_as(C.POINTER(C.c_double)),
-                            self.idx.ctypes.data_as(C.POINTER(C.c_int32)),
+        self.ids = np.empty(self.kk, np.int64)
+        self.top = np.empty(self.kk, np.float64)
+        self.idx = np.empty(self.kk, np.int32)
+        self.c = _c.ResultC(_ptr(self.scores, _PF64), k, _ptr(self.ids, _PI64),
+                            _ptr(self.top, _PF64), _ptr(self.idx, _PI32),
                             _c.FlopReportC(), 0.0, 0)
+
+    def topk(self, name) -> List[tuple]:
+        """(item id, score) of the returned top-k; ``name(i)`` maps an item
+        index to its id (a negative index, no local item: the global doc id)."""
+        kr = self.c.k_returned
+        return [(name(i) if i >= 0 else str(g), t) for i, g, t in
+                zip(self.idx[:kr].tolist(), self.ids[:kr].tolist(), self.top[:kr].tolist())]
 
 
 @dataclass
@@ -655,10 +679,9 @@ class ScoringEngine:
                           flops=FlopReport._from_c(rb.c.flops),
                           kv_incremental_per_item=rb.c.kv_incremental_per_item,
                           scores=rb.scores[:n].copy())
-        res.items = _LazyItemScores([it.id for it in req.items], res.scores, self.task_names)
-        for j in range(rb.c.k_returned):
-            res.topk.append((req.items[int(rb.idx[j])].id if rb.idx[j] >= 0 else str(rb.ids[j]),
-                             float(rb.top[j])))
+        items = req.items
+        res.items = _LazyItemScores([it.id for it in items], res.scores, self.task_names)
+        res.topk = rb.topk(lambda i: items[i].id)
         return res
 
     def score(self, request: ScoreRequest, k: int = 0) -> ScoreResult:
@@ -726,9 +749,7 @@ class ScoringEngine:
                           kv_incremental_per_item=rb.c.kv_incremental_per_item,
                           scores=rb.scores[:nv].copy())
         res.items = _LazyItemScores(ids, res.scores, self.task_names)
-        for j in range(rb.c.k_returned):
-            res.topk.append((ids[int(rb.idx[j])] if rb.idx[j] >= 0 else str(rb.ids[j]),
-                             float(rb.top[j])))
+        res.topk = rb.topk(ids.__getitem__)
         if self._post:
             res.final_scores = self._final(nv)
         return res
@@ -797,8 +818,7 @@ class ScoringEngine:
                           kv_incremental_per_item=rb.c.kv_incremental_per_item,
                           scores=rb.scores[:n].copy())
         res.items = _LazyItemScores(names, res.scores, self.task_names)
-        for j in range(rb.c.k_returned):
-            res.topk.append((names[int(rb.idx[j])], float(rb.top[j])))
+        res.topk = rb.topk(names.__getitem__)
         if self._post:
             res.final_scores = self._final(n)
         return res
@@ -1116,8 +1136,7 @@ class Scheduler:
         else:
             res = ScoreResult(request_id=request.request_id, mode=ScoreMode(request.mode),
                               scores=rb.scores[:len(request.items)].copy())
-            for j in range(rb.c.k_returned):
-                res.topk.append((request.items[int(rb.idx[j])].id, float(rb.top[j])))
+            res.topk = rb.topk(lambda i: request.items[i].id)
         return res, lat.value, nb.value
 
     def stats(self, reset: bool = False) -> dict:

@@ -1,4 +1,7 @@
-"""Where the C3 end-to-end call spends its time (host packing vs device)."""
+"""Where an end-to-end call spends its time (host packing vs device):
+
+  REPS=200 python tools/e2e_probe.py c1
+"""
 import ctypes as C
 import os
 import sys
@@ -20,7 +23,10 @@ eng = sr.ScoringEngine(sr.init_model(cfg, 2026, "fan_in"), device=0)
 req, ids = bench.make_request(sr, wl, 1, 0)
 
 
-def t(fn, reps=10):
+REPS = int(os.environ.get("REPS", "10"))
+
+
+def t(fn, reps=REPS):
     fn()
     torch.cuda.synchronize()
     a = time.perf_counter()
@@ -38,3 +44,7 @@ print("sr_engine_score ms", round(t(lambda: S._check(S._lib.sr_engine_score(eng.
 print("to_result ms", round(t(lambda: eng._to_result(req, rb)), 3))
 plan = eng.plan(req, 10)
 print("plan run (device) ms", round(t(lambda: (plan.run(), plan.sync())), 3))
+print("plan fetch ms", round(t(lambda: plan.fetch()), 3))
+print("python pack+resbuf+result ms", round(t(lambda: (S._PackedRequest(req, d),
+                                                       S._ResultBuf(len(req.items), len(eng.task_names), 10),
+                                                       eng._to_result(req, rb))), 3))
