@@ -82,6 +82,10 @@ Engine::Engine(const ModelWeights& w, int device) : cfg_(w.config), device_(devi
     // LPT order of the attention work items (SRK_ATTN_LPT=0: head-major)
     const char* av = std::getenv("SRK_ATTN_LPT");
     attn_lpt_ = av == nullptr || std::atoi(av) != 0;
+    // a request with the plan's last layout re-uploads only its token ids and
+    // doc ids (SRK_LAYOUT_REUSE=0: full repack and upload every call)
+    const char* rv = std::getenv("SRK_LAYOUT_REUSE");
+    layout_reuse_ = rv == nullptr || std::atoi(rv) != 0;
     const char* lv = std::getenv("SRK_LN_AFTER");
     ln_after_ = !fold_ln_ && lv != nullptr && std::atoi(lv) != 0 && srk::gemm_use_pair(d) &&
                 d % 4 == 0 && d <= 2048;
@@ -528,25 +532,37 @@ void Engine::refill_plan(Plan& p, const sr_request* reqs, int n_req) {
   p.lens.resize(n_req);
   for (int q = 0; q < n_req; ++q) p.lens[q] = validate_request(cfg_, reqs[q]);
   p.reqs.assign(reqs, reqs + n_req);
-  pack_requests(cfg_, reqs, n_req, p.lens, p.pack);
+  layout_signature(reqs, n_req, p.lens, sig_);
   const auto& pk = p.pack;
-  put(p.src, pk.row_src, stream_);
-  put(p.pos, pk.row_pos, stream_);
-  put(p.spans, pk.spans, stream_);
-  put(p.tiles, pk.tiles, stream_);
-  p.n_attn_work = 0;
-  if (attn_lpt_ && cfg_.head_dim() >= 64 && !pk.tiles.empty()) {
-    // longest-processing-time order of the (tile, head) items over the
-    // persistent attention CTAs (attention_work_lpt)
-    const int ctas = srk::attention_ctas(static_cast<int>(pk.tiles.size()), cfg_.n_heads, device_);
-    srk::attention_work_lpt(pk.tiles.data(), static_cast<int>(pk.tiles.size()), cfg_.n_heads, ctas,
-                            p.attn_work_host);
-    put(p.attn_work, p.attn_work_host, stream_);
-    p.n_attn_work = static_cast<int32_t>(p.attn_work_host.size());
+  if (layout_reuse_ && p.layout_ok && sig_ == p.layout_sig) {
+    // same (t_q, mode, item lengths) as the arrays on the device: only the
+    // token ids and doc ids change
+    pack_sources(reqs, n_req, p.lens, p.pack);
+    put(p.src, pk.row_src, stream_);
+    put(p.ids, pk.ids, stream_);
+  } else {
+    p.layout_ok = false;
+    pack_requests(cfg_, reqs, n_req, p.lens, p.pack);
+    put(p.src, pk.row_src, stream_);
+    put(p.pos, pk.row_pos, stream_);
+    put(p.spans, pk.spans, stream_);
+    put(p.tiles, pk.tiles, stream_);
+    p.n_attn_work = 0;
+    if (attn_lpt_ && cfg_.head_dim() >= 64 && !pk.tiles.empty()) {
+      // longest-processing-time order of the (tile, head) items over the
+      // persistent attention CTAs (attention_work_lpt)
+      const int ctas = srk::attention_ctas(static_cast<int>(pk.tiles.size()), cfg_.n_heads, device_);
+      srk::attention_work_lpt(pk.tiles.data(), static_cast<int>(pk.tiles.size()), cfg_.n_heads,
+                              ctas, p.attn_work_host);
+      put(p.attn_work, p.attn_work_host, stream_);
+      p.n_attn_work = static_cast<int32_t>(p.attn_work_host.size());
+    }
+    put(p.last_rows, pk.last_rows, stream_);
+    put(p.ids, pk.ids, stream_);
+    put(p.seg_off, pk.seg_off, stream_);
+    p.layout_sig.swap(sig_);
+    p.layout_ok = true;
   }
-  put(p.last_rows, pk.last_rows, stream_);
-  put(p.ids, pk.ids, stream_);
-  put(p.seg_off, pk.seg_off, stream_);
   {
     // soft rows straight from the callers' buffers (one copy per request)
     const size_t d = cfg_.d_model;

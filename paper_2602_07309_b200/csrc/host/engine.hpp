@@ -97,6 +97,8 @@ struct Profiler {
 struct Plan {
   Engine* eng = nullptr;
   PackedBatch pack;         // host copy of the packed layout
+  std::vector<int32_t> layout_sig;  // layout_signature of the uploaded layout
+  bool layout_ok = false;           // the device layout arrays match layout_sig
   std::vector<sr_request> reqs;
   std::vector<std::vector<int32_t>> lens;
   int32_t k = 0;
@@ -229,6 +231,8 @@ class Engine {
   // block (EPI_RESID_F32_LN) instead of separate LayerNorm launches.
   bool ln_after_ = false;
   bool attn_lpt_ = true;
+  bool layout_reuse_ = true;
+  std::vector<int32_t> sig_;  // layout_signature scratch
   cudaStream_t side_ = nullptr;  // LN-after kernels (concurrent with the residual GEMM)
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   bool post_on_ = false;

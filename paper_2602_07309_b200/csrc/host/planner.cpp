@@ -224,6 +224,40 @@ void pack_requests(const ModelConfig& cfg, const sr_request* reqs, int n_req,
   }
 }
 
+void layout_signature(const sr_request* reqs, int n_req,
+                      const std::vector<std::vector<int32_t>>& lens, std::vector<int32_t>& sig) {
+  sig.clear();
+  sig.push_back(n_req);
+  for (int q = 0; q < n_req; ++q) {
+    sig.push_back(reqs[q].t_q);
+    sig.push_back(reqs[q].mode == SR_MODE_MIXED);
+    sig.push_back(reqs[q].n_items);
+    sig.insert(sig.end(), lens[q].begin(), lens[q].end());
+  }
+}
+
+void pack_sources(const sr_request* reqs, int n_req,
+                  const std::vector<std::vector<int32_t>>& lens, PackedBatch& out) {
+  out.soft_src.clear();
+  int32_t row = 0, item = 0;
+  for (int q = 0; q < n_req; ++q) {
+    const sr_request& rq = reqs[q];
+    std::copy(rq.prefix_tokens, rq.prefix_tokens + rq.t_q, out.row_src.begin() + row);
+    row += rq.t_q;
+    const bool mixed = rq.mode == SR_MODE_MIXED;
+    if (mixed && rq.n_items > 0)
+      out.soft_src.push_back({rq.item_rows, static_cast<size_t>(rq.item_offsets[rq.n_items])});
+    for (int i = 0; i < rq.n_items; ++i) {
+      const int32_t L = lens[q][i];
+      if (!mixed)  // mixed rows keep their soft-row indices (layout only)
+        std::copy(rq.item_tokens + rq.item_offsets[i], rq.item_tokens + rq.item_offsets[i] + L,
+                  out.row_src.begin() + row);
+      row += L;
+      out.ids[item++] = rq.item_ids != nullptr ? rq.item_ids[i] : static_cast<int64_t>(i);
+    }
+  }
+}
+
 int64_t multi_item_pair_count(int32_t prefix_len, const int32_t* lens, int n) {
   // engine.cpp:147-155
   const int64_t tq = prefix_len;

@@ -130,6 +130,16 @@ struct PackedBatch {
 void pack_requests(const ModelConfig& cfg, const sr_request* reqs, int n_req,
                    const std::vector<std::vector<int32_t>>& lens, PackedBatch& out);
 
+// The packed layout (row_pos, spans, tiles, last_rows, seg_off, M, n_items,
+// n_soft) depends only on each request's (t_q, mode, item lengths):
+// layout_signature writes that key; pack_sources refills what changes between
+// requests of one layout (row_src token ids, ids, soft-row sources) into an
+// `out` that pack_requests filled for the same signature.
+void layout_signature(const sr_request* reqs, int n_req,
+                      const std::vector<std::vector<int32_t>>& lens, std::vector<int32_t>& sig);
+void pack_sources(const sr_request* reqs, int n_req,
+                  const std::vector<std::vector<int32_t>>& lens, PackedBatch& out);
+
 int64_t multi_item_pair_count(int32_t prefix_len, const int32_t* lens, int n);
 
 struct BatchEntry {
