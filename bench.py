@@ -632,7 +632,7 @@ def c5_single_gpu(sr, eng, torch, stream, steps=3, warmup=2):
 
 
 SERVE_BUDGETS_MS = (50.0, 500.0)  # p99 targets: interactive, and the paper's 500 ms
-SERVE_LOADS = (0.3, 0.5, 0.7, 0.85, 0.95, 1.05)  # offered load, fraction of the 1-query pass rate
+SERVE_LOADS = (0.3, 0.4, 0.5, 0.6, 0.7, 0.85, 0.95, 1.05)  # offered load, fraction of the 1-query pass rate
 
 
 def serving_sweep(sr, eng, wl, pass_ms, seconds=3.0, max_queries=8):
