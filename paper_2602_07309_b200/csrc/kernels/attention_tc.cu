@@ -99,6 +99,15 @@ constexpr bool kShortPV = SRK_ATTN_SHORT_PV != 0;
 #define SRK_ATTN_SHORT_S 0
 #endif
 constexpr bool kShortS = SRK_ATTN_SHORT_S != 0;
+// Exponentials before the pair max exchange for every block of an item but
+// its first (recomputed when the max moves the base), so the max reduction
+// and the exchange overlap the MUFU work. Bit-identical scores
+// (tools/scores_dump.py), but measured slower at C2 (28.37k vs 28.53k pairs/s,
+// attention class within noise, 3 interleaved rounds): off.
+#ifndef SRK_ATTN_OPT_EXP
+#define SRK_ATTN_OPT_EXP 0
+#endif
+constexpr bool kOptExp = SRK_ATTN_OPT_EXP != 0 && !kPrefetchS;
 #ifndef SRK_ATTN_SKIP_HALVES
 #define SRK_ATTN_SKIP_HALVES 0
 #endif
@@ -727,9 +736,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
         bool half_on[KEYS / 32];
 #pragma unroll
         for (int hf = 0; hf < KEYS / 32; ++hf) half_on[hf] = true;
-        if (__all_sync(0xffffffff, full)) {
-          mx = max_tree<KEYS>(s);
-        } else {
+        if (!__all_sync(0xffffffff, full)) {
           auto ivl = [&](int lo, int hi) -> uint64_t {
             lo = max(lo - kh, 0);
             hi = min(hi - kh, KEYS);
@@ -750,26 +757,22 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
               const bool ok = ((i < 32 ? v0 : v1) >> (i & 31)) & 1u;
               s[i] = ok ? s[i] : -INFINITY;
             }
-            mx = max_tree<KEYS>(s);
           }
         }
         // Pair max exchange (double-buffered by block parity). Only the two
         // warps sharing this row quadrant meet (named barrier 1 + quad, 64
         // threads), not all eight; the barrier also orders both halves' S
         // reads before either writes P over S (same TMEM lanes).
-        SRK_PHASE(warp == SM_BASE && lane == 0, g, 1);
         float* slot = red + (g & 1) * SL * 128;
-        slot[slice * 128 + r] = mx;
-        named_bar_sync(qbar, qbar_n);
+        auto exchange = [&](float m) -> float {
+          slot[slice * 128 + r] = m;
+          named_bar_sync(qbar, qbar_n);
 #pragma unroll
-        for (int k = 0; k < SL; ++k) mx = fmaxf(mx, slot[k * 128 + r]);
-        SRK_PHASE(warp == SM_BASE && lane == 0, g, 2);
-
-        const bool move =
-            mx > m_used && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2);
-        const float m_new = move ? mx : m_used;
-        if (c.j > 0 && __any_sync(0xffffffff, move)) {
-          // Every PV of this item so far used the old base: rescale O rows.
+          for (int k = 0; k < SL; ++k) m = fmaxf(m, slot[k * 128 + r]);
+          return m;
+        };
+        // Every PV of this item so far used the old base: rescale O rows.
+        auto rescale_o = [&](bool move, float m_new) {
           mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
           tc_fence_after();
           const float corr = move ? ex2_approx((m_used - m_new) * scale_log2) : 1.f;
@@ -784,36 +787,20 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
             for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * corr);
             tmem_st_32x32b_x32(a, v);
           }
-        }
-        m_used = m_new;
-        SRK_PHASE(warp == SM_BASE && lane == 0, g, 3);
-        if constexpr (kPrefetchS) {
-          // Load the next block's S now, so the TMEM read (64 KB per block
-          // over all softmax warps, ~1k cycles at the TMEM read rate) overlaps
-          // this block's exponentials instead of following them.
-          Cursor cn = c;
-          cn.advance(tiles, n_tiles, n_items);
-          // only when S_{g+1} is already complete (never stall this block on it)
-          if (cn.valid && __all_sync(0xffffffff, mbar_test(&s_full[(g + 1) & 1], ((g + 1) >> 1) & 1))) {
-            tc_fence_after();
-#pragma unroll
-            for (int cc = 0; cc < KEYS / 32; ++cc)
-              tmem_ld_32x32b_x32(tmem + lane_off + ((g + 1) & 1) * kBK + slice * KEYS + cc * 32,
-                                 *reinterpret_cast<uint32_t(*)[32]>(&nv[cc * 32]));
-            pre = true;
-          }
-        }
-        const float base = m_used == -INFINITY ? 0.f : m_used * scale_log2;
-        float rs = 0.f;
+        };
         uint32_t pk[KEYS / 2];
-        if (warp_empty) {
+        // P = 2^(s * scale - base) as packed bf16x2 + this thread's row sum.
+        // Packed fp32x2 scale-subtract and row sums (FFMA2 / FADD2), MUFU
+        // exponentials: the softmax is issue-bound (ncu: 41% issue active,
+        // XU 19%), so the FMA-pipe exp2 emulation of earlier rounds cost
+        // more issue slots than the MUFU time it saved.
+        auto exps = [&]() -> float {
+          if (warp_empty) {
 #pragma unroll
-          for (int i = 0; i < KEYS / 2; ++i) pk[i] = 0u;
-        } else {
-          // Packed fp32x2 scale-subtract and row sums (FFMA2 / FADD2), MUFU
-          // exponentials: the softmax is issue-bound (ncu: 41% issue active,
-          // XU 19%), so the FMA-pipe exp2 emulation of earlier rounds cost
-          // more issue slots than the MUFU time it saved.
+            for (int i = 0; i < KEYS / 2; ++i) pk[i] = 0u;
+            return 0.f;
+          }
+          const float base = m_used == -INFINITY ? 0.f : m_used * scale_log2;
           const uint64_t sc2 = f32x2(scale_log2, scale_log2), nb2 = f32x2(-base, -base);
           uint64_t acc0 = f32x2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
@@ -840,7 +827,58 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
           float r0, r1, r2, r3;
           f32x2_split(acc0, r0, r1);
           f32x2_split(acc1, r2, r3);
-          rs = (r0 + r1) + (r2 + r3);
+          return (r0 + r1) + (r2 + r3);
+        };
+        auto moves = [&](float m) {
+          return m > m_used && (m_used == -INFINITY || (m - m_used) * scale_log2 > kRescaleLog2);
+        };
+        float rs;
+        if (kOptExp && c.j > 0) {
+          // Optimistic order (every block of an item but its first): the
+          // exponentials run against the current base while this block's max
+          // is still unknown, so the max reduction overlaps the MUFU work and
+          // the pair exchange follows it. If the max moved the base (rare with
+          // the 2^8 lazy-rescale margin), O is rescaled and the block's
+          // exponentials are recomputed: P, the row sums and O are
+          // bit-identical to the max-first order.
+          SRK_PHASE(warp == SM_BASE && lane == 0, g, 1);
+          rs = exps();
+          mx = exchange(warp_empty ? -INFINITY : max_tree<KEYS>(s));
+          SRK_PHASE(warp == SM_BASE && lane == 0, g, 2);
+          const bool move = moves(mx);
+          if (__any_sync(0xffffffff, move)) {
+            const float m_new = move ? mx : m_used;
+            rescale_o(move, m_new);
+            m_used = m_new;
+            rs = exps();
+          }
+          SRK_PHASE(warp == SM_BASE && lane == 0, g, 3);
+        } else {
+          SRK_PHASE(warp == SM_BASE && lane == 0, g, 1);
+          mx = exchange(warp_empty ? -INFINITY : max_tree<KEYS>(s));
+          SRK_PHASE(warp == SM_BASE && lane == 0, g, 2);
+          const bool move = moves(mx);
+          const float m_new = move ? mx : m_used;
+          if (c.j > 0 && __any_sync(0xffffffff, move)) rescale_o(move, m_new);
+          m_used = m_new;
+          SRK_PHASE(warp == SM_BASE && lane == 0, g, 3);
+          if constexpr (kPrefetchS) {
+            // Load the next block's S now, so the TMEM read (64 KB per block
+            // over all softmax warps, ~1k cycles at the TMEM read rate) overlaps
+            // this block's exponentials instead of following them.
+            Cursor cn = c;
+            cn.advance(tiles, n_tiles, n_items);
+            // only when S_{g+1} is already complete (never stall this block on it)
+            if (cn.valid && __all_sync(0xffffffff, mbar_test(&s_full[(g + 1) & 1], ((g + 1) >> 1) & 1))) {
+              tc_fence_after();
+#pragma unroll
+              for (int cc = 0; cc < KEYS / 32; ++cc)
+                tmem_ld_32x32b_x32(tmem + lane_off + ((g + 1) & 1) * kBK + slice * KEYS + cc * 32,
+                                   *reinterpret_cast<uint32_t(*)[32]>(&nv[cc * 32]));
+              pre = true;
+            }
+          }
+          rs = exps();
         }
         l += rs;
         SRK_PHASE(warp == SM_BASE && lane == 0, g, 4);
