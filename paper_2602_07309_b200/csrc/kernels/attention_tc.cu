@@ -103,7 +103,8 @@ constexpr bool kShortS = SRK_ATTN_SHORT_S != 0;
 // its first (recomputed when the max moves the base), so the max reduction
 // and the exchange overlap the MUFU work. Bit-identical scores
 // (tools/scores_dump.py), but measured slower at C2 (28.37k vs 28.53k pairs/s,
-// attention class within noise, 3 interleaved rounds): off.
+// attention class within noise, 3 interleaved rounds; 29.01k vs 29.23k with
+// the max accumulated inside the exponential loop): off.
 #ifndef SRK_ATTN_OPT_EXP
 #define SRK_ATTN_OPT_EXP 0
 #endif
@@ -794,7 +795,10 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
         // exponentials: the softmax is issue-bound (ncu: 41% issue active,
         // XU 19%), so the FMA-pipe exp2 emulation of earlier rounds cost
         // more issue slots than the MUFU time it saved.
-        auto exps = [&]() -> float {
+        // with_max: the block's max accumulated inside the exponential loop
+        // (4 FMNMX3 chains), so its ALU work issues between the MUFU ops.
+        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        auto exps = [&](bool with_max) -> float {
           if (warp_empty) {
 #pragma unroll
             for (int i = 0; i < KEYS / 2; ++i) pk[i] = 0u;
@@ -810,6 +814,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
               continue;
             }
             const uint64_t a2 = fma_f32x2(f32x2(s[i], s[i + 1]), sc2, nb2);
+            if (with_max) mq[(i >> 1) & 3] = fmax3f(mq[(i >> 1) & 3], s[i], s[i + 1]);
             float p0, p1;
             if (kPolyEvery > 0 && (i >> 1) % kPolyEvery == kPolyEvery - 1) {
               // this pair on the FMA pipe: MUFU is the softmax's binding unit
@@ -842,15 +847,15 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
           // exponentials are recomputed: P, the row sums and O are
           // bit-identical to the max-first order.
           SRK_PHASE(warp == SM_BASE && lane == 0, g, 1);
-          rs = exps();
-          mx = exchange(warp_empty ? -INFINITY : max_tree<KEYS>(s));
+          rs = exps(true);
+          mx = exchange(warp_empty ? -INFINITY : fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])));
           SRK_PHASE(warp == SM_BASE && lane == 0, g, 2);
           const bool move = moves(mx);
           if (__any_sync(0xffffffff, move)) {
             const float m_new = move ? mx : m_used;
             rescale_o(move, m_new);
             m_used = m_new;
-            rs = exps();
+            rs = exps(false);
           }
           SRK_PHASE(warp == SM_BASE && lane == 0, g, 3);
         } else {
@@ -878,7 +883,7 @@ __global__ void __launch_bounds__(EW ? 512 : Slices<HD>::THREADS, 1)
               pre = true;
             }
           }
-          rs = exps();
+          rs = exps(false);
         }
         l += rs;
         SRK_PHASE(warp == SM_BASE && lane == 0, g, 4);
