@@ -649,8 +649,12 @@ def serving_sweep(sr, eng, wl, pass_ms, seconds=3.0, max_queries=8):
     import threading
     pool = make_queries(sr, wl, max_queries, rank=7)
     n_items = len(pool[0].items)
-    # every pass shape the scheduler can form, captured before timing
-    for b in range(1, max_queries + 1):
+    # the largest pass's workspace first (a later growth would invalidate the
+    # captured graphs), then every pass shape the scheduler can form, captured
+    # before timing
+    eng.reserve(sum(len(r.prefix_tokens) + sum(len(it.tokens) or it.n_emb_tokens for it in r.items)
+                    for r in pool))
+    for b in range(max_queries, 0, -1):
         eng.score_batch(pool[:b], TOPK)
     cap_qps = 1000.0 / pass_ms
     rng = np.random.default_rng(2027)
@@ -667,9 +671,9 @@ def serving_sweep(sr, eng, wl, pass_ms, seconds=3.0, max_queries=8):
             for frac in SERVE_LOADS:
                 rate = frac * cap_qps
                 # enough arrivals that the drain after the last one (about one
-                # latency) stays small against the window: >= 150 queries,
+                # latency) stays small against the window: >= 300 queries (p99 = the 4th largest),
                 # at most 12 s per point (slow passes, e.g. C4 at 50 ms)
-                n = max(40, int(rate * min(12.0, max(seconds, 150.0 / rate))))
+                n = max(40, int(rate * min(12.0, max(seconds, 300.0 / rate))))
                 gaps = rng.exponential(1.0 / rate, n)
                 tickets, done = [], threading.Event()
                 lock = threading.Condition()
@@ -711,6 +715,10 @@ def serving_sweep(sr, eng, wl, pass_ms, seconds=3.0, max_queries=8):
                       "sustained": achieved_qps >= 0.97 * (n / (float(np.sum(gaps)) or 1e-9)),
                       "pairs_per_s": round(n * n_items / elapsed, 1),
                       "p50_ms": round(st["p50_ms"], 3), "p99_ms": round(st["p99_ms"], 3),
+                      "max_ms": round(st["max_ms"], 3), "mean_ms": round(st["mean_ms"], 3),
+                      "mean_pass_ms": round(st["busy_ms"] / max(st["batches"], 1), 3),
+                      "max_pass_ms": round(st["max_pass_ms"], 3),
+                      "max_wait_ms": round(st["max_wait_ms"], 3),
                       "mean_queries_per_pass": round(st["mean_batch"], 2),
                       "meets_budget": st["p99_ms"] <= budget}
                 points.append(pt)

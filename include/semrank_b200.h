@@ -245,6 +245,14 @@ int32_t sr_engine_set_projection(sr_engine* e, const float* proj, int32_t d_emb,
 int32_t sr_engine_score_emb(sr_engine* e, const int32_t* prefix, int32_t t_q, const float* emb,
                             int32_t d_emb, int32_t n_items, const int64_t* item_ids,
                             int32_t form, sr_result* res);
+/* Sizes the engine's packed-row workspace for passes of up to `rows` rows
+ * (prefix + item tokens summed over a pass's requests). Growing the workspace
+ * invalidates every captured pass graph (each is re-captured on its next run),
+ * so a server reserves its largest pass once, before it warms its pass
+ * shapes; later passes that fit never move it. SR_PARAMETER for rows < 1 or
+ * rows > 2^29. No reference counterpart (the reference has no device
+ * workspace); serving-side addition next to ScoringEngine (engine.hpp:91-103). */
+int32_t sr_engine_reserve(sr_engine* e, int64_t rows);
 /* Device / stream the engine runs on. */
 int32_t sr_engine_device(const sr_engine* e);
 void* sr_engine_stream(const sr_engine* e);
@@ -304,6 +312,8 @@ typedef struct sr_sched_stats {
   double mean_batch, p50_ms, p99_ms, max_ms, mean_ms;
   double ms_per_row; /* current pass-time estimate */
   double busy_ms;    /* summed pass durations */
+  double max_pass_ms;   /* longest pass */
+  double max_wait_ms;   /* longest queue wait (submit -> pass start) */
 } sr_sched_stats;
 /* One pass over n_req requests (tests: a host stand-in for the engine). */
 typedef int32_t (*sr_sched_exec_fn)(const sr_request* reqs, int32_t n_req, sr_result* res,

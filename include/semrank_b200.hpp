@@ -407,6 +407,8 @@ class ScoringEngine {  // engine.hpp:109-119
   // the device; EmbForm::Pad is the service's one zero-padded row per item
   // (service.cpp:208-217). Item i's id is item_ids[i] (default: its index).
   enum class EmbForm { Pad = SR_EMB_PAD, Project = SR_EMB_PROJECT };
+  // Workspace for passes of up to `rows` packed rows (sr_engine_reserve).
+  void reserve(std::int64_t rows) { check(sr_engine_reserve(e_.get(), rows)); }
   void set_projection(const std::vector<float>& proj, int d_emb, int n_soft) {
     check(sr_engine_set_projection(e_.get(), proj.empty() ? nullptr : proj.data(), d_emb,
                                    n_soft));

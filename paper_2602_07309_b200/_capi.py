@@ -88,6 +88,7 @@ _sig("sr_engine_score", i32, vp, P(RequestC), P(ResultC))
 _sig("sr_engine_score_batch", i32, vp, P(RequestC), i32, P(ResultC))
 _sig("sr_engine_item_hidden", i32, vp, P(RequestC), P(f32))
 _sig("sr_engine_set_projection", i32, vp, P(f32), i32, i32)
+_sig("sr_engine_reserve", i32, vp, i64)
 _sig("sr_engine_score_emb", i32, vp, P(i32), i32, P(f32), i32, i32, P(i64), i32, P(ResultC))
 _sig("sr_plan_create_emb", i32, vp, P(i32), i32, P(f32), i32, i32, P(i64), i32, i32, P(vp))
 _sig("sr_engine_device", i32, vp)
@@ -110,7 +111,8 @@ class SchedOptionsC(C.Structure):
 class SchedStatsC(C.Structure):
     _fields_ = [("submitted", i64), ("completed", i64), ("failed", i64), ("batches", i64),
                 ("mean_batch", f64), ("p50_ms", f64), ("p99_ms", f64), ("max_ms", f64),
-                ("mean_ms", f64), ("ms_per_row", f64), ("busy_ms", f64)]
+                ("mean_ms", f64), ("ms_per_row", f64), ("busy_ms", f64),
+                ("max_pass_ms", f64), ("max_wait_ms", f64)]
 
 
 SCHED_EXEC_FN = C.CFUNCTYPE(i32, P(RequestC), i32, P(ResultC), vp)
@@ -173,7 +175,7 @@ HEADER_SYMBOLS = [
     "sr_multi_item_pair_count", "sr_multi_item_mask", "sr_plan_batches", "sr_request_report",
     "sr_topk_host", "sr_build_prompt", "sr_score_result_to_json",
     "sr_engine_create", "sr_engine_destroy", "sr_engine_score", "sr_engine_score_batch",
-    "sr_engine_item_hidden", "sr_engine_set_projection", "sr_engine_score_emb",
+    "sr_engine_item_hidden", "sr_engine_reserve", "sr_engine_set_projection", "sr_engine_score_emb",
     "sr_plan_create_emb", "sr_engine_device", "sr_engine_stream", "sr_plan_create",
     "sr_plan_create_batch", "sr_plan_fetch_batch", "sr_plan_run", "sr_plan_sync", "sr_plan_fetch", "sr_plan_kernel_count", "sr_plan_destroy",
     "sr_plan_profile", "sr_plan_shape", "sr_sched_create", "sr_sched_create_host",

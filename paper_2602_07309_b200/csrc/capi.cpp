@@ -481,6 +481,8 @@ int32_t sr_sched_get_stats(sr_sched* s, int32_t reset, sr_sched_stats* out) {
     out->mean_ms = st.mean_ms;
     out->ms_per_row = st.ms_per_row;
     out->busy_ms = st.busy_ms;
+    out->max_pass_ms = st.max_pass_ms;
+    out->max_wait_ms = st.max_wait_ms;
   });
 }
 
@@ -697,6 +699,15 @@ int32_t sr_engine_score_cached(sr_engine* e, sr_score_cache* c, const char* sear
       srh::fail(SR_SPEC_VIOLATION, "null argument");
     std::lock_guard<std::mutex> lock(e->e->mutex());
     e->e->score_cached(*c->c, searcher_id, query_signature, model_version, *req, res, n_hits);
+  });
+}
+
+int32_t sr_engine_reserve(sr_engine* e, int64_t rows) {
+  return guard([&] {
+    if (!e) srh::fail(SR_SPEC_VIOLATION, "null argument");
+    if (rows < 1 || rows > (int64_t(1) << 29)) srh::fail(SR_PARAMETER, "reserve rows must be in [1, 2^29]");
+    std::lock_guard<std::mutex> lock(e->e->mutex());
+    e->e->reserve(static_cast<int32_t>(rows));
   });
 }
 

@@ -209,6 +209,12 @@ class Engine {
   // per-class mean ms and launch counts per forward, averaged over `reps`.
   void profile(Plan& p, int reps, float* ms_out, int32_t* launches_out);
 
+  // sr_engine_reserve: workspace for passes of up to M packed rows
+  void reserve(int32_t M) {
+    SR_CUDA_CHECK(cudaSetDevice(device_));
+    ensure_workspace(M);
+  }
+
  private:
   void ensure_workspace(int32_t M);
 

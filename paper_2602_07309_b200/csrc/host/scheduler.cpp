@@ -158,11 +158,13 @@ SchedStats Scheduler::stats(bool reset) {
   s.max_ms = mx;
   s.ms_per_row = ms_per_row_;
   s.busy_ms = busy_ms_;
+  s.max_pass_ms = max_pass_ms_;
+  s.max_wait_ms = max_wait_ms_;
   if (reset) {
     lat_.clear();
     batch_sizes_.clear();
     submitted_ = failed_ = 0;
-    busy_ms_ = 0;
+    busy_ms_ = max_pass_ms_ = max_wait_ms_ = 0;
   }
   return s;
 }
@@ -241,6 +243,7 @@ void Scheduler::loop() {
       const double per_row = (t1 - t0) / static_cast<double>(std::max<int64_t>(rows, 1));
       if (status == SR_OK) ms_per_row_ = ms_per_row_ == 0 ? per_row : 0.7 * ms_per_row_ + 0.3 * per_row;
       busy_ms_ += t1 - t0;
+      max_pass_ms_ = std::max(max_pass_ms_, t1 - t0);
       batch_sizes_.push_back(static_cast<int32_t>(batch.size()));
       for (size_t i = 0; i < batch.size(); ++i) {
         Ticket* t = batch[i];
@@ -251,6 +254,7 @@ void Scheduler::loop() {
         t->t_done = t1;
         t->batch_queries = static_cast<int32_t>(batch.size());
         t->done = true;
+        max_wait_ms_ = std::max(max_wait_ms_, t0 - t->t_submit);
         if (status == SR_OK)
           lat_.push_back(t1 - t->t_submit);
         else

@@ -78,6 +78,8 @@ struct SchedStats {
   double mean_batch = 0, p50_ms = 0, p99_ms = 0, max_ms = 0, mean_ms = 0;
   double ms_per_row = 0;  // current estimate
   double busy_ms = 0;     // sum of pass durations
+  double max_pass_ms = 0; // longest pass
+  double max_wait_ms = 0; // longest queue wait (submit -> pass start)
 };
 
 double percentile_nearest_rank(std::vector<double> v, double q);
@@ -116,6 +118,8 @@ class Scheduler {
   std::vector<int32_t> batch_sizes_;
   int64_t submitted_ = 0, failed_ = 0;
   double busy_ms_ = 0;
+  double max_pass_ms_ = 0;
+  double max_wait_ms_ = 0;
   std::thread thread_;
 };
 

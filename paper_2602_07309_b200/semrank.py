@@ -770,6 +770,12 @@ class ScoringEngine:
     # ------------------------------------------------ compact embeddings
     EMB_PAD, EMB_PROJECT = 0, 1  # sr_emb_form
 
+    def reserve(self, rows: int) -> None:
+        """Workspace for passes of up to `rows` packed rows (sr_engine_reserve):
+        call once with the largest pass before warming pass shapes, so no later
+        growth invalidates their captured graphs."""
+        _check(_lib.sr_engine_reserve(self._h, int(rows)))
+
     def set_projection(self, proj: Optional[np.ndarray], n_soft: int = 0) -> None:
         """Context compression (north_star (d)): P [d_emb x n_soft*d_model] in
         the reference's weight layout; each item's compact embedding becomes

@@ -45,6 +45,7 @@ int main(int argc, char** argv) {
   }
   if (argc > 1 && std::string(argv[1]) == "gpu") {
     ScoringEngine engine(w, 0);
+    engine.reserve(4096);  // the serving warm-up order: workspace first
     ScoreRequest req;
     req.request_id = "facade";
     req.mode = ScoreMode::MultiItem;

@@ -62,3 +62,22 @@ def test_mixed_requests_same_layout(cuda):
     got = [warm.score(r, k=3) for r in reqs]
     for r, g in zip(reqs, got):
         _same(g, sr.ScoringEngine(w, device=0).score(r, k=3))
+
+
+def test_reserve_keeps_results_and_rejects_bad_sizes(cuda):
+    """sr_engine_reserve: a workspace reserved up front (the serving warm-up
+    order) gives the same bits as growth on demand, for a small pass captured
+    before a larger one and replayed after it."""
+    w = sr.init_model(_cfg(), 5, "fan_in")
+    rng = np.random.default_rng(23)
+    small = request(*_tokens(rng, [40, 9, 96]))
+    big = request(*_tokens(rng, [96] * 40))
+    eng = sr.ScoringEngine(w, device=0)
+    eng.reserve(70 + 96 * 40)
+    got = [eng.score(small, k=3), eng.score(big, k=5), eng.score(small, k=3)]
+    for r, k, g in zip([small, big, small], [3, 5, 3], got):
+        _same(g, sr.ScoringEngine(w, device=0).score(r, k=k))
+    with pytest.raises(sr.SemrankError):
+        eng.reserve(0)
+    with pytest.raises(sr.SemrankError):
+        eng.reserve(1 << 30)
