@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define SR_ABI_VERSION 1
+#define SR_ABI_VERSION 2  /* 2: sr_sched_stats gained max_pass_ms / max_wait_ms; sr_engine_reserve */
 
 /* Status codes. 1..15 mirror semrank::ErrorCode in declaration order
  * (include/semrank/error.hpp:13-29) so a facade can rethrow

@@ -30,7 +30,7 @@ def test_library_exports_every_header_symbol():
     assert declared == set(_capi.HEADER_SYMBOLS), declared ^ set(_capi.HEADER_SYMBOLS)
     for name in declared:
         assert hasattr(_capi.lib, name), name
-    assert _capi.lib.sr_abi_version() == 1
+    assert _capi.lib.sr_abi_version() == 2
 
 
 def test_status_names_mirror_error_codes():
