@@ -131,7 +131,8 @@ int Corpus::topk(const float* query, int d_query, double w0, const double* w, in
   if (n_keep == 0) return 0;
   if (k > kScanMaxK) {
     // Large K (the reference allows K up to and past the corpus size): every
-    // doc rescored in double, then a full stable sort.
+    // doc rescored in double, then the multi-level bitonic selection of the
+    // exact top K (K <= 2048) or, past that, a full stable sort.
     SR_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 2 * sizeof(int32_t), stream_));
     entries_.ensure(static_cast<size_t>(n_));
     SR_CUDA_CHECK(srk::retrieval_refine(a, nullptr, n_, entries_.ptr, counters_, stream_));
@@ -141,9 +142,15 @@ int Corpus::topk(const float* query, int d_query, double w0, const double* w, in
                                   stream_));
     SR_CUDA_CHECK(cudaStreamSynchronize(stream_));
     if (cnt[1] & 1) fail(SR_DEGENERATE_INPUT, "cosine of a zero vector");
-    const size_t bytes = srk::retrieval_sort_scratch(n_);
-    sort_.ensure(bytes);
-    SR_CUDA_CHECK(srk::retrieval_sort_topk(entries_.ptr, n_, k, sort_.ptr, bytes, dev_out, stream_));
+    if (k <= srk::kTopkSelectMaxK) {
+      select_.ensure(srk::topk_select_scratch(n_, k));
+      SR_CUDA_CHECK(srk::topk_select(entries_.ptr, n_, k, select_.ptr, dev_out, stream_));
+    } else {
+      const size_t bytes = srk::retrieval_sort_scratch(n_);
+      sort_.ensure(bytes);
+      SR_CUDA_CHECK(
+          srk::retrieval_sort_topk(entries_.ptr, n_, k, sort_.ptr, bytes, dev_out, stream_));
+    }
     last_candidates_ = n_;
     return static_cast<int>(std::min<long long>(k, n_keep));
   }

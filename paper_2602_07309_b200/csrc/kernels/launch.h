@@ -211,7 +211,8 @@ cudaError_t topk(const double* scores, int stride, const int64_t* ids, const int
 // Merge: entries [n] (already candidates) -> best k.
 cudaError_t topk_merge(const TopkEntry* in, int n, int k, TopkEntry* out, cudaStream_t stream);
 // Best k of any number of entries (multi-level: groups of 4096 -> k each);
-// k <= 2048; scratch holds topk_select_scratch(n, k) entries.
+// k <= kTopkSelectMaxK; scratch holds topk_select_scratch(n, k) entries.
+constexpr int kTopkSelectMaxK = 2048;
 size_t topk_select_scratch(long long n, int k);
 cudaError_t topk_select(const TopkEntry* in, long long n, int k, TopkEntry* scratch,
                         TopkEntry* out, cudaStream_t stream);

@@ -36,7 +36,8 @@ def test_golden_cases_bit_identical(cuda):
     (100_003, 48, 3, 64, True, False),   # ragged tail, D > 32 chunks, non-unit vectors
     (5000, 7, 0, 512, True, True),       # D % 4 != 0, no features, k = max
     (10, 4, 1, 50, False, True),         # k above the corpus size
-    (20_000, 16, 1, 1500, True, True),   # k > 512: full device sort path
+    (20_000, 16, 1, 1500, True, True),   # 512 < k <= 2048: every doc rescored + multi-level select
+    (9_000, 16, 1, 3000, True, False),   # k > 2048: every doc rescored + full device sort
     (300_000, 32, 1, 256, True, True),   # largest k of the 3-CTA x 1024-candidate scan
     (60_000, 32, 2, 400, False, False),  # 257..512: the 2-CTA x 2048-candidate scan
 ])
