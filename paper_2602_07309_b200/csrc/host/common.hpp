@@ -48,7 +48,9 @@ int32_t guard(F&& f) {
 #define SR_CUDA_CHECK(expr)                                                               \
   do {                                                                                    \
     cudaError_t _e = (expr);                                                              \
-    if (_e != cudaSuccess)                                                                \
+    if (_e != cudaSuccess) {                                                              \
+      cudaGetLastError(); /* a non-sticky error must not fail the next launch check */    \
       ::srh::fail(SR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e) + " at " + \
                                __FILE__ + ":" + std::to_string(__LINE__));                \
+    }                                                                                     \
   } while (0)

@@ -239,6 +239,10 @@ void Engine::ensure_workspace(int32_t M) {
   xb_.release();
   stats_.release();
   ln_cnt_.release();
+  // a failed allocation below leaves no workspace (not a stale size over freed
+  // buffers), so the next call allocates again; captured graphs are stale
+  ws_rows_ = 0;
+  ++ws_epoch_;
   SR_CUDA_CHECK(cudaMalloc(&x_.ptr, rows * d * sizeof(float)));
   x_.cap = rows * d;
   SR_CUDA_CHECK(cudaMalloc(&xn_.ptr, rows * d * sizeof(__nv_bfloat16)));

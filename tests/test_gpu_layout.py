@@ -81,3 +81,7 @@ def test_reserve_keeps_results_and_rejects_bad_sizes(cuda):
         eng.reserve(0)
     with pytest.raises(sr.SemrankError):
         eng.reserve(1 << 30)
+    # a reservation the device cannot hold fails cleanly; the engine recovers
+    with pytest.raises(sr.SemrankError):
+        eng.reserve(1 << 29)
+    _same(eng.score(small, k=3), got[0])
