@@ -633,6 +633,10 @@ def c5_single_gpu(sr, eng, torch, stream, steps=3, warmup=2):
 
 SERVE_BUDGETS_MS = (50.0, 500.0)  # p99 targets: interactive, and the paper's 500 ms
 SERVE_LOADS = (0.3, 0.4, 0.5, 0.6, 0.7, 0.85, 0.95, 1.05)  # offered load, fraction of the 1-query pass rate
+# A pass stops taking requests at this many packed rows: one C2 / C4 request
+# (~24.8k rows) already fills the GPU's GEMM waves, so batching them adds
+# latency and no throughput; C3 requests (8.4k rows) still pair up.
+SERVE_SAT_ROWS = 16384
 
 
 def serving_sweep(sr, eng, wl, pass_ms, seconds=3.0, max_queries=8):
@@ -660,10 +664,12 @@ def serving_sweep(sr, eng, wl, pass_ms, seconds=3.0, max_queries=8):
     rng = np.random.default_rng(2027)
     out = {"arrivals": "open-loop Poisson, whole requests (host arrays) into sr_sched_submit",
            "latency": "submit -> completion, host clock; p99 nearest rank (service.cpp:28-34)",
-           "pass_capacity_qps": cap_qps, "max_queries_per_pass": max_queries, "budgets": {}}
+           "pass_capacity_qps": cap_qps, "max_queries_per_pass": max_queries,
+           "sat_rows": SERVE_SAT_ROWS, "budgets": {}}
     for budget in SERVE_BUDGETS_MS:
         points, best = [], None
-        with sr.Scheduler(eng, k=TOPK, max_queries=max_queries, budget_ms=budget) as s:
+        with sr.Scheduler(eng, k=TOPK, max_queries=max_queries, budget_ms=budget,
+                          sat_rows=SERVE_SAT_ROWS) as s:
             packed = [s.pack(r) for r in pool]
             for j in range(3):  # learn the pass time
                 s.wait(s.submit(pool[j % len(pool)], packed[j % len(pool)]))

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define SR_ABI_VERSION 2  /* 2: sr_sched_stats gained max_pass_ms / max_wait_ms; sr_engine_reserve */
+#define SR_ABI_VERSION 2  /* 2: sr_sched_stats gained max_pass_ms / max_wait_ms, sr_sched_options sat_rows; sr_engine_reserve */
 
 /* Status codes. 1..15 mirror semrank::ErrorCode in declaration order
  * (include/semrank/error.hpp:13-29) so a facade can rethrow
@@ -306,6 +306,9 @@ typedef struct sr_sched_options {
   int32_t k;           /* top-k per request */
   int32_t borrow;      /* nonzero: request arrays are borrowed until sr_sched_wait
                           returns (no copy at submit) */
+  int64_t sat_rows;    /* a pass stops taking requests once it holds this many
+                          rows (the device is already saturated: batching adds
+                          latency, not throughput); 0 = off */
 } sr_sched_options;
 typedef struct sr_sched_stats {
   int64_t submitted, completed, failed, batches;

@@ -607,6 +607,7 @@ class Scheduler {
     double budget_ms = 0.0;                 // latency rule (0 = off)
     int max_wait_us = 0;                    // hold an unfilled pass this long
     int k = 10;                             // top-k per request
+    std::int64_t sat_rows = 0;              // stop batching at this many rows (0 = off)
   };
   struct Stats {
     std::int64_t submitted = 0, completed = 0, failed = 0, batches = 0;
@@ -614,7 +615,7 @@ class Scheduler {
   };
 
   Scheduler(ScoringEngine& engine, const Options& o) : engine_(engine), k_(o.k) {
-    sr_sched_options so{o.max_queries, o.max_rows, o.budget_ms, o.max_wait_us, o.k, 0};
+    sr_sched_options so{o.max_queries, o.max_rows, o.budget_ms, o.max_wait_us, o.k, 0, o.sat_rows};
     sr_sched* s = nullptr;
     check(sr_sched_create(engine.e_.get(), &so, &s));
     s_.reset(s);

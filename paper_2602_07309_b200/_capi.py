@@ -105,7 +105,7 @@ _sig("sr_plan_profile", i32, vp, i32, P(f32), P(i32))
 _sig("sr_plan_shape", i32, vp, P(i64))
 class SchedOptionsC(C.Structure):
     _fields_ = [("max_queries", i32), ("max_rows", i64), ("budget_ms", f64),
-                ("max_wait_us", i32), ("k", i32), ("borrow", i32)]
+                ("max_wait_us", i32), ("k", i32), ("borrow", i32), ("sat_rows", i64)]
 
 
 class SchedStatsC(C.Structure):

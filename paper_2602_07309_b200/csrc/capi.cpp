@@ -415,6 +415,7 @@ static srh::SchedOptions sched_options(const sr_sched_options* o) {
     so.max_wait_us = o->max_wait_us;
     so.k = o->k;
     so.borrow = o->borrow != 0;
+    so.sat_rows = o->sat_rows;
   }
   return so;
 }

@@ -47,7 +47,7 @@ Scheduler::Scheduler(SchedExec exec, const ModelConfig& cfg, const SchedOptions&
     : exec_(std::move(exec)), cfg_(cfg), opt_(opt) {
   if (opt_.max_queries < 1) fail(SR_PARAMETER, "scheduler max_queries must be >= 1");
   if (opt_.max_rows < 1) fail(SR_PARAMETER, "scheduler max_rows must be >= 1");
-  if (opt_.budget_ms < 0 || opt_.max_wait_us < 0)
+  if (opt_.budget_ms < 0 || opt_.max_wait_us < 0 || opt_.sat_rows < 0)
     fail(SR_PARAMETER, "scheduler budget and wait must be >= 0");
   if (opt_.k < 0 || opt_.k > 4096) fail(SR_PARAMETER, "top-k must be in [0, 4096]");
   thread_ = std::thread([this] { loop(); });
@@ -197,7 +197,8 @@ void Scheduler::loop() {
           }
           rows = r2;
           ++take;
-          if (static_cast<int32_t>(take) >= opt_.max_queries) {
+          if (static_cast<int32_t>(take) >= opt_.max_queries ||
+              (opt_.sat_rows > 0 && rows >= opt_.sat_rows)) {
             limited = true;
             break;
           }

@@ -18,7 +18,10 @@
 //     age(oldest) + est_ms(rows + r.rows) <= budget_ms,
 //   where est_ms(rows) = ms_per_row * rows is learned from the passes run so
 //   far (EWMA). With max_wait_us > 0 an unfilled batch waits up to that long
-//   after its oldest request's arrival for more arrivals.
+//   after its oldest request's arrival for more arrivals. With sat_rows > 0 a
+//   pass also stops once it holds sat_rows rows: past the row count that fills
+//   the device a bigger pass costs the same time per row, so batching would
+//   only lengthen the wait of the requests behind it.
 #pragma once
 
 #include <condition_variable>
@@ -44,6 +47,7 @@ struct SchedOptions {
   int32_t max_wait_us = 0;  // 0 = dispatch what is queued
   int32_t k = 10;
   bool borrow = false;  // inputs borrowed until wait() instead of copied at submit
+  int64_t sat_rows = 0;  // stop adding requests once a pass holds this many rows (0 = off)
 };
 
 // A request deep-copied at submit (callers' buffers are borrowed per call).

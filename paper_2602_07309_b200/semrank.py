@@ -1077,13 +1077,13 @@ class Scheduler:
     def __init__(self, engine: Optional["ScoringEngine"] = None, *, max_queries: int = 8,
                  max_rows: int = 1 << 22, budget_ms: float = 0.0, max_wait_us: int = 0,
                  k: int = 10, borrow: bool = True, executor=None,
-                 config: Optional[ModelConfig] = None):
+                 config: Optional[ModelConfig] = None, sat_rows: int = 0):
         self.engine = engine
         self.k = k
         self.config = engine.config if engine is not None else config
         self.task_names = [kRelevanceTask] + [h.name for h in self.config.head_specs]
         opt = _c.SchedOptionsC(max_queries, max_rows, float(budget_ms), max_wait_us, k,
-                               int(bool(borrow)))
+                               int(bool(borrow)), int(sat_rows))
         self.borrow = bool(borrow)
         h = C.c_void_p()
         self._pending: Dict[int, tuple] = {}

@@ -89,6 +89,21 @@ def test_fifo_batches_respect_cap_and_rows():
         for t in ts:
             s.wait(t)
     assert max(len(ps) for ps in dev.passes) == 3  # the backlog fills passes to the cap
+    # sat_rows: a pass stops once it holds that many rows (9 per request here:
+    # 18 saturates after two), while the backlog would otherwise fill it to 8
+    dev = FakeDevice(delay=0.05)
+    with sr.Scheduler(executor=dev, config=CFG, k=1, max_queries=8, sat_rows=18) as s:
+        ts = [s.submit(req(f"q{j}", n_items=1, base=j)) for j in range(9)]
+        for t in ts:
+            s.wait(t)
+    assert [p for ps in dev.passes for p in ps] == [1 + j for j in range(9)]
+    assert max(len(ps) for ps in dev.passes) == 2
+    dev = FakeDevice(delay=0.05)
+    with sr.Scheduler(executor=dev, config=CFG, k=1, max_queries=8, sat_rows=1) as s:
+        ts = [s.submit(req(f"q{j}", n_items=1, base=j)) for j in range(5)]
+        for t in ts:
+            s.wait(t)
+    assert all(len(ps) == 1 for ps in dev.passes)  # one saturating request per pass
     # a request larger than the row budget still runs (alone)
     dev = FakeDevice()
     with sr.Scheduler(executor=dev, config=CFG, k=1, max_rows=4) as s:
