@@ -633,9 +633,9 @@ def c5_single_gpu(sr, eng, torch, stream, steps=3, warmup=2):
 
 SERVE_BUDGETS_MS = (50.0, 500.0)  # p99 targets: interactive, and the paper's 500 ms
 SERVE_LOADS = (0.3, 0.4, 0.5, 0.6, 0.7, 0.85, 0.95, 1.05)  # offered load, fraction of the 1-query pass rate
-# A pass stops taking requests at this many packed rows: one C2 / C4 request
-# (~24.8k rows) already fills the GPU's GEMM waves, so batching them adds
-# latency and no throughput; C3 requests (8.4k rows) still pair up.
+# Requests of at least this many packed rows run alone: one C2 / C4 request
+# (~24.8k rows) already fills the GPU's GEMM waves, so batching it adds
+# latency and no throughput; C3 requests (8.4k rows) batch as before.
 SERVE_SAT_ROWS = 16384
 
 

@@ -306,9 +306,9 @@ typedef struct sr_sched_options {
   int32_t k;           /* top-k per request */
   int32_t borrow;      /* nonzero: request arrays are borrowed until sr_sched_wait
                           returns (no copy at submit) */
-  int64_t sat_rows;    /* a pass stops taking requests once it holds this many
-                          rows (the device is already saturated: batching adds
-                          latency, not throughput); 0 = off */
+  int64_t sat_rows;    /* a request of at least this many packed rows runs in a
+                          pass of its own (it saturates the device alone:
+                          batching it adds latency, not throughput); 0 = off */
 } sr_sched_options;
 typedef struct sr_sched_stats {
   int64_t submitted, completed, failed, batches;

@@ -607,7 +607,7 @@ class Scheduler {
     double budget_ms = 0.0;                 // latency rule (0 = off)
     int max_wait_us = 0;                    // hold an unfilled pass this long
     int k = 10;                             // top-k per request
-    std::int64_t sat_rows = 0;              // stop batching at this many rows (0 = off)
+    std::int64_t sat_rows = 0;              // requests this large run alone (0 = off)
   };
   struct Stats {
     std::int64_t submitted = 0, completed = 0, failed = 0, batches = 0;

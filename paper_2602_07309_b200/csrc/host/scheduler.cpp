@@ -189,7 +189,10 @@ void Scheduler::loop() {
         for (uint64_t id : queue_) {
           const Ticket* t = tickets_[id].get();
           const int64_t r2 = rows + t->req.n_rows;
+          // a request that fills the device alone (sat_rows) is never batched
+          const bool alone = opt_.sat_rows > 0 && t->req.n_rows >= opt_.sat_rows;
           if (take > 0 && (static_cast<int32_t>(take) >= opt_.max_queries || r2 > opt_.max_rows ||
+                           alone ||
                            (opt_.budget_ms > 0 && ms_per_row_ > 0 &&
                             age + ms_per_row_ * static_cast<double>(r2) > opt_.budget_ms))) {
             limited = true;
@@ -197,8 +200,7 @@ void Scheduler::loop() {
           }
           rows = r2;
           ++take;
-          if (static_cast<int32_t>(take) >= opt_.max_queries ||
-              (opt_.sat_rows > 0 && rows >= opt_.sat_rows)) {
+          if (static_cast<int32_t>(take) >= opt_.max_queries || alone) {
             limited = true;
             break;
           }

@@ -19,9 +19,10 @@
 //   where est_ms(rows) = ms_per_row * rows is learned from the passes run so
 //   far (EWMA). With max_wait_us > 0 an unfilled batch waits up to that long
 //   after its oldest request's arrival for more arrivals. With sat_rows > 0 a
-//   pass also stops once it holds sat_rows rows: past the row count that fills
-//   the device a bigger pass costs the same time per row, so batching would
-//   only lengthen the wait of the requests behind it.
+//   request of at least sat_rows rows runs in a pass of its own: it fills the
+//   device alone, a bigger pass costs the same time per row, so batching it
+//   would only lengthen the wait of the requests behind it. Smaller requests
+//   batch as above (their passes amortise per-pass host work).
 #pragma once
 
 #include <condition_variable>
@@ -47,7 +48,7 @@ struct SchedOptions {
   int32_t max_wait_us = 0;  // 0 = dispatch what is queued
   int32_t k = 10;
   bool borrow = false;  // inputs borrowed until wait() instead of copied at submit
-  int64_t sat_rows = 0;  // stop adding requests once a pass holds this many rows (0 = off)
+  int64_t sat_rows = 0;  // requests of at least this many rows run alone (0 = off)
 };
 
 // A request deep-copied at submit (callers' buffers are borrowed per call).

@@ -89,21 +89,18 @@ def test_fifo_batches_respect_cap_and_rows():
         for t in ts:
             s.wait(t)
     assert max(len(ps) for ps in dev.passes) == 3  # the backlog fills passes to the cap
-    # sat_rows: a pass stops once it holds that many rows (9 per request here:
-    # 18 saturates after two), while the backlog would otherwise fill it to 8
+    # sat_rows: requests of at least that many rows run alone (13 rows: 2
+    # items), smaller ones (9 rows: 1 item) still batch from the backlog
     dev = FakeDevice(delay=0.05)
-    with sr.Scheduler(executor=dev, config=CFG, k=1, max_queries=8, sat_rows=18) as s:
-        ts = [s.submit(req(f"q{j}", n_items=1, base=j)) for j in range(9)]
+    with sr.Scheduler(executor=dev, config=CFG, k=1, max_queries=8, sat_rows=13) as s:
+        ts = [s.submit(req(f"q{j}", n_items=2 if j in (3, 4) else 1, base=j)) for j in range(10)]
         for t in ts:
             s.wait(t)
-    assert [p for ps in dev.passes for p in ps] == [1 + j for j in range(9)]
-    assert max(len(ps) for ps in dev.passes) == 2
-    dev = FakeDevice(delay=0.05)
-    with sr.Scheduler(executor=dev, config=CFG, k=1, max_queries=8, sat_rows=1) as s:
-        ts = [s.submit(req(f"q{j}", n_items=1, base=j)) for j in range(5)]
-        for t in ts:
-            s.wait(t)
-    assert all(len(ps) == 1 for ps in dev.passes)  # one saturating request per pass
+    assert [p for ps in dev.passes for p in ps] == [1 + j for j in range(10)]  # FIFO
+    for ps in dev.passes:
+        if 4 in ps or 5 in ps:  # the two 13-row requests (base 3, 4)
+            assert len(ps) == 1
+    assert max(len(ps) for ps in dev.passes) > 1
     # a request larger than the row budget still runs (alone)
     dev = FakeDevice()
     with sr.Scheduler(executor=dev, config=CFG, k=1, max_rows=4) as s:
