@@ -20,6 +20,14 @@ if not os.path.exists(LIB_PATH):
 
 lib = C.CDLL(LIB_PATH)
 
+# The structs below mirror include/semrank_b200.h at this ABI version; a
+# stale build with other layouts would corrupt memory, so refuse it.
+ABI_VERSION = 2
+lib.sr_abi_version.restype = C.c_int32
+if lib.sr_abi_version() != ABI_VERSION:
+    raise ImportError(f"{LIB_PATH} has C-ABI version {lib.sr_abi_version()}, this binding needs "
+                      f"{ABI_VERSION}: rebuild it with `python -c 'import __graft_entry__ as g; g.build()'`")
+
 i32, i64, u64, f32, f64, sz = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double, C.c_size_t
 P = C.POINTER
 
