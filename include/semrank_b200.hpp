@@ -351,6 +351,8 @@ class Comm {
 class ScoringEngine {  // engine.hpp:109-119
  public:
   explicit ScoringEngine(const ModelWeights& weights, int device = 0) : weights_(weights) {
+    if (sr_abi_version() != SR_ABI_VERSION)  // header and library built apart
+      throw Error(ErrorCode::StateInvalid, "libsemrank_b200 C-ABI version differs from the header's");
     sr_engine* e = nullptr;
     check(sr_engine_create(weights.handle(), device, &e));
     e_.reset(e);
